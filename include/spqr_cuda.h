@@ -1,0 +1,221 @@
+/*
+ * spqr_cuda.h -- C ABI of the B200-native SpQR decode path.
+ *
+ * Plain C: pointers, sizes and status codes only (no torch, no C++ types).
+ * Every entry point names the reference interface it replaces
+ * (/root/reference/proj/include/spqr/<file>:<line>).  The reference is a
+ * header-only C++ library with no FFI of its own; these are the functions a
+ * binding (ctypes / cgo / JNI) for its decode path binds.
+ * shows the bindings.
+ *
+ * Status codes: 0 = OK; 1 + Errc for the reference's error enum, in the same
+ * enumerator order as common.hpp:10-27; SPQR_E_CUDA for CUDA runtime
+ * failures; SPQR_E_UNSUPPORTED is never returned for a valid stream -- layers
+ * outside the fast-path geometry run the generic CUDA kernels.  There is no
+ * CPU fallback for any compute entry point.  spqr_last_error() returns the
+ * calling thread's last message ("<ErrcName>: <what>", as spqr::Error::what()).
+ *
+ * Layout of the stream arguments: a complete .spqr stream (48-byte header,
+ * optional permutation, column-block-major group records, CSR outliers) as
+ * produced by the reference encode (format.hpp:269-352).
+ */
+#ifndef SPQR_CUDA_H
+#define SPQR_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum spqr_status {
+    SPQR_OK = 0,
+    SPQR_E_MALFORMED_HEADER = 1,
+    SPQR_E_SHAPE_MISMATCH = 2,
+    SPQR_E_NON_FINITE_VALUE = 3,
+    SPQR_E_IO_FAILURE = 4,
+    SPQR_E_PARSE_ERROR = 5,
+    SPQR_E_MISSING_FILE = 6,
+    SPQR_E_EMPTY_INPUT = 7,
+    SPQR_E_NOT_POSITIVE_DEFINITE = 8,
+    SPQR_E_DIMENSION_MISMATCH = 9,
+    SPQR_E_CONFIG_INVALID = 10,
+    SPQR_E_COLUMN_INDEX_OVERFLOW = 11,
+    SPQR_E_MALFORMED_STREAM = 12,
+    SPQR_E_VERSION_UNSUPPORTED = 13,
+    SPQR_E_CORRUPT_CSR = 14,
+    SPQR_E_ILL_CONDITIONED = 15,
+    SPQR_E_OUTLIER_BUDGET_EXCEEDED = 16,
+    SPQR_E_CUDA = 100,
+    SPQR_E_BUFFER_TOO_SMALL = 101
+};
+
+enum spqr_dtype { SPQR_F16 = 0, SPQR_F32 = 1 };
+
+/* Header fields of a validated stream (format.hpp:366-398). */
+typedef struct spqr_layer_info {
+    uint32_t rows, cols;
+    int32_t weight_bits, scale_bits, zero_bits;
+    uint32_t beta1, beta2;
+    uint32_t outlier_count;
+    uint32_t flags;             /* stream flag bits (format.hpp:21-27) */
+    int32_t has_permutation;    /* SpqrTensor::has_permutation() (non-identity order) */
+    float tau, lambda_rel;
+    uint64_t payload_bytes;     /* stream_payload_bytes (layout.hpp:47-64): algorithmic bytes */
+    uint64_t device_bytes;      /* HBM held by a layer handle (0 from spqr_stream_validate) */
+    int32_t fast_path;          /* 1 when the fused tiled kernel serves this layer */
+    int32_t device;             /* CUDA ordinal of a layer handle */
+} spqr_layer_info;
+
+/* Size model -- LayoutSpec + stream_payload_bytes, layout.hpp:18-64. */
+typedef struct spqr_layout_spec {
+    uint32_t rows, cols;
+    int32_t weight_bits, scale_bits, zero_bits;
+    uint32_t beta1, beta2;
+    uint32_t outlier_count;
+    int32_t has_permutation;
+} spqr_layout_spec;
+
+/* Flat view of an in-memory SpqrTensor (format.hpp:32-67).  Arrays are
+ * row-major / block-major exactly as the reference's vectors:
+ *   codes          rows*cols           CodeMatrix::codes (solve order)
+ *   scale_codes    nblocks*rows        BlockStats::scale_codes, block k at k*rows (bits<=8)
+ *   zero_codes     nblocks*rows        BlockStats::zero_codes
+ *   raw_scales     nblocks*rows        BlockStats::raw_scales (bits==16)
+ *   raw_zeros      nblocks*rows        BlockStats::raw_zeros
+ *   group_scalars  nblocks*ngroups*4   StatGroupScalars {scale_s,scale_z,zero_s,zero_z}
+ *   order          cols or NULL        Permutation::order (NULL = identity)
+ *   outlier_*      outlier_count       OutlierSet::items (row, col, value16)
+ * For spqr_decode_arrays the caller allocates every array it passes (sizes
+ * from spqr_stream_validate); NULL arrays are skipped. */
+typedef struct spqr_tensor_arrays {
+    uint32_t rows, cols;
+    int32_t weight_bits, scale_bits, zero_bits;
+    uint32_t beta1, beta2;
+    uint32_t flags;  /* act_order / integer_zero / full_range_sign / outliers_enabled bits */
+    float tau, lambda_rel;
+    uint32_t* order;
+    uint8_t* codes;
+    uint8_t* scale_codes;
+    uint8_t* zero_codes;
+    float* raw_scales;
+    float* raw_zeros;
+    uint16_t* group_scalars;
+    uint32_t outlier_count;
+    uint32_t* outlier_rows;
+    uint32_t* outlier_cols;
+    uint16_t* outlier_vals;
+} spqr_tensor_arrays;
+
+typedef struct spqr_layer spqr_layer;
+
+typedef struct spqr_layer_opts {
+    int32_t device;        /* CUDA ordinal; -1 = current device */
+    int32_t force_generic; /* 1: never build the tiled planes (tests / comparison) */
+    int32_t keep_stream;   /* 1: keep the raw stream on the device even on the fast path */
+    uint32_t row_begin;    /* row band [row_begin, row_end) of the stream; 0,0 = all rows */
+    uint32_t row_end;
+} spqr_layer_opts;
+
+/* ---------------------------------------------------------------- host -- */
+/* Last error message of the calling thread ("" when none). */
+const char* spqr_last_error(void);
+/* Library / layout version string. */
+const char* spqr_version(void);
+
+/* decode()'s validation without materialising codes (format.hpp:354-500).
+ * Returns the reference's Errc for every malformed input. */
+int spqr_stream_validate(const uint8_t* stream, size_t nbytes, spqr_layer_info* info);
+
+/* decode(std::span<const uint8_t>) -> SpqrTensor, format.hpp:354. */
+int spqr_decode_arrays(const uint8_t* stream, size_t nbytes, spqr_tensor_arrays* out);
+
+/* encode(const SpqrTensor&) -> bytes, format.hpp:269.  *len receives the
+ * required size; SPQR_E_BUFFER_TOO_SMALL when cap < *len (out may be NULL). */
+int spqr_encode_arrays(const spqr_tensor_arrays* t, uint8_t* out, size_t cap, size_t* len);
+
+/* stream_payload_bytes(const LayoutSpec&), layout.hpp:47. */
+uint64_t spqr_payload_bytes(const spqr_layout_spec* ls);
+
+/* estimate_avg_bits(...), format.hpp:531.  out5 = {avg, base, first, second, outliers}. */
+int spqr_estimate_avg_bits(int b_w, int b_s, int b_z, uint32_t beta1, uint32_t beta2, double r_o,
+                           double* out5);
+
+/* measure_actual_bits(const SpqrTensor&), format.hpp:550, from a stream.
+ * out3 = {bits_per_param, per_outlier_bits, payload_bytes}. */
+int spqr_measure_actual_bits(const uint8_t* stream, size_t nbytes, double* out3);
+
+/* Row band [r0, r1) of a stream as a standalone, valid stream (CSR rebased,
+ * same permutation).  The row-sharded multi-GPU wrapper loads these. */
+int spqr_stream_slice_rows(const uint8_t* stream, size_t nbytes, uint32_t r0, uint32_t r1,
+                           uint8_t* out, size_t cap, size_t* len);
+
+/* Host-only check of the device-layout transcoder: stream -> tiled planes ->
+ * stream, no GPU involved.  Returns SPQR_E_CONFIG_INVALID if the layer is
+ * outside the fast-path geometry. */
+int spqr_transcode_roundtrip_host(const uint8_t* stream, size_t nbytes, uint8_t* out, size_t cap,
+                                  size_t* len);
+
+/* Test hook: the tiled HBM image the loader would upload, in host memory.
+ * dims4 = {Gn, Pn, cell_bytes, outlier_count}.  Call with NULL buffers to
+ * query dims; then cells (Gn*Pn*cell_bytes), cell_off (Gn*Pn+1), entries. */
+int spqr_debug_tiled_host(const uint8_t* stream, size_t nbytes, uint32_t* dims4, uint8_t* cells,
+                          uint32_t* cell_off, uint32_t* entries);
+
+/* -------------------------------------------------------------- device -- */
+/* decode (format.hpp:354) + build_tile_plan (kernel.hpp:54) + upload:
+ * validates exactly like decode, transcodes to the HBM layout, uploads once. */
+int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opts* opts,
+                      spqr_layer** out);
+void spqr_layer_destroy(spqr_layer* layer);
+int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info);
+
+/* encode() of the device-resident layer (format.hpp:269): reads the HBM
+ * layout back and re-encodes it; byte-identical to the input stream. */
+int spqr_layer_export_stream(const spqr_layer* layer, uint8_t* out, size_t cap, size_t* len);
+
+/* dequantize_full (kernel.hpp:17-25): W (rows x cols, fp32, row-major,
+ * ORIGINAL column order) into caller device memory.  Bit-exact. */
+int spqr_dequantize(const spqr_layer* layer, float* w_dev, void* cuda_stream);
+
+/* Scratch for spqr_matvec_ws (bytes). */
+uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
+
+/* matvec (kernel.hpp:89-124) on device buffers: y[b] = W * x[b] for b < batch.
+ * x: batch x cols (f16 or f32, original column order), y: batch x rows fp32.
+ * Asynchronous on cuda_stream; allocates nothing.  spqr_matvec uses the
+ * layer's own workspace (one stream at a time); spqr_matvec_ws takes a caller
+ * workspace (concurrent streams). */
+int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
+                void* cuda_stream);
+int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,
+                   int batch, void* workspace, uint64_t ws_bytes, void* cuda_stream);
+
+/* matvec(const SpqrTensor&, std::span<const float>) drop-in with HOST buffers
+ * (kernel.hpp:126-128): copies x in, computes, copies y out, synchronises. */
+int spqr_matvec_host(const spqr_layer* layer, const float* x_host, float* y_host, int batch);
+
+/* Comparator: dense fp16 GEMV y = W16 * x (our own 128-bit-load kernel),
+ * W16 rows x cols row-major fp16, x fp16, y fp32. */
+int spqr_dense_gemv_f16(const void* w_dev, const void* x_dev, float* y_dev, uint32_t rows,
+                        uint32_t cols, void* cuda_stream);
+
+/* Number of kernel launches the last spqr_matvec* on this thread issued. */
+int spqr_last_launch_count(void);
+
+/* bench_matvec (kernel.hpp:185-226) timings on the device, CUDA-event timed,
+ * median over `repeats`: ns3 = {fused matvec, dequantize_full (the naive
+ * path's reconstruction), dense fp16 GEMV of the same shape}. */
+int spqr_bench_layer(const spqr_layer* layer, int repeats, double* ns3);
+
+/* Minimal device-memory helpers for C/C++ hosts without a CUDA toolchain. */
+int spqr_dev_alloc(void** ptr, size_t bytes);
+void spqr_dev_free(void* ptr);
+int spqr_dev_copy_to_host(void* dst, const void* src, size_t bytes);
+int spqr_dev_copy_to_device(void* dst, const void* src, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPQR_CUDA_H */

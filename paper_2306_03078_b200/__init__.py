@@ -1,0 +1,364 @@
+"""paper_2306_03078_b200 -- B200-native SpQR decode path (y = W x, W in SpQR format).
+
+Python face of the C ABI in include/spqr_cuda.h (libspqr_b200.so, built in-tree
+by ``paper_2306_03078_b200.build``).  Mirrors the reference's decode-path API
+(/root/reference/proj/include/spqr: format.hpp encode/decode/save/load,
+kernel.hpp dequantize_full/matvec) with the same error codes.
+
+There is no CPU fallback: the compute calls launch sm_100a kernels, and the
+module raises if the library is missing.  Device buffers are passed as raw
+pointers (torch tensors are accepted for convenience: torch is plumbing for
+device memory and streams here, never the compute path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libspqr_b200.so")
+
+ERRC = [
+    "malformed_header", "shape_mismatch", "non_finite_value", "io_failure", "parse_error",
+    "missing_file", "empty_input", "not_positive_definite", "dimension_mismatch",
+    "config_invalid", "column_index_overflow", "malformed_stream", "version_unsupported",
+    "corrupt_csr", "ill_conditioned", "outlier_budget_exceeded",
+]
+F16, F32 = 0, 1
+
+
+class SpqrError(RuntimeError):
+    """spqr::Error across the C ABI: .status (1 + Errc) and .errc name."""
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        if 1 <= status <= len(ERRC):
+            self.errc = ERRC[status - 1]
+        elif status == 100:
+            self.errc = "cuda"
+        elif status == 101:
+            self.errc = "buffer_too_small"
+        else:
+            self.errc = f"status{status}"
+        super().__init__(msg or self.errc)
+
+
+class LayerInfo(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("cols", C.c_uint32), ("weight_bits", C.c_int32),
+                ("scale_bits", C.c_int32), ("zero_bits", C.c_int32), ("beta1", C.c_uint32),
+                ("beta2", C.c_uint32), ("outlier_count", C.c_uint32), ("flags", C.c_uint32),
+                ("has_permutation", C.c_int32), ("tau", C.c_float), ("lambda_rel", C.c_float),
+                ("payload_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
+                ("fast_path", C.c_int32), ("device", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class LayoutSpec(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("cols", C.c_uint32), ("weight_bits", C.c_int32),
+                ("scale_bits", C.c_int32), ("zero_bits", C.c_int32), ("beta1", C.c_uint32),
+                ("beta2", C.c_uint32), ("outlier_count", C.c_uint32), ("has_permutation", C.c_int32)]
+
+
+class TensorArrays(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("cols", C.c_uint32), ("weight_bits", C.c_int32),
+                ("scale_bits", C.c_int32), ("zero_bits", C.c_int32), ("beta1", C.c_uint32),
+                ("beta2", C.c_uint32), ("flags", C.c_uint32), ("tau", C.c_float),
+                ("lambda_rel", C.c_float), ("order", C.c_void_p), ("codes", C.c_void_p),
+                ("scale_codes", C.c_void_p), ("zero_codes", C.c_void_p), ("raw_scales", C.c_void_p),
+                ("raw_zeros", C.c_void_p), ("group_scalars", C.c_void_p),
+                ("outlier_count", C.c_uint32), ("outlier_rows", C.c_void_p),
+                ("outlier_cols", C.c_void_p), ("outlier_vals", C.c_void_p)]
+
+
+class LayerOpts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("force_generic", C.c_int32), ("keep_stream", C.c_int32),
+                ("row_begin", C.c_uint32), ("row_end", C.c_uint32)]
+
+
+_lib = None
+
+# every symbol include/spqr_cuda.h declares (tests check the .so exports them)
+EXPORTS = [
+    "spqr_last_error", "spqr_version", "spqr_stream_validate", "spqr_decode_arrays",
+    "spqr_encode_arrays", "spqr_payload_bytes", "spqr_estimate_avg_bits",
+    "spqr_measure_actual_bits", "spqr_stream_slice_rows", "spqr_transcode_roundtrip_host",
+    "spqr_layer_create", "spqr_layer_destroy", "spqr_layer_get_info", "spqr_layer_export_stream",
+    "spqr_dequantize", "spqr_workspace_bytes", "spqr_matvec", "spqr_matvec_ws", "spqr_matvec_host",
+    "spqr_dense_gemv_f16", "spqr_last_launch_count", "spqr_debug_tiled_host",
+]
+
+
+def lib() -> C.CDLL:
+    """Load libspqr_b200.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2306_03078_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, u32, i32 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_int
+    sig = {
+        "spqr_last_error": (C.c_char_p, []),
+        "spqr_version": (C.c_char_p, []),
+        "spqr_stream_validate": (i32, [vp, sz, C.POINTER(LayerInfo)]),
+        "spqr_decode_arrays": (i32, [vp, sz, C.POINTER(TensorArrays)]),
+        "spqr_encode_arrays": (i32, [C.POINTER(TensorArrays), vp, sz, C.POINTER(C.c_size_t)]),
+        "spqr_payload_bytes": (C.c_uint64, [C.POINTER(LayoutSpec)]),
+        "spqr_estimate_avg_bits": (i32, [i32, i32, i32, u32, u32, C.c_double, vp]),
+        "spqr_measure_actual_bits": (i32, [vp, sz, vp]),
+        "spqr_stream_slice_rows": (i32, [vp, sz, u32, u32, vp, sz, C.POINTER(C.c_size_t)]),
+        "spqr_transcode_roundtrip_host": (i32, [vp, sz, vp, sz, C.POINTER(C.c_size_t)]),
+        "spqr_layer_create": (i32, [vp, sz, C.POINTER(LayerOpts), C.POINTER(vp)]),
+        "spqr_layer_destroy": (None, [vp]),
+        "spqr_layer_get_info": (i32, [vp, C.POINTER(LayerInfo)]),
+        "spqr_layer_export_stream": (i32, [vp, vp, sz, C.POINTER(C.c_size_t)]),
+        "spqr_dequantize": (i32, [vp, vp, vp]),
+        "spqr_workspace_bytes": (C.c_uint64, [vp, i32]),
+        "spqr_matvec": (i32, [vp, vp, i32, vp, i32, vp]),
+        "spqr_matvec_ws": (i32, [vp, vp, i32, vp, i32, vp, C.c_uint64, vp]),
+        "spqr_matvec_host": (i32, [vp, vp, vp, i32]),
+        "spqr_dense_gemv_f16": (i32, [vp, vp, vp, u32, u32, vp]),
+        "spqr_last_launch_count": (i32, []),
+        "spqr_debug_tiled_host": (i32, [vp, sz, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc:
+        raise SpqrError(rc, lib().spqr_last_error().decode())
+
+
+def _buf(stream: bytes):
+    a = np.frombuffer(stream, dtype=np.uint8)
+    return a, a.ctypes.data_as(C.c_void_p), a.size
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor / numpy array / int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data_as(C.c_void_p)
+    raise TypeError(type(x))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+# ---------------------------------------------------------------- format --
+def validate(stream: bytes) -> dict:
+    """decode()'s validation (format.hpp:354-500); returns the header info."""
+    _, p, n = _buf(stream)
+    info = LayerInfo()
+    _check(lib().spqr_stream_validate(p, n, C.byref(info)))
+    return info.as_dict()
+
+
+def decode_arrays(stream: bytes) -> dict:
+    """decode() (format.hpp:354) into flat numpy arrays (SpqrTensor fields)."""
+    info = validate(stream)
+    m, n = info["rows"], info["cols"]
+    nb = (n + info["beta1"] - 1) // info["beta1"]
+    ng = (m + info["beta2"] - 1) // info["beta2"]
+    sb, zb = info["scale_bits"], info["zero_bits"]
+    out = {
+        "order": np.zeros(n, np.uint32), "codes": np.zeros(m * n, np.uint8),
+        "scale_codes": np.zeros(nb * m, np.uint8) if sb != 16 else None,
+        "zero_codes": np.zeros(nb * m, np.uint8) if zb != 16 else None,
+        "raw_scales": np.zeros(nb * m, np.float32) if sb == 16 else None,
+        "raw_zeros": np.zeros(nb * m, np.float32) if zb == 16 else None,
+        "group_scalars": np.zeros(nb * ng * 4, np.uint16) if (sb != 16 or zb != 16) else None,
+        "outlier_rows": np.zeros(info["outlier_count"], np.uint32),
+        "outlier_cols": np.zeros(info["outlier_count"], np.uint32),
+        "outlier_vals": np.zeros(info["outlier_count"], np.uint16),
+    }
+    ta = TensorArrays()
+    for k, v in out.items():
+        setattr(ta, k, None if v is None else v.ctypes.data)
+    _, p, nn = _buf(stream)
+    _check(lib().spqr_decode_arrays(p, nn, C.byref(ta)))
+    for k in ("rows", "cols", "weight_bits", "scale_bits", "zero_bits", "beta1", "beta2", "flags",
+              "tau", "lambda_rel"):
+        out[k] = getattr(ta, k)
+    if not (out["flags"] & 1):
+        out["order"] = None
+    out["flags"] &= ~1
+    return out
+
+
+def encode_arrays(a: dict) -> bytes:
+    """encode() (format.hpp:269) of a tensor given as flat arrays."""
+    keep = {}
+
+    def arr(key, dt):
+        v = a.get(key)
+        if v is None:
+            return None
+        keep[key] = np.ascontiguousarray(v, dtype=dt)
+        return keep[key].ctypes.data
+
+    ta = TensorArrays(rows=a["rows"], cols=a["cols"], weight_bits=a["weight_bits"],
+                      scale_bits=a["scale_bits"], zero_bits=a["zero_bits"], beta1=a["beta1"],
+                      beta2=a["beta2"], flags=a.get("flags", 0x18), tau=a.get("tau", 0.0),
+                      lambda_rel=a.get("lambda_rel", 0.0))
+    ta.order = arr("order", np.uint32)
+    ta.codes = arr("codes", np.uint8)
+    ta.scale_codes = arr("scale_codes", np.uint8)
+    ta.zero_codes = arr("zero_codes", np.uint8)
+    ta.raw_scales = arr("raw_scales", np.float32)
+    ta.raw_zeros = arr("raw_zeros", np.float32)
+    ta.group_scalars = arr("group_scalars", np.uint16)
+    ta.outlier_rows = arr("outlier_rows", np.uint32)
+    ta.outlier_cols = arr("outlier_cols", np.uint32)
+    ta.outlier_vals = arr("outlier_vals", np.uint16)
+    ta.outlier_count = int(np.asarray(a["outlier_rows"]).size)
+    n = C.c_size_t()
+    rc = lib().spqr_encode_arrays(C.byref(ta), None, 0, C.byref(n))
+    if rc not in (0, 101):
+        _check(rc)
+    out = np.empty(n.value, np.uint8)
+    _check(lib().spqr_encode_arrays(C.byref(ta), out.ctypes.data_as(C.c_void_p), out.size, C.byref(n)))
+    return out.tobytes()
+
+
+def payload_bytes(rows, cols, weight_bits, scale_bits, zero_bits, beta1, beta2, outlier_count,
+                  has_permutation) -> int:
+    """stream_payload_bytes (layout.hpp:47-64): the algorithmic bytes."""
+    ls = LayoutSpec(rows, cols, weight_bits, scale_bits, zero_bits, beta1, beta2, outlier_count,
+                    int(bool(has_permutation)))
+    return int(lib().spqr_payload_bytes(C.byref(ls)))
+
+
+def estimate_avg_bits(b_w, b_s, b_z, beta1, beta2, r_o) -> np.ndarray:
+    out = np.zeros(5, np.float64)
+    _check(lib().spqr_estimate_avg_bits(b_w, b_s, b_z, beta1, beta2, r_o, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def measure_actual_bits(stream: bytes) -> np.ndarray:
+    out = np.zeros(3, np.float64)
+    _, p, n = _buf(stream)
+    _check(lib().spqr_measure_actual_bits(p, n, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def _sized_call(f, *args) -> bytes:
+    n = C.c_size_t()
+    rc = f(*args, None, 0, C.byref(n))
+    if rc not in (0, 101):
+        _check(rc)
+    out = np.empty(max(n.value, 1), np.uint8)
+    _check(f(*args, out.ctypes.data_as(C.c_void_p), out.size, C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def slice_rows(stream: bytes, r0: int, r1: int) -> bytes:
+    """Rows [r0, r1) as a standalone stream (row-sharding helper)."""
+    a, p, n = _buf(stream)
+    return _sized_call(lib().spqr_stream_slice_rows, p, n, r0, r1)
+
+
+def transcode_roundtrip_host(stream: bytes) -> bytes:
+    a, p, n = _buf(stream)
+    return _sized_call(lib().spqr_transcode_roundtrip_host, p, n)
+
+
+def debug_tiled_host(stream: bytes) -> dict:
+    """The tiled HBM image (host copy) -- test hook for the kernel model."""
+    a, p, n = _buf(stream)
+    dims = np.zeros(4, np.uint32)
+    _check(lib().spqr_debug_tiled_host(p, n, dims.ctypes.data_as(C.c_void_p), None, None, None))
+    Gn, Pn, cb, nnz = (int(v) for v in dims)
+    cells = np.zeros(Gn * Pn * cb, np.uint8)
+    off = np.zeros(Gn * Pn + 1, np.uint32)
+    ent = np.zeros(max(nnz, 1), np.uint32)
+    _check(lib().spqr_debug_tiled_host(p, n, dims.ctypes.data_as(C.c_void_p), cells.ctypes.data_as(C.c_void_p),
+                                       off.ctypes.data_as(C.c_void_p), ent.ctypes.data_as(C.c_void_p)))
+    return {"Gn": Gn, "Pn": Pn, "cell_bytes": cb, "cells": cells, "cell_off": off, "entries": ent[:nnz]}
+
+
+# ---------------------------------------------------------------- device --
+class Layer:
+    """A layer resident in HBM (spqr_layer_create: decode + plan + upload)."""
+
+    def __init__(self, stream: bytes, device: int = -1, force_generic: bool = False,
+                 rows: tuple[int, int] | None = None):
+        a, p, n = _buf(stream)
+        opts = LayerOpts(device=device, force_generic=int(force_generic), keep_stream=1,
+                         row_begin=rows[0] if rows else 0, row_end=rows[1] if rows else 0)
+        h = C.c_void_p()
+        _check(lib().spqr_layer_create(p, n, C.byref(opts), C.byref(h)))
+        self._h = h
+        info = LayerInfo()
+        _check(lib().spqr_layer_get_info(h, C.byref(info)))
+        self.info = info.as_dict()
+        self.rows, self.cols = self.info["rows"], self.info["cols"]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().spqr_layer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def matvec(self, x, y, batch: int = 1, stream=None, workspace=None) -> None:
+        """y (batch x rows, fp32, device) = W x (batch x cols, f16/f32, device)."""
+        dt = F16 if str(getattr(x, "dtype", "")).endswith("float16") else F32
+        if workspace is None:
+            _check(lib().spqr_matvec(self._h, _ptr(x), dt, _ptr(y), batch, _stream_ptr(stream)))
+        else:
+            _check(lib().spqr_matvec_ws(self._h, _ptr(x), dt, _ptr(y), batch, _ptr(workspace),
+                                        workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+    def matvec_host(self, x: np.ndarray) -> np.ndarray:
+        """Drop-in matvec(t, x) with host buffers (kernel.hpp:126)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        batch = x.size // self.cols
+        y = np.empty(batch * self.rows, np.float32)
+        _check(lib().spqr_matvec_host(self._h, x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), batch))
+        return y.reshape(batch, self.rows) if batch > 1 else y
+
+    def dequantize(self, w, stream=None) -> None:
+        """dequantize_full (kernel.hpp:17) into a rows x cols fp32 device buffer."""
+        _check(lib().spqr_dequantize(self._h, _ptr(w), _stream_ptr(stream)))
+
+    def workspace_bytes(self, batch: int = 1) -> int:
+        return int(lib().spqr_workspace_bytes(self._h, batch))
+
+    def export_stream(self) -> bytes:
+        return _sized_call(lib().spqr_layer_export_stream, self._h)
+
+
+def dense_gemv_f16(w, x, y, rows: int, cols: int, stream=None) -> None:
+    _check(lib().spqr_dense_gemv_f16(_ptr(w), _ptr(x), _ptr(y), rows, cols, _stream_ptr(stream)))
+
+
+def last_launch_count() -> int:
+    return int(lib().spqr_last_launch_count())

@@ -1,0 +1,575 @@
+// capi.cu -- device side of the C ABI: layer handles (validate, transcode,
+// upload), matvec / dequantize launches, export, dense comparator.
+//
+// Replaces (reference, /root/reference/proj/include/spqr):
+//   decode + build_tile_plan ... spqr_layer_create   (format.hpp:354, kernel.hpp:54)
+//   dequantize_full ............ spqr_dequantize     (kernel.hpp:17-25)
+//   matvec ..................... spqr_matvec[_ws|_host] (kernel.hpp:89-128)
+//   encode (of the layer) ...... spqr_layer_export_stream (format.hpp:269)
+// No CPU fallback: every compute entry point launches sm_100a kernels or fails
+// with SPQR_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "kernels.cuh"
+
+using spqr::detail::guard;
+namespace T = spqr_tiled;
+
+namespace {
+
+constexpr int kNW = 8;       // consumer warps per CTA (one CTA per SM)
+constexpr int kNSlot = 4;    // TMA ring depth per warp
+constexpr std::uint32_t kEntCapBytes = 2048;
+
+thread_local int g_launches = 0;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA: ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T_>
+T_* dalloc(std::size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMalloc(&p, count * sizeof(T_)), "cudaMalloc");
+    return static_cast<T_*>(p);
+}
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DevGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct spqr_layer {
+    int device = 0;
+    spqr_layer_info info{};
+    std::vector<std::uint8_t> prefix;  // header + permutation (for export)
+    spqr::detail::StreamView geo;      // geometry (base -> prefix)
+    // raw stream (dequantize + generic matvec)
+    std::uint8_t* d_stream = nullptr;
+    std::uint32_t* d_order = nullptr;  // solve position -> source column, or null
+    // tiled fast path
+    bool fast = false;
+    std::uint8_t* d_cells = nullptr;
+    std::uint32_t* d_cell_off = nullptr;
+    std::uint32_t* d_ent = nullptr;
+    std::uint32_t* d_warp_start = nullptr;
+    std::uint32_t* d_wfirst = nullptr;
+    std::uint32_t* d_wlast = nullptr;
+    std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, nwarps = 0, grid = 0, n_pad = 0;
+    // own workspace
+    mutable std::mutex mu;
+    mutable void* d_ws = nullptr;
+    mutable std::uint64_t ws_bytes = 0;
+    mutable float* d_xh = nullptr;  // host-API staging
+    mutable float* d_yh = nullptr;
+    mutable std::size_t xh_cap = 0, yh_cap = 0;
+
+    ~spqr_layer() {
+        for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
+                        static_cast<void*>(d_cell_off), static_cast<void*>(d_ent), static_cast<void*>(d_warp_start),
+                        static_cast<void*>(d_wfirst), static_cast<void*>(d_wlast), d_ws,
+                        static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
+            if (p) cudaFree(p);
+    }
+};
+
+namespace {
+
+spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
+    const auto& v = L->geo;
+    spqr_dev::RawGeom g{};
+    g.s = L->d_stream;
+    g.order = L->d_order;
+    g.rows = v.rows; g.cols = v.cols; g.b1 = v.b1; g.b2 = v.b2;
+    g.nblocks = v.nblocks; g.ngroups = v.ngroups;
+    g.wb = v.wb; g.sb = v.sb; g.zb = v.zb;
+    g.rec_off = v.rec_off; g.col_block_bytes = v.col_block_bytes;
+    g.csr_off = v.csr_off; g.ent_off = v.ent_off;
+    return g;
+}
+
+// Workspace carve-up (bytes, 256-aligned pieces).
+struct WsLayout {
+    std::uint64_t xfrag = 0, xlo = 0, xsc = 0, xp = 0, partial = 0, counters = 0, total = 0;
+};
+std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
+WsLayout ws_layout(const spqr_layer* L, int batch) {
+    WsLayout w;
+    const std::uint64_t b = static_cast<std::uint64_t>(std::max(batch, 1));
+    std::uint64_t o = 0;
+    if (L->fast) {
+        const std::uint64_t nblk = L->n_pad / 16;
+        w.xfrag = o; o += al(b * nblk * 32);
+        w.xlo = o; o += al(b * nblk * 32);
+        w.xsc = o; o += al(b * nblk * 8);
+        w.xp = o; o += al(b * L->n_pad * 4);
+        w.partial = o; o += al(static_cast<std::uint64_t>(L->nwarps) * 2 * 32 * 4);
+        w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
+    } else {
+        w.xp = o; o += al(b * L->info.cols * 4);
+    }
+    w.total = o;
+    return w;
+}
+
+template <int BW, int BSZ, bool XLO>
+void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::size_t smem, cudaStream_t st) {
+    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, kNW, kNSlot>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+           "cudaFuncSetAttribute(smem)");
+        attr_set[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemv_tiled");
+    ++g_launches;
+}
+
+template <int BW, bool XLO>
+void launch_xprep_t(const void* x, int f16, const spqr_layer* L, int batch, uint2* xf, uint2* xl, float2* xs,
+                    float* xp, cudaStream_t st) {
+    const std::uint32_t work = (L->n_pad / 16) * static_cast<std::uint32_t>(batch);
+    spqr_dev::xprep_tiled<BW, XLO><<<(work + 127) / 128, 128, 0, st>>>(x, f16, L->info.cols, L->n_pad,
+                                                                    static_cast<std::uint32_t>(batch), L->d_order,
+                                                                    xf, xl, xs, xp);
+    ck(cudaGetLastError(), "launch xprep_tiled");
+    ++g_launches;
+}
+
+void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, uint2* xf, uint2* xl, float2* xs,
+                    float* xp, cudaStream_t st) {
+    const bool lo = !f16;
+    switch (L->info.weight_bits * 2 + (lo ? 1 : 0)) {
+        case 4: launch_xprep_t<2, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+        case 5: launch_xprep_t<2, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+        case 6: launch_xprep_t<3, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+        case 7: launch_xprep_t<3, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+        case 8: launch_xprep_t<4, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+        default: launch_xprep_t<4, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+    }
+}
+
+std::size_t tiled_smem(const spqr_layer* L, std::uint32_t* slot_bytes) {
+    *slot_bytes = (L->cell_bytes + kEntCapBytes + 127u) & ~127u;
+    return static_cast<std::size_t>(kNW) * kNSlot * *slot_bytes;
+}
+
+void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xlo, std::size_t smem,
+                    cudaStream_t st) {
+    const int key = L->info.weight_bits * 100 + L->info.scale_bits * 10 + (xlo ? 1 : 0);
+    switch (key) {
+#define SPQR_CASE(BW, BSZ)                                                            \
+    case BW * 100 + BSZ * 10 + 0: launch_tiled_t<BW, BSZ, false>(p, L->grid, smem, st); break; \
+    case BW * 100 + BSZ * 10 + 1: launch_tiled_t<BW, BSZ, true>(p, L->grid, smem, st); break;
+        SPQR_CASE(2, 2) SPQR_CASE(2, 3) SPQR_CASE(2, 4)
+        SPQR_CASE(3, 2) SPQR_CASE(3, 3) SPQR_CASE(3, 4)
+        SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
+#undef SPQR_CASE
+        default: spqr::fail(spqr::Errc::config_invalid, "no tiled kernel instantiated for this layer");
+    }
+}
+
+void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int batch, void* ws, std::uint64_t wsb,
+                cudaStream_t st) {
+    if (batch < 1) spqr::fail(spqr::Errc::shape_mismatch, "batch must be >= 1");
+    if (dtype != SPQR_F16 && dtype != SPQR_F32) spqr::fail(spqr::Errc::config_invalid, "x dtype must be f16 or f32");
+    const WsLayout w = ws_layout(L, batch);
+    if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
+    auto* base = static_cast<std::uint8_t*>(ws);
+    const int f16 = dtype == SPQR_F16;
+    if (L->fast) {
+        auto* xf = reinterpret_cast<uint2*>(base + w.xfrag);
+        auto* xl = reinterpret_cast<uint2*>(base + w.xlo);
+        auto* xs = reinterpret_cast<float2*>(base + w.xsc);
+        auto* xp = reinterpret_cast<float*>(base + w.xp);
+        dispatch_xprep(x, f16, L, batch, xf, xl, xs, xp, st);
+        std::uint32_t slot_bytes = 0;
+        const std::size_t smem = tiled_smem(L, &slot_bytes);
+        const std::uint32_t nblk = L->n_pad / 16;
+        for (int b = 0; b < batch; ++b) {
+            spqr_dev::TiledParams p{};
+            p.cells = L->d_cells; p.cell_off = L->d_cell_off; p.ent = L->d_ent;
+            p.warp_start = L->d_warp_start; p.wfirst = L->d_wfirst; p.wlast = L->d_wlast;
+            p.xfrag = xf + static_cast<std::size_t>(b) * nblk * 4;
+            p.xlo = xl + static_cast<std::size_t>(b) * nblk * 4;
+            p.xsc = reinterpret_cast<const float4*>(xs + static_cast<std::size_t>(b) * nblk);
+            p.xp = xp + static_cast<std::size_t>(b) * L->n_pad;
+            p.y = y + static_cast<std::size_t>(b) * L->info.rows;
+            p.partial = reinterpret_cast<float*>(base + w.partial);
+            p.counters = reinterpret_cast<std::uint32_t*>(base + w.counters);
+            p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps;
+            p.ent_cap_bytes = kEntCapBytes; p.slot_bytes = slot_bytes;
+            dispatch_tiled(p, L, !f16, smem, st);
+        }
+    } else {
+        auto* xp = reinterpret_cast<float*>(base + w.xp);
+        const std::uint64_t nx = static_cast<std::uint64_t>(L->info.cols) * batch;
+        spqr_dev::xprep_raw<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, st>>>(x, f16, L->info.cols, batch,
+                                                                                  L->d_order, xp);
+        ck(cudaGetLastError(), "launch xprep_raw");
+        ++g_launches;
+        const spqr_dev::RawGeom geo = raw_geom(L);
+        for (int b = 0; b < batch; ++b) {
+            spqr_dev::gemv_raw<<<(L->info.rows + 7) / 8, 256, 0, st>>>(
+                geo, xp + static_cast<std::size_t>(b) * L->info.cols, y + static_cast<std::size_t>(b) * L->info.rows);
+            ck(cudaGetLastError(), "launch gemv_raw");
+            ++g_launches;
+        }
+    }
+}
+
+void ensure_own_ws(const spqr_layer* L, int batch) {
+    const std::uint64_t need = ws_layout(L, batch).total;
+    if (L->ws_bytes >= need) return;
+    if (L->d_ws) {
+        ck(cudaDeviceSynchronize(), "sync before workspace growth");
+        cudaFree(L->d_ws);
+        L->d_ws = nullptr;
+    }
+    L->d_ws = dalloc<std::uint8_t>(need);
+    ck(cudaMemset(L->d_ws, 0, need), "zero workspace");
+    L->ws_bytes = need;
+}
+
+// Static split of the cell sequence over all warps, balanced by bytes
+// (dense cell bytes + a per-outlier instruction cost in byte units).
+void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms) {
+    const std::uint32_t Q = t.Gn * t.Pn;
+    L->grid = static_cast<std::uint32_t>(sms);
+    L->nwarps = L->grid * kNW;
+    std::vector<double> pre(Q + 1, 0.0);
+    for (std::uint32_t q = 0; q < Q; ++q)
+        pre[q + 1] = pre[q] + t.cell_bytes + 12.0 * (t.cell_off[q + 1] - t.cell_off[q]);
+    const double total = pre[Q];
+    std::vector<std::uint32_t> ws(L->nwarps + 1, Q);
+    std::uint32_t q = 0;
+    for (std::uint32_t k = 0; k < L->nwarps; ++k) {
+        const double target = total * k / L->nwarps;
+        while (q < Q && pre[q] + 0.5 * (pre[q + 1] - pre[q]) < target) ++q;
+        ws[k] = q;
+    }
+    ws[L->nwarps] = Q;
+    std::vector<std::uint32_t> wf(t.Gn, UINT32_MAX), wl(t.Gn, 0);
+    for (std::uint32_t k = 0; k < L->nwarps; ++k) {
+        if (ws[k] >= ws[k + 1]) continue;
+        for (std::uint32_t G = ws[k] / t.Pn; G <= (ws[k + 1] - 1) / t.Pn; ++G) {
+            wf[G] = std::min(wf[G], k);
+            wl[G] = std::max(wl[G], k);
+        }
+    }
+    L->d_warp_start = dalloc<std::uint32_t>(ws.size());
+    L->d_wfirst = dalloc<std::uint32_t>(t.Gn);
+    L->d_wlast = dalloc<std::uint32_t>(t.Gn);
+    ck(cudaMemcpy(L->d_warp_start, ws.data(), 4 * ws.size(), cudaMemcpyHostToDevice), "H2D warp_start");
+    ck(cudaMemcpy(L->d_wfirst, wf.data(), 4ull * t.Gn, cudaMemcpyHostToDevice), "H2D wfirst");
+    ck(cudaMemcpy(L->d_wlast, wl.data(), 4ull * t.Gn, cudaMemcpyHostToDevice), "H2D wlast");
+}
+
+}  // namespace
+
+// ================================================================ C ABI ====
+extern "C" {
+
+int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opts* opts, spqr_layer** out) {
+    *out = nullptr;
+    return guard([&] {
+        spqr_layer_opts o{};
+        o.device = -1;
+        if (opts) o = *opts;
+        std::vector<std::uint8_t> band;
+        const std::uint8_t* s = stream;
+        std::size_t n = nbytes;
+        if (o.row_end > o.row_begin) {
+            band = spqr::slice_rows(std::span<const std::uint8_t>(stream, nbytes), o.row_begin, o.row_end);
+            s = band.data();
+            n = band.size();
+        }
+        const spqr::detail::StreamView v = spqr::detail::parse_stream(s, n);
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (ndev == 0) throw CudaError("CUDA: no device");
+        DevGuard dg(o.device);
+        auto L = std::make_unique<spqr_layer>();
+        ck(cudaGetDevice(&L->device), "cudaGetDevice");
+        L->prefix.assign(s, s + v.rec_off);
+        L->geo = spqr::detail::geometry_from_prefix(L->prefix.data(), L->prefix.size());
+        std::memset(&L->info, 0, sizeof(L->info));
+        L->info.rows = v.rows; L->info.cols = v.cols; L->info.weight_bits = v.wb;
+        L->info.scale_bits = v.sb; L->info.zero_bits = v.zb; L->info.beta1 = v.b1; L->info.beta2 = v.b2;
+        L->info.outlier_count = v.nnz; L->info.flags = v.flags; L->info.has_permutation = v.has_permutation;
+        L->info.tau = v.tau; L->info.lambda_rel = v.lambda_rel;
+        L->info.payload_bytes = n - spqr::kSpqrHeaderBytes;
+        L->info.device = L->device;
+        std::uint64_t dev_bytes = 0;
+
+        if (v.has_permutation) {
+            std::vector<std::uint32_t> ord(v.cols);
+            for (std::uint32_t k = 0; k < v.cols; ++k) ord[k] = v.order(k);
+            L->d_order = dalloc<std::uint32_t>(v.cols);
+            ck(cudaMemcpy(L->d_order, ord.data(), 4ull * v.cols, cudaMemcpyHostToDevice), "H2D order");
+            dev_bytes += 4ull * v.cols;
+        }
+        L->fast = !o.force_generic && spqr::detail::tiled_supported(v);
+        if (!L->fast || o.keep_stream || true) {  // dequantize reads the raw stream (v1)
+            L->d_stream = dalloc<std::uint8_t>(n + 16);
+            ck(cudaMemcpy(L->d_stream, s, n, cudaMemcpyHostToDevice), "H2D stream");
+            dev_bytes += n;
+        }
+        if (L->fast) {
+            const spqr::detail::TiledHost t = spqr::detail::transcode_to_tiled(v, 0);
+            L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
+            L->d_cells = dalloc<std::uint8_t>(t.cells.size());
+            ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
+            L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size());
+            ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice),
+               "H2D cell_off");
+            L->d_ent = dalloc<std::uint32_t>(t.entries.size() + 8);  // TMA may round the tail up to 16 B
+            ck(cudaMemset(L->d_ent, 0, 4 * (t.entries.size() + 8)), "zero entries");
+            if (!t.entries.empty())
+                ck(cudaMemcpy(L->d_ent, t.entries.data(), 4 * t.entries.size(), cudaMemcpyHostToDevice), "H2D ent");
+            int sms = 0;
+            ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
+            plan_partition(L.get(), t, sms);
+            dev_bytes += t.cells.size() + 4 * t.cell_off.size() + 4 * t.entries.size();
+        }
+        L->info.fast_path = L->fast;
+        ensure_own_ws(L.get(), 1);
+        dev_bytes += L->ws_bytes;
+        L->info.device_bytes = dev_bytes;
+        *out = L.release();
+    });
+}
+
+void spqr_layer_destroy(spqr_layer* layer) {
+    if (!layer) return;
+    DevGuard dg(layer->device);
+    delete layer;
+}
+
+int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info) {
+    return guard([&] { *info = layer->info; });
+}
+
+int spqr_layer_export_stream(const spqr_layer* L, uint8_t* out, size_t cap, size_t* len) {
+    int rc = SPQR_OK;
+    const int g = guard([&] {
+        DevGuard dg(L->device);
+        std::vector<std::uint8_t> bytes;
+        if (L->fast) {
+            spqr::detail::TiledHost t;
+            t.Gn = L->Gn; t.Pn = L->Pn; t.cell_bytes = L->cell_bytes; t.prefix = L->prefix;
+            t.cells.resize(static_cast<std::size_t>(t.Gn) * t.Pn * t.cell_bytes);
+            t.cell_off.resize(static_cast<std::size_t>(t.Gn) * t.Pn + 1);
+            ck(cudaMemcpy(t.cells.data(), L->d_cells, t.cells.size(), cudaMemcpyDeviceToHost), "D2H cells");
+            ck(cudaMemcpy(t.cell_off.data(), L->d_cell_off, 4 * t.cell_off.size(), cudaMemcpyDeviceToHost),
+               "D2H cell_off");
+            t.entries.resize(L->info.outlier_count);
+            if (!t.entries.empty())
+                ck(cudaMemcpy(t.entries.data(), L->d_ent, 4 * t.entries.size(), cudaMemcpyDeviceToHost), "D2H ent");
+            bytes = spqr::detail::tiled_to_stream(L->geo, t, 0);
+        } else {
+            bytes.resize(L->info.payload_bytes + spqr::kSpqrHeaderBytes);
+            ck(cudaMemcpy(bytes.data(), L->d_stream, bytes.size(), cudaMemcpyDeviceToHost), "D2H stream");
+        }
+        *len = bytes.size();
+        if (!out || cap < bytes.size()) {
+            spqr::detail::set_last_error("buffer too small");
+            rc = SPQR_E_BUFFER_TOO_SMALL;
+            return;
+        }
+        std::memcpy(out, bytes.data(), bytes.size());
+    });
+    return g ? g : rc;
+}
+
+int spqr_dequantize(const spqr_layer* L, float* w_dev, void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        auto st = static_cast<cudaStream_t>(cuda_stream);
+        g_launches = 0;
+        const spqr_dev::RawGeom geo = raw_geom(L);
+        const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
+        const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((total + 255) / 256, 1u << 20));
+        spqr_dev::dequant_raw<<<blocks, 256, 0, st>>>(geo, w_dev);
+        ck(cudaGetLastError(), "launch dequant_raw");
+        spqr_dev::outliers_raw<<<(geo.rows + 255) / 256, 256, 0, st>>>(geo, w_dev);
+        ck(cudaGetLastError(), "launch outliers_raw");
+        g_launches = 2;
+    });
+}
+
+uint64_t spqr_workspace_bytes(const spqr_layer* L, int batch) { return ws_layout(L, batch).total; }
+
+int spqr_matvec_ws(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_dev, int batch, void* ws,
+                   uint64_t ws_bytes, void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        g_launches = 0;
+        run_matvec(L, x_dev, x_dtype, y_dev, batch, ws, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    });
+}
+
+int spqr_matvec(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_dev, int batch, void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        g_launches = 0;
+        std::lock_guard<std::mutex> lk(L->mu);
+        ensure_own_ws(L, batch);
+        run_matvec(L, x_dev, x_dtype, y_dev, batch, L->d_ws, L->ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    });
+}
+
+int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, int batch) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        g_launches = 0;
+        std::lock_guard<std::mutex> lk(L->mu);
+        if (batch < 1) spqr::fail(spqr::Errc::shape_mismatch, "batch must be >= 1");
+        ensure_own_ws(L, batch);
+        const std::size_t nx = static_cast<std::size_t>(L->info.cols) * batch;
+        const std::size_t ny = static_cast<std::size_t>(L->info.rows) * batch;
+        if (L->xh_cap < nx) {
+            if (L->d_xh) cudaFree(L->d_xh);
+            L->d_xh = dalloc<float>(nx);
+            L->xh_cap = nx;
+        }
+        if (L->yh_cap < ny) {
+            if (L->d_yh) cudaFree(L->d_yh);
+            L->d_yh = dalloc<float>(ny);
+            L->yh_cap = ny;
+        }
+        cudaStream_t st = nullptr;
+        ck(cudaMemcpyAsync(L->d_xh, x_host, 4 * nx, cudaMemcpyHostToDevice, st), "H2D x");
+        run_matvec(L, L->d_xh, SPQR_F32, L->d_yh, batch, L->d_ws, L->ws_bytes, st);
+        ck(cudaMemcpyAsync(y_host, L->d_yh, 4 * ny, cudaMemcpyDeviceToHost, st), "D2H y");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int spqr_dense_gemv_f16(const void* w_dev, const void* x_dev, float* y_dev, uint32_t rows, uint32_t cols,
+                        void* cuda_stream) {
+    return guard([&] {
+        g_launches = 0;
+        int sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid = std::min<unsigned>((rows + 7) / 8, static_cast<unsigned>(sms) * 8);
+        spqr_dev::dense_gemv_f16<<<grid, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+            static_cast<const __half*>(w_dev), static_cast<const __half*>(x_dev), y_dev, rows, cols);
+        ck(cudaGetLastError(), "launch dense_gemv_f16");
+        g_launches = 1;
+    });
+}
+
+int spqr_last_launch_count(void) { return g_launches; }
+
+int spqr_bench_layer(const spqr_layer* L, int repeats, double* ns3) {
+    return guard([&] {
+        if (repeats < 1) spqr::fail(spqr::Errc::config_invalid, "repeats must be >= 1");
+        DevGuard dg(L->device);
+        const std::size_t m = L->info.rows, n = L->info.cols;
+        float* x = dalloc<float>(n);
+        float* y = dalloc<float>(m);
+        float* w = dalloc<float>(m * n);
+        __half* w16 = dalloc<__half>(m * n);
+        __half* x16 = dalloc<__half>(n);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        auto cleanup = [&] {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            cudaFree(x); cudaFree(y); cudaFree(w); cudaFree(w16); cudaFree(x16);
+        };
+        try {
+            ck(cudaMemset(x, 0, 4 * n), "memset");
+            ck(cudaMemset(w16, 0, 2 * m * n), "memset");
+            ck(cudaMemset(x16, 0, 2 * n), "memset");
+            ensure_own_ws(L, 1);
+            auto time_it = [&](auto&& body) {
+                body();  // warm-up
+                std::vector<float> ms(repeats);
+                for (int i = 0; i < repeats; ++i) {
+                    cudaEventRecord(e0, nullptr);
+                    body();
+                    cudaEventRecord(e1, nullptr);
+                    ck(cudaEventSynchronize(e1), "event sync");
+                    cudaEventElapsedTime(&ms[i], e0, e1);
+                }
+                std::sort(ms.begin(), ms.end());
+                const int mid = repeats / 2;
+                return 1e6 * (repeats % 2 ? ms[mid] : 0.5 * (ms[mid - 1] + ms[mid]));
+            };
+            ns3[0] = time_it([&] { run_matvec(L, x, SPQR_F32, y, 1, L->d_ws, L->ws_bytes, nullptr); });
+            const spqr_dev::RawGeom geo = raw_geom(L);
+            const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
+            const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((total + 255) / 256, 1u << 20));
+            ns3[1] = time_it([&] {
+                spqr_dev::dequant_raw<<<blocks, 256>>>(geo, w);
+                spqr_dev::outliers_raw<<<(geo.rows + 255) / 256, 256>>>(geo, w);
+            });
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device);
+            const unsigned grid = std::min<unsigned>((m + 7) / 8, static_cast<unsigned>(sms) * 8);
+            ns3[2] = time_it([&] {
+                spqr_dev::dense_gemv_f16<<<grid, 256>>>(w16, x16, y, static_cast<std::uint32_t>(m),
+                                                        static_cast<std::uint32_t>(n));
+            });
+            ck(cudaGetLastError(), "bench launches");
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
+int spqr_dev_alloc(void** ptr, size_t bytes) {
+    return guard([&] { ck(cudaMalloc(ptr, bytes ? bytes : 1), "cudaMalloc"); });
+}
+void spqr_dev_free(void* ptr) {
+    if (ptr) cudaFree(ptr);
+}
+int spqr_dev_copy_to_host(void* dst, const void* src, size_t bytes) {
+    return guard([&] { ck(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "D2H"); });
+}
+int spqr_dev_copy_to_device(void* dst, const void* src, size_t bytes) {
+    return guard([&] { ck(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "H2D"); });
+}
+
+}  // extern "C"

@@ -1,0 +1,628 @@
+// kernels.cuh -- sm_100a kernels of the SpQR decode path.
+//
+//   xprep_tiled ........ x gather through the permutation (kernel.hpp:93-98) +
+//                        per-block power-of-two scaling + per-column 2^-p
+//                        pre-scale into m16n8k16 B fragments + block sums.
+//   gemv_tiled ......... THE hot kernel: fused dequant-GEMV + CSR outlier merge
+//                        (kernel.hpp:89-124) over the tiled HBM layout, one
+//                        output write per row, deterministic.
+//   dequant_raw / outliers_raw ... bit-exact dequantize_full (kernel.hpp:17-25,
+//                        solver.hpp:345-362) on the raw stream, any geometry.
+//   xprep_raw / gemv_raw ......... generic matvec on the raw stream for layers
+//                        outside the tiled geometry (any bits / group sizes).
+//   dense_gemv_f16 ..... comparator: dense fp16 GEMV.
+//
+// Build: -gencode arch=compute_100a,code=sm_100a, no fast-math (IEEE fp32 with
+// subnormals is part of the bit-exact contract).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "tiled.hpp"
+
+namespace spqr_dev {
+
+namespace T = spqr_tiled;
+
+// ------------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion on an mbarrier (UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// D(16x8, fp32) += A(16x16, f16 row) * B(16x8, f16 col)
+__device__ __forceinline__ void mma16816(float (&c)[4], const std::uint32_t (&a)[4], std::uint32_t b0,
+                                         std::uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float u2f_small(std::uint32_t v) {  // exact for v < 2^23
+    return __int_as_float(0x4B000000u | v) - 8388608.0f;
+}
+
+__device__ __forceinline__ float h2f_bits(std::uint32_t h16) {
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(h16)));
+}
+
+// ============================================================ tiled path ====
+struct TiledParams {
+    const std::uint8_t* cells;
+    const std::uint32_t* cell_off;
+    const std::uint32_t* ent;
+    const std::uint32_t* warp_start;  // [nwarps+1]
+    const std::uint32_t* wfirst;      // [Gn]
+    const std::uint32_t* wlast;       // [Gn]
+    const uint2* xfrag;               // [nblk_pad*4] per batch
+    const uint2* xlo;                 // same (fp32 inputs)
+    const float4* xsc;                // [nblk_pad/2] per batch: {SC,XX} x 2 blocks
+    const float* xp;                  // [n_pad] per batch, solve order
+    float* y;                         // [m] per batch
+    float* partial;                   // [nwarps*2*32]
+    std::uint32_t* counters;          // [Gn]
+    std::uint32_t m, Pn, Gn, nwarps;
+    std::uint32_t ent_cap_bytes;      // per slot
+    std::uint32_t slot_bytes;
+};
+
+template <int BW>
+struct Geo {
+    static constexpr int CW = T::words_per_container(BW);
+    static constexpr int MPC = T::mmas_per_container(BW);
+    static constexpr int NP = T::pairs_per_container(BW);
+    static constexpr int CPU = T::containers_per_unit(BW);
+    static constexpr int LANE_WORDS = 4 * BW;  // 16*BW bytes
+};
+
+// 16-bit window of a container's lo/hi streams starting at stream byte B.
+template <int CW>
+__device__ __forceinline__ std::uint32_t window(const std::uint32_t* w, int B) {
+    if ((B & 1) == 0) return w[B >> 1];
+    if ((B >> 1) + 1 < CW) return __byte_perm(w[B >> 1], w[(B >> 1) + 1], 0x6341);
+    return w[B >> 1] >> 8;
+}
+
+// Load `SB` bytes at 2-byte or 4-byte granularity into two 64-bit words.
+template <int SB>
+__device__ __forceinline__ void load_stat_bits(const std::uint8_t* p, std::uint64_t (&v)[2]) {
+    v[0] = v[1] = 0;
+    if constexpr (SB % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < SB / 4; ++i)
+            v[i >> 1] |= static_cast<std::uint64_t>(reinterpret_cast<const std::uint32_t*>(p)[i]) << (32 * (i & 1));
+    } else if constexpr (SB % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < SB / 2; ++i)
+            v[i >> 2] |= static_cast<std::uint64_t>(reinterpret_cast<const std::uint16_t*>(p)[i]) << (16 * (i & 3));
+    } else {
+#pragma unroll
+        for (int i = 0; i < SB; ++i) v[i >> 3] |= static_cast<std::uint64_t>(p[i]) << (8 * (i & 7));
+    }
+}
+
+template <int NBITS>
+__device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int pos) {
+    // pos and NBITS are compile-time after unrolling; fields never straddle
+    // more than the two words.
+    const int w = pos >> 6, s = pos & 63;
+    std::uint64_t x = v[w] >> s;
+    if (s + NBITS > 64 && w == 0) x |= v[1] << (64 - s);
+    return static_cast<std::uint32_t>(x) & ((1u << NBITS) - 1u);
+}
+
+template <int BW, int BS, int BZ, bool XLO, int NW, int NSLOT>
+__global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
+    using G = Geo<BW>;
+    constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
+    constexpr std::uint32_t CELL = 2 * UNIT;
+    constexpr std::uint32_t CODEB = T::code_bytes(BW);
+    constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
+    constexpr int SB = BS + BZ;
+    constexpr std::uint32_t MASK = (1u << BW) - 1u;
+
+    extern __shared__ __align__(128) std::uint8_t smem[];
+    __shared__ std::uint64_t bars[NW][NSLOT];
+    __shared__ float oacc[NW][32];
+    __shared__ std::uint32_t slot_e[NW][NSLOT][2];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const std::uint32_t wk = blockIdx.x * NW + warp;
+    const std::uint32_t q0 = p.warp_start[wk], q1 = p.warp_start[wk + 1];
+    std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * NSLOT * p.slot_bytes;
+
+    if (lane == 0) {
+        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[warp][s], 1);
+        fence_mbar_init();
+    }
+    oacc[warp][lane] = 0.0f;
+    __syncwarp();
+    if (q0 >= q1) {
+        pdl_wait();
+        return;
+    }
+
+    // per-cell outlier offsets, 32 cells at a time in lanes
+    std::uint32_t off_base = q0;
+    std::uint32_t off_lane = (q0 + lane <= q1) ? __ldg(p.cell_off + q0 + lane) : 0u;
+    auto cell_offset = [&](std::uint32_t q) -> std::uint32_t {  // warp-uniform q, all lanes call
+        if (q >= off_base + 32) {
+            off_base = q;
+            off_lane = (q + lane <= q1) ? __ldg(p.cell_off + q + lane) : 0u;
+        }
+        return __shfl_sync(0xffffffffu, off_lane, static_cast<int>(q - off_base));
+    };
+
+    auto issue = [&](std::uint32_t q, int slot) {  // whole warp calls (shuffles inside)
+        const std::uint32_t e0 = cell_offset(q), e1 = cell_offset(q + 1);
+        if (lane == 0) {
+            slot_e[warp][slot][0] = e0;
+            slot_e[warp][slot][1] = e1;
+            std::uint8_t* dst = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
+            std::uint32_t nb = 0, a0 = 0;
+            if (e1 > e0) {
+                a0 = (e0 * 4u) & ~15u;
+                nb = min(((e1 * 4u + 15u) & ~15u) - a0, p.ent_cap_bytes);
+            }
+            fence_proxy_async();
+            mbar_expect_tx(&bars[warp][slot], CELL + nb);
+            bulk_g2s(dst, p.cells + static_cast<std::size_t>(q) * CELL, CELL, &bars[warp][slot]);
+            if (nb) bulk_g2s(dst + CELL, reinterpret_cast<const std::uint8_t*>(p.ent) + a0, nb, &bars[warp][slot]);
+        }
+    };
+
+    const std::uint32_t ncell = q1 - q0;
+#pragma unroll 1
+    for (int s = 0; s < NSLOT; ++s)
+        if (static_cast<std::uint32_t>(s) < ncell) issue(q0 + s, s);
+
+    // weights stream before the x preparation of the previous kernel finishes
+    pdl_wait();
+
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // [unit][rho]
+    std::uint32_t curG = q0 / p.Pn;
+    const std::uint32_t Gq0 = curG;
+
+    auto flush = [&](std::uint32_t Gf, bool whole) {
+        float v[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                float a = acc[u][r];
+                a += __shfl_xor_sync(0xffffffffu, a, 1);
+                a += __shfl_xor_sync(0xffffffffu, a, 2);
+                v[u][r] = a;
+            }
+        __syncwarp();
+        // lane L ends up owning local row L = 16u + 8rho + g (collect from lane 4g)
+        const int R = lane, u = R >> 4, rho = (R >> 3) & 1, gg = R & 7;
+        float mine = 0.f;
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu)
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const float o = __shfl_sync(0xffffffffu, v[uu][rr], gg * 4);
+                if (uu == u && rr == rho) mine = o;
+            }
+        mine += oacc[warp][R];
+        oacc[warp][R] = 0.f;
+        const std::uint32_t row = 32u * Gf + R;
+        if (whole) {
+            if (row < p.m) p.y[row] = mine;
+        } else {
+            const std::uint32_t side = (Gf == Gq0) ? 0u : 1u;
+            p.partial[(wk * 2 + side) * 32 + R] = mine;
+            __threadfence();
+            __syncwarp();
+            std::uint32_t prev = 0;
+            const std::uint32_t expect = p.wlast[Gf] - p.wfirst[Gf] + 1;
+            if (lane == 0) prev = atomicAdd(p.counters + Gf, 1u);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == expect - 1) {  // last contributor reduces in warp order
+                __threadfence();
+                float sum = 0.f;
+                for (std::uint32_t k = p.wfirst[Gf]; k <= p.wlast[Gf]; ++k) {
+                    const std::uint32_t sk = (p.warp_start[k] / p.Pn == Gf) ? 0u : 1u;
+                    sum += __ldcg(p.partial + (k * 2 + sk) * 32 + R);
+                }
+                if (row < p.m) p.y[row] = sum;
+                if (lane == 0) p.counters[Gf] = 0;
+            }
+        }
+        acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.f;
+    };
+
+#pragma unroll 1
+    for (std::uint32_t it = 0; it < ncell; ++it) {
+        const std::uint32_t q = q0 + it;
+        const int slot = static_cast<int>(it % NSLOT);
+        const std::uint32_t phase = (it / NSLOT) & 1u;
+        const std::uint32_t Gc = q / p.Pn, P = q - Gc * p.Pn;
+        if (Gc != curG) {
+            flush(curG, curG * p.Pn >= q0);
+            curG = Gc;
+        }
+        // x operands of this panel (L1/L2 resident, shared by both units)
+        uint2 xf[2], xl[2];
+        float4 xs[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            xf[h] = __ldg(p.xfrag + (16u * P + 8u * h + g) * 4u + t);
+            if constexpr (XLO) xl[h] = __ldg(p.xlo + (16u * P + 8u * h + g) * 4u + t);
+            xs[h] = __ldg(p.xsc + 8u * P + 4u * h + t);
+        }
+        mbar_wait(&bars[warp][slot], phase);
+        const std::uint32_t e0 = slot_e[warp][slot][0], e1 = slot_e[warp][slot][1];
+        const std::uint8_t* cell = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
+
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const std::uint8_t* unit = cell + u * UNIT;
+            std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+            for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                const uint4 v = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                cw[4 * i] = v.x; cw[4 * i + 1] = v.y; cw[4 * i + 2] = v.z; cw[4 * i + 3] = v.w;
+            }
+            std::uint64_t sbits[2];
+            load_stat_bits<SB>(unit + CODEB + lane * SB, sbits);
+            uint4 sc[2];
+            sc[0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
+            sc[1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
+
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
+                    const std::uint32_t* w = cw + G::CW * cidx;
+                    std::uint32_t a[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                        const int i = rho * (G::NP / 2) + qq;
+                        const int B = (BW * i) >> 3, pp = (BW * i) & 7;
+                        a[r] = window<G::CW>(w, B) & ((MASK << pp) * 0x00010001u);
+                    }
+                    const bool mine = (g == j);
+                    mma16816(c, a, mine ? xf[h].x : 0u, mine ? xf[h].y : 0u);
+                    if constexpr (XLO) mma16816(c, a, mine ? xl[h].x : 0u, mine ? xl[h].y : 0u);
+                }
+                // epilogue: lane holds D(row g+8rho, block 8h+2t+bs) in c[2rho+bs]
+                const uint4 s4 = sc[h];
+                const float sc_b[2] = {xs[h].x, xs[h].z}, xx_b[2] = {xs[h].y, xs[h].w};
+#pragma unroll
+                for (int bs = 0; bs < 2; ++bs) {
+                    const std::uint32_t w01 = bs ? s4.z : s4.x;  // scale_s | scale_z
+                    const std::uint32_t w23 = bs ? s4.w : s4.y;  // zero_s  | zero_z
+                    const float Ss = h2f_bits(w01 & 0xffffu), Zs = h2f_bits(w01 >> 16);
+                    const float Sz = h2f_bits(w23 & 0xffffu), Zz = h2f_bits(w23 >> 16);
+                    const float A1 = Ss * sc_b[bs], A0 = -A1 * Zs;
+                    const float B0 = -Sz * Zz;
+#pragma unroll
+                    for (int rho = 0; rho < 2; ++rho) {
+                        const int eps = 4 * h + 2 * bs + rho;
+                        const float cs = u2f_small(field<BS>(sbits, eps * BS));
+                        const float cz = u2f_small(field<BZ>(sbits, 8 * BS + eps * BZ));
+                        const float shat = fmaf(A1, cs, A0);
+                        const float zhat = fmaf(Sz, cz, B0);
+                        const float tt = fmaf(zhat, xx_b[bs], c[2 * rho + bs]);
+                        acc[u][rho] = fmaf(shat, tt, acc[u][rho]);
+                    }
+                }
+            }
+        }
+
+        // outliers of this cell: segmented scan by local row, one add per row run
+        const std::uint32_t cnt = e1 - e0;
+        if (cnt) {
+            const std::uint32_t a0 = (e0 * 4u) & ~15u;
+            const std::uint32_t have = min(((e1 * 4u + 15u) & ~15u) - a0, p.ent_cap_bytes);
+            const std::uint8_t* es = cell + CELL + (e0 * 4u - a0);
+            const std::uint32_t in_smem = (have - (e0 * 4u - a0)) / 4u;
+            const float* xpanel = p.xp + 256u * P;
+#pragma unroll 1
+            for (std::uint32_t base = 0; base < cnt; base += 32) {
+                const std::uint32_t i = base + lane;
+                const bool valid = i < cnt;
+                std::uint32_t e = 0;
+                if (valid) e = (i < in_smem) ? reinterpret_cast<const std::uint32_t*>(es)[i] : __ldg(p.ent + e0 + i);
+                int r = valid ? static_cast<int>(e >> 24) : 64 + lane;
+                float v = valid ? h2f_bits(e & 0xffffu) * __ldg(xpanel + ((e >> 16) & 255u)) : 0.f;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const float vv = __shfl_up_sync(0xffffffffu, v, d);
+                    const int rr = __shfl_up_sync(0xffffffffu, r, d);
+                    if (lane >= d && rr == r) v += vv;
+                }
+                const int rn = __shfl_down_sync(0xffffffffu, r, 1);
+                if (valid && (lane == 31 || rn != r)) oacc[warp][r] += v;
+                __syncwarp();
+            }
+        }
+
+        __syncwarp();
+        if (it + NSLOT < ncell) issue(q + NSLOT, slot);
+    }
+    flush(curG, curG * p.Pn >= q0 && (curG + 1) * p.Pn <= q1);
+}
+
+// x preparation for the tiled path: one thread per (16-column block, batch).
+template <int BW, bool XLO>
+__global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t n_pad,
+                            std::uint32_t batch, const std::uint32_t* __restrict__ order, uint2* xfrag,
+                            uint2* xlo, float2* xsc, float* xp) {
+    const std::uint32_t nblk = n_pad / 16;
+    const std::uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < nblk * batch) {
+        const std::uint32_t b = idx / nblk, k = idx - b * nblk;
+        float v[16];
+        float mx = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+            const std::uint32_t col = 16 * k + cc;
+            float val = 0.f;
+            if (col < n) {
+                const std::uint32_t src = order ? __ldg(order + col) : col;
+                val = x_f16 ? __half2float(reinterpret_cast<const __half*>(x)[static_cast<std::size_t>(b) * n + src])
+                            : reinterpret_cast<const float*>(x)[static_cast<std::size_t>(b) * n + src];
+            }
+            v[cc] = val;
+            mx = fmaxf(mx, fabsf(val));
+            xp[static_cast<std::size_t>(b) * n_pad + col] = val;
+        }
+        int e = 0;
+        if (mx > 0.f && mx < INFINITY) {
+            int E;
+            frexpf(mx, &E);  // mx = f * 2^E, f in [0.5, 1)
+            e = 15 - E;      // mx * 2^e in [2^14, 2^15)
+        }
+        __half hi[16], lo[16];
+        float X = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+            const int pp = T::column_prescale(BW, k, cc);
+            const float s = ldexpf(v[cc], e - pp);
+            hi[cc] = __float2half_rn(s);
+            float eff = __half2float(hi[cc]);
+            if constexpr (XLO) {
+                lo[cc] = __float2half_rn(s - eff);
+                eff += __half2float(lo[cc]);
+            }
+            X += ldexpf(eff, pp);
+        }
+        // fragment order per t: columns 2t, 2t+1, 2t+8, 2t+9
+        uint2* fr = xfrag + (static_cast<std::size_t>(b) * nblk + k) * 4;
+        uint2* fl = XLO ? xlo + (static_cast<std::size_t>(b) * nblk + k) * 4 : nullptr;
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+            const int c0 = 2 * tt;
+            uint2 f;
+            f.x = static_cast<std::uint32_t>(__half_as_ushort(hi[c0])) |
+                  (static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 1])) << 16);
+            f.y = static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 8])) |
+                  (static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 9])) << 16);
+            fr[tt] = f;
+            if constexpr (XLO) {
+                uint2 l;
+                l.x = static_cast<std::uint32_t>(__half_as_ushort(lo[c0])) |
+                      (static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 1])) << 16);
+                l.y = static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 8])) |
+                      (static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 9])) << 16);
+                fl[tt] = l;
+            }
+        }
+        xsc[static_cast<std::size_t>(b) * nblk + k] = make_float2(ldexpf(1.0f, 24 - e), -X * 5.9604644775390625e-08f);
+    }
+    pdl_launch();
+}
+
+// ============================================================== raw path ====
+// Geometry of a raw .spqr stream resident in device memory (any config).
+struct RawGeom {
+    const std::uint8_t* s;         // whole stream
+    const std::uint32_t* order;    // solve k -> source column (nullptr = identity)
+    std::uint32_t rows, cols, b1, b2, nblocks, ngroups;
+    int wb, sb, zb;
+    std::uint64_t rec_off, col_block_bytes, csr_off, ent_off;
+
+    __device__ __forceinline__ std::uint32_t block_width(std::uint32_t k) const {
+        return k + 1 < nblocks ? b1 : cols - k * b1;
+    }
+    __device__ __forceinline__ std::uint32_t group_rows(std::uint32_t g) const {
+        return g + 1 < ngroups ? b2 : rows - g * b2;
+    }
+    __device__ __forceinline__ static std::uint64_t packed(std::uint64_t count, int bits) {
+        return (count * bits + 7) / 8;
+    }
+    __device__ __forceinline__ std::uint64_t side_bytes(std::uint32_t gr, int bits) const {
+        return bits <= 8 ? 4 + packed(gr, bits) : 4ull * gr;
+    }
+    __device__ __forceinline__ std::uint64_t record_bytes(std::uint32_t gr, std::uint32_t bw) const {
+        return side_bytes(gr, sb) + side_bytes(gr, zb) + packed(static_cast<std::uint64_t>(gr) * bw, wb);
+    }
+    __device__ __forceinline__ std::uint64_t record_offset(std::uint32_t k, std::uint32_t g) const {
+        return rec_off + k * col_block_bytes + g * record_bytes(b2, block_width(k));
+    }
+    __device__ __forceinline__ std::uint32_t u16(std::uint64_t off) const {
+        return static_cast<std::uint32_t>(s[off]) | (static_cast<std::uint32_t>(s[off + 1]) << 8);
+    }
+    __device__ __forceinline__ std::uint32_t u32(std::uint64_t off) const {
+        return u16(off) | (u16(off + 2) << 16);
+    }
+    // element i of a packed field of `bits` (<= 8) starting at byte `off`
+    __device__ __forceinline__ std::uint32_t bits_at(std::uint64_t off, std::uint64_t i, int bits) const {
+        const std::uint64_t pos = i * bits;
+        const std::uint32_t two = u16(off + (pos >> 3));  // the stream always has bytes after a field
+        return (two >> (pos & 7)) & ((1u << bits) - 1u);
+    }
+    // first-level statistics of (block k, row r), bit-exact stat_dequant
+    __device__ __forceinline__ void stats(std::uint32_t k, std::uint32_t r, float& sv, float& zv,
+                                          std::uint64_t& wfield, std::uint32_t& rr, std::uint32_t& bw) const {
+        const std::uint32_t g = r / b2;
+        const std::uint32_t gr = group_rows(g);
+        rr = r - g * b2;
+        bw = block_width(k);
+        std::uint64_t o = record_offset(k, g);
+        const std::uint64_t sfield = o + (sb <= 8 ? 4 : 0) + (zb <= 8 ? 4 : 0);
+        const std::uint64_t zfield = sfield + side_bytes(gr, sb) - (sb <= 8 ? 4 : 0);
+        wfield = zfield + side_bytes(gr, zb) - (zb <= 8 ? 4 : 0);
+        if (sb == 16) {
+            sv = __uint_as_float(u32(sfield + 4ull * rr));
+        } else {
+            const float S = h2f_bits(u16(o)), Z = h2f_bits(u16(o + 2));
+            sv = __fmul_rn(S, __fsub_rn(static_cast<float>(bits_at(sfield, rr, sb)), Z));
+        }
+        if (zb == 16) {
+            zv = __uint_as_float(u32(zfield + 4ull * rr));
+        } else {
+            const std::uint64_t zh = o + (sb <= 8 ? 4 : 0);
+            const float S = h2f_bits(u16(zh)), Z = h2f_bits(u16(zh + 2));
+            zv = __fmul_rn(S, __fsub_rn(static_cast<float>(bits_at(zfield, rr, zb)), Z));
+        }
+    }
+};
+
+// W[r, order[c]] = s * (q - z), binary32 (dequant_value, quantizer.hpp:60-62)
+__global__ void dequant_raw(const RawGeom geo, float* __restrict__ w) {
+    const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
+    for (std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        // consecutive threads take consecutive blocks of the same row
+        const std::uint32_t r = static_cast<std::uint32_t>(idx / geo.nblocks);
+        const std::uint32_t k = static_cast<std::uint32_t>(idx - static_cast<std::uint64_t>(r) * geo.nblocks);
+        float sv, zv;
+        std::uint64_t wf;
+        std::uint32_t rr, bw;
+        geo.stats(k, r, sv, zv, wf, rr, bw);
+        for (std::uint32_t c = 0; c < bw; ++c) {
+            const std::uint32_t q = geo.bits_at(wf, static_cast<std::uint64_t>(rr) * bw + c, geo.wb);
+            const std::uint32_t col = k * geo.b1 + c;
+            const std::uint32_t dst = geo.order ? __ldg(geo.order + col) : col;
+            w[static_cast<std::uint64_t>(r) * geo.cols + dst] = __fmul_rn(sv, __fsub_rn(static_cast<float>(q), zv));
+        }
+    }
+}
+
+// outlier corrections: a separate binary32 add (solver.hpp:360)
+__global__ void outliers_raw(const RawGeom geo, float* __restrict__ w) {
+    const std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= geo.rows) return;
+    const std::uint32_t i0 = geo.u32(geo.csr_off + 4ull * r), i1 = geo.u32(geo.csr_off + 4ull * r + 4);
+    for (std::uint32_t i = i0; i < i1; ++i) {
+        const std::uint32_t col = geo.u16(geo.ent_off + 4ull * i);
+        const float v = h2f_bits(geo.u16(geo.ent_off + 4ull * i + 2));
+        const std::uint32_t dst = geo.order ? __ldg(geo.order + col) : col;
+        float* pw = w + static_cast<std::uint64_t>(r) * geo.cols + dst;
+        *pw = __fadd_rn(*pw, v);
+    }
+}
+
+// xp[b][k] = x[b][order[k]] in fp32 (kernel.hpp:93-98)
+__global__ void xprep_raw(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t batch,
+                          const std::uint32_t* __restrict__ order, float* __restrict__ xp) {
+    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<std::uint64_t>(n) * batch) return;
+    const std::uint32_t b = static_cast<std::uint32_t>(idx / n), k = static_cast<std::uint32_t>(idx % n);
+    const std::uint32_t src = order ? __ldg(order + k) : k;
+    const std::uint64_t si = static_cast<std::uint64_t>(b) * n + src;
+    xp[idx] = x_f16 ? __half2float(reinterpret_cast<const __half*>(x)[si]) : reinterpret_cast<const float*>(x)[si];
+}
+
+// generic matvec: one warp per row, lanes over column blocks, fp32 accumulate
+__global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp, float* __restrict__ y) {
+    const std::uint32_t warps = blockDim.x >> 5;
+    const std::uint32_t r = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= geo.rows) return;
+    float acc = 0.f;
+    for (std::uint32_t k = lane; k < geo.nblocks; k += 32) {
+        float sv, zv;
+        std::uint64_t wf;
+        std::uint32_t rr, bw;
+        geo.stats(k, r, sv, zv, wf, rr, bw);
+        float part = 0.f;
+        for (std::uint32_t c = 0; c < bw; ++c) {
+            const std::uint32_t q = geo.bits_at(wf, static_cast<std::uint64_t>(rr) * bw + c, geo.wb);
+            part = fmaf(__fsub_rn(static_cast<float>(q), zv), xp[k * geo.b1 + c], part);
+        }
+        acc = fmaf(sv, part, acc);
+    }
+    const std::uint32_t i0 = geo.u32(geo.csr_off + 4ull * r), i1 = geo.u32(geo.csr_off + 4ull * r + 4);
+    for (std::uint32_t i = i0 + lane; i < i1; i += 32)
+        acc = fmaf(h2f_bits(geo.u16(geo.ent_off + 4ull * i + 2)), xp[geo.u16(geo.ent_off + 4ull * i)], acc);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) y[r] = acc;
+}
+
+// ========================================================= dense baseline ==
+// y = W16 * x16, fp32 accumulate; one warp per row, 128-bit loads.
+__global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __restrict__ x, float* __restrict__ y,
+                               std::uint32_t rows, std::uint32_t cols) {
+    const std::uint32_t warps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
+    for (std::uint32_t r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+        const uint4* wr = reinterpret_cast<const uint4*>(w + static_cast<std::uint64_t>(r) * cols);
+        const uint4* xr = reinterpret_cast<const uint4*>(x);
+        float acc = 0.f;
+        const std::uint32_t n8 = cols / 8;
+#pragma unroll 4
+        for (std::uint32_t i = lane; i < n8; i += 32) {
+            const uint4 a = __ldcs(wr + i);
+            const uint4 b = __ldg(xr + i);
+            const __half2* ah = reinterpret_cast<const __half2*>(&a);
+            const __half2* bh = reinterpret_cast<const __half2*>(&b);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 fa = __half22float2(ah[j]), fb = __half22float2(bh[j]);
+                acc = fmaf(fa.x, fb.x, acc);
+                acc = fmaf(fa.y, fb.y, acc);
+            }
+        }
+        for (std::uint32_t c = n8 * 8 + lane; c < cols; c += 32)
+            acc = fmaf(__half2float(w[static_cast<std::uint64_t>(r) * cols + c]), __half2float(x[c]), acc);
+#pragma unroll
+        for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        if (lane == 0) y[r] = acc;
+    }
+}
+
+}  // namespace spqr_dev

@@ -1,0 +1,96 @@
+// tiled.hpp -- geometry of the HBM "tiled planes" layout of a fast-path layer.
+// Shared by the host transcoder (transcode.cpp) and the CUDA kernels.
+//
+// Fast path: beta1 = beta2 = 16, weight_bits in {2,3,4}, scale/zero bits in
+// [1,8].  The layer is cut into CELLS of 32 rows x 256 columns (a row-group
+// pair x a 16-block panel); cell (G, P) is stored contiguously at
+// (G * Pn + P) * cell_bytes, cells in row-major order, so a warp streaming a
+// contiguous cell range streams contiguous bytes.  A cell is two UNITS (one
+// per 16-row group), each unit =
+//
+//   [codes  : 32 lanes x 16*BW bytes ]  lane L's A-fragment codes for the 16
+//                                       m16n8k16 MMAs of the unit (2 super-
+//                                       tiles x 8 blocks), in "containers"
+//   [stats  : 32 lanes x (BS+BZ) bytes] lane L's 8 scale codes then 8 zero
+//                                       codes, LSB-first
+//   [scalars: 16 blocks x 8 bytes     ]  binary16 {scale_s, scale_z, zero_s, zero_z}
+//
+// unit_bytes = 512*BW + 32*(BS+BZ) + 128 = 16 group records of the stream
+// (1856 B = 16 x 116 B at 3/3/3): the layout adds no bytes.  Rows / columns
+// beyond the layer are zero padding (m -> multiple of 32, n -> of 256).
+//
+// Lane L = 4g + t holds, for MMA mu = 8h + j (block 16P + 8h + j):
+//   A register r = 2*kh + rho : rows g + 8*rho, columns 2t + 8*kh + {0,1}
+// (the m16n8k16 row-major A fragment).  A "container" of CW 32-bit words
+// carries NPAIR (lo, hi) code pairs: lo codes form a 16*CW-bit stream in the
+// low halves of the words, hi codes in the high halves; pair i sits at bit
+// BW*i of both streams.  Pair i of container c is
+//   rho = i / (NPAIR/2),  q = i % (NPAIR/2),  m = q / 2,  kh = q % 2,
+//   mu = MPC*c + m.
+// The kernel turns a pair into an f16x2 A register with ONE LOP3 mask: the
+// codes land at bit offset p(q) of a window of the stream, i.e. as binary16
+// subnormals worth code * 2^(p-24); the x operand is pre-scaled by 2^-p per
+// column (xprep), so the product is exact and p cancels.
+//
+// Stats entry eps = 4h + 2*bs + rho  (block 16P + 8h + 2t + bs, row g + 8*rho):
+//   scale code at bit eps*BS, zero code at bit 8*BS + eps*BZ of the lane's
+//   (BS+BZ)-byte little-endian field.
+//
+// Outliers are re-bucketed per cell: offsets u32[cells+1] and entries u32
+//   value16 | (col & 255) << 16 | (row - 32G) << 24
+// sorted by (cell, row, col) -- 4 bytes per outlier like the stream.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define SPQR_HD __host__ __device__ __forceinline__
+#else
+#define SPQR_HD inline
+#endif
+
+namespace spqr_tiled {
+
+inline constexpr std::uint32_t kCellRows = 32;
+inline constexpr std::uint32_t kCellCols = 256;
+inline constexpr std::uint32_t kUnitRows = 16;
+inline constexpr std::uint32_t kScalarBytes = 128;
+
+// The layout itself is defined for any bs, bz in [1, 8]; the kernel is
+// instantiated for the statistic widths below (others use the raw-stream
+// kernels, which are generic).
+SPQR_HD constexpr bool supported(int bw, int bs, int bz, std::uint32_t b1, std::uint32_t b2) {
+    return b1 == 16 && b2 == 16 && (bw == 2 || bw == 3 || bw == 4) && bs == bz && bs >= 2 && bs <= 4;
+}
+SPQR_HD constexpr int words_per_container(int bw) { return bw == 3 ? 3 : 1; }
+SPQR_HD constexpr int mmas_per_container(int bw) { return bw == 3 ? 4 : (bw == 4 ? 1 : 2); }
+SPQR_HD constexpr int pairs_per_container(int bw) { return 16 * words_per_container(bw) / bw; }
+SPQR_HD constexpr int containers_per_unit(int bw) { return 16 / mmas_per_container(bw); }
+SPQR_HD constexpr std::uint32_t code_bytes(int bw) { return 512u * bw; }
+SPQR_HD constexpr std::uint32_t stat_bytes(int bs, int bz) { return 32u * (bs + bz); }
+SPQR_HD constexpr std::uint32_t unit_bytes(int bw, int bs, int bz) {
+    return code_bytes(bw) + stat_bytes(bs, bz) + kScalarBytes;
+}
+SPQR_HD constexpr std::uint32_t cell_bytes(int bw, int bs, int bz) { return 2u * unit_bytes(bw, bs, bz); }
+
+// Pair i of a container starts at stream bit BW*i; the kernel reads it through
+// the 16-bit window starting at byte floor(BW*i/8), where it sits at bit
+// p = (BW*i) mod 8 (p + BW - 1 <= 9 keeps it inside the binary16 mantissa).
+// p depends only on the pair class q = i % (NPAIR/2) = 2m + kh, so both rows of
+// an MMA column pair share it: it is the per-column x pre-scale exponent.
+SPQR_HD constexpr int prescale_p(int bw, int q) { return (bw * q) & 7; }
+
+// Column (block k, column cc in block) -> pre-scale exponent.
+SPQR_HD constexpr int column_prescale(int bw, std::uint32_t k, std::uint32_t cc) {
+    const int m = static_cast<int>(k % 8) % mmas_per_container(bw);
+    const int kh = static_cast<int>(cc / 8);
+    return prescale_p(bw, 2 * m + kh);
+}
+
+// Entry packing of the per-cell outlier lists.
+SPQR_HD constexpr std::uint32_t pack_entry(std::uint32_t local_row, std::uint32_t col_in_cell,
+                                           std::uint16_t v) {
+    return static_cast<std::uint32_t>(v) | ((col_in_cell & 255u) << 16) | (local_row << 24);
+}
+
+}  // namespace spqr_tiled

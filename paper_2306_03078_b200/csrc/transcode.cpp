@@ -1,0 +1,285 @@
+// transcode.cpp -- stream <-> tiled HBM layout (see tiled.hpp for the layout).
+//
+// The stream stores group records column-block-major (format.hpp:300-333):
+// record (k, g) for all row groups of block k, then block k+1.  The GPU wants
+// a 32-row strip to stream contiguously with every lane's MMA fragment in one
+// 16-byte-aligned slice, so the loader re-lays the records once at load time.
+// The transform is lossless (tiled_to_stream is its inverse; tests check the
+// round trip byte-for-byte) and adds no bytes beyond zero padding of ragged
+// edges.  Parallel over row-group pairs with std::thread.
+#include <algorithm>
+#include <thread>
+
+#include "internal.hpp"
+#include "tiled.hpp"
+
+namespace spqr::detail {
+
+namespace T = spqr_tiled;
+
+bool tiled_supported(const StreamView& v) { return T::supported(v.wb, v.sb, v.zb, v.b1, v.b2); }
+
+namespace {
+
+// Dense staging of one unit (16 rows x 256 columns = 16 blocks).
+struct UnitStage {
+    std::uint8_t codes[16][256];
+    std::uint8_t scode[16][16];  // [block][row]
+    std::uint8_t zcode[16][16];
+    std::uint16_t scal[16][4];
+};
+
+template <class F>
+void parallel_for(std::uint32_t n, int threads, F&& f) {
+    if (threads <= 0) threads = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    threads = static_cast<int>(std::min<std::uint32_t>(threads, std::max(1u, n)));
+    if (threads <= 1) {
+        for (std::uint32_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int w = 0; w < threads; ++w)
+        th.emplace_back([&, w] {
+            for (std::uint32_t i = w; i < n; i += threads) f(i);
+        });
+    for (auto& t : th) t.join();
+}
+
+// Stream record (k, g) -> stage block `blk`, rows [0, gr).
+void load_record(const StreamView& v, std::uint32_t k, std::uint32_t g, int blk, UnitStage& u) {
+    const std::uint32_t gr = v.group_rows(g), bw = v.block_width(k);
+    const std::uint8_t* p = v.base + v.record_offset(k, g);
+    for (int i = 0; i < 4; ++i) u.scal[blk][i] = StreamView::load_u16(p + 2 * i);
+    p += 8;
+    unpack_bits(p, u.scode[blk], gr, v.sb);
+    p += packed_field_bytes(gr, v.sb);
+    unpack_bits(p, u.zcode[blk], gr, v.zb);
+    p += packed_field_bytes(gr, v.zb);
+    std::uint8_t w[256];
+    unpack_bits(p, w, static_cast<std::size_t>(gr) * bw, v.wb);
+    for (std::uint32_t r = 0; r < gr; ++r)
+        std::memcpy(&u.codes[r][16 * blk], w + r * bw, bw);
+}
+
+template <int BW>
+void pack_unit_codes(const UnitStage& u, std::uint8_t* dst) {
+    constexpr int CW = T::words_per_container(BW), MPC = T::mmas_per_container(BW);
+    constexpr int NP = T::pairs_per_container(BW), CPU = T::containers_per_unit(BW);
+    for (int L = 0; L < 32; ++L) {
+        const int g = L >> 2, t = L & 3;
+        std::uint8_t* lane = dst + L * 16 * BW;
+        for (int c = 0; c < CPU; ++c) {
+            std::uint64_t lo = 0, hi = 0;
+            for (int i = 0; i < NP; ++i) {
+                const int rho = i / (NP / 2), q = i % (NP / 2), m = q / 2, kh = q % 2;
+                const int mu = MPC * c + m, blk = mu;  // mu = 8h + j = block within unit
+                const int row = g + 8 * rho, col = 16 * blk + 2 * t + 8 * kh;
+                lo |= static_cast<std::uint64_t>(u.codes[row][col]) << (BW * i);
+                hi |= static_cast<std::uint64_t>(u.codes[row][col + 1]) << (BW * i);
+            }
+            for (int w = 0; w < CW; ++w) {
+                const std::uint32_t word = static_cast<std::uint32_t>((lo >> (16 * w)) & 0xffffu) |
+                                           (static_cast<std::uint32_t>((hi >> (16 * w)) & 0xffffu) << 16);
+                std::memcpy(lane + 4 * (CW * c + w), &word, 4);
+            }
+        }
+    }
+}
+
+template <int BW>
+void unpack_unit_codes(const std::uint8_t* src, UnitStage& u) {
+    constexpr int CW = T::words_per_container(BW), MPC = T::mmas_per_container(BW);
+    constexpr int NP = T::pairs_per_container(BW), CPU = T::containers_per_unit(BW);
+    constexpr std::uint64_t mask = (1u << BW) - 1u;
+    for (int L = 0; L < 32; ++L) {
+        const int g = L >> 2, t = L & 3;
+        const std::uint8_t* lane = src + L * 16 * BW;
+        for (int c = 0; c < CPU; ++c) {
+            std::uint64_t lo = 0, hi = 0;
+            for (int w = 0; w < CW; ++w) {
+                std::uint32_t word;
+                std::memcpy(&word, lane + 4 * (CW * c + w), 4);
+                lo |= static_cast<std::uint64_t>(word & 0xffffu) << (16 * w);
+                hi |= static_cast<std::uint64_t>(word >> 16) << (16 * w);
+            }
+            for (int i = 0; i < NP; ++i) {
+                const int rho = i / (NP / 2), q = i % (NP / 2), m = q / 2, kh = q % 2;
+                const int blk = MPC * c + m;
+                const int row = g + 8 * rho, col = 16 * blk + 2 * t + 8 * kh;
+                u.codes[row][col] = static_cast<std::uint8_t>((lo >> (BW * i)) & mask);
+                u.codes[row][col + 1] = static_cast<std::uint8_t>((hi >> (BW * i)) & mask);
+            }
+        }
+    }
+}
+
+void pack_unit_stats(const UnitStage& u, int bs, int bz, std::uint8_t* dst) {
+    const int sbytes = bs + bz;
+    for (int L = 0; L < 32; ++L) {
+        const int g = L >> 2, t = L & 3;
+        std::uint64_t bits[2] = {0, 0};
+        auto put = [&](int pos, int nb, std::uint32_t v) {
+            for (int b = 0; b < nb; ++b, ++pos)
+                if ((v >> b) & 1u) bits[pos >> 6] |= std::uint64_t{1} << (pos & 63);
+        };
+        for (int eps = 0; eps < 8; ++eps) {
+            const int h = eps >> 2, s = (eps >> 1) & 1, rho = eps & 1;
+            const int blk = 8 * h + 2 * t + s, row = g + 8 * rho;
+            put(eps * bs, bs, u.scode[blk][row]);
+            put(8 * bs + eps * bz, bz, u.zcode[blk][row]);
+        }
+        for (int b = 0; b < sbytes; ++b)
+            dst[L * sbytes + b] = static_cast<std::uint8_t>(bits[b >> 3] >> (8 * (b & 7)));
+    }
+}
+
+void unpack_unit_stats(const std::uint8_t* src, int bs, int bz, UnitStage& u) {
+    const int sbytes = bs + bz;
+    for (int L = 0; L < 32; ++L) {
+        const int g = L >> 2, t = L & 3;
+        std::uint64_t bits[2] = {0, 0};
+        for (int b = 0; b < sbytes; ++b)
+            bits[b >> 3] |= static_cast<std::uint64_t>(src[L * sbytes + b]) << (8 * (b & 7));
+        auto get = [&](int pos, int nb) {
+            std::uint32_t v = 0;
+            for (int b = 0; b < nb; ++b, ++pos) v |= static_cast<std::uint32_t>((bits[pos >> 6] >> (pos & 63)) & 1u) << b;
+            return static_cast<std::uint8_t>(v);
+        };
+        for (int eps = 0; eps < 8; ++eps) {
+            const int h = eps >> 2, s = (eps >> 1) & 1, rho = eps & 1;
+            const int blk = 8 * h + 2 * t + s, row = g + 8 * rho;
+            u.scode[blk][row] = get(eps * bs, bs);
+            u.zcode[blk][row] = get(8 * bs + eps * bz, bz);
+        }
+    }
+}
+
+void pack_unit(const UnitStage& u, int bw, int bs, int bz, std::uint8_t* dst) {
+    switch (bw) {
+        case 2: pack_unit_codes<2>(u, dst); break;
+        case 3: pack_unit_codes<3>(u, dst); break;
+        default: pack_unit_codes<4>(u, dst); break;
+    }
+    pack_unit_stats(u, bs, bz, dst + T::code_bytes(bw));
+    std::memcpy(dst + T::code_bytes(bw) + T::stat_bytes(bs, bz), u.scal, T::kScalarBytes);
+}
+
+void unpack_unit(const std::uint8_t* src, int bw, int bs, int bz, UnitStage& u) {
+    switch (bw) {
+        case 2: unpack_unit_codes<2>(src, u); break;
+        case 3: unpack_unit_codes<3>(src, u); break;
+        default: unpack_unit_codes<4>(src, u); break;
+    }
+    unpack_unit_stats(src + T::code_bytes(bw), bs, bz, u);
+    std::memcpy(u.scal, src + T::code_bytes(bw) + T::stat_bytes(bs, bz), T::kScalarBytes);
+}
+
+}  // namespace
+
+TiledHost transcode_to_tiled(const StreamView& v, int threads) {
+    if (!tiled_supported(v)) fail(Errc::config_invalid, "layer outside the tiled geometry");
+    TiledHost t;
+    t.Gn = (v.rows + 31) / 32;
+    t.Pn = (v.cols + 255) / 256;
+    t.cell_bytes = T::cell_bytes(v.wb, v.sb, v.zb);
+    t.prefix.assign(v.base, v.base + v.rec_off);
+    const std::size_t ncell = static_cast<std::size_t>(t.Gn) * t.Pn;
+    t.cells.assign(ncell * t.cell_bytes, 0);
+    const std::uint32_t ub = T::unit_bytes(v.wb, v.sb, v.zb);
+
+    parallel_for(t.Gn, threads, [&](std::uint32_t G) {
+        UnitStage u;
+        for (std::uint32_t P = 0; P < t.Pn; ++P) {
+            for (int rg = 0; rg < 2; ++rg) {
+                std::memset(&u, 0, sizeof(u));
+                const std::uint32_t gg = 2 * G + rg;
+                if (gg < v.ngroups)
+                    for (int blk = 0; blk < 16; ++blk) {
+                        const std::uint32_t k = 16 * P + blk;
+                        if (k < v.nblocks) load_record(v, k, gg, blk, u);
+                    }
+                pack_unit(u, v.wb, v.sb, v.zb,
+                          t.cells.data() + (static_cast<std::size_t>(G) * t.Pn + P) * t.cell_bytes + rg * ub);
+            }
+        }
+    });
+
+    // outliers, re-bucketed per cell in (cell, row, col) order
+    t.cell_off.assign(ncell + 1, 0);
+    for (std::uint32_t r = 0; r < v.rows; ++r)
+        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i)
+            t.cell_off[static_cast<std::size_t>(r / 32) * t.Pn + v.ent_col(i) / 256 + 1]++;
+    for (std::size_t q = 0; q < ncell; ++q) t.cell_off[q + 1] += t.cell_off[q];
+    t.entries.assign(v.nnz, 0);
+    std::vector<std::uint32_t> cursor(t.cell_off.begin(), t.cell_off.end() - 1);
+    for (std::uint32_t r = 0; r < v.rows; ++r)  // rows ascending, cols ascending -> order kept
+        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i) {
+            const std::uint32_t c = v.ent_col(i);
+            const std::size_t q = static_cast<std::size_t>(r / 32) * t.Pn + c / 256;
+            t.entries[cursor[q]++] = T::pack_entry(r % 32, c % 256, v.ent_val(i));
+        }
+    return t;
+}
+
+std::vector<std::uint8_t> tiled_to_stream(const StreamView& hdr, const TiledHost& t, int threads) {
+    // geometry from the header prefix (the layer keeps header + permutation)
+    const StreamView& v = hdr;
+    const std::uint32_t ub = T::unit_bytes(v.wb, v.sb, v.zb);
+    std::vector<std::uint8_t> out(t.prefix);
+    out.resize(v.csr_off, 0);
+    std::uint8_t* recs = out.data();
+    parallel_for(t.Gn, threads, [&](std::uint32_t G) {
+        UnitStage u;
+        std::vector<std::uint8_t> buf;
+        for (std::uint32_t P = 0; P < t.Pn; ++P)
+            for (int rg = 0; rg < 2; ++rg) {
+                const std::uint32_t gg = 2 * G + rg;
+                if (gg >= v.ngroups) continue;
+                unpack_unit(t.cells.data() + (static_cast<std::size_t>(G) * t.Pn + P) * t.cell_bytes + rg * ub,
+                            v.wb, v.sb, v.zb, u);
+                const std::uint32_t gr = v.group_rows(gg);
+                for (int blk = 0; blk < 16; ++blk) {
+                    const std::uint32_t k = 16 * P + blk;
+                    if (k >= v.nblocks) break;
+                    const std::uint32_t bw = v.block_width(k);
+                    buf.clear();
+                    for (int i = 0; i < 4; ++i) {
+                        buf.push_back(static_cast<std::uint8_t>(u.scal[blk][i]));
+                        buf.push_back(static_cast<std::uint8_t>(u.scal[blk][i] >> 8));
+                    }
+                    pack_bits(u.scode[blk], gr, v.sb, buf);
+                    pack_bits(u.zcode[blk], gr, v.zb, buf);
+                    std::uint8_t w[256];
+                    for (std::uint32_t r = 0; r < gr; ++r) std::memcpy(w + r * bw, &u.codes[r][16 * blk], bw);
+                    pack_bits(w, static_cast<std::size_t>(gr) * bw, v.wb, buf);
+                    std::memcpy(recs + v.record_offset(k, gg), buf.data(), buf.size());
+                }
+            }
+    });
+    // CSR: per row, walk the row's cells left to right
+    std::vector<std::uint32_t> rs(v.rows + 1, 0);
+    std::vector<std::uint8_t> ent;
+    ent.reserve(4ull * t.entries.size());
+    for (std::uint32_t r = 0; r < v.rows; ++r) {
+        const std::uint32_t G = r / 32, lr = r % 32;
+        for (std::uint32_t P = 0; P < t.Pn; ++P) {
+            const std::size_t q = static_cast<std::size_t>(G) * t.Pn + P;
+            for (std::uint32_t i = t.cell_off[q]; i < t.cell_off[q + 1]; ++i) {
+                const std::uint32_t e = t.entries[i];
+                if ((e >> 24) != lr) continue;
+                const std::uint16_t col = static_cast<std::uint16_t>(256 * P + ((e >> 16) & 255u));
+                ent.push_back(static_cast<std::uint8_t>(col));
+                ent.push_back(static_cast<std::uint8_t>(col >> 8));
+                ent.push_back(static_cast<std::uint8_t>(e));
+                ent.push_back(static_cast<std::uint8_t>(e >> 8));
+            }
+        }
+        rs[r + 1] = static_cast<std::uint32_t>(ent.size() / 4);
+    }
+    for (std::uint32_t r = 0; r <= v.rows; ++r)
+        for (int b = 0; b < 4; ++b) out.push_back(static_cast<std::uint8_t>(rs[r] >> (8 * b)));
+    out.insert(out.end(), ent.begin(), ent.end());
+    return out;
+}
+
+}  // namespace spqr::detail

@@ -46,8 +46,8 @@ def _quant_code(v, s, z, maxq: int):
     """quant_code (quantizer.hpp:50-56), float64, round half up, clamped."""
     with np.errstate(divide="ignore", invalid="ignore"):
         t = np.floor(v / s + z + 0.5)
-    t = np.where(~(s > 0.0), 0.0, t)
-    t = np.where(~(t > 0.0), 0.0, t)
+    t = np.where(np.logical_not(s > 0.0), 0.0, t)
+    t = np.where(np.logical_not(t > 0.0), 0.0, t)
     t = np.minimum(t, float(maxq))
     return t.astype(np.uint8)
 
