@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""bench.py -- SpQR decode path on B200: effective HBM GB/s and us/layer on
+LLaMA-65B layer shapes, against the roofline, a dense fp16 GEMV, and the
+reference's CPU path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], LLaMA-65B layer shapes): one decoder
+block's seven linear layers -- q,k,v,o 8192x8192, gate,up 22016x8192 and down
+8192x22016 -- each a 3-bit SpQR layer (beta1 = beta2 = 16, 3-bit statistics,
+1% CSR outliers), batch-1 matvec with fp16 x.  A step = one pass over the
+seven layers.  Synthetic data: uniform-random codes with plausible binary16
+statistics (bytes are identical to real layers).
+
+Metric: effective GB/s = algorithmic bytes / time, algorithmic bytes per layer
+= stream_payload_bytes (layout.hpp:47-64, the compressed layer) + 2n (fp16 x)
++ 4m (fp32 y).  The block's weights are 400 MB (> 126 MB L2), so every step
+re-reads them from HBM (no flush needed).
+
+N > 1 (torchrun): each rank holds a 1/N row band of every layer (the
+row-sharded wrapper) and all-gathers y over NCCL after each layer; value is
+the whole-job bytes / max-over-ranks time ("scaling": "strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpQR matvec µs/layer & HBM GB/s vs roofline (LLaMA shapes) vs fp16 GEMV"
+LAYERS = [("q_proj", 8192, 8192), ("k_proj", 8192, 8192), ("v_proj", 8192, 8192),
+          ("o_proj", 8192, 8192), ("gate_proj", 22016, 8192), ("up_proj", 22016, 8192),
+          ("down_proj", 8192, 22016)]
+BITS, RATE = 3, 0.01
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+
+def workload_config(n_gpus: int) -> dict:
+    return {
+        "workload": "llama65b-block: q,k,v,o 8192x8192; gate,up 22016x8192; down 8192x22016",
+        "weight_bits": BITS, "stat_bits": 3, "beta1": 16, "beta2": 16, "outlier_rate": RATE,
+        "batch": 1, "x_dtype": "f16", "layers": len(LAYERS),
+        "l2": "weights 400 MB per step > 126 MB L2: inputs larger than L2, no flush",
+        "parallelism": f"row-shard x{n_gpus} + NCCL all-gather of y" if n_gpus > 1 else "single GPU",
+    }
+
+
+def make_streams():
+    from paper_2306_03078_b200 import synth
+
+    cache = os.environ.get("SPQR_BENCH_CACHE", "/tmp/spqr_bench_streams")
+    os.makedirs(cache, exist_ok=True)
+    out = []
+    for i, (name, m, n) in enumerate(LAYERS):
+        path = os.path.join(cache, f"{name}_{m}x{n}_b{BITS}_r{RATE}_s{i}.spqr")
+        if os.path.exists(path):
+            s = open(path, "rb").read()
+        else:
+            s = synth.random_stream(m, n, BITS, 3, 3, RATE, seed=100 + i)
+            with open(path + ".tmp", "wb") as f:
+                f.write(s)
+            os.replace(path + ".tmp", path)
+        out.append(s)
+    return out
+
+
+def alg_bytes(payload: int, m: int, n: int, x_bytes: int = 2) -> int:
+    return payload + x_bytes * n + 4 * m
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons while the GPU works."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 4:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), float(parts[3])))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        busy = [s for s in self.samples if s[3] > 0 and not (s[2] & 0x1)] or self.samples
+        if not busy:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for s in busy:
+            for bit, name in REASONS.items():
+                if s[2] & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": max(s[1] for s in busy),
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+def load_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def cpu_reference_sample(streams) -> dict:
+    """The reference's own matvec(t, x, plan) (oracle/_ref, kernel.hpp:89) on
+    one pass over the block's seven layers, single thread (the reference is
+    single-threaded by construction)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    ref = O.Reference()
+    total_bytes, total_t = 0, 0.0
+    for (name, m, n), s in zip(LAYERS, streams):
+        t = ref.decode(s)
+        x = np.random.default_rng(2).standard_normal(n).astype(np.float16).astype(np.float32)
+        t0 = time.perf_counter()
+        t.matvec(x)
+        total_t += time.perf_counter() - t0
+        total_bytes += alg_bytes(len(s) - 48, m, n, 4)
+        del t
+    return {"value": total_bytes / total_t / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": "one pass over the 7 layers of the block, reference matvec(t, x, plan), 1 thread",
+            "seconds": round(total_t, 3)}
+
+
+# ------------------------------------------------------------ reference arm --
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_2306_03078_b200 as P
+
+    ref = O.Reference()
+    streams = make_streams()
+    threads = max(1, len(os.sched_getaffinity(0)))
+    bands = []  # per layer: list of reference tensors over row bands
+    bytes_step = 0
+    for (name, m, n), s in zip(LAYERS, streams):
+        nb = min(threads, m // 16)
+        edges = [16 * ((m // 16) * i // nb) for i in range(nb)] + [m]
+        bands.append([ref.decode(P.slice_rows(s, edges[i], edges[i + 1])) for i in range(nb)])
+        bytes_step += alg_bytes(len(s) - 48, m, n, 4)
+    xs = [np.random.default_rng(2).standard_normal(n).astype(np.float16).astype(np.float32) for _, _, n in LAYERS]
+
+    def step(layer_ids):
+        for i in layer_ids:
+            ref.matvec_bands(bands[i], xs[i], threads)
+
+    t0 = time.perf_counter()
+    step(range(len(LAYERS)))
+    t_full = time.perf_counter() - t0
+    budget = 150.0
+    layer_ids = list(range(len(LAYERS)))
+    sample = "full block (7 layers) per step"
+    if t_full * (args.steps + args.warmup) > budget:  # bound the run: one layer per step
+        layer_ids = [0]
+        sample = "q_proj 8192x8192 per step (bounded sample)"
+    sample_bytes = sum(alg_bytes(len(streams[i]) - 48, LAYERS[i][1], LAYERS[i][2], 4) for i in layer_ids)
+    for _ in range(max(0, args.warmup - 1)):
+        step(layer_ids)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(layer_ids)
+    dt = time.perf_counter() - t0
+    value = sample_bytes * args.steps / dt / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dt / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args.gpus),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample}; reference matvec(t, x, plan) on {threads} row bands, "
+                                   f"{threads} threads (oracle/_ref, unmodified headers)"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm --
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_03078_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    streams = make_streams()
+    layers, xs, ys, yfull, xs32 = [], [], [], [], []
+    bytes_step = 0  # whole-job algorithmic bytes per step
+    gen = torch.Generator(device="cpu").manual_seed(2)
+    for (name, m, n), s in zip(LAYERS, streams):
+        assert m % (32 * world) == 0
+        r0, r1 = rank * m // world, (rank + 1) * m // world
+        L = P.Layer(s, device=dev.index, rows=(r0, r1) if world > 1 else None)
+        assert L.info["fast_path"] == 1
+        layers.append(L)
+        x = torch.randn(n, generator=gen).to(torch.float16)
+        xs.append(x.to(dev))
+        xs32.append(x.float().pin_memory())
+        ys.append(torch.empty(r1 - r0, device=dev))
+        yfull.append(torch.empty(m, device=dev) if world > 1 else None)
+        bytes_step += alg_bytes(len(s) - 48, m, n) + 2 * n * (world - 1)
+    payload_step = sum(len(s) - 48 for s in streams)
+
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for i, L in enumerate(layers):
+            L.matvec(xs[i], ys[i], stream=stream)
+            if world > 1:
+                dist.all_gather_into_tensor(yfull[i], ys[i])
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    torch.cuda.synchronize()
+
+    def replay(n):
+        with torch.cuda.stream(stream):
+            for _ in range(n):
+                graph.replay()
+
+    # clocks: sample through a ~1.5 s soak plus the timed region
+    with ClockSampler(dev.index) as clk:
+        t_end = time.time() + 1.5
+        while time.time() < t_end:
+            replay(50)
+            stream.synchronize()
+        replay(args.warmup)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        replay(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = bytes_step / (ms_per_step * 1e-3) / 1e9
+
+    # ---- dominant kernel alone: the fused GEMV, cycling all seven layers ----
+    for i, L in enumerate(layers):
+        L.matvec_stage(xs[i], ys[i], stage=1, stream=stream)
+    torch.cuda.synchronize()
+    kgraph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(kgraph, stream=stream):
+        for i, L in enumerate(layers):
+            L.matvec_stage(xs[i], ys[i], stage=2, stream=stream)
+    reps = max(20, args.steps // 5)
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            kgraph.replay()
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            kgraph.replay()
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kms = k0.elapsed_time(k1) / reps  # one cycle = 7 launches
+    kbytes = sum(alg_bytes(L.info["payload_bytes"], L.rows, L.cols) for L in layers)  # this rank
+    peak, peak_kind = load_peaks()
+    achieved = kbytes / (kms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                traffic = json.load(f).get("dram_bytes_per_cycle")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "gemv_tiled (fused decode-GEMV + CSR merge)",
+                "us_per_launch": round(1e3 * kms / len(layers), 3),
+                "bytes_per_cycle": kbytes}
+
+    # ---- per-shape microseconds (full matvec incl. x preparation) ----
+    per_layer = {}
+    for i, (name, m, n) in enumerate(LAYERS):
+        shape = f"{m}x{n}"
+        if shape in per_layer:
+            continue
+        same = [j for j, l in enumerate(LAYERS) if f"{l[1]}x{l[2]}" == shape]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for j in same:
+                layers[j].matvec(xs[j], ys[j], stream=stream)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r = 50
+        a.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(r):
+                g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        us = 1e3 * a.elapsed_time(b) / (r * len(same))
+        pb = layers[i].info["payload_bytes"]
+        per_layer[shape] = {"us": round(us, 3), "GB/s": round(alg_bytes(pb, layers[i].rows, n) / (us * 1e-6) / 1e9, 1),
+                            "copies_cycled": len(same),
+                            "l2_resident_risk": len(same) * pb < 126e6}
+
+    # ---- dense fp16 GEMV comparator (ours and cuBLAS), same shapes ----
+    dense = {}
+    if world == 1:
+        W16 = [torch.randn(m, n, device=dev, dtype=torch.float16) * 0.02 for _, m, n in LAYERS]
+        yd = [torch.empty(m, device=dev) for _, m, _ in LAYERS]
+        for label, fn in (("ours", lambda i: P.dense_gemv_f16(W16[i], xs[i], yd[i], LAYERS[i][1], LAYERS[i][2],
+                                                               stream=stream)),
+                          ("cublas", lambda i: torch.mv(W16[i], xs[i]))):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(len(LAYERS)):
+                    fn(i)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(20):
+                    g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            dense[label] = a.elapsed_time(b) / 20
+        best = min(dense.values())
+        dense = {"ms_per_step_ours": round(dense["ours"], 4), "ms_per_step_cublas": round(dense["cublas"], 4),
+                 "dense_bytes_per_step": sum(2 * m * n + 2 * n + 4 * m for _, m, n in LAYERS),
+                 "speedup_spqr_vs_best_dense": round(best / ms_per_step, 3)}
+        del W16, yd
+
+    # ---- end to end through the public API with host buffers ----
+    e2e_steps = max(5, min(args.steps, 50))
+    ys_h = [torch.empty(m, dtype=torch.float32).pin_memory() for _, m, _ in LAYERS]
+    xd32 = [torch.empty(n, device=dev, dtype=torch.float32) for _, _, n in LAYERS]
+
+    def e2e_step():
+        for i, L in enumerate(layers):
+            if world == 1:
+                ys_h[i].numpy()[:] = L.matvec_host(xs32[i].numpy())
+            else:
+                xd32[i].copy_(xs32[i], non_blocking=True)
+                L.matvec(xd32[i], ys[i], stream=torch.cuda.current_stream())
+                dist.all_gather_into_tensor(yfull[i], ys[i])
+                ys_h[i].copy_(yfull[i], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(bytes_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": sum(4 * n for _, _, n in LAYERS),
+           "d2h_bytes_per_step": sum(4 * m for _, m, _ in LAYERS),
+           "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3),
+           "path": "spqr_matvec_host (C ABI: H2D fp32 x, fused kernels, D2H y, sync) per layer"
+                   if world == 1 else "H2D x, spqr_matvec, NCCL all-gather, D2H y per layer"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(streams)
+        except Exception as ex:  # noqa: BLE001 -- reported, never fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "us_per_layer": round(1e3 * ms_per_step / len(LAYERS), 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f16", "data": "synthetic",
+            "config": workload_config(world),
+            "bytes_per_step": bytes_step, "payload_bytes_per_step": payload_step,
+            "roofline": roofline, "per_layer": per_layer, "dense_fp16": dense or None,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": args.steps * 2 * len(LAYERS),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

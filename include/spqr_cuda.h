@@ -192,6 +192,12 @@ int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* 
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,
                    int batch, void* workspace, uint64_t ws_bytes, void* cuda_stream);
 
+/* The two launches of spqr_matvec separately (profiling): stage 1 = x
+ * preparation only (gather + scaling into the layer workspace), stage 2 = the
+ * fused product only (reuses the last stage-1 preparation), 0 = both. */
+int spqr_matvec_stage(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
+                      int stage, void* cuda_stream);
+
 /* matvec(const SpqrTensor&, std::span<const float>) drop-in with HOST buffers
  * (kernel.hpp:126-128): copies x in, computes, copies y out, synchronises. */
 int spqr_matvec_host(const spqr_layer* layer, const float* x_host, float* y_host, int batch);

@@ -89,6 +89,8 @@ EXPORTS = [
     "spqr_layer_create", "spqr_layer_destroy", "spqr_layer_get_info", "spqr_layer_export_stream",
     "spqr_dequantize", "spqr_workspace_bytes", "spqr_matvec", "spqr_matvec_ws", "spqr_matvec_host",
     "spqr_dense_gemv_f16", "spqr_last_launch_count", "spqr_debug_tiled_host",
+    "spqr_matvec_stage", "spqr_bench_layer", "spqr_dev_alloc", "spqr_dev_free",
+    "spqr_dev_copy_to_host", "spqr_dev_copy_to_device",
 ]
 
 
@@ -124,6 +126,12 @@ def lib() -> C.CDLL:
         "spqr_dense_gemv_f16": (i32, [vp, vp, vp, u32, u32, vp]),
         "spqr_last_launch_count": (i32, []),
         "spqr_debug_tiled_host": (i32, [vp, sz, vp, vp, vp, vp]),
+        "spqr_matvec_stage": (i32, [vp, vp, i32, vp, i32, i32, vp]),
+        "spqr_bench_layer": (i32, [vp, i32, vp]),
+        "spqr_dev_alloc": (i32, [C.POINTER(vp), sz]),
+        "spqr_dev_free": (None, [vp]),
+        "spqr_dev_copy_to_host": (i32, [vp, vp, sz]),
+        "spqr_dev_copy_to_device": (i32, [vp, vp, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -336,6 +344,17 @@ class Layer:
         else:
             _check(lib().spqr_matvec_ws(self._h, _ptr(x), dt, _ptr(y), batch, _ptr(workspace),
                                         workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+    def matvec_stage(self, x, y, stage: int, batch: int = 1, stream=None) -> None:
+        """Launch only the x preparation (1), only the fused product (2), or both (0)."""
+        dt = F16 if str(getattr(x, "dtype", "")).endswith("float16") else F32
+        _check(lib().spqr_matvec_stage(self._h, _ptr(x), dt, _ptr(y), batch, stage, _stream_ptr(stream)))
+
+    def bench(self, repeats: int = 20) -> np.ndarray:
+        """ns per op: fused matvec, dequantize_full, dense fp16 GEMV (CUDA events)."""
+        out = np.zeros(3, np.float64)
+        _check(lib().spqr_bench_layer(self._h, repeats, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def matvec_host(self, x: np.ndarray) -> np.ndarray:
         """Drop-in matvec(t, x) with host buffers (kernel.hpp:126)."""

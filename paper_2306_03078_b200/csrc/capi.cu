@@ -204,8 +204,11 @@ void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xl
     }
 }
 
+// stage: 0 = x preparation + product, 1 = x preparation only, 2 = product only
+// (reuses the workspace the last stage-1 call prepared; used to time the hot
+// kernel alone).
 void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int batch, void* ws, std::uint64_t wsb,
-                cudaStream_t st) {
+                cudaStream_t st, int stage = 0) {
     if (batch < 1) spqr::fail(spqr::Errc::shape_mismatch, "batch must be >= 1");
     if (dtype != SPQR_F16 && dtype != SPQR_F32) spqr::fail(spqr::Errc::config_invalid, "x dtype must be f16 or f32");
     const WsLayout w = ws_layout(L, batch);
@@ -217,14 +220,18 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
         auto* xl = reinterpret_cast<uint2*>(base + w.xlo);
         auto* xs = reinterpret_cast<float2*>(base + w.xsc);
         auto* xp = reinterpret_cast<float*>(base + w.xp);
-        dispatch_xprep(x, f16, L, batch, xf, xl, xs, xp, st);
+        if (stage != 2) dispatch_xprep(x, f16, L, batch, xf, xl, xs, xp, st);
+        if (stage == 1) return;
         std::uint32_t slot_bytes = 0;
         const std::size_t smem = tiled_smem(L, &slot_bytes);
         const std::uint32_t nblk = L->n_pad / 16;
         for (int b = 0; b < batch; ++b) {
             spqr_dev::TiledParams p{};
             p.cells = L->d_cells; p.cell_off = L->d_cell_off; p.ent = L->d_ent;
-            p.warp_start = L->d_warp_start; p.wfirst = L->d_wfirst; p.wlast = L->d_wlast;
+            p.warp_start = L->d_warp_start;
+            p.wfirst = L->d_wfirst;
+            p.wlast = L->d_wfirst + L->Gn;
+            p.wcnt = L->d_wfirst + 2 * L->Gn;
             p.xfrag = xf + static_cast<std::size_t>(b) * nblk * 4;
             p.xlo = xl + static_cast<std::size_t>(b) * nblk * 4;
             p.xsc = reinterpret_cast<const float4*>(xs + static_cast<std::size_t>(b) * nblk);
@@ -239,10 +246,13 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     } else {
         auto* xp = reinterpret_cast<float*>(base + w.xp);
         const std::uint64_t nx = static_cast<std::uint64_t>(L->info.cols) * batch;
-        spqr_dev::xprep_raw<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, st>>>(x, f16, L->info.cols, batch,
-                                                                                  L->d_order, xp);
-        ck(cudaGetLastError(), "launch xprep_raw");
-        ++g_launches;
+        if (stage != 2) {
+            spqr_dev::xprep_raw<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, st>>>(x, f16, L->info.cols,
+                                                                                      batch, L->d_order, xp);
+            ck(cudaGetLastError(), "launch xprep_raw");
+            ++g_launches;
+        }
+        if (stage == 1) return;
         const spqr_dev::RawGeom geo = raw_geom(L);
         for (int b = 0; b < batch; ++b) {
             spqr_dev::gemv_raw<<<(L->info.rows + 7) / 8, 256, 0, st>>>(
@@ -284,20 +294,25 @@ void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms) {
         ws[k] = q;
     }
     ws[L->nwarps] = Q;
-    std::vector<std::uint32_t> wf(t.Gn, UINT32_MAX), wl(t.Gn, 0);
+    // per row-group pair: first / last contributing warp and how many warps
+    // (with a non-empty range) contribute -- the finaliser's expected count
+    std::vector<std::uint32_t> wfl(3ull * t.Gn, 0);
+    std::uint32_t* wf = wfl.data();
+    std::uint32_t* wl = wf + t.Gn;
+    std::uint32_t* wc = wl + t.Gn;
+    std::fill(wf, wf + t.Gn, UINT32_MAX);
     for (std::uint32_t k = 0; k < L->nwarps; ++k) {
         if (ws[k] >= ws[k + 1]) continue;
         for (std::uint32_t G = ws[k] / t.Pn; G <= (ws[k + 1] - 1) / t.Pn; ++G) {
             wf[G] = std::min(wf[G], k);
             wl[G] = std::max(wl[G], k);
+            wc[G] += 1;
         }
     }
     L->d_warp_start = dalloc<std::uint32_t>(ws.size());
-    L->d_wfirst = dalloc<std::uint32_t>(t.Gn);
-    L->d_wlast = dalloc<std::uint32_t>(t.Gn);
+    L->d_wfirst = dalloc<std::uint32_t>(wfl.size());
     ck(cudaMemcpy(L->d_warp_start, ws.data(), 4 * ws.size(), cudaMemcpyHostToDevice), "H2D warp_start");
-    ck(cudaMemcpy(L->d_wfirst, wf.data(), 4ull * t.Gn, cudaMemcpyHostToDevice), "H2D wfirst");
-    ck(cudaMemcpy(L->d_wlast, wl.data(), 4ull * t.Gn, cudaMemcpyHostToDevice), "H2D wlast");
+    ck(cudaMemcpy(L->d_wfirst, wfl.data(), 4 * wfl.size(), cudaMemcpyHostToDevice), "H2D warp map");
 }
 
 }  // namespace
@@ -451,6 +466,19 @@ int spqr_matvec(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_de
         std::lock_guard<std::mutex> lk(L->mu);
         ensure_own_ws(L, batch);
         run_matvec(L, x_dev, x_dtype, y_dev, batch, L->d_ws, L->ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    });
+}
+
+int spqr_matvec_stage(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_dev, int batch, int stage,
+                      void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        g_launches = 0;
+        if (stage < 0 || stage > 2) spqr::fail(spqr::Errc::config_invalid, "stage must be 0, 1 or 2");
+        std::lock_guard<std::mutex> lk(L->mu);
+        ensure_own_ws(L, batch);
+        run_matvec(L, x_dev, x_dtype, y_dev, batch, L->d_ws, L->ws_bytes, static_cast<cudaStream_t>(cuda_stream),
+                   stage);
     });
 }
 

@@ -88,6 +88,7 @@ struct TiledParams {
     const std::uint32_t* warp_start;  // [nwarps+1]
     const std::uint32_t* wfirst;      // [Gn]
     const std::uint32_t* wlast;       // [Gn]
+    const std::uint32_t* wcnt;        // [Gn] warps with a non-empty range touching G
     const uint2* xfrag;               // [nblk_pad*4] per batch
     const uint2* xlo;                 // same (fp32 inputs)
     const float4* xsc;                // [nblk_pad/2] per batch: {SC,XX} x 2 blocks
@@ -251,14 +252,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             __threadfence();
             __syncwarp();
             std::uint32_t prev = 0;
-            const std::uint32_t expect = p.wlast[Gf] - p.wfirst[Gf] + 1;
+            const std::uint32_t expect = p.wcnt[Gf];
             if (lane == 0) prev = atomicAdd(p.counters + Gf, 1u);
             prev = __shfl_sync(0xffffffffu, prev, 0);
             if (prev == expect - 1) {  // last contributor reduces in warp order
                 __threadfence();
                 float sum = 0.f;
                 for (std::uint32_t k = p.wfirst[Gf]; k <= p.wlast[Gf]; ++k) {
-                    const std::uint32_t sk = (p.warp_start[k] / p.Pn == Gf) ? 0u : 1u;
+                    const std::uint32_t s0 = __ldg(p.warp_start + k);
+                    if (s0 == __ldg(p.warp_start + k + 1)) continue;  // idle warp
+                    const std::uint32_t sk = (s0 / p.Pn == Gf) ? 0u : 1u;
                     sum += __ldcg(p.partial + (k * 2 + sk) * 32 + R);
                 }
                 if (row < p.m) p.y[row] = sum;
@@ -603,7 +606,7 @@ __global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __res
         const uint4* wr = reinterpret_cast<const uint4*>(w + static_cast<std::uint64_t>(r) * cols);
         const uint4* xr = reinterpret_cast<const uint4*>(x);
         float acc = 0.f;
-        const std::uint32_t n8 = cols / 8;
+        const std::uint32_t n8 = (cols % 8 == 0) ? cols / 8 : 0;  // 128-bit rows need 16-B alignment
 #pragma unroll 4
         for (std::uint32_t i = lane; i < n8; i += 32) {
             const uint4 a = __ldcs(wr + i);
