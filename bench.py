@@ -375,6 +375,10 @@ def run_ours(args) -> None:
         for label, fn in (("ours", lambda i: P.dense_gemv_f16(W16[i], xs[i], yd[i], LAYERS[i][1], LAYERS[i][2],
                                                                stream=stream)),
                           ("cublas", lambda i: torch.mv(W16[i], xs[i]))):
+            with torch.cuda.stream(stream):
+                for i in range(len(LAYERS)):  # eager warm-up (creates the cuBLAS handle)
+                    fn(i)
+            torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
                 for i in range(len(LAYERS)):

@@ -25,9 +25,28 @@ namespace T = spqr_tiled;
 
 namespace {
 
-constexpr int kNW = 8;       // consumer warps per CTA (one CTA per SM)
-constexpr int kNSlot = 4;    // TMA ring depth per warp
-constexpr std::uint32_t kEntCapBytes = 2048;
+constexpr int kNW = 16;                       // consumer warps per CTA (one CTA per SM)
+constexpr std::uint32_t kSmemLimit = 232448;  // 227 KB per CTA on sm_100
+constexpr std::uint32_t kStaticSmem = 4096;   // mbarriers, slot offsets, row heads
+constexpr std::uint32_t kMaxEntCap = 2048;    // outlier bytes staged per cell (rest: LDG)
+
+// A TMA slot holds one cell, its panel's x operands and up to ent_cap bytes
+// of the cell's outlier entries.
+constexpr std::uint32_t slot_base(int bw, int bsz, bool xlo) {
+    return spqr_tiled::cell_bytes(bw, bsz, bsz) + spqr_tiled::panel_bytes(xlo);
+}
+// ring depth per warp: 3 slots when they fit with >= 1 KB of entries, else 2
+constexpr int nslot_for(int bw, int bsz, bool xlo) {
+    return kNW * 3 * (slot_base(bw, bsz, xlo) + 1024) + kStaticSmem <= kSmemLimit ? 3 : 2;
+}
+constexpr std::uint32_t slot_bytes_for(int bw, int bsz, bool xlo) {
+    const std::uint32_t avail = ((kSmemLimit - kStaticSmem) / (kNW * nslot_for(bw, bsz, xlo))) & ~127u;
+    const std::uint32_t want = (slot_base(bw, bsz, xlo) + kMaxEntCap + 127u) & ~127u;
+    return want < avail ? want : avail;
+}
+constexpr std::uint32_t ent_cap_for(int bw, int bsz, bool xlo) {
+    return slot_bytes_for(bw, bsz, xlo) - slot_base(bw, bsz, xlo);
+}
 
 thread_local int g_launches = 0;
 
@@ -137,7 +156,7 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
 
 template <int BW, int BSZ, bool XLO>
 void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::size_t smem, cudaStream_t st) {
-    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, kNW, kNSlot>;
+    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, kNW, nslot_for(BW, BSZ, XLO)>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -184,9 +203,11 @@ void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, uint
     }
 }
 
-std::size_t tiled_smem(const spqr_layer* L, std::uint32_t* slot_bytes) {
-    *slot_bytes = (L->cell_bytes + kEntCapBytes + 127u) & ~127u;
-    return static_cast<std::size_t>(kNW) * kNSlot * *slot_bytes;
+std::size_t tiled_smem(const spqr_layer* L, bool xlo, std::uint32_t* slot_bytes, std::uint32_t* ent_cap) {
+    const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
+    *slot_bytes = slot_bytes_for(bw, bsz, xlo);
+    *ent_cap = ent_cap_for(bw, bsz, xlo);
+    return static_cast<std::size_t>(kNW) * nslot_for(bw, bsz, xlo) * *slot_bytes;
 }
 
 void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xlo, std::size_t smem,
@@ -222,8 +243,8 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
         auto* xp = reinterpret_cast<float*>(base + w.xp);
         if (stage != 2) dispatch_xprep(x, f16, L, batch, xf, xl, xs, xp, st);
         if (stage == 1) return;
-        std::uint32_t slot_bytes = 0;
-        const std::size_t smem = tiled_smem(L, &slot_bytes);
+        std::uint32_t slot_bytes = 0, ent_cap = 0;
+        const std::size_t smem = tiled_smem(L, !f16, &slot_bytes, &ent_cap);
         const std::uint32_t nblk = L->n_pad / 16;
         for (int b = 0; b < batch; ++b) {
             spqr_dev::TiledParams p{};
@@ -240,7 +261,7 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
             p.partial = reinterpret_cast<float*>(base + w.partial);
             p.counters = reinterpret_cast<std::uint32_t*>(base + w.counters);
             p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps;
-            p.ent_cap_bytes = kEntCapBytes; p.slot_bytes = slot_bytes;
+            p.ent_cap_bytes = ent_cap; p.slot_bytes = slot_bytes;
             dispatch_tiled(p, L, !f16, smem, st);
         }
     } else {

@@ -146,246 +146,7 @@ __device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int 
     return static_cast<std::uint32_t>(x) & ((1u << NBITS) - 1u);
 }
 
-template <int BW, int BS, int BZ, bool XLO, int NW, int NSLOT>
-__global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
-    using G = Geo<BW>;
-    constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
-    constexpr std::uint32_t CELL = 2 * UNIT;
-    constexpr std::uint32_t CODEB = T::code_bytes(BW);
-    constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
-    constexpr int SB = BS + BZ;
-    constexpr std::uint32_t MASK = (1u << BW) - 1u;
-
-    extern __shared__ __align__(128) std::uint8_t smem[];
-    __shared__ std::uint64_t bars[NW][NSLOT];
-    __shared__ float oacc[NW][32];
-    __shared__ std::uint32_t slot_e[NW][NSLOT][2];
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const std::uint32_t wk = blockIdx.x * NW + warp;
-    const std::uint32_t q0 = p.warp_start[wk], q1 = p.warp_start[wk + 1];
-    std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * NSLOT * p.slot_bytes;
-
-    if (lane == 0) {
-        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[warp][s], 1);
-        fence_mbar_init();
-    }
-    oacc[warp][lane] = 0.0f;
-    __syncwarp();
-    if (q0 >= q1) {
-        pdl_wait();
-        return;
-    }
-
-    // per-cell outlier offsets, 32 cells at a time in lanes
-    std::uint32_t off_base = q0;
-    std::uint32_t off_lane = (q0 + lane <= q1) ? __ldg(p.cell_off + q0 + lane) : 0u;
-    auto cell_offset = [&](std::uint32_t q) -> std::uint32_t {  // warp-uniform q, all lanes call
-        if (q >= off_base + 32) {
-            off_base = q;
-            off_lane = (q + lane <= q1) ? __ldg(p.cell_off + q + lane) : 0u;
-        }
-        return __shfl_sync(0xffffffffu, off_lane, static_cast<int>(q - off_base));
-    };
-
-    auto issue = [&](std::uint32_t q, int slot) {  // whole warp calls (shuffles inside)
-        const std::uint32_t e0 = cell_offset(q), e1 = cell_offset(q + 1);
-        if (lane == 0) {
-            slot_e[warp][slot][0] = e0;
-            slot_e[warp][slot][1] = e1;
-            std::uint8_t* dst = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
-            std::uint32_t nb = 0, a0 = 0;
-            if (e1 > e0) {
-                a0 = (e0 * 4u) & ~15u;
-                nb = min(((e1 * 4u + 15u) & ~15u) - a0, p.ent_cap_bytes);
-            }
-            fence_proxy_async();
-            mbar_expect_tx(&bars[warp][slot], CELL + nb);
-            bulk_g2s(dst, p.cells + static_cast<std::size_t>(q) * CELL, CELL, &bars[warp][slot]);
-            if (nb) bulk_g2s(dst + CELL, reinterpret_cast<const std::uint8_t*>(p.ent) + a0, nb, &bars[warp][slot]);
-        }
-    };
-
-    const std::uint32_t ncell = q1 - q0;
-#pragma unroll 1
-    for (int s = 0; s < NSLOT; ++s)
-        if (static_cast<std::uint32_t>(s) < ncell) issue(q0 + s, s);
-
-    // weights stream before the x preparation of the previous kernel finishes
-    pdl_wait();
-
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // [unit][rho]
-    std::uint32_t curG = q0 / p.Pn;
-    const std::uint32_t Gq0 = curG;
-
-    auto flush = [&](std::uint32_t Gf, bool whole) {
-        float v[2][2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                float a = acc[u][r];
-                a += __shfl_xor_sync(0xffffffffu, a, 1);
-                a += __shfl_xor_sync(0xffffffffu, a, 2);
-                v[u][r] = a;
-            }
-        __syncwarp();
-        // lane L ends up owning local row L = 16u + 8rho + g (collect from lane 4g)
-        const int R = lane, u = R >> 4, rho = (R >> 3) & 1, gg = R & 7;
-        float mine = 0.f;
-#pragma unroll
-        for (int uu = 0; uu < 2; ++uu)
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const float o = __shfl_sync(0xffffffffu, v[uu][rr], gg * 4);
-                if (uu == u && rr == rho) mine = o;
-            }
-        mine += oacc[warp][R];
-        oacc[warp][R] = 0.f;
-        const std::uint32_t row = 32u * Gf + R;
-        if (whole) {
-            if (row < p.m) p.y[row] = mine;
-        } else {
-            const std::uint32_t side = (Gf == Gq0) ? 0u : 1u;
-            p.partial[(wk * 2 + side) * 32 + R] = mine;
-            __threadfence();
-            __syncwarp();
-            std::uint32_t prev = 0;
-            const std::uint32_t expect = p.wcnt[Gf];
-            if (lane == 0) prev = atomicAdd(p.counters + Gf, 1u);
-            prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev == expect - 1) {  // last contributor reduces in warp order
-                __threadfence();
-                float sum = 0.f;
-                for (std::uint32_t k = p.wfirst[Gf]; k <= p.wlast[Gf]; ++k) {
-                    const std::uint32_t s0 = __ldg(p.warp_start + k);
-                    if (s0 == __ldg(p.warp_start + k + 1)) continue;  // idle warp
-                    const std::uint32_t sk = (s0 / p.Pn == Gf) ? 0u : 1u;
-                    sum += __ldcg(p.partial + (k * 2 + sk) * 32 + R);
-                }
-                if (row < p.m) p.y[row] = sum;
-                if (lane == 0) p.counters[Gf] = 0;
-            }
-        }
-        acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.f;
-    };
-
-#pragma unroll 1
-    for (std::uint32_t it = 0; it < ncell; ++it) {
-        const std::uint32_t q = q0 + it;
-        const int slot = static_cast<int>(it % NSLOT);
-        const std::uint32_t phase = (it / NSLOT) & 1u;
-        const std::uint32_t Gc = q / p.Pn, P = q - Gc * p.Pn;
-        if (Gc != curG) {
-            flush(curG, curG * p.Pn >= q0);
-            curG = Gc;
-        }
-        // x operands of this panel (L1/L2 resident, shared by both units)
-        uint2 xf[2], xl[2];
-        float4 xs[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            xf[h] = __ldg(p.xfrag + (16u * P + 8u * h + g) * 4u + t);
-            if constexpr (XLO) xl[h] = __ldg(p.xlo + (16u * P + 8u * h + g) * 4u + t);
-            xs[h] = __ldg(p.xsc + 8u * P + 4u * h + t);
-        }
-        mbar_wait(&bars[warp][slot], phase);
-        const std::uint32_t e0 = slot_e[warp][slot][0], e1 = slot_e[warp][slot][1];
-        const std::uint8_t* cell = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
-
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const std::uint8_t* unit = cell + u * UNIT;
-            std::uint32_t cw[G::LANE_WORDS];
-#pragma unroll
-            for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                const uint4 v = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                cw[4 * i] = v.x; cw[4 * i + 1] = v.y; cw[4 * i + 2] = v.z; cw[4 * i + 3] = v.w;
-            }
-            std::uint64_t sbits[2];
-            load_stat_bits<SB>(unit + CODEB + lane * SB, sbits);
-            uint4 sc[2];
-            sc[0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
-            sc[1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
-
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float c[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                    const std::uint32_t* w = cw + G::CW * cidx;
-                    std::uint32_t a[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                        const int i = rho * (G::NP / 2) + qq;
-                        const int B = (BW * i) >> 3, pp = (BW * i) & 7;
-                        a[r] = window<G::CW>(w, B) & ((MASK << pp) * 0x00010001u);
-                    }
-                    const bool mine = (g == j);
-                    mma16816(c, a, mine ? xf[h].x : 0u, mine ? xf[h].y : 0u);
-                    if constexpr (XLO) mma16816(c, a, mine ? xl[h].x : 0u, mine ? xl[h].y : 0u);
-                }
-                // epilogue: lane holds D(row g+8rho, block 8h+2t+bs) in c[2rho+bs]
-                const uint4 s4 = sc[h];
-                const float sc_b[2] = {xs[h].x, xs[h].z}, xx_b[2] = {xs[h].y, xs[h].w};
-#pragma unroll
-                for (int bs = 0; bs < 2; ++bs) {
-                    const std::uint32_t w01 = bs ? s4.z : s4.x;  // scale_s | scale_z
-                    const std::uint32_t w23 = bs ? s4.w : s4.y;  // zero_s  | zero_z
-                    const float Ss = h2f_bits(w01 & 0xffffu), Zs = h2f_bits(w01 >> 16);
-                    const float Sz = h2f_bits(w23 & 0xffffu), Zz = h2f_bits(w23 >> 16);
-                    const float A1 = Ss * sc_b[bs], A0 = -A1 * Zs;
-                    const float B0 = -Sz * Zz;
-#pragma unroll
-                    for (int rho = 0; rho < 2; ++rho) {
-                        const int eps = 4 * h + 2 * bs + rho;
-                        const float cs = u2f_small(field<BS>(sbits, eps * BS));
-                        const float cz = u2f_small(field<BZ>(sbits, 8 * BS + eps * BZ));
-                        const float shat = fmaf(A1, cs, A0);
-                        const float zhat = fmaf(Sz, cz, B0);
-                        const float tt = fmaf(zhat, xx_b[bs], c[2 * rho + bs]);
-                        acc[u][rho] = fmaf(shat, tt, acc[u][rho]);
-                    }
-                }
-            }
-        }
-
-        // outliers of this cell: segmented scan by local row, one add per row run
-        const std::uint32_t cnt = e1 - e0;
-        if (cnt) {
-            const std::uint32_t a0 = (e0 * 4u) & ~15u;
-            const std::uint32_t have = min(((e1 * 4u + 15u) & ~15u) - a0, p.ent_cap_bytes);
-            const std::uint8_t* es = cell + CELL + (e0 * 4u - a0);
-            const std::uint32_t in_smem = (have - (e0 * 4u - a0)) / 4u;
-            const float* xpanel = p.xp + 256u * P;
-#pragma unroll 1
-            for (std::uint32_t base = 0; base < cnt; base += 32) {
-                const std::uint32_t i = base + lane;
-                const bool valid = i < cnt;
-                std::uint32_t e = 0;
-                if (valid) e = (i < in_smem) ? reinterpret_cast<const std::uint32_t*>(es)[i] : __ldg(p.ent + e0 + i);
-                int r = valid ? static_cast<int>(e >> 24) : 64 + lane;
-                float v = valid ? h2f_bits(e & 0xffffu) * __ldg(xpanel + ((e >> 16) & 255u)) : 0.f;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const float vv = __shfl_up_sync(0xffffffffu, v, d);
-                    const int rr = __shfl_up_sync(0xffffffffu, r, d);
-                    if (lane >= d && rr == r) v += vv;
-                }
-                const int rn = __shfl_down_sync(0xffffffffu, r, 1);
-                if (valid && (lane == 31 || rn != r)) oacc[warp][r] += v;
-                __syncwarp();
-            }
-        }
-
-        __syncwarp();
-        if (it + NSLOT < ncell) issue(q + NSLOT, slot);
-    }
-    flush(curG, curG * p.Pn >= q0 && (curG + 1) * p.Pn <= q1);
-}
+#include "gemv_tiled.cuh"
 
 // x preparation for the tiled path: one thread per (16-column block, batch).
 template <int BW, bool XLO>

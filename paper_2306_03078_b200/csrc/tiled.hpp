@@ -87,6 +87,17 @@ SPQR_HD constexpr int column_prescale(int bw, std::uint32_t k, std::uint32_t cc)
     return prescale_p(bw, 2 * m + kh);
 }
 
+// x operands of one 256-column panel as prepared by xprep_tiled, staged into
+// the kernel's TMA slot next to the cell: B fragments (16 blocks x 32 B),
+// {SC, XX} per block (16 x 8 B), the fp32 solve-order x for the outlier merge
+// (256 x 4 B) and, for fp32 inputs, the low-half B fragments (16 x 32 B).
+inline constexpr std::uint32_t kPanelFragBytes = 512;
+inline constexpr std::uint32_t kPanelScBytes = 128;
+inline constexpr std::uint32_t kPanelXpBytes = 1024;
+SPQR_HD constexpr std::uint32_t panel_bytes(bool xlo) {
+    return kPanelFragBytes + kPanelScBytes + kPanelXpBytes + (xlo ? kPanelFragBytes : 0u);
+}
+
 // Entry packing of the per-cell outlier lists.
 SPQR_HD constexpr std::uint32_t pack_entry(std::uint32_t local_row, std::uint32_t col_in_cell,
                                            std::uint16_t v) {
