@@ -158,8 +158,10 @@ int spqr_transcode_roundtrip_host(const uint8_t* stream, size_t nbytes, uint8_t*
                                   size_t* len);
 
 /* Test hook: the tiled HBM image the loader would upload, in host memory.
- * dims4 = {Gn, Pn, cell_bytes, outlier_count}.  Call with NULL buffers to
- * query dims; then cells (Gn*Pn*cell_bytes), cell_off (Gn*Pn+1), entries. */
+ * dims4 = {Gn, Pn, cell_bytes, record_bytes}.  Call with NULL buffers to
+ * query dims; then cells (record_bytes: cell records = cell + its outlier
+ * entries, 16-B padded with 0xffffffff), cell_off (Gn*Pn+1 byte offsets).
+ * `entries` is unused (kept for ABI stability). */
 int spqr_debug_tiled_host(const uint8_t* stream, size_t nbytes, uint32_t* dims4, uint8_t* cells,
                           uint32_t* cell_off, uint32_t* entries);
 

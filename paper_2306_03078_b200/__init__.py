@@ -295,13 +295,12 @@ def debug_tiled_host(stream: bytes) -> dict:
     a, p, n = _buf(stream)
     dims = np.zeros(4, np.uint32)
     _check(lib().spqr_debug_tiled_host(p, n, dims.ctypes.data_as(C.c_void_p), None, None, None))
-    Gn, Pn, cb, nnz = (int(v) for v in dims)
-    cells = np.zeros(Gn * Pn * cb, np.uint8)
+    Gn, Pn, cb, total = (int(v) for v in dims)
+    cells = np.zeros(total, np.uint8)
     off = np.zeros(Gn * Pn + 1, np.uint32)
-    ent = np.zeros(max(nnz, 1), np.uint32)
     _check(lib().spqr_debug_tiled_host(p, n, dims.ctypes.data_as(C.c_void_p), cells.ctypes.data_as(C.c_void_p),
-                                       off.ctypes.data_as(C.c_void_p), ent.ctypes.data_as(C.c_void_p)))
-    return {"Gn": Gn, "Pn": Pn, "cell_bytes": cb, "cells": cells, "cell_off": off, "entries": ent[:nnz]}
+                                       off.ctypes.data_as(C.c_void_p), None))
+    return {"Gn": Gn, "Pn": Pn, "cell_bytes": cb, "cells": cells, "cell_off": off}
 
 
 # ---------------------------------------------------------------- device --

@@ -30,8 +30,8 @@ constexpr std::uint32_t kSmemLimit = 232448;  // 227 KB per CTA on sm_100
 constexpr std::uint32_t kStaticSmem = 4096;   // mbarriers, slot offsets, row heads
 constexpr std::uint32_t kMaxEntCap = 2048;    // outlier bytes staged per cell (rest: LDG)
 
-// A TMA slot holds one cell, its panel's x operands and up to ent_cap bytes
-// of the cell's outlier entries.
+// A TMA slot holds the panel's x operands, then one cell record (cell bytes +
+// as many of the cell's outlier entries as fit; the rest are read from HBM).
 constexpr std::uint32_t slot_base(int bw, int bsz, bool xlo) {
     return spqr_tiled::cell_bytes(bw, bsz, bsz) + spqr_tiled::panel_bytes(xlo);
 }
@@ -44,9 +44,10 @@ constexpr std::uint32_t slot_bytes_for(int bw, int bsz, bool xlo) {
     const std::uint32_t want = (slot_base(bw, bsz, xlo) + kMaxEntCap + 127u) & ~127u;
     return want < avail ? want : avail;
 }
-constexpr std::uint32_t ent_cap_for(int bw, int bsz, bool xlo) {
-    return slot_bytes_for(bw, bsz, xlo) - slot_base(bw, bsz, xlo);
+constexpr std::uint32_t rec_cap_for(int bw, int bsz, bool xlo) {  // record bytes per slot
+    return slot_bytes_for(bw, bsz, xlo) - spqr_tiled::panel_bytes(xlo);
 }
+static_assert(rec_cap_for(4, 4, true) >= spqr_tiled::cell_bytes(4, 4, 4), "slot must hold a cell");
 
 thread_local int g_launches = 0;
 
@@ -93,7 +94,6 @@ struct spqr_layer {
     bool fast = false;
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
-    std::uint32_t* d_ent = nullptr;
     std::uint32_t* d_warp_start = nullptr;
     std::uint32_t* d_wfirst = nullptr;
     std::uint32_t* d_wlast = nullptr;
@@ -108,7 +108,7 @@ struct spqr_layer {
 
     ~spqr_layer() {
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
-                        static_cast<void*>(d_cell_off), static_cast<void*>(d_ent), static_cast<void*>(d_warp_start),
+                        static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start),
                         static_cast<void*>(d_wfirst), static_cast<void*>(d_wlast), d_ws,
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
@@ -132,7 +132,7 @@ spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
 
 // Workspace carve-up (bytes, 256-aligned pieces).
 struct WsLayout {
-    std::uint64_t xfrag = 0, xlo = 0, xsc = 0, xp = 0, partial = 0, counters = 0, total = 0;
+    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, total = 0;
 };
 std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 WsLayout ws_layout(const spqr_layer* L, int batch) {
@@ -140,11 +140,9 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
     const std::uint64_t b = static_cast<std::uint64_t>(std::max(batch, 1));
     std::uint64_t o = 0;
     if (L->fast) {
-        const std::uint64_t nblk = L->n_pad / 16;
-        w.xfrag = o; o += al(b * nblk * 32);
-        w.xlo = o; o += al(b * nblk * 32);
-        w.xsc = o; o += al(b * nblk * 8);
-        w.xp = o; o += al(b * L->n_pad * 4);
+        // x panels sized for the fp32-input layout (the larger of the two)
+        w.panel_stride = static_cast<std::uint64_t>(L->Pn) * spqr_tiled::panel_bytes(true);
+        w.panels = o; o += al(b * w.panel_stride);
         w.partial = o; o += al(static_cast<std::uint64_t>(L->nwarps) * 2 * 32 * 4);
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
@@ -179,34 +177,38 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
     ++g_launches;
 }
 
+// x panels for `batch` columns; column b's panels start at b * panel_stride.
 template <int BW, bool XLO>
-void launch_xprep_t(const void* x, int f16, const spqr_layer* L, int batch, uint2* xf, uint2* xl, float2* xs,
-                    float* xp, cudaStream_t st) {
-    const std::uint32_t work = (L->n_pad / 16) * static_cast<std::uint32_t>(batch);
-    spqr_dev::xprep_tiled<BW, XLO><<<(work + 127) / 128, 128, 0, st>>>(x, f16, L->info.cols, L->n_pad,
-                                                                    static_cast<std::uint32_t>(batch), L->d_order,
-                                                                    xf, xl, xs, xp);
-    ck(cudaGetLastError(), "launch xprep_tiled");
-    ++g_launches;
-}
-
-void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, uint2* xf, uint2* xl, float2* xs,
-                    float* xp, cudaStream_t st) {
-    const bool lo = !f16;
-    switch (L->info.weight_bits * 2 + (lo ? 1 : 0)) {
-        case 4: launch_xprep_t<2, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
-        case 5: launch_xprep_t<2, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
-        case 6: launch_xprep_t<3, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
-        case 7: launch_xprep_t<3, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
-        case 8: launch_xprep_t<4, false>(x, f16, L, batch, xf, xl, xs, xp, st); break;
-        default: launch_xprep_t<4, true>(x, f16, L, batch, xf, xl, xs, xp, st); break;
+void launch_xprep_t(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,
+                    std::uint64_t panel_stride, cudaStream_t st) {
+    const std::uint32_t nblk = L->n_pad / 16;
+    for (int b = 0; b < batch; ++b) {  // one launch per column keeps the stride explicit
+        const void* xb = static_cast<const std::uint8_t*>(x) +
+                         static_cast<std::size_t>(b) * L->info.cols * (f16 ? 2 : 4);
+        spqr_dev::xprep_tiled<BW, XLO><<<(nblk + 127) / 128, 128, 0, st>>>(
+            xb, f16, L->info.cols, L->n_pad, 1u, L->d_order, panels + b * panel_stride);
+        ck(cudaGetLastError(), "launch xprep_tiled");
+        ++g_launches;
     }
 }
 
-std::size_t tiled_smem(const spqr_layer* L, bool xlo, std::uint32_t* slot_bytes, std::uint32_t* ent_cap) {
+void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,
+                    std::uint64_t stride, cudaStream_t st) {
+    const bool lo = !f16;
+    switch (L->info.weight_bits * 2 + (lo ? 1 : 0)) {
+        case 4: launch_xprep_t<2, false>(x, f16, L, batch, panels, stride, st); break;
+        case 5: launch_xprep_t<2, true>(x, f16, L, batch, panels, stride, st); break;
+        case 6: launch_xprep_t<3, false>(x, f16, L, batch, panels, stride, st); break;
+        case 7: launch_xprep_t<3, true>(x, f16, L, batch, panels, stride, st); break;
+        case 8: launch_xprep_t<4, false>(x, f16, L, batch, panels, stride, st); break;
+        default: launch_xprep_t<4, true>(x, f16, L, batch, panels, stride, st); break;
+    }
+}
+
+std::size_t tiled_smem(const spqr_layer* L, bool xlo, std::uint32_t* slot_bytes, std::uint32_t* rec_cap) {
     const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
     *slot_bytes = slot_bytes_for(bw, bsz, xlo);
-    *ent_cap = ent_cap_for(bw, bsz, xlo);
+    *rec_cap = rec_cap_for(bw, bsz, xlo);
     return static_cast<std::size_t>(kNW) * nslot_for(bw, bsz, xlo) * *slot_bytes;
 }
 
@@ -237,31 +239,25 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
     if (L->fast) {
-        auto* xf = reinterpret_cast<uint2*>(base + w.xfrag);
-        auto* xl = reinterpret_cast<uint2*>(base + w.xlo);
-        auto* xs = reinterpret_cast<float2*>(base + w.xsc);
-        auto* xp = reinterpret_cast<float*>(base + w.xp);
-        if (stage != 2) dispatch_xprep(x, f16, L, batch, xf, xl, xs, xp, st);
+        auto* panels = base + w.panels;
+        if (stage != 2) dispatch_xprep(x, f16, L, batch, panels, w.panel_stride, st);
         if (stage == 1) return;
-        std::uint32_t slot_bytes = 0, ent_cap = 0;
-        const std::size_t smem = tiled_smem(L, !f16, &slot_bytes, &ent_cap);
-        const std::uint32_t nblk = L->n_pad / 16;
+        std::uint32_t slot_bytes = 0, rec_cap = 0;
+        const std::size_t smem = tiled_smem(L, !f16, &slot_bytes, &rec_cap);
         for (int b = 0; b < batch; ++b) {
             spqr_dev::TiledParams p{};
-            p.cells = L->d_cells; p.cell_off = L->d_cell_off; p.ent = L->d_ent;
+            p.cells = L->d_cells;
+            p.cell_off = L->d_cell_off;
             p.warp_start = L->d_warp_start;
             p.wfirst = L->d_wfirst;
             p.wlast = L->d_wfirst + L->Gn;
             p.wcnt = L->d_wfirst + 2 * L->Gn;
-            p.xfrag = xf + static_cast<std::size_t>(b) * nblk * 4;
-            p.xlo = xl + static_cast<std::size_t>(b) * nblk * 4;
-            p.xsc = reinterpret_cast<const float4*>(xs + static_cast<std::size_t>(b) * nblk);
-            p.xp = xp + static_cast<std::size_t>(b) * L->n_pad;
+            p.xpanel = panels + b * w.panel_stride;
             p.y = y + static_cast<std::size_t>(b) * L->info.rows;
             p.partial = reinterpret_cast<float*>(base + w.partial);
             p.counters = reinterpret_cast<std::uint32_t*>(base + w.counters);
             p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps;
-            p.ent_cap_bytes = ent_cap; p.slot_bytes = slot_bytes;
+            p.rec_cap_bytes = rec_cap; p.slot_bytes = slot_bytes;
             dispatch_tiled(p, L, !f16, smem, st);
         }
     } else {
@@ -305,7 +301,7 @@ void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms) {
     L->nwarps = L->grid * kNW;
     std::vector<double> pre(Q + 1, 0.0);
     for (std::uint32_t q = 0; q < Q; ++q)
-        pre[q + 1] = pre[q] + t.cell_bytes + 12.0 * (t.cell_off[q + 1] - t.cell_off[q]);
+        pre[q + 1] = pre[q] + 1024.0 + (t.cell_off[q + 1] - t.cell_off[q]);  // x panel + record
     const double total = pre[Q];
     std::vector<std::uint32_t> ws(L->nwarps + 1, Q);
     std::uint32_t q = 0;
@@ -389,19 +385,15 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
         if (L->fast) {
             const spqr::detail::TiledHost t = spqr::detail::transcode_to_tiled(v, 0);
             L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
-            L->d_cells = dalloc<std::uint8_t>(t.cells.size());
+            L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
             ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
             L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size());
             ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice),
                "H2D cell_off");
-            L->d_ent = dalloc<std::uint32_t>(t.entries.size() + 8);  // TMA may round the tail up to 16 B
-            ck(cudaMemset(L->d_ent, 0, 4 * (t.entries.size() + 8)), "zero entries");
-            if (!t.entries.empty())
-                ck(cudaMemcpy(L->d_ent, t.entries.data(), 4 * t.entries.size(), cudaMemcpyHostToDevice), "H2D ent");
             int sms = 0;
             ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
             plan_partition(L.get(), t, sms);
-            dev_bytes += t.cells.size() + 4 * t.cell_off.size() + 4 * t.entries.size();
+            dev_bytes += t.cells.size() + 4 * t.cell_off.size();
         }
         L->info.fast_path = L->fast;
         ensure_own_ws(L.get(), 1);
@@ -429,14 +421,11 @@ int spqr_layer_export_stream(const spqr_layer* L, uint8_t* out, size_t cap, size
         if (L->fast) {
             spqr::detail::TiledHost t;
             t.Gn = L->Gn; t.Pn = L->Pn; t.cell_bytes = L->cell_bytes; t.prefix = L->prefix;
-            t.cells.resize(static_cast<std::size_t>(t.Gn) * t.Pn * t.cell_bytes);
             t.cell_off.resize(static_cast<std::size_t>(t.Gn) * t.Pn + 1);
-            ck(cudaMemcpy(t.cells.data(), L->d_cells, t.cells.size(), cudaMemcpyDeviceToHost), "D2H cells");
             ck(cudaMemcpy(t.cell_off.data(), L->d_cell_off, 4 * t.cell_off.size(), cudaMemcpyDeviceToHost),
                "D2H cell_off");
-            t.entries.resize(L->info.outlier_count);
-            if (!t.entries.empty())
-                ck(cudaMemcpy(t.entries.data(), L->d_ent, 4 * t.entries.size(), cudaMemcpyDeviceToHost), "D2H ent");
+            t.cells.resize(t.cell_off.back());
+            ck(cudaMemcpy(t.cells.data(), L->d_cells, t.cells.size(), cudaMemcpyDeviceToHost), "D2H cells");
             bytes = spqr::detail::tiled_to_stream(L->geo, t, 0);
         } else {
             bytes.resize(L->info.payload_bytes + spqr::kSpqrHeaderBytes);

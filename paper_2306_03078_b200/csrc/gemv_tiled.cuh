@@ -9,17 +9,17 @@
 // (exact products, fp32 accumulate) and XX_k = -2^-24 sum_c x_c 2^e_k (xprep).
 //
 // Work: a persistent grid, one CTA per SM, NW warps per CTA; warp k streams a
-// contiguous range of 32x256 cells (host-balanced by bytes incl. outliers)
-// through its own TMA ring (cp.async.bulk + mbarrier, NSLOT cells in flight).
-// Each slot receives the cell, the panel's prepared x operands and the cell's
-// outlier entries, so the inner loop touches only shared memory and registers.
+// contiguous range of cell records (32x256 weights + that cell's outliers,
+// host-balanced by bytes) through its own TMA ring (cp.async.bulk + mbarrier,
+// NSLOT records in flight).  Each slot also receives the panel's prepared x
+// operands, so the inner loop touches only shared memory and registers.
 // MMA j of super-tile h routes block 8h+j to output column j by zeroing the B
 // fragment in every lane but those with g == j, so the 8 MMAs of a super-tile
 // accumulate into one C and each lane ends up holding 4 distinct
 // (row, block) dot products -- one statistics decode per 16 weights.
 // Outliers of a cell are merged by their row's owner lane (lane = local row).
-// Rows split between warps are combined deterministically by the last arriving
-// warp in warp order; every y row is written exactly once.
+// Rows split between warps are combined by the last arriving warp in warp
+// order; every y row is written exactly once.
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     float2 d;
@@ -39,12 +39,28 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
 }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
 
-// code -> (2^23 + code) as float bits; fadd2 with -2^23 makes it exact.
-__device__ __forceinline__ float magic_code(std::uint32_t v) { return __int_as_float(0x4B000000u | v); }
+// ((w >> shift) & M) | 2^23-pattern: the code as the float 2^23 + code, with
+// SHF + ONE LOP3 (the exponent pattern lives in a register: LOP3 takes a
+// single immediate).  `shift` is a compile-time constant after unrolling.
+template <std::uint32_t M>
+__device__ __forceinline__ float magic_field_rt(std::uint32_t w, int shift, std::uint32_t magic) {
+    std::uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w >> shift), "n"(M), "r"(magic));
+    return __uint_as_float(r);
+}
 
 // Lane statistics field (SB bytes at 2-byte alignment) as two 32-bit words:
-// s = bits [0, 32), z = bits [8*BS, 8*BS + 32) (all zero codes, aligned at 0).
+// s = bits [0, 32) (scale codes), z = bits [8*BS, 8*BS + 32) (zero codes).
 template <int BS, int BZ>
 __device__ __forceinline__ void load_stats(const std::uint8_t* p, std::uint32_t& s, std::uint32_t& z) {
     std::uint64_t v[2];
@@ -63,17 +79,18 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     constexpr std::uint32_t CODEB = T::code_bytes(BW);
     constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
     constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
-    constexpr std::uint32_t O_FRAG = CELL, O_SC = CELL + T::kPanelFragBytes;
-    constexpr std::uint32_t O_XP = O_SC + T::kPanelScBytes, O_LO = O_XP + T::kPanelXpBytes;
-    constexpr std::uint32_t O_ENT = CELL + PANEL;
+    constexpr std::uint32_t O_FRAG = 0, O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
+    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
+    constexpr std::uint32_t O_REC = PANEL;  // cell record follows the panel in a slot
     constexpr int SB = BS + BZ;
     constexpr std::uint32_t MASK = (1u << BW) - 1u;
+    constexpr std::uint32_t SMASK = (1u << BS) - 1u, ZMASK = (1u << BZ) - 1u;
     constexpr float kMagic = 8388608.0f;
 
     extern __shared__ __align__(128) std::uint8_t smem[];
     __shared__ std::uint64_t bars[NW][NSLOT];
-    __shared__ std::uint32_t slot_e[NW][NSLOT][2];
-    __shared__ std::uint32_t heads[NW][32];
+    __shared__ std::uint32_t slot_r[NW][NSLOT][2];  // record byte range of the slot's cell
+    __shared__ std::uint32_t hist[NW][32];           // outlier count per local row of a cell
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -91,48 +108,34 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         return;
     }
 
-    // per-cell outlier offsets, 32 cells at a time across the lanes
+    // record byte offsets of 32 consecutive cells at a time across the lanes
     std::uint32_t off_base = q0;
     std::uint32_t off_lane = (q0 + lane <= q1) ? __ldg(p.cell_off + q0 + lane) : 0u;
-    auto cell_offset = [&](std::uint32_t q) -> std::uint32_t {  // monotone q, whole warp
+    auto rec_offset = [&](std::uint32_t q) -> std::uint32_t {  // monotone q, whole warp
         if (q >= off_base + 32) {
             off_base = q;
             off_lane = (q + lane <= q1) ? __ldg(p.cell_off + q + lane) : 0u;
         }
         return __shfl_sync(0xffffffffu, off_lane, static_cast<int>(q - off_base));
     };
-    // Panel of cell q = q % Pn, tracked incrementally for the issue pointer.
-    // weights + outlier entries of cell q into `slot` (arms the barrier for the
-    // whole slot including the x panel, which issue_x adds)
+    // cell record q -> slot (arms the barrier for record + panel)
     auto issue_w = [&](std::uint32_t q, int slot) {
-        const std::uint32_t e0 = cell_offset(q), e1 = cell_offset(q + 1);
+        const std::uint32_t r0 = rec_offset(q), r1 = rec_offset(q + 1);
         if (lane == 0) {
-            slot_e[warp][slot][0] = e0;
-            slot_e[warp][slot][1] = e1;
-            std::uint8_t* dst = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
-            std::uint32_t nb = 0, a0 = 0;
-            if (e1 > e0) {
-                a0 = (e0 * 4u) & ~15u;
-                nb = min(((e1 * 4u + 15u) & ~15u) - a0, p.ent_cap_bytes);
-            }
+            slot_r[warp][slot][0] = r0;
+            slot_r[warp][slot][1] = r1;
+            const std::uint32_t nb = min(r1 - r0, p.rec_cap_bytes);
             std::uint64_t* bar = &bars[warp][slot];
             fence_proxy_async();
-            mbar_expect_tx(bar, CELL + PANEL + nb);
-            bulk_g2s(dst, p.cells + static_cast<std::size_t>(q) * CELL, CELL, bar);
-            if (nb) bulk_g2s(dst + O_ENT, reinterpret_cast<const std::uint8_t*>(p.ent) + a0, nb, bar);
+            mbar_expect_tx(bar, PANEL + nb);
+            bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes + O_REC, p.cells + r0, nb, bar);
         }
     };
     // x operands of panel P (written by the preceding xprep kernel)
     auto issue_x = [&](std::uint32_t P, int slot) {
-        if (lane == 0) {
-            std::uint8_t* dst = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
-            std::uint64_t* bar = &bars[warp][slot];
-            bulk_g2s(dst + O_FRAG, reinterpret_cast<const std::uint8_t*>(p.xfrag) + 512u * P, 512u, bar);
-            bulk_g2s(dst + O_SC, reinterpret_cast<const std::uint8_t*>(p.xsc) + 128u * P, 128u, bar);
-            bulk_g2s(dst + O_XP, reinterpret_cast<const std::uint8_t*>(p.xp) + 1024u * P, 1024u, bar);
-            if constexpr (XLO)
-                bulk_g2s(dst + O_LO, reinterpret_cast<const std::uint8_t*>(p.xlo) + 512u * P, 512u, bar);
-        }
+        if (lane == 0)
+            bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes, p.xpanel + PANEL * P, PANEL,
+                     &bars[warp][slot]);
     };
 
     const std::uint32_t ncell = q1 - q0;
@@ -140,9 +143,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
 #pragma unroll 1
     for (int s = 0; s < NSLOT; ++s)
         if (static_cast<std::uint32_t>(s) < ncell) issue_w(q0 + s, s);
-    pdl_wait();  // xprep has completed: x, partials and y are ours from here on
+    pdl_wait();  // xprep has completed: x panels, partials and y are ours from here on
+    std::uint32_t Gc = q0 / p.Pn, P = q0 - Gc * p.Pn;
     {
-        std::uint32_t Pi = q0 % p.Pn;
+        std::uint32_t Pi = P;
 #pragma unroll 1
         for (int s = 0; s < NSLOT; ++s) {
             if (static_cast<std::uint32_t>(s) < ncell) issue_x(Pi, s);
@@ -150,23 +154,25 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         }
     }
 
-    float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // [unit] = rows (g, g+8)
-    float oacc = 0.f;  // outliers of local row `lane`
-    std::uint32_t Gc = q0 / p.Pn, P = q0 - Gc * p.Pn;
+    float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
+#pragma unroll
+    for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
     const std::uint32_t Gq0 = Gc;
+    const std::uint32_t magic = 0x4B000000u;
+    float orow_reg = 0.f;  // outlier sum of local row `lane` (current row-group pair)
 
     auto flush = [&](std::uint32_t Gf, bool whole) {
         float v[2][2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            float a = acc[u].x, b = acc[u].y;
-            a += __shfl_xor_sync(0xffffffffu, a, 1);
-            b += __shfl_xor_sync(0xffffffffu, b, 1);
-            a += __shfl_xor_sync(0xffffffffu, a, 2);
-            b += __shfl_xor_sync(0xffffffffu, b, 2);
-            v[u][0] = a;
-            v[u][1] = b;
-        }
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                float a = acc[u][r].x + acc[u][r].y;
+                a += __shfl_xor_sync(0xffffffffu, a, 1);
+                a += __shfl_xor_sync(0xffffffffu, a, 2);
+                v[u][r] = a;
+                acc[u][r] = make_float2(0.f, 0.f);
+            }
         // lane R owns local row R = 16u + 8rho + gg; the value sits in lane 4gg
         const int R = lane, u = R >> 4, rho = (R >> 3) & 1, gg = R & 7;
         float mine = 0.f;
@@ -177,9 +183,8 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                 const float o = __shfl_sync(0xffffffffu, v[uu][rr], gg * 4);
                 if (uu == u && rr == rho) mine = o;
             }
-        mine += oacc;
-        oacc = 0.f;
-        acc[0] = acc[1] = make_float2(0.f, 0.f);
+        mine += orow_reg;
+        orow_reg = 0.f;
         const std::uint32_t row = 32u * Gf + R;
         if (whole) {
             if (row < p.m) p.y[row] = mine;
@@ -214,17 +219,18 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         const std::uint32_t phase = (it / NSLOT) & 1u;
 
         mbar_wait(&bars[warp][slot], phase);
-        const std::uint8_t* cell = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
-        const std::uint32_t e0 = slot_e[warp][slot][0], e1 = slot_e[warp][slot][1];
+        const std::uint8_t* sl = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
+        const std::uint8_t* cell = sl + O_REC;
+        const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
 
         // x operands of this panel (shared by both units)
         uint2 xf[2], xl[2];
-        float4 xs[2];
+        float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            xf[h] = reinterpret_cast<const uint2*>(cell + O_FRAG)[(8 * h + g) * 4 + t];
-            if constexpr (XLO) xl[h] = reinterpret_cast<const uint2*>(cell + O_LO)[(8 * h + g) * 4 + t];
-            xs[h] = reinterpret_cast<const float4*>(cell + O_SC)[4 * h + t];
+            xf[h] = reinterpret_cast<const uint2*>(sl + O_FRAG)[(8 * h + g) * 4 + t];
+            if constexpr (XLO) xl[h] = reinterpret_cast<const uint2*>(sl + O_LO)[(8 * h + g) * 4 + t];
+            xs[h] = reinterpret_cast<const float4*>(sl + O_SC)[4 * h + t];
         }
 
         // lane data of both units
@@ -275,78 +281,87 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                     if constexpr (XLO) mma16816(c[u], a, l0, l1);
                 }
             }
-            // epilogue: lane holds D(row g+8rho, block 8h+2t+bs) in c[u][2rho+bs]
+            // epilogue: lane holds D(row g+8rho, block 8h+2t+bs) in c[u][2rho+bs];
+            // everything is paired over bs = (block 2t, block 2t+1)
+            const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
 #pragma unroll
-            for (int bs = 0; bs < 2; ++bs) {
-                const float scb = bs ? xs[h].z : xs[h].x, xxb = bs ? xs[h].w : xs[h].y;
-                const int e0i = 4 * h + 2 * bs;  // entries eps = e0i + rho
+            for (int u = 0; u < 2; ++u) {
+                const uint4 s4 = sc[u][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
+                const float2 Ss = make_float2(h2f_bits(s4.x & 0xffffu), h2f_bits(s4.z & 0xffffu));
+                const float2 Zs = make_float2(h2f_bits(s4.x >> 16), h2f_bits(s4.z >> 16));
+                const float2 Sz = make_float2(h2f_bits(s4.y & 0xffffu), h2f_bits(s4.w & 0xffffu));
+                const float2 Zz = make_float2(-h2f_bits(s4.y >> 16), -h2f_bits(s4.w >> 16));
+                const float2 A1 = fmul2(Ss, SC);                             // s_s * 2^(24-e)
+                const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));      // -s_s z_s 2^(24-e)
+                const float2 B0 = fmul2(Sz, Zz);                             // -z_s z_z
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const std::uint32_t w01 = bs ? sc[u][h].z : sc[u][h].x;  // scale_s | scale_z
-                    const std::uint32_t w23 = bs ? sc[u][h].w : sc[u][h].y;  // zero_s  | zero_z
-                    const float2 S = __half22float2(*reinterpret_cast<const __half2*>(&w01));
-                    const float2 Z = __half22float2(*reinterpret_cast<const __half2*>(&w23));
-                    const float A1 = S.x * scb, A0 = -A1 * S.y, B0 = -Z.x * Z.y;
-                    constexpr std::uint32_t SM = (1u << BS) - 1u, ZM = (1u << BZ) - 1u;
-                    const float2 cs = fadd2(make_float2(magic_code((ss[u] >> (e0i * BS)) & SM),
-                                                        magic_code((ss[u] >> ((e0i + 1) * BS)) & SM)),
+                for (int rho = 0; rho < 2; ++rho) {
+                    const int e0i = 4 * h + rho, e1i = 4 * h + 2 + rho;  // eps of (bs=0, bs=1)
+                    const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss[u], e0i * BS, magic),
+                                                        magic_field_rt<SMASK>(ss[u], e1i * BS, magic)),
                                             make_float2(-kMagic, -kMagic));
-                    const float2 cz = fadd2(make_float2(magic_code((zz[u] >> (e0i * BZ)) & ZM),
-                                                        magic_code((zz[u] >> ((e0i + 1) * BZ)) & ZM)),
+                    const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz[u], e0i * BZ, magic),
+                                                        magic_field_rt<ZMASK>(zz[u], e1i * BZ, magic)),
                                             make_float2(-kMagic, -kMagic));
-                    const float2 shat = ffma2(make_float2(A1, A1), cs, make_float2(A0, A0));
-                    const float2 zhat = ffma2(make_float2(Z.x, Z.x), cz, make_float2(B0, B0));
-                    const float2 tt = ffma2(zhat, make_float2(xxb, xxb), make_float2(c[u][bs], c[u][2 + bs]));
-                    acc[u] = ffma2(shat, tt, acc[u]);
+                    const float2 shat = ffma2(A1, cs, A0);
+                    const float2 zhat = ffma2(Sz, cz, B0);
+                    const float2 tt = ffma2(zhat, XX, make_float2(c[u][2 * rho], c[u][2 * rho + 1]));
+                    acc[u][rho] = ffma2(shat, tt, acc[u][rho]);
                 }
             }
         }
 
-        // outliers: lane R accumulates the entries of local row R (column order)
-        const std::uint32_t cnt = e1 - e0;
+        // outliers: entries (row, col, value) of this cell, sorted by (row, col),
+        // 0xffffffff padding.  Row counts (integer smem atomics, order-free) ->
+        // exclusive scan -> lane R sums the entries of local row R in column
+        // order: deterministic by construction.
+        const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
         if (cnt) {
-            const std::uint32_t lead = e0 * 4u - ((e0 * 4u) & ~15u);
-            const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + O_ENT + lead);
-            const std::uint32_t got = min(((e1 * 4u + 15u) & ~15u) - (e0 * 4u - lead), p.ent_cap_bytes);
-            const std::uint32_t in_smem = got > lead ? (got - lead) / 4u : 0u;
-            const float* xpanel = reinterpret_cast<const float*>(cell + O_XP);
+            const std::uint32_t in_smem = (min(r1 - r0, p.rec_cap_bytes) - CELL) / 4u;
+            const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+            const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+            auto x_at = [&](std::uint32_t col) -> float {
+                if constexpr (XLO)
+                    return reinterpret_cast<const float*>(sl + O_XP)[col];
+                else
+                    return __half2float(reinterpret_cast<const __half*>(sl + O_XP)[col]);
+            };
             auto merge = [&](auto entry) {
-                heads[warp][lane] = cnt;
+                hist[warp][lane] = 0u;
                 __syncwarp();
-                int last = -1;
 #pragma unroll 1
                 for (std::uint32_t base = 0; base < cnt; base += 32) {
                     const std::uint32_t i = base + lane;
-                    const int r = i < cnt ? static_cast<int>(entry(i) >> 24) : 64;
-                    int rp = __shfl_up_sync(0xffffffffu, r, 1);
-                    if (lane == 0) rp = last;
-                    if (i < cnt && r != rp) heads[warp][r] = i;
-                    last = __shfl_sync(0xffffffffu, r, 31);
+                    if (i < cnt) {
+                        const std::uint32_t r = entry(i) >> 24;
+                        if (r < 32u) atomicAdd(&hist[warp][r], 1u);
+                    }
                 }
                 __syncwarp();
-                std::uint32_t st = heads[warp][lane];
+                const std::uint32_t c = hist[warp][lane];
+                std::uint32_t s = c;  // inclusive scan over rows
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {  // suffix minimum: first entry with row >= lane
-                    const std::uint32_t o = __shfl_down_sync(0xffffffffu, st, d);
-                    if (lane + d < 32) st = min(st, o);
+                for (int d = 1; d < 32; d <<= 1) {
+                    const std::uint32_t o = __shfl_up_sync(0xffffffffu, s, d);
+                    if (lane >= d) s += o;
                 }
-                std::uint32_t en = __shfl_down_sync(0xffffffffu, st, 1);
-                if (lane == 31) en = cnt;
-                std::uint32_t i = st;
-                for (; i + 1 < en; i += 2) {
+                std::uint32_t i = s - c;
+                float o = orow_reg;
+                for (; i + 1 < s; i += 2) {
                     const std::uint32_t ea = entry(i), eb = entry(i + 1);
-                    oacc = fmaf(h2f_bits(ea & 0xffffu), xpanel[(ea >> 16) & 255u], oacc);
-                    oacc = fmaf(h2f_bits(eb & 0xffffu), xpanel[(eb >> 16) & 255u], oacc);
+                    o = fmaf(h2f_bits(ea & 0xffffu), x_at((ea >> 16) & 255u), o);
+                    o = fmaf(h2f_bits(eb & 0xffffu), x_at((eb >> 16) & 255u), o);
                 }
-                if (i < en) {
+                if (i < s) {
                     const std::uint32_t ea = entry(i);
-                    oacc = fmaf(h2f_bits(ea & 0xffffu), xpanel[(ea >> 16) & 255u], oacc);
+                    o = fmaf(h2f_bits(ea & 0xffffu), x_at((ea >> 16) & 255u), o);
                 }
+                orow_reg = o;
             };
             if (cnt <= in_smem)
                 merge([&](std::uint32_t i) { return es[i]; });
             else
-                merge([&](std::uint32_t i) { return i < in_smem ? es[i] : __ldg(p.ent + e0 + i); });
+                merge([&](std::uint32_t i) { return i < in_smem ? es[i] : __ldg(eg + i); });
         }
 
         __syncwarp();

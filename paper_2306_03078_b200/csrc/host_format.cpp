@@ -745,10 +745,10 @@ int spqr_debug_tiled_host(const uint8_t* stream, size_t nbytes, uint32_t* dims4,
             spqr::fail(spqr::Errc::config_invalid, "layer is outside the tiled fast-path geometry");
         const spqr::detail::TiledHost t = spqr::detail::transcode_to_tiled(v, 0);
         dims4[0] = t.Gn; dims4[1] = t.Pn; dims4[2] = t.cell_bytes;
-        dims4[3] = static_cast<std::uint32_t>(t.entries.size());
+        dims4[3] = static_cast<std::uint32_t>(t.cells.size());
         if (cells) std::memcpy(cells, t.cells.data(), t.cells.size());
         if (cell_off) std::memcpy(cell_off, t.cell_off.data(), 4 * t.cell_off.size());
-        if (entries && !t.entries.empty()) std::memcpy(entries, t.entries.data(), 4 * t.entries.size());
+        (void)entries;
     });
 }
 

@@ -63,10 +63,9 @@ void pack_bits(const std::uint8_t* src, std::size_t count, int bits, std::vector
 struct TiledHost {
     std::uint32_t Gn = 0, Pn = 0;       // cell grid
     std::uint32_t cell_bytes = 0;
-    std::vector<std::uint8_t> prefix;   // stream header + permutation section
-    std::vector<std::uint8_t> cells;    // Gn*Pn*cell_bytes
-    std::vector<std::uint32_t> cell_off;  // Gn*Pn+1
-    std::vector<std::uint32_t> entries;   // nnz
+    std::vector<std::uint8_t> prefix;     // stream header + permutation section
+    std::vector<std::uint8_t> cells;      // cell records: cell_bytes + entries (16-B padded)
+    std::vector<std::uint32_t> cell_off;  // byte offset of record q, Gn*Pn+1 entries
 };
 bool tiled_supported(const StreamView& v);
 TiledHost transcode_to_tiled(const StreamView& v, int threads);

@@ -82,22 +82,18 @@ __device__ __forceinline__ float h2f_bits(std::uint32_t h16) {
 
 // ============================================================ tiled path ====
 struct TiledParams {
-    const std::uint8_t* cells;
-    const std::uint32_t* cell_off;
-    const std::uint32_t* ent;
-    const std::uint32_t* warp_start;  // [nwarps+1]
-    const std::uint32_t* wfirst;      // [Gn]
-    const std::uint32_t* wlast;       // [Gn]
+    const std::uint8_t* cells;        // cell records (cell bytes + outlier entries, 16-B padded)
+    const std::uint32_t* cell_off;    // [ncell+1] byte offset of each record
+    const std::uint32_t* warp_start;  // [nwarps+1] first cell of each warp
+    const std::uint32_t* wfirst;      // [Gn] first warp touching row-group pair G
+    const std::uint32_t* wlast;       // [Gn] last warp touching G
     const std::uint32_t* wcnt;        // [Gn] warps with a non-empty range touching G
-    const uint2* xfrag;               // [nblk_pad*4] per batch
-    const uint2* xlo;                 // same (fp32 inputs)
-    const float4* xsc;                // [nblk_pad/2] per batch: {SC,XX} x 2 blocks
-    const float* xp;                  // [n_pad] per batch, solve order
-    float* y;                         // [m] per batch
+    const std::uint8_t* xpanel;       // [Pn] x panels of this batch column (xprep_tiled)
+    float* y;                         // [m] this batch column
     float* partial;                   // [nwarps*2*32]
-    std::uint32_t* counters;          // [Gn]
+    std::uint32_t* counters;          // [Gn], zero between launches
     std::uint32_t m, Pn, Gn, nwarps;
-    std::uint32_t ent_cap_bytes;      // per slot
+    std::uint32_t rec_cap_bytes;      // record bytes a slot holds (outliers beyond: LDG)
     std::uint32_t slot_bytes;
 };
 
@@ -149,14 +145,26 @@ __device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int 
 #include "gemv_tiled.cuh"
 
 // x preparation for the tiled path: one thread per (16-column block, batch).
+// Writes the panel layout the GEMV stages per cell (tiled.hpp panel_bytes):
+//   [B fragments 16 x 32 B][{SC(2i), SC(2i+1), XX(2i), XX(2i+1)} x 8]
+//   [x in solve order: 256 x f16 (fp16 input) or f32 (fp32 input)]
+//   [low-half B fragments 16 x 32 B (fp32 input only)]
+// B fragments hold fp16(x * 2^(e - p)) for the lane order of the m16n8k16 B
+// operand (columns 2t, 2t+1, 2t+8, 2t+9), e = per-block power-of-two scale
+// (max |x| in [2^14, 2^15)), p = the column's code pre-scale (tiled.hpp).
 template <int BW, bool XLO>
 __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t n_pad,
-                            std::uint32_t batch, const std::uint32_t* __restrict__ order, uint2* xfrag,
-                            uint2* xlo, float2* xsc, float* xp) {
+                            std::uint32_t batch, const std::uint32_t* __restrict__ order,
+                            std::uint8_t* __restrict__ panels) {
+    constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
+    constexpr std::uint32_t O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
+    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
     const std::uint32_t nblk = n_pad / 16;
     const std::uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < nblk * batch) {
         const std::uint32_t b = idx / nblk, k = idx - b * nblk;
+        std::uint8_t* pan = panels + (static_cast<std::size_t>(b) * (nblk / 16) + k / 16) * PANEL;
+        const std::uint32_t kk = k % 16;
         float v[16];
         float mx = 0.f;
 #pragma unroll
@@ -170,7 +178,15 @@ __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t
             }
             v[cc] = val;
             mx = fmaxf(mx, fabsf(val));
-            xp[static_cast<std::size_t>(b) * n_pad + col] = val;
+        }
+        if constexpr (XLO) {
+            float4* xo = reinterpret_cast<float4*>(pan + O_XP + 64u * kk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xo[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+            __half2* xo = reinterpret_cast<__half2*>(pan + O_XP + 32u * kk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xo[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
         }
         int e = 0;
         if (mx > 0.f && mx < INFINITY) {
@@ -192,9 +208,8 @@ __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t
             }
             X += ldexpf(eff, pp);
         }
-        // fragment order per t: columns 2t, 2t+1, 2t+8, 2t+9
-        uint2* fr = xfrag + (static_cast<std::size_t>(b) * nblk + k) * 4;
-        uint2* fl = XLO ? xlo + (static_cast<std::size_t>(b) * nblk + k) * 4 : nullptr;
+        uint2* fr = reinterpret_cast<uint2*>(pan + 32u * kk);
+        uint2* fl = reinterpret_cast<uint2*>(pan + O_LO + 32u * kk);
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
             const int c0 = 2 * tt;
@@ -213,7 +228,9 @@ __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t
                 fl[tt] = l;
             }
         }
-        xsc[static_cast<std::size_t>(b) * nblk + k] = make_float2(ldexpf(1.0f, 24 - e), -X * 5.9604644775390625e-08f);
+        float* scp = reinterpret_cast<float*>(pan + O_SC + 16u * (kk / 2));
+        scp[kk & 1] = ldexpf(1.0f, 24 - e);
+        scp[2 + (kk & 1)] = -X * 5.9604644775390625e-08f;
     }
     pdl_launch();
 }

@@ -184,8 +184,33 @@ TiledHost transcode_to_tiled(const StreamView& v, int threads) {
     t.cell_bytes = T::cell_bytes(v.wb, v.sb, v.zb);
     t.prefix.assign(v.base, v.base + v.rec_off);
     const std::size_t ncell = static_cast<std::size_t>(t.Gn) * t.Pn;
-    t.cells.assign(ncell * t.cell_bytes, 0);
     const std::uint32_t ub = T::unit_bytes(v.wb, v.sb, v.zb);
+
+    // outliers per cell -> record sizes: cell bytes + entries padded to 16 B
+    std::vector<std::uint32_t> cnt(ncell, 0);
+    for (std::uint32_t r = 0; r < v.rows; ++r)
+        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i)
+            cnt[static_cast<std::size_t>(r / 32) * t.Pn + v.ent_col(i) / 256]++;
+    t.cell_off.assign(ncell + 1, 0);
+    std::uint64_t total = 0;
+    for (std::size_t q = 0; q < ncell; ++q) {
+        t.cell_off[q] = static_cast<std::uint32_t>(total);
+        total += t.cell_bytes + 16ull * ((cnt[q] + 3) / 4);
+        if (total > 0xfffffff0ull) fail(Errc::config_invalid, "layer too large for 32-bit record offsets");
+    }
+    t.cell_off[ncell] = static_cast<std::uint32_t>(total);
+    t.cells.assign(total, 0xff);  // entry padding = 0xffffffff sentinels (row 255)
+    // entries in (row, col) order within each cell
+    std::vector<std::uint32_t> cursor(ncell);
+    for (std::size_t q = 0; q < ncell; ++q) cursor[q] = t.cell_off[q] + t.cell_bytes;
+    for (std::uint32_t r = 0; r < v.rows; ++r)  // rows ascending, cols ascending -> order kept
+        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i) {
+            const std::uint32_t c = v.ent_col(i);
+            const std::size_t q = static_cast<std::size_t>(r / 32) * t.Pn + c / 256;
+            const std::uint32_t e = T::pack_entry(r % 32, c % 256, v.ent_val(i));
+            std::memcpy(t.cells.data() + cursor[q], &e, 4);
+            cursor[q] += 4;
+        }
 
     parallel_for(t.Gn, threads, [&](std::uint32_t G) {
         UnitStage u;
@@ -199,25 +224,10 @@ TiledHost transcode_to_tiled(const StreamView& v, int threads) {
                         if (k < v.nblocks) load_record(v, k, gg, blk, u);
                     }
                 pack_unit(u, v.wb, v.sb, v.zb,
-                          t.cells.data() + (static_cast<std::size_t>(G) * t.Pn + P) * t.cell_bytes + rg * ub);
+                          t.cells.data() + t.cell_off[static_cast<std::size_t>(G) * t.Pn + P] + rg * ub);
             }
         }
     });
-
-    // outliers, re-bucketed per cell in (cell, row, col) order
-    t.cell_off.assign(ncell + 1, 0);
-    for (std::uint32_t r = 0; r < v.rows; ++r)
-        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i)
-            t.cell_off[static_cast<std::size_t>(r / 32) * t.Pn + v.ent_col(i) / 256 + 1]++;
-    for (std::size_t q = 0; q < ncell; ++q) t.cell_off[q + 1] += t.cell_off[q];
-    t.entries.assign(v.nnz, 0);
-    std::vector<std::uint32_t> cursor(t.cell_off.begin(), t.cell_off.end() - 1);
-    for (std::uint32_t r = 0; r < v.rows; ++r)  // rows ascending, cols ascending -> order kept
-        for (std::uint32_t i = v.row_start(r); i < v.row_start(r + 1); ++i) {
-            const std::uint32_t c = v.ent_col(i);
-            const std::size_t q = static_cast<std::size_t>(r / 32) * t.Pn + c / 256;
-            t.entries[cursor[q]++] = T::pack_entry(r % 32, c % 256, v.ent_val(i));
-        }
     return t;
 }
 
@@ -235,7 +245,7 @@ std::vector<std::uint8_t> tiled_to_stream(const StreamView& hdr, const TiledHost
             for (int rg = 0; rg < 2; ++rg) {
                 const std::uint32_t gg = 2 * G + rg;
                 if (gg >= v.ngroups) continue;
-                unpack_unit(t.cells.data() + (static_cast<std::size_t>(G) * t.Pn + P) * t.cell_bytes + rg * ub,
+                unpack_unit(t.cells.data() + t.cell_off[static_cast<std::size_t>(G) * t.Pn + P] + rg * ub,
                             v.wb, v.sb, v.zb, u);
                 const std::uint32_t gr = v.group_rows(gg);
                 for (int blk = 0; blk < 16; ++blk) {
@@ -259,14 +269,15 @@ std::vector<std::uint8_t> tiled_to_stream(const StreamView& hdr, const TiledHost
     // CSR: per row, walk the row's cells left to right
     std::vector<std::uint32_t> rs(v.rows + 1, 0);
     std::vector<std::uint8_t> ent;
-    ent.reserve(4ull * t.entries.size());
+    ent.reserve(4ull * v.nnz);
     for (std::uint32_t r = 0; r < v.rows; ++r) {
         const std::uint32_t G = r / 32, lr = r % 32;
         for (std::uint32_t P = 0; P < t.Pn; ++P) {
             const std::size_t q = static_cast<std::size_t>(G) * t.Pn + P;
-            for (std::uint32_t i = t.cell_off[q]; i < t.cell_off[q + 1]; ++i) {
-                const std::uint32_t e = t.entries[i];
-                if ((e >> 24) != lr) continue;
+            for (std::uint32_t b = t.cell_off[q] + t.cell_bytes; b < t.cell_off[q + 1]; b += 4) {
+                std::uint32_t e;
+                std::memcpy(&e, t.cells.data() + b, 4);
+                if ((e >> 24) != lr) continue;  // other row, or 0xffffffff padding
                 const std::uint16_t col = static_cast<std::uint16_t>(256 * P + ((e >> 16) & 255u));
                 ent.push_back(static_cast<std::uint8_t>(col));
                 ent.push_back(static_cast<std::uint8_t>(col >> 8));

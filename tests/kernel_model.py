@@ -53,7 +53,7 @@ def extract_codes(stream: bytes):
     cells = t["cells"]
     for G in range(Gn):
         for Pp in range(Pn):
-            base = (G * Pn + Pp) * cb
+            base = int(t["cell_off"][G * Pn + Pp])
             for u in range(2):
                 ub = base + u * unit
                 for lane in range(32):
