@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libspqr_b200.so")
+LIB_PATH = os.environ.get("SPQR_LIB") or os.path.join(PKG, "libspqr_b200.so")
 
 ERRC = [
     "malformed_header", "shape_mismatch", "non_finite_value", "io_failure", "parse_error",

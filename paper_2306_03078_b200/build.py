@@ -56,8 +56,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in cpp + cu + hdr)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile the library.  `out`/`defines` build an experimental variant
+    (e.g. -DSPQR_MAX_NW=16) next to the default one; the loader picks it up
+    through $SPQR_LIB."""
+    lib_path = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     cpp, cu, _ = _sources()
@@ -71,7 +76,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     for src in cu:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         extra = ["-Xptxas", "-v"] if ptxas_info else []
-        cmd = [NVCC, *NVFLAGS, *extra, "-c", src, "-o", obj]
+        cmd = [NVCC, *NVFLAGS, *extra, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     failed = False
@@ -87,8 +92,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
                 print(out + err)
     if failed:
         raise RuntimeError("compilation failed")
-    _run([NVCC, *GENCODE, "-shared", "-o", LIB, *objs, "-lpthread"], verbose)
-    return LIB
+    _run([NVCC, *GENCODE, "-shared", "-o", lib_path, *objs, "-lpthread"], verbose)
+    return lib_path
 
 
 if __name__ == "__main__":
@@ -96,5 +101,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas-info", action="store_true")
+    ap.add_argument("--out")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose, ptxas_info=a.ptxas_info))
+    print(build(force=a.force, verbose=a.verbose, ptxas_info=a.ptxas_info, out=a.out, defines=tuple(a.defines)))

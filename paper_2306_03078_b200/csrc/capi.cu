@@ -25,7 +25,6 @@ namespace T = spqr_tiled;
 
 namespace {
 
-constexpr int kNW = 16;                       // consumer warps per CTA (one CTA per SM)
 constexpr std::uint32_t kSmemLimit = 232448;  // 227 KB per CTA on sm_100
 constexpr std::uint32_t kStaticSmem = 4096;   // mbarriers, slot offsets, row heads
 constexpr std::uint32_t kMaxEntCap = 2048;    // outlier bytes staged per cell (rest: LDG)
@@ -35,12 +34,22 @@ constexpr std::uint32_t kMaxEntCap = 2048;    // outlier bytes staged per cell (
 constexpr std::uint32_t slot_base(int bw, int bsz, bool xlo) {
     return spqr_tiled::cell_bytes(bw, bsz, bsz) + spqr_tiled::panel_bytes(xlo);
 }
+// consumer warps per CTA (one CTA per SM): as many as fit two slots each with
+// >= 512 B of staged outliers -- latency is hidden by warps, not deep rings
+#ifndef SPQR_MAX_NW
+#define SPQR_MAX_NW 16
+#endif
+constexpr int kMaxNW = SPQR_MAX_NW;
+constexpr int nw_for(int bw, int bsz, bool xlo) {
+    return kMaxNW * 2 * (slot_base(bw, bsz, xlo) + 512) + kStaticSmem <= kSmemLimit ? kMaxNW : 16;
+}
 // ring depth per warp: 3 slots when they fit with >= 1 KB of entries, else 2
 constexpr int nslot_for(int bw, int bsz, bool xlo) {
-    return kNW * 3 * (slot_base(bw, bsz, xlo) + 1024) + kStaticSmem <= kSmemLimit ? 3 : 2;
+    return nw_for(bw, bsz, xlo) * 3 * (slot_base(bw, bsz, xlo) + 1024) + kStaticSmem <= kSmemLimit ? 3 : 2;
 }
 constexpr std::uint32_t slot_bytes_for(int bw, int bsz, bool xlo) {
-    const std::uint32_t avail = ((kSmemLimit - kStaticSmem) / (kNW * nslot_for(bw, bsz, xlo))) & ~127u;
+    const std::uint32_t avail =
+        ((kSmemLimit - kStaticSmem) / (nw_for(bw, bsz, xlo) * nslot_for(bw, bsz, xlo))) & ~127u;
     const std::uint32_t want = (slot_base(bw, bsz, xlo) + kMaxEntCap + 127u) & ~127u;
     return want < avail ? want : avail;
 }
@@ -48,6 +57,7 @@ constexpr std::uint32_t rec_cap_for(int bw, int bsz, bool xlo) {  // record byte
     return slot_bytes_for(bw, bsz, xlo) - spqr_tiled::panel_bytes(xlo);
 }
 static_assert(rec_cap_for(4, 4, true) >= spqr_tiled::cell_bytes(4, 4, 4), "slot must hold a cell");
+static_assert(nw_for(3, 3, false) <= kMaxNW && nw_for(3, 3, true) <= kMaxNW, "warp count");
 
 thread_local int g_launches = 0;
 
@@ -94,10 +104,12 @@ struct spqr_layer {
     bool fast = false;
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
-    std::uint32_t* d_warp_start = nullptr;
-    std::uint32_t* d_wfirst = nullptr;
+    std::uint32_t* d_warp_start[2] = {nullptr, nullptr};  // per x dtype (f16, f32): warp count differs
+    std::uint32_t* d_wfirst[2] = {nullptr, nullptr};
     std::uint32_t* d_wlast = nullptr;
-    std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, nwarps = 0, grid = 0, n_pad = 0;
+    std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, grid = 0, n_pad = 0;
+    std::uint32_t nwarps[2] = {0, 0};
+    std::uint32_t partial_slots[2] = {0, 0};
     // own workspace
     mutable std::mutex mu;
     mutable void* d_ws = nullptr;
@@ -108,8 +120,9 @@ struct spqr_layer {
 
     ~spqr_layer() {
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
-                        static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start),
-                        static_cast<void*>(d_wfirst), static_cast<void*>(d_wlast), d_ws,
+                        static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start[0]),
+                        static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
+                        static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws,
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
     }
@@ -143,7 +156,7 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
         // x panels sized for the fp32-input layout (the larger of the two)
         w.panel_stride = static_cast<std::uint64_t>(L->Pn) * spqr_tiled::panel_bytes(true);
         w.panels = o; o += al(b * w.panel_stride);
-        w.partial = o; o += al(static_cast<std::uint64_t>(L->nwarps) * 2 * 32 * 4);
+        w.partial = o; o += al(static_cast<std::uint64_t>(std::max(L->partial_slots[0], L->partial_slots[1])) * 32 * 4);
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
         w.xp = o; o += al(b * L->info.cols * 4);
@@ -154,7 +167,8 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
 
 template <int BW, int BSZ, bool XLO>
 void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::size_t smem, cudaStream_t st) {
-    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, kNW, nslot_for(BW, BSZ, XLO)>;
+    constexpr int NW = nw_for(BW, BSZ, XLO);
+    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, NW, nslot_for(BW, BSZ, XLO)>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -165,7 +179,7 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kNW * 32);
+    cfg.blockDim = dim3(NW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -209,7 +223,7 @@ std::size_t tiled_smem(const spqr_layer* L, bool xlo, std::uint32_t* slot_bytes,
     const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
     *slot_bytes = slot_bytes_for(bw, bsz, xlo);
     *rec_cap = rec_cap_for(bw, bsz, xlo);
-    return static_cast<std::size_t>(kNW) * nslot_for(bw, bsz, xlo) * *slot_bytes;
+    return static_cast<std::size_t>(nw_for(bw, bsz, xlo)) * nslot_for(bw, bsz, xlo) * *slot_bytes;
 }
 
 void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xlo, std::size_t smem,
@@ -248,15 +262,15 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
             spqr_dev::TiledParams p{};
             p.cells = L->d_cells;
             p.cell_off = L->d_cell_off;
-            p.warp_start = L->d_warp_start;
-            p.wfirst = L->d_wfirst;
-            p.wlast = L->d_wfirst + L->Gn;
-            p.wcnt = L->d_wfirst + 2 * L->Gn;
+            const int xi = f16 ? 0 : 1;
+            p.warp_start = L->d_warp_start[xi];
+            p.gmap = L->d_wfirst[xi];
+            p.wmap = L->d_wfirst[xi] + 2 * L->Gn;
             p.xpanel = panels + b * w.panel_stride;
             p.y = y + static_cast<std::size_t>(b) * L->info.rows;
             p.partial = reinterpret_cast<float*>(base + w.partial);
             p.counters = reinterpret_cast<std::uint32_t*>(base + w.counters);
-            p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps;
+            p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps[xi];
             p.rec_cap_bytes = rec_cap; p.slot_bytes = slot_bytes;
             dispatch_tiled(p, L, !f16, smem, st);
         }
@@ -295,41 +309,53 @@ void ensure_own_ws(const spqr_layer* L, int batch) {
 
 // Static split of the cell sequence over all warps, balanced by bytes
 // (dense cell bytes + a per-outlier instruction cost in byte units).
-void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms) {
+void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) {
     const std::uint32_t Q = t.Gn * t.Pn;
     L->grid = static_cast<std::uint32_t>(sms);
-    L->nwarps = L->grid * kNW;
+    const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
+    const std::uint32_t nw = static_cast<std::uint32_t>(nw_for(bw, bsz, xi == 1));
+    std::uint32_t& nwarps = L->nwarps[xi];
+    nwarps = L->grid * nw;
     std::vector<double> pre(Q + 1, 0.0);
     for (std::uint32_t q = 0; q < Q; ++q)
         pre[q + 1] = pre[q] + 1024.0 + (t.cell_off[q + 1] - t.cell_off[q]);  // x panel + record
     const double total = pre[Q];
-    std::vector<std::uint32_t> ws(L->nwarps + 1, Q);
+    std::vector<std::uint32_t> ws(nwarps + 1, Q);
     std::uint32_t q = 0;
-    for (std::uint32_t k = 0; k < L->nwarps; ++k) {
-        const double target = total * k / L->nwarps;
+    for (std::uint32_t k = 0; k < nwarps; ++k) {
+        const double target = total * k / nwarps;
         while (q < Q && pre[q] + 0.5 * (pre[q + 1] - pre[q]) < target) ++q;
         ws[k] = q;
     }
-    ws[L->nwarps] = Q;
-    // per row-group pair: first / last contributing warp and how many warps
-    // (with a non-empty range) contribute -- the finaliser's expected count
-    std::vector<std::uint32_t> wfl(3ull * t.Gn, 0);
-    std::uint32_t* wf = wfl.data();
-    std::uint32_t* wl = wf + t.Gn;
-    std::uint32_t* wc = wl + t.Gn;
-    std::fill(wf, wf + t.Gn, UINT32_MAX);
-    for (std::uint32_t k = 0; k < L->nwarps; ++k) {
+    ws[nwarps] = Q;
+    // Row-group pairs split between warps are reduced through partial slots:
+    // G's contributors (warps whose range touches G, in warp order) get slots
+    // pbase[G] + 0 .. count-1; each warp records its ordinal in its first and
+    // last G.  gmap[G] = {pbase, count}; wmap[k] = {ord_first, ord_last}.
+    std::vector<std::uint32_t> gmap(2ull * t.Gn, 0), wmap(2ull * nwarps, 0);
+    for (std::uint32_t k = 0; k < nwarps; ++k) {
         if (ws[k] >= ws[k + 1]) continue;
-        for (std::uint32_t G = ws[k] / t.Pn; G <= (ws[k + 1] - 1) / t.Pn; ++G) {
-            wf[G] = std::min(wf[G], k);
-            wl[G] = std::max(wl[G], k);
-            wc[G] += 1;
+        const std::uint32_t ga = ws[k] / t.Pn, gb = (ws[k + 1] - 1) / t.Pn;
+        wmap[2 * k] = gmap[2 * ga + 1]++;
+        if (gb != ga) {
+            for (std::uint32_t G = ga + 1; G < gb; ++G) gmap[2 * G + 1]++;  // fully covered: 1 contributor
+            wmap[2 * k + 1] = gmap[2 * gb + 1]++;
+        } else {
+            wmap[2 * k + 1] = wmap[2 * k];
         }
     }
-    L->d_warp_start = dalloc<std::uint32_t>(ws.size());
-    L->d_wfirst = dalloc<std::uint32_t>(wfl.size());
-    ck(cudaMemcpy(L->d_warp_start, ws.data(), 4 * ws.size(), cudaMemcpyHostToDevice), "H2D warp_start");
-    ck(cudaMemcpy(L->d_wfirst, wfl.data(), 4 * wfl.size(), cudaMemcpyHostToDevice), "H2D warp map");
+    std::uint32_t slots = 0;
+    for (std::uint32_t G = 0; G < t.Gn; ++G) {
+        gmap[2 * G] = slots;
+        slots += gmap[2 * G + 1];
+    }
+    L->partial_slots[xi] = slots;
+    L->d_warp_start[xi] = dalloc<std::uint32_t>(ws.size());
+    L->d_wfirst[xi] = dalloc<std::uint32_t>(gmap.size() + wmap.size());
+    ck(cudaMemcpy(L->d_warp_start[xi], ws.data(), 4 * ws.size(), cudaMemcpyHostToDevice), "H2D warp_start");
+    ck(cudaMemcpy(L->d_wfirst[xi], gmap.data(), 4 * gmap.size(), cudaMemcpyHostToDevice), "H2D gmap");
+    ck(cudaMemcpy(L->d_wfirst[xi] + gmap.size(), wmap.data(), 4 * wmap.size(), cudaMemcpyHostToDevice),
+       "H2D wmap");
 }
 
 }  // namespace
@@ -392,7 +418,8 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
                "H2D cell_off");
             int sms = 0;
             ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
-            plan_partition(L.get(), t, sms);
+            plan_partition(L.get(), t, sms, 0);
+            plan_partition(L.get(), t, sms, 1);
             dev_bytes += t.cells.size() + 4 * t.cell_off.size();
         }
         L->info.fast_path = L->fast;

@@ -49,13 +49,29 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
     return d;
 }
 
-// ((w >> shift) & M) | 2^23-pattern: the code as the float 2^23 + code, with
-// SHF + ONE LOP3 (the exponent pattern lives in a register: LOP3 takes a
-// single immediate).  `shift` is a compile-time constant after unrolling.
+// The issue-rate budget is set by the ALU pipe (LOP3/SHF/SEL/PRMT issue at
+// half rate per SMSP); the helpers below move what they can to the FMA pipe.
+
+// w >> s as IMAD.HI (FMA pipe) instead of SHF (ALU pipe); s in [1, 31].
+__device__ __forceinline__ std::uint32_t shr_fma(std::uint32_t w, int s) {
+    std::uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(1u << (32 - s)));
+    return r;
+}
+// a * m for m in {0, 1}: the B-fragment lane mask as IMAD (FMA pipe), not SEL.
+__device__ __forceinline__ std::uint32_t mask01(std::uint32_t a, std::uint32_t m) {
+    std::uint32_t r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(m));
+    return r;
+}
+// ((w >> shift) & M) | 2^23-pattern: the code as the float 2^23 + code with
+// ONE LOP3 (the exponent pattern lives in a register: LOP3 takes a single
+// immediate).  `shift` is a compile-time constant after unrolling.
 template <std::uint32_t M>
 __device__ __forceinline__ float magic_field_rt(std::uint32_t w, int shift, std::uint32_t magic) {
     std::uint32_t r;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w >> shift), "n"(M), "r"(magic));
+    const std::uint32_t x = shift ? shr_fma(w, shift) : w;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "n"(M), "r"(magic));
     return __uint_as_float(r);
 }
 
@@ -108,13 +124,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         return;
     }
 
-    // record byte offsets of 32 consecutive cells at a time across the lanes
+    // record byte offsets of 32 consecutive cells at a time across the lanes;
+    // the following window is prefetched one window ahead
     std::uint32_t off_base = q0;
     std::uint32_t off_lane = (q0 + lane <= q1) ? __ldg(p.cell_off + q0 + lane) : 0u;
+    std::uint32_t off_next = (q0 + 32 + lane <= q1) ? __ldg(p.cell_off + q0 + 32 + lane) : 0u;
     auto rec_offset = [&](std::uint32_t q) -> std::uint32_t {  // monotone q, whole warp
         if (q >= off_base + 32) {
-            off_base = q;
-            off_lane = (q + lane <= q1) ? __ldg(p.cell_off + q + lane) : 0u;
+            off_base += 32;
+            off_lane = off_next;
+            off_next = (off_base + 32 + lane <= q1) ? __ldg(p.cell_off + off_base + 32 + lane) : 0u;
         }
         return __shfl_sync(0xffffffffu, off_lane, static_cast<int>(q - off_base));
     };
@@ -126,7 +145,6 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             slot_r[warp][slot][1] = r1;
             const std::uint32_t nb = min(r1 - r0, p.rec_cap_bytes);
             std::uint64_t* bar = &bars[warp][slot];
-            fence_proxy_async();
             mbar_expect_tx(bar, PANEL + nb);
             bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes + O_REC, p.cells + r0, nb, bar);
         }
@@ -159,6 +177,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
     const std::uint32_t Gq0 = Gc;
     const std::uint32_t magic = 0x4B000000u;
+    std::uint32_t sel[8];  // 1 in the lanes whose B column is MMA j's output column
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sel[j] = (g == j) ? 1u : 0u;
     float orow_reg = 0.f;  // outlier sum of local row `lane` (current row-group pair)
 
     auto flush = [&](std::uint32_t Gf, bool whole) {
@@ -190,23 +211,30 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             if (row < p.m) p.y[row] = mine;
             return;
         }
-        const std::uint32_t side = (Gf == Gq0) ? 0u : 1u;
-        p.partial[(wk * 2 + side) * 32 + R] = mine;
-        __threadfence();
+        // split row-group pair: contributor slot = pbase[G] + this warp's ordinal
+        const uint2 gm = __ldg(reinterpret_cast<const uint2*>(p.gmap) + Gf);  // {pbase, count}
+        const std::uint32_t ord = __ldg(p.wmap + 2 * wk + ((Gf == Gq0) ? 0u : 1u));
+        p.partial[(gm.x + ord) * 32 + R] = mine;
         __syncwarp();
         std::uint32_t prev = 0;
-        if (lane == 0) prev = atomicAdd(p.counters + Gf, 1u);
+        if (lane == 0) {  // release our partial, acquire the others'
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.counters + Gf) : "memory");
+        }
         prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == __ldg(p.wcnt + Gf) - 1) {  // last contributor reduces in warp order
-            __threadfence();
+        if (prev == gm.y - 1) {  // last contributor: reduce in contributor (warp) order
+            __syncwarp();
             float sum = 0.f;
-            const std::uint32_t k1 = __ldg(p.wlast + Gf);
-            for (std::uint32_t k = __ldg(p.wfirst + Gf); k <= k1; ++k) {
-                const std::uint32_t s0 = __ldg(p.warp_start + k);
-                if (s0 == __ldg(p.warp_start + k + 1)) continue;  // idle warp
-                const std::uint32_t sk = (s0 / p.Pn == Gf) ? 0u : 1u;
-                sum += __ldcg(p.partial + (k * 2 + sk) * 32 + R);
+            const float* src = p.partial + gm.x * 32 + R;
+            std::uint32_t j = 0;
+            for (; j + 4 <= gm.y; j += 4) {
+                const float a = __ldcg(src + 32 * j), b = __ldcg(src + 32 * (j + 1));
+                const float c = __ldcg(src + 32 * (j + 2)), d = __ldcg(src + 32 * (j + 3));
+                sum += a;
+                sum += b;
+                sum += c;
+                sum += d;
             }
+            for (; j < gm.y; ++j) sum += __ldcg(src + 32 * j);
             if (row < p.m) p.y[row] = sum;
             if (lane == 0) p.counters[Gf] = 0;
         }
@@ -253,21 +281,27 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             sc[u][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
         }
 
+        // 4 independent MMA chains (super-tile h x unit u), interleaved
+        float cc[2][2][4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cc[h][u][i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
                 const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                const bool mine = (g == j);
-                const std::uint32_t b0 = mine ? xf[h].x : 0u, b1 = mine ? xf[h].y : 0u;
+                const std::uint32_t b0 = mask01(xf[h].x, sel[j]), b1 = mask01(xf[h].y, sel[j]);
                 std::uint32_t l0 = 0, l1 = 0;
                 if constexpr (XLO) {
-                    l0 = mine ? xl[h].x : 0u;
-                    l1 = mine ? xl[h].y : 0u;
+                    l0 = mask01(xl[h].x, sel[j]);
+                    l1 = mask01(xl[h].y, sel[j]);
                 }
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {  // two independent MMA chains
+                for (int u = 0; u < 2; ++u) {
                     const std::uint32_t* w = cw[u] + G::CW * cidx;
                     std::uint32_t a[4];
 #pragma unroll
@@ -277,20 +311,25 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                         const int B = (BW * i) >> 3, pp = (BW * i) & 7;
                         a[r] = window<G::CW>(w, B) & ((MASK << pp) * 0x00010001u);
                     }
-                    mma16816(c[u], a, b0, b1);
-                    if constexpr (XLO) mma16816(c[u], a, l0, l1);
+                    mma16816(cc[h][u], a, b0, b1);
+                    if constexpr (XLO) mma16816(cc[h][u], a, l0, l1);
                 }
             }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float (&c)[2][4] = cc[h];
             // epilogue: lane holds D(row g+8rho, block 8h+2t+bs) in c[u][2rho+bs];
             // everything is paired over bs = (block 2t, block 2t+1)
             const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const uint4 s4 = sc[u][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
-                const float2 Ss = make_float2(h2f_bits(s4.x & 0xffffu), h2f_bits(s4.z & 0xffffu));
-                const float2 Zs = make_float2(h2f_bits(s4.x >> 16), h2f_bits(s4.z >> 16));
-                const float2 Sz = make_float2(h2f_bits(s4.y & 0xffffu), h2f_bits(s4.w & 0xffffu));
-                const float2 Zz = make_float2(-h2f_bits(s4.y >> 16), -h2f_bits(s4.w >> 16));
+                const __half2 s0 = u32_as_h2(s4.x), z0 = u32_as_h2(s4.y), s1 = u32_as_h2(s4.z), z1 = u32_as_h2(s4.w);
+                const float2 Ss = make_float2(__low2float(s0), __low2float(s1));
+                const float2 Zs = make_float2(__high2float(s0), __high2float(s1));
+                const float2 Sz = make_float2(__low2float(z0), __low2float(z1));
+                const float2 Zz = make_float2(-__high2float(z0), -__high2float(z1));
                 const float2 A1 = fmul2(Ss, SC);                             // s_s * 2^(24-e)
                 const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));      // -s_s z_s 2^(24-e)
                 const float2 B0 = fmul2(Sz, Zz);                             // -z_s z_z

@@ -76,6 +76,12 @@ __device__ __forceinline__ float u2f_small(std::uint32_t v) {  // exact for v < 
     return __int_as_float(0x4B000000u | v) - 8388608.0f;
 }
 
+__device__ __forceinline__ __half2 u32_as_h2(std::uint32_t v) {
+    __half2 h;
+    memcpy(&h, &v, 4);
+    return h;
+}
+
 __device__ __forceinline__ float h2f_bits(std::uint32_t h16) {
     return __half2float(__ushort_as_half(static_cast<unsigned short>(h16)));
 }
@@ -85,9 +91,8 @@ struct TiledParams {
     const std::uint8_t* cells;        // cell records (cell bytes + outlier entries, 16-B padded)
     const std::uint32_t* cell_off;    // [ncell+1] byte offset of each record
     const std::uint32_t* warp_start;  // [nwarps+1] first cell of each warp
-    const std::uint32_t* wfirst;      // [Gn] first warp touching row-group pair G
-    const std::uint32_t* wlast;       // [Gn] last warp touching G
-    const std::uint32_t* wcnt;        // [Gn] warps with a non-empty range touching G
+    const std::uint32_t* gmap;        // [Gn][2] {partial slot base, contributing warps} of G
+    const std::uint32_t* wmap;        // [nwarps][2] ordinal of the warp in its first / last G
     const std::uint8_t* xpanel;       // [Pn] x panels of this batch column (xprep_tiled)
     float* y;                         // [m] this batch column
     float* partial;                   // [nwarps*2*32]
@@ -111,7 +116,9 @@ template <int CW>
 __device__ __forceinline__ std::uint32_t window(const std::uint32_t* w, int B) {
     if ((B & 1) == 0) return w[B >> 1];
     if ((B >> 1) + 1 < CW) return __byte_perm(w[B >> 1], w[(B >> 1) + 1], 0x6341);
-    return w[B >> 1] >> 8;
+    std::uint32_t r;  // w >> 8 on the FMA pipe (IMAD.HI)
+    asm("mul.hi.u32 %0, %1, 16777216;" : "=r"(r) : "r"(w[B >> 1]));
+    return r;
 }
 
 // Load `SB` bytes at 2-byte or 4-byte granularity into two 64-bit words.

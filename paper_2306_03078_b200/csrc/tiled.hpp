@@ -93,9 +93,9 @@ SPQR_HD constexpr int column_prescale(int bw, std::uint32_t k, std::uint32_t cc)
 // (256 x 4 B) and, for fp32 inputs, the low-half B fragments (16 x 32 B).
 inline constexpr std::uint32_t kPanelFragBytes = 512;
 inline constexpr std::uint32_t kPanelScBytes = 128;
-inline constexpr std::uint32_t kPanelXpBytes = 1024;
+SPQR_HD constexpr std::uint32_t panel_xp_bytes(bool xlo) { return xlo ? 1024u : 512u; }  // f32 / f16 x
 SPQR_HD constexpr std::uint32_t panel_bytes(bool xlo) {
-    return kPanelFragBytes + kPanelScBytes + kPanelXpBytes + (xlo ? kPanelFragBytes : 0u);
+    return kPanelFragBytes + kPanelScBytes + panel_xp_bytes(xlo) + (xlo ? kPanelFragBytes : 0u);
 }
 
 // Entry packing of the per-cell outlier lists.
