@@ -235,12 +235,14 @@ def run_ours(args) -> None:
     torch.cuda.set_device(dev)
 
     streams = make_streams()
-    layers, xs, ys, yfull, xs32 = [], [], [], [], []
+    from paper_2306_03078_b200.sharded import gather_rows, row_bands
+
+    layers, xs, ys, yfull, xs32, bands = [], [], [], [], [], []
     bytes_step = 0  # whole-job algorithmic bytes per step
     gen = torch.Generator(device="cpu").manual_seed(2)
     for (name, m, n), s in zip(LAYERS, streams):
-        assert m % (32 * world) == 0
-        r0, r1 = rank * m // world, (rank + 1) * m // world
+        bands.append(row_bands(m, world))
+        r0, r1 = bands[-1][rank]
         L = P.Layer(s, device=dev.index, rows=(r0, r1) if world > 1 else None)
         assert L.info["fast_path"] == 1
         layers.append(L)
@@ -248,7 +250,7 @@ def run_ours(args) -> None:
         xs.append(x.to(dev))
         xs32.append(x.float().pin_memory())
         ys.append(torch.empty(r1 - r0, device=dev))
-        yfull.append(torch.empty(m, device=dev) if world > 1 else None)
+        yfull.append(torch.empty(world * max(b - a for a, b in bands[-1]), device=dev) if world > 1 else None)
         bytes_step += alg_bytes(len(s) - 48, m, n) + 2 * n * (world - 1)
     payload_step = sum(len(s) - 48 for s in streams)
 
@@ -258,7 +260,7 @@ def run_ours(args) -> None:
         for i, L in enumerate(layers):
             L.matvec(xs[i], ys[i], stream=stream)
             if world > 1:
-                dist.all_gather_into_tensor(yfull[i], ys[i])
+                gather_rows(ys[i], bands[i], out=yfull[i])
 
     with torch.cuda.stream(stream):
         for _ in range(3):
@@ -324,19 +326,19 @@ def run_ours(args) -> None:
     kbytes = sum(alg_bytes(L.info["payload_bytes"], L.rows, L.cols) for L in layers)  # this rank
     peak, peak_kind = load_peaks()
     achieved = kbytes / (kms * 1e-3) / 1e9
-    traffic = None
+    traffic = None  # ncu dram__bytes_read+write per launch, averaged over the 7 launches
     tf = os.path.join(ROOT, "profiles", "gemv_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and world == 1:
         try:
             with open(tf) as f:
-                traffic = json.load(f).get("dram_bytes_per_cycle")
+                traffic = json.load(f).get("dram_bytes_per_launch_avg")
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                 "kernel": "gemv_tiled (fused decode-GEMV + CSR merge)",
                 "us_per_launch": round(1e3 * kms / len(layers), 3),
-                "bytes_per_cycle": kbytes}
+                "alg_bytes_per_launch": kbytes // len(layers)}
 
     # ---- per-shape microseconds (full matvec incl. x preparation) ----
     per_layer = {}
@@ -413,8 +415,8 @@ def run_ours(args) -> None:
             else:
                 xd32[i].copy_(xs32[i], non_blocking=True)
                 L.matvec(xd32[i], ys[i], stream=torch.cuda.current_stream())
-                dist.all_gather_into_tensor(yfull[i], ys[i])
-                ys_h[i].copy_(yfull[i], non_blocking=True)
+                gather_rows(ys[i], bands[i], out=yfull[i])
+                ys_h[i].copy_(yfull[i][: LAYERS[i][1]], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
 
     for _ in range(2):

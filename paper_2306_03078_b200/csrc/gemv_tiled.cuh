@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     __shared__ std::uint64_t bars[NW][NSLOT];
     __shared__ std::uint32_t slot_r[NW][NSLOT][2];  // record byte range of the slot's cell
     __shared__ std::uint32_t hist[NW][32];           // outlier count per local row of a cell
+    __shared__ __align__(16) std::uint32_t zrow[NW][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             slot_r[warp][slot][1] = r1;
             const std::uint32_t nb = min(r1 - r0, p.rec_cap_bytes);
             std::uint64_t* bar = &bars[warp][slot];
+            fence_proxy_async();  // the slot's outlier area was rewritten by generic stores
             mbar_expect_tx(bar, PANEL + nb);
             bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes + O_REC, p.cells + r0, nb, bar);
         }
@@ -177,9 +179,13 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
     const std::uint32_t Gq0 = Gc;
     const std::uint32_t magic = 0x4B000000u;
-    std::uint32_t sel[8];  // 1 in the lanes whose B column is MMA j's output column
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sel[j] = (g == j) ? 1u : 0u;
+    // ldmatrix row addresses for the masked B operand: MMA j of a super-tile
+    // routes block j to output column j, so B^T row n is block j's x when
+    // n == j and zero otherwise.  Call c loads MMAs 2c, 2c+1 (x4: k halves).
+    const int lm = lane >> 3, lr = lane & 7;  // matrix, row this lane addresses
+    const std::uint32_t zero_sa = smem_u32(&zrow[warp][0]);
+    if (lane < 4) zrow[warp][lane] = 0u;
+    __syncwarp();
     float orow_reg = 0.f;  // outlier sum of local row `lane` (current row-group pair)
 
     auto flush = [&](std::uint32_t Gf, bool whole) {
@@ -252,14 +258,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
 
         // x operands of this panel (shared by both units)
-        uint2 xf[2], xl[2];
         float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            xf[h] = reinterpret_cast<const uint2*>(sl + O_FRAG)[(8 * h + g) * 4 + t];
-            if constexpr (XLO) xl[h] = reinterpret_cast<const uint2*>(sl + O_LO)[(8 * h + g) * 4 + t];
-            xs[h] = reinterpret_cast<const float4*>(sl + O_SC)[4 * h + t];
-        }
+        for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(sl + O_SC)[4 * h + t];
+        const std::uint32_t frag_sa = smem_u32(sl) + O_FRAG + 16u * (lm & 1);
 
         // lane data of both units
         std::uint32_t cw[2][G::LANE_WORDS];
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         }
 
         // 4 independent MMA chains (super-tile h x unit u), interleaved
+        std::uint32_t bfr[2][4], lfr[2][4];
         float cc[2][2][4];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -294,11 +297,23 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                const std::uint32_t b0 = mask01(xf[h].x, sel[j]), b1 = mask01(xf[h].y, sel[j]);
+                // B fragments of MMAs (2c, 2c+1), c = j/2, fetched at the even j
+                std::uint32_t bq[4], lq[4];
+                if ((j & 1) == 0) {
+                    const int jm = j + (lm >> 1);
+                    const std::uint32_t off = static_cast<std::uint32_t>((8 * h + jm) * 32);
+                    ldsm_x4(lr == jm ? frag_sa + off : zero_sa, bq);
+                    if constexpr (XLO) ldsm_x4(lr == jm ? frag_sa + (O_LO - O_FRAG) + off : zero_sa, lq);
+                    bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
+                    if constexpr (XLO) {
+                        lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
+                    }
+                }
+                const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
                 std::uint32_t l0 = 0, l1 = 0;
                 if constexpr (XLO) {
-                    l0 = mask01(xl[h].x, sel[j]);
-                    l1 = mask01(xl[h].y, sel[j]);
+                    l0 = lfr[h][2 * (j & 1)];
+                    l1 = lfr[h][2 * (j & 1) + 1];
                 }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -357,7 +372,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
         if (cnt) {
             const std::uint32_t in_smem = (min(r1 - r0, p.rec_cap_bytes) - CELL) / 4u;
-            const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+            const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);  // in our slot
             const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
             auto x_at = [&](std::uint32_t col) -> float {
                 if constexpr (XLO)
@@ -365,42 +380,66 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                 else
                     return __half2float(reinterpret_cast<const __half*>(sl + O_XP)[col]);
             };
-            auto merge = [&](auto entry) {
-                hist[warp][lane] = 0u;
-                __syncwarp();
+            // pass 1 (entry-parallel, no divergence): product v*x written over
+            // the entry in the slot + row histogram; pass 2: exclusive scan of
+            // the row counts; pass 3: lane R sums its row's products in column
+            // order (deterministic).  Entries beyond the staged part of the
+            // record are read from HBM and summed directly by their row lane.
+            std::uint32_t* ew = const_cast<std::uint32_t*>(es);
+            hist[warp][lane] = 0u;
+            __syncwarp();
+            const std::uint32_t nfast = min(cnt, in_smem);
 #pragma unroll 1
-                for (std::uint32_t base = 0; base < cnt; base += 32) {
+            for (std::uint32_t base = 0; base < nfast; base += 32) {
+                const std::uint32_t i = base + lane;
+                if (i < nfast) {
+                    const std::uint32_t e = ew[i];
+                    const std::uint32_t r = e >> 24;
+                    if (r < 32u) {
+                        ew[i] = __float_as_uint(h2f_bits(e & 0xffffu) * x_at((e >> 16) & 255u));
+                        atomicAdd(&hist[warp][r], 1u);
+                    }
+                }
+            }
+            if (cnt > nfast) {  // rare: record larger than the slot
+#pragma unroll 1
+                for (std::uint32_t base = nfast; base < cnt; base += 32) {
                     const std::uint32_t i = base + lane;
                     if (i < cnt) {
-                        const std::uint32_t r = entry(i) >> 24;
+                        const std::uint32_t r = __ldg(eg + i) >> 24;
                         if (r < 32u) atomicAdd(&hist[warp][r], 1u);
                     }
                 }
-                __syncwarp();
-                const std::uint32_t c = hist[warp][lane];
-                std::uint32_t s = c;  // inclusive scan over rows
+            }
+            __syncwarp();
+            const std::uint32_t c = hist[warp][lane];
+            std::uint32_t s = c;  // inclusive scan over rows
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const std::uint32_t o = __shfl_up_sync(0xffffffffu, s, d);
-                    if (lane >= d) s += o;
-                }
-                std::uint32_t i = s - c;
-                float o = orow_reg;
-                for (; i + 1 < s; i += 2) {
-                    const std::uint32_t ea = entry(i), eb = entry(i + 1);
-                    o = fmaf(h2f_bits(ea & 0xffffu), x_at((ea >> 16) & 255u), o);
-                    o = fmaf(h2f_bits(eb & 0xffffu), x_at((eb >> 16) & 255u), o);
-                }
-                if (i < s) {
-                    const std::uint32_t ea = entry(i);
-                    o = fmaf(h2f_bits(ea & 0xffffu), x_at((ea >> 16) & 255u), o);
-                }
-                orow_reg = o;
-            };
-            if (cnt <= in_smem)
-                merge([&](std::uint32_t i) { return es[i]; });
-            else
-                merge([&](std::uint32_t i) { return i < in_smem ? es[i] : __ldg(eg + i); });
+            for (int d = 1; d < 32; d <<= 1) {
+                const std::uint32_t o = __shfl_up_sync(0xffffffffu, s, d);
+                if (lane >= d) s += o;
+            }
+            const std::uint32_t st0 = s - c;
+            std::uint32_t i = st0;
+            float o = 0.f;
+            const std::uint32_t fend = min(s, nfast);
+            // row sum in column order, 4 products per step without branches
+            for (; i < fend; i += 4) {
+                const float p0 = __uint_as_float(ew[i]);
+                const float p1 = i + 1 < fend ? __uint_as_float(ew[i + 1]) : 0.f;
+                const float p2 = i + 2 < fend ? __uint_as_float(ew[i + 2]) : 0.f;
+                const float p3 = i + 3 < fend ? __uint_as_float(ew[i + 3]) : 0.f;
+                o += p0;
+                o += p1;
+                o += p2;
+                o += p3;
+            }
+            i = max(st0, fend);
+            for (; i < s; ++i) {
+                const std::uint32_t e = __ldg(eg + i);
+                o = fmaf(h2f_bits(e & 0xffffu), x_at((e >> 16) & 255u), o);
+            }
+            orow_reg += o;
         }
 
         __syncwarp();

@@ -72,6 +72,13 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const std::uint32_t (&a)
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// four 8x8 b16 matrices from shared memory (rows addressed per lane)
+__device__ __forceinline__ void ldsm_x4(std::uint32_t addr, std::uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+
 __device__ __forceinline__ float u2f_small(std::uint32_t v) {  // exact for v < 2^23
     return __int_as_float(0x4B000000u | v) - 8388608.0f;
 }
@@ -153,12 +160,12 @@ __device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int 
 
 // x preparation for the tiled path: one thread per (16-column block, batch).
 // Writes the panel layout the GEMV stages per cell (tiled.hpp panel_bytes):
-//   [B fragments 16 x 32 B][{SC(2i), SC(2i+1), XX(2i), XX(2i+1)} x 8]
+//   [B rows 16 blocks x 16 fp16][{SC(2i), SC(2i+1), XX(2i), XX(2i+1)} x 8]
 //   [x in solve order: 256 x f16 (fp16 input) or f32 (fp32 input)]
-//   [low-half B fragments 16 x 32 B (fp32 input only)]
-// B fragments hold fp16(x * 2^(e - p)) for the lane order of the m16n8k16 B
-// operand (columns 2t, 2t+1, 2t+8, 2t+9), e = per-block power-of-two scale
-// (max |x| in [2^14, 2^15)), p = the column's code pre-scale (tiled.hpp).
+//   [low-half B rows 16 x 16 fp16 (fp32 input only)]
+// B rows hold fp16(x * 2^(e - p)) in column order (ldmatrix rows of B^T),
+// e = per-block power-of-two scale (max |x| in [2^14, 2^15)), p = the
+// column's code pre-scale (tiled.hpp).
 template <int BW, bool XLO>
 __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t n_pad,
                             std::uint32_t batch, const std::uint32_t* __restrict__ order,
@@ -215,25 +222,22 @@ __global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t
             }
             X += ldexpf(eff, pp);
         }
-        uint2* fr = reinterpret_cast<uint2*>(pan + 32u * kk);
-        uint2* fl = reinterpret_cast<uint2*>(pan + O_LO + 32u * kk);
-#pragma unroll
-        for (int tt = 0; tt < 4; ++tt) {
-            const int c0 = 2 * tt;
-            uint2 f;
-            f.x = static_cast<std::uint32_t>(__half_as_ushort(hi[c0])) |
-                  (static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 1])) << 16);
-            f.y = static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 8])) |
-                  (static_cast<std::uint32_t>(__half_as_ushort(hi[c0 + 9])) << 16);
-            fr[tt] = f;
-            if constexpr (XLO) {
-                uint2 l;
-                l.x = static_cast<std::uint32_t>(__half_as_ushort(lo[c0])) |
-                      (static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 1])) << 16);
-                l.y = static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 8])) |
-                      (static_cast<std::uint32_t>(__half_as_ushort(lo[c0 + 9])) << 16);
-                fl[tt] = l;
-            }
+        // natural column order: the GEMV reads these rows with ldmatrix (rows of B^T)
+        uint4* fr = reinterpret_cast<uint4*>(pan + 32u * kk);
+        uint4* fl = reinterpret_cast<uint4*>(pan + O_LO + 32u * kk);
+        auto pack = [](const __half* h8) {
+            uint4 r;
+            r.x = static_cast<std::uint32_t>(__half_as_ushort(h8[0])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[1])) << 16);
+            r.y = static_cast<std::uint32_t>(__half_as_ushort(h8[2])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[3])) << 16);
+            r.z = static_cast<std::uint32_t>(__half_as_ushort(h8[4])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[5])) << 16);
+            r.w = static_cast<std::uint32_t>(__half_as_ushort(h8[6])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[7])) << 16);
+            return r;
+        };
+        fr[0] = pack(hi);
+        fr[1] = pack(hi + 8);
+        if constexpr (XLO) {
+            fl[0] = pack(lo);
+            fl[1] = pack(lo + 8);
         }
         float* scp = reinterpret_cast<float*>(pan + O_SC + 16u * (kk / 2));
         scp[kk & 1] = ldexpf(1.0f, 24 - e);

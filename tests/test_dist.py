@@ -1,0 +1,45 @@
+"""Multi-process host logic of the row-sharded path (gloo, world size 2, CPU)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from paper_2306_03078_b200.sharded import row_bands
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("m,world", [(8192, 8), (22016, 8), (22016, 4), (4096, 2), (208, 2), (96, 4), (4, 2)])
+def test_row_bands_cover_and_align(m, world):
+    bands = row_bands(m, world)
+    assert len(bands) == world
+    assert bands[0][0] == 0 and bands[-1][1] == m
+    for (a, b), (c, _) in zip(bands, bands[1:]):
+        assert b == c
+    assert all(a % 32 == 0 or a == m for a, _ in bands)  # empty tail bands allowed
+    units = [-(-(b - a) // 32) for a, b in bands]  # 32-row cells per band
+    assert max(units) - min(units) <= 1
+
+
+def test_llama_bands_are_equal():
+    for m in (4096, 8192, 11008, 22016):
+        for w in (1, 2, 4, 8):
+            sizes = {b - a for a, b in row_bands(m, w)}
+            assert len(sizes) == 1, (m, w)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_gather_matches_full_product_world2(oracle_c):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(HERE, "dist", "band_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "band gather ok" in r.stdout
