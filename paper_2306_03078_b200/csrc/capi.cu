@@ -195,15 +195,20 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
 template <int BW, bool XLO>
 void launch_xprep_t(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,
                     std::uint64_t panel_stride, cudaStream_t st) {
-    const std::uint32_t nblk = L->n_pad / 16;
-    for (int b = 0; b < batch; ++b) {  // one launch per column keeps the stride explicit
-        const void* xb = static_cast<const std::uint8_t*>(x) +
-                         static_cast<std::size_t>(b) * L->info.cols * (f16 ? 2 : 4);
-        spqr_dev::xprep_tiled<BW, XLO><<<(nblk + 127) / 128, 128, 0, st>>>(
-            xb, f16, L->info.cols, L->n_pad, 1u, L->d_order, panels + b * panel_stride);
-        ck(cudaGetLastError(), "launch xprep_tiled");
-        ++g_launches;
-    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L->n_pad / 128, static_cast<unsigned>(batch), 1);
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_tiled<BW, XLO>, x, f16, L->info.cols, L->n_pad,
+                          static_cast<const std::uint32_t*>(L->d_order), panels, panel_stride),
+       "launch xprep_tiled");
+    ++g_launches;
 }
 
 void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,

@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     const std::uint32_t q0 = p.warp_start[wk], q1 = p.warp_start[wk + 1];
     std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * NSLOT * p.slot_bytes;
 
+    // the next layer's xprep may launch now; it reads x only after this grid
+    // has completed (its griddepcontrol.wait), so the tails of consecutive
+    // layers overlap
+    pdl_launch();
     if (lane == 0) {
         for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[warp][s], 1);
         fence_mbar_init();

@@ -158,92 +158,66 @@ __device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int 
 
 #include "gemv_tiled.cuh"
 
-// x preparation for the tiled path: one thread per (16-column block, batch).
-// Writes the panel layout the GEMV stages per cell (tiled.hpp panel_bytes):
+// x preparation for the tiled path: one thread per (column, batch column);
+// the 16 lanes of a half-warp form one 16-column block.  Writes the panel
+// layout the GEMV stages per cell (tiled.hpp panel_bytes):
 //   [B rows 16 blocks x 16 fp16][{SC(2i), SC(2i+1), XX(2i), XX(2i+1)} x 8]
 //   [x in solve order: 256 x f16 (fp16 input) or f32 (fp32 input)]
 //   [low-half B rows 16 x 16 fp16 (fp32 input only)]
 // B rows hold fp16(x * 2^(e - p)) in column order (ldmatrix rows of B^T),
 // e = per-block power-of-two scale (max |x| in [2^14, 2^15)), p = the
 // column's code pre-scale (tiled.hpp).
+// PDL: the dependent GEMV may launch (and start streaming weights) at once;
+// x is read only after the preceding kernel in the stream has completed.
 template <int BW, bool XLO>
-__global__ void xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t n_pad,
-                            std::uint32_t batch, const std::uint32_t* __restrict__ order,
-                            std::uint8_t* __restrict__ panels) {
+__global__ void __launch_bounds__(128) xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n,
+                                                   std::uint32_t n_pad, const std::uint32_t* __restrict__ order,
+                                                   std::uint8_t* __restrict__ panels, std::uint64_t panel_stride) {
     constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
     constexpr std::uint32_t O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
     constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
-    const std::uint32_t nblk = n_pad / 16;
-    const std::uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < nblk * batch) {
-        const std::uint32_t b = idx / nblk, k = idx - b * nblk;
-        std::uint8_t* pan = panels + (static_cast<std::size_t>(b) * (nblk / 16) + k / 16) * PANEL;
-        const std::uint32_t kk = k % 16;
-        float v[16];
-        float mx = 0.f;
+    pdl_launch();
+    const std::uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;  // n_pad is a multiple of 256
+    const std::uint32_t b = blockIdx.y;
+    const std::uint32_t k = col >> 4, cc = col & 15, kk = k & 15;
+    std::uint8_t* pan = panels + b * panel_stride + static_cast<std::size_t>(col >> 8) * PANEL;
+    const std::uint32_t src = (col < n) ? (order ? __ldg(order + col) : col) : 0u;
+    pdl_wait();
+    float v = 0.f;
+    if (col < n)
+        v = x_f16 ? __half2float(reinterpret_cast<const __half*>(x)[static_cast<std::size_t>(b) * n + src])
+                  : reinterpret_cast<const float*>(x)[static_cast<std::size_t>(b) * n + src];
+    float mx = fabsf(v);
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-            const std::uint32_t col = 16 * k + cc;
-            float val = 0.f;
-            if (col < n) {
-                const std::uint32_t src = order ? __ldg(order + col) : col;
-                val = x_f16 ? __half2float(reinterpret_cast<const __half*>(x)[static_cast<std::size_t>(b) * n + src])
-                            : reinterpret_cast<const float*>(x)[static_cast<std::size_t>(b) * n + src];
-            }
-            v[cc] = val;
-            mx = fmaxf(mx, fabsf(val));
-        }
-        if constexpr (XLO) {
-            float4* xo = reinterpret_cast<float4*>(pan + O_XP + 64u * kk);
+    for (int d = 1; d < 16; d <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    if constexpr (XLO)
+        reinterpret_cast<float*>(pan + O_XP)[16 * kk + cc] = v;
+    else
+        reinterpret_cast<__half*>(pan + O_XP)[16 * kk + cc] = __float2half_rn(v);
+    int e = 0;
+    if (mx > 0.f && mx < INFINITY) {
+        int E;
+        frexpf(mx, &E);  // mx = f * 2^E, f in [0.5, 1)
+        e = 15 - E;      // mx * 2^e in [2^14, 2^15)
+    }
+    const int pp = T::column_prescale(BW, k, cc);
+    const float s = ldexpf(v, e - pp);
+    const __half hi = __float2half_rn(s);
+    float eff = __half2float(hi);
+    reinterpret_cast<__half*>(pan)[16 * kk + cc] = hi;  // natural column order (ldmatrix rows of B^T)
+    if constexpr (XLO) {
+        const __half lo = __float2half_rn(s - eff);
+        eff += __half2float(lo);
+        reinterpret_cast<__half*>(pan + O_LO)[16 * kk + cc] = lo;
+    }
+    float X = ldexpf(eff, pp);  // block sum of the effective scaled x, fixed tree order
 #pragma unroll
-            for (int i = 0; i < 4; ++i) xo[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-            __half2* xo = reinterpret_cast<__half2*>(pan + O_XP + 32u * kk);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) xo[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-        }
-        int e = 0;
-        if (mx > 0.f && mx < INFINITY) {
-            int E;
-            frexpf(mx, &E);  // mx = f * 2^E, f in [0.5, 1)
-            e = 15 - E;      // mx * 2^e in [2^14, 2^15)
-        }
-        __half hi[16], lo[16];
-        float X = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-            const int pp = T::column_prescale(BW, k, cc);
-            const float s = ldexpf(v[cc], e - pp);
-            hi[cc] = __float2half_rn(s);
-            float eff = __half2float(hi[cc]);
-            if constexpr (XLO) {
-                lo[cc] = __float2half_rn(s - eff);
-                eff += __half2float(lo[cc]);
-            }
-            X += ldexpf(eff, pp);
-        }
-        // natural column order: the GEMV reads these rows with ldmatrix (rows of B^T)
-        uint4* fr = reinterpret_cast<uint4*>(pan + 32u * kk);
-        uint4* fl = reinterpret_cast<uint4*>(pan + O_LO + 32u * kk);
-        auto pack = [](const __half* h8) {
-            uint4 r;
-            r.x = static_cast<std::uint32_t>(__half_as_ushort(h8[0])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[1])) << 16);
-            r.y = static_cast<std::uint32_t>(__half_as_ushort(h8[2])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[3])) << 16);
-            r.z = static_cast<std::uint32_t>(__half_as_ushort(h8[4])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[5])) << 16);
-            r.w = static_cast<std::uint32_t>(__half_as_ushort(h8[6])) | (static_cast<std::uint32_t>(__half_as_ushort(h8[7])) << 16);
-            return r;
-        };
-        fr[0] = pack(hi);
-        fr[1] = pack(hi + 8);
-        if constexpr (XLO) {
-            fl[0] = pack(lo);
-            fl[1] = pack(lo + 8);
-        }
+    for (int d = 1; d < 16; d <<= 1) X += __shfl_xor_sync(0xffffffffu, X, d);
+    if (cc == 0) {
         float* scp = reinterpret_cast<float*>(pan + O_SC + 16u * (kk / 2));
         scp[kk & 1] = ldexpf(1.0f, 24 - e);
         scp[2 + (kk & 1)] = -X * 5.9604644775390625e-08f;
     }
-    pdl_launch();
 }
 
 // ============================================================== raw path ====

@@ -99,7 +99,7 @@ def model_matvec(stream: bytes, x: np.ndarray, xlo: bool = True) -> np.ndarray:
         v = xs[16 * k:16 * k + 16]
         mx = float(np.max(np.abs(v)))
         e = 15 - int(np.frexp(mx)[1]) if mx > 0 else 0
-        X = np.float32(0)
+        Xs = np.zeros(16, np.float32)
         for cc in range(16):
             p = column_prescale(bw, k, cc)
             assert pre[:, 16 * k + cc].min() in (p, -1) and pre[:, 16 * k + cc].max() == p
@@ -110,7 +110,10 @@ def model_matvec(stream: bytes, x: np.ndarray, xlo: bool = True) -> np.ndarray:
                 lo = np.float16(np.float32(s - ef))
                 ef = np.float32(ef + np.float32(lo))
             eff[16 * k + cc] = np.ldexp(np.float64(ef), p)
-            X = np.float32(X + np.float32(np.ldexp(np.float64(ef), p)))
+            Xs[cc] = np.float32(np.ldexp(np.float64(ef), p))
+        for d in (1, 2, 4, 8):  # xprep's butterfly order
+            Xs = (Xs + Xs[np.arange(16) ^ d]).astype(np.float32)
+        X = Xs[0]
         SC[k] = np.float32(2.0 ** (24 - e))
         XX[k] = np.float32(-X * np.float32(5.9604644775390625e-08))
     # "MMA": C = sum code * 2^(p-24) * eff * 2^-p  (exact in float64)
