@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     extern __shared__ __align__(128) std::uint8_t smem[];
     __shared__ std::uint64_t bars[NW][NSLOT];
     __shared__ std::uint32_t slot_r[NW][NSLOT][2];  // record byte range of the slot's cell
-    __shared__ std::uint32_t hist[NW][32];           // outlier count per local row of a cell
+    __shared__ float rowsum[NW][32];                 // outlier row sums of a cell (zero between cells)
     __shared__ __align__(16) std::uint32_t zrow[NW][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -186,9 +186,19 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     // ldmatrix row addresses for the masked B operand: MMA j of a super-tile
     // routes block j to output column j, so B^T row n is block j's x when
     // n == j and zero otherwise.  Call c loads MMAs 2c, 2c+1 (x4: k halves).
-    const int lm = lane >> 3, lr = lane & 7;  // matrix, row this lane addresses
+    // Lane (lm, lr) = (lane / 8, lane % 8) addresses row lr of matrix lm; it
+    // carries data only in the call whose MMA j + lm/2 == lr, i.e. j == jact,
+    // and then always the same 16 bytes of the panel (block 8h + lr, k half
+    // lm % 2), at a fixed lane offset -- the per-call offset 256h is an
+    // immediate, so the zero row is pre-biased by -256h.
+    const int lm = lane >> 3, lr = lane & 7;
+    const int jact = lr - (lm >> 1);
+    const std::uint32_t lane_off = O_FRAG + 32u * lr + 16u * (lm & 1);
     const std::uint32_t zero_sa = smem_u32(&zrow[warp][0]);
+    const std::uint32_t zb[2] = {zero_sa, zero_sa - 256u};
+    const std::uint32_t zl[2] = {zero_sa - (O_LO - O_FRAG), zero_sa - 256u - (O_LO - O_FRAG)};
     if (lane < 4) zrow[warp][lane] = 0u;
+    rowsum[warp][lane] = 0.f;
     __syncwarp();
     float orow_reg = 0.f;  // outlier sum of local row `lane` (current row-group pair)
 
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
 #pragma unroll
         for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(sl + O_SC)[4 * h + t];
-        const std::uint32_t frag_sa = smem_u32(sl) + O_FRAG + 16u * (lm & 1);
+        const std::uint32_t lane_sa = smem_u32(sl) + lane_off;
 
         // lane data of both units
         std::uint32_t cw[2][G::LANE_WORDS];
@@ -304,10 +314,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                 // B fragments of MMAs (2c, 2c+1), c = j/2, fetched at the even j
                 std::uint32_t bq[4], lq[4];
                 if ((j & 1) == 0) {
-                    const int jm = j + (lm >> 1);
-                    const std::uint32_t off = static_cast<std::uint32_t>((8 * h + jm) * 32);
-                    ldsm_x4(lr == jm ? frag_sa + off : zero_sa, bq);
-                    if constexpr (XLO) ldsm_x4(lr == jm ? frag_sa + (O_LO - O_FRAG) + off : zero_sa, lq);
+                    const bool act = jact == j;
+                    ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bq);  // constant offset folds into LDSM
+                    if constexpr (XLO) ldsm_x4((act ? lane_sa : zl[h]) + (256u * h + (O_LO - O_FRAG)), lq);
                     bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
                     if constexpr (XLO) {
                         lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
@@ -370,80 +379,82 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         }
 
         // outliers: entries (row, col, value) of this cell, sorted by (row, col),
-        // 0xffffffff padding.  Row counts (integer smem atomics, order-free) ->
-        // exclusive scan -> lane R sums the entries of local row R in column
-        // order: deterministic by construction.
+        // 0xffffffff padding (row 255).  Chunks of 128 entries, 4 consecutive
+        // per lane (one 16-byte load): products, a segmented inclusive scan by
+        // row (in-lane, then across lanes by the lanes' last row), and the
+        // last entry of each row in the chunk adds the row total to rowsum.
+        // Chunks run in order, so the sums are deterministic.  Entries beyond
+        // the staged part of the record are read from global memory.
         const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
         if (cnt) {
-            const std::uint32_t in_smem = (min(r1 - r0, p.rec_cap_bytes) - CELL) / 4u;
+            const std::uint32_t nfast = (min(r1 - r0, p.rec_cap_bytes) - CELL) / 4u;
             const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);  // in our slot
-            const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
-            auto x_at = [&](std::uint32_t col) -> float {
-                if constexpr (XLO)
-                    return reinterpret_cast<const float*>(sl + O_XP)[col];
-                else
-                    return __half2float(reinterpret_cast<const __half*>(sl + O_XP)[col]);
-            };
-            // pass 1 (entry-parallel, no divergence): product v*x written over
-            // the entry in the slot + row histogram; pass 2: exclusive scan of
-            // the row counts; pass 3: lane R sums its row's products in column
-            // order (deterministic).  Entries beyond the staged part of the
-            // record are read from HBM and summed directly by their row lane.
-            std::uint32_t* ew = const_cast<std::uint32_t*>(es);
-            hist[warp][lane] = 0u;
-            __syncwarp();
-            const std::uint32_t nfast = min(cnt, in_smem);
-#pragma unroll 1
-            for (std::uint32_t base = 0; base < nfast; base += 32) {
-                const std::uint32_t i = base + lane;
-                if (i < nfast) {
-                    const std::uint32_t e = ew[i];
-                    const std::uint32_t r = e >> 24;
-                    if (r < 32u) {
-                        ew[i] = __float_as_uint(h2f_bits(e & 0xffffu) * x_at((e >> 16) & 255u));
-                        atomicAdd(&hist[warp][r], 1u);
-                    }
-                }
-            }
-            if (cnt > nfast) {  // rare: record larger than the slot
-#pragma unroll 1
-                for (std::uint32_t base = nfast; base < cnt; base += 32) {
-                    const std::uint32_t i = base + lane;
-                    if (i < cnt) {
-                        const std::uint32_t r = __ldg(eg + i) >> 24;
-                        if (r < 32u) atomicAdd(&hist[warp][r], 1u);
-                    }
-                }
-            }
-            __syncwarp();
-            const std::uint32_t c = hist[warp][lane];
-            std::uint32_t s = c;  // inclusive scan over rows
+            const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
+            float* rs = rowsum[warp];
+            auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
+                uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
+                const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                std::uint32_t k[4];
+                float sv[4];
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const std::uint32_t o = __shfl_up_sync(0xffffffffu, s, d);
-                if (lane >= d) s += o;
+                for (int j = 0; j < 4; ++j) {
+                    k[j] = e[j] >> 24;
+                    const std::uint32_t c = (e[j] >> 16) & 255u;
+                    float xv;
+                    if constexpr (XLO)
+                        xv = reinterpret_cast<const float*>(sl + O_XP)[c];
+                    else
+                        xv = __half2float(reinterpret_cast<const __half*>(sl + O_XP)[c]);
+                    sv[j] = h2f_bits(e[j] & 0xffffu) * xv;
+                }
+                bool same[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    same[j] = k[j + 1] == k[j];
+                    if (same[j]) sv[j + 1] += sv[j];
+                }
+                // across lanes: segments of equal last-row keys (sorted => contiguous)
+                const std::uint32_t K = k[3];
+                const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
+                const bool head = lane == 0 || pK != K;
+                const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
+                const int seg0 = 31 - __clz(heads);
+                float V = sv[3];
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const float o = __shfl_up_sync(0xffffffffu, V, d);
+                    if (lane - d >= seg0) V += o;
+                }
+                float cin = __shfl_up_sync(0xffffffffu, V, 1);
+                if (lane == 0 || pK != k[0]) cin = 0.f;
+                const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
+                    if (tail && k[j] < 32u) {
+                        const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
+                        if (first)
+                            rs[k[j]] = tot;
+                        else
+                            rs[k[j]] += tot;
+                    }
+                }
+            };
+            chunk(es, 4u * lane, nfast, true);
+#pragma unroll 1
+            for (std::uint32_t base = 128; base < nfast; base += 128) {
+                __syncwarp();
+                chunk(es, base + 4u * lane, nfast, false);
             }
-            const std::uint32_t st0 = s - c;
-            std::uint32_t i = st0;
-            float o = 0.f;
-            const std::uint32_t fend = min(s, nfast);
-            // row sum in column order, 4 products per step without branches
-            for (; i < fend; i += 4) {
-                const float p0 = __uint_as_float(ew[i]);
-                const float p1 = i + 1 < fend ? __uint_as_float(ew[i + 1]) : 0.f;
-                const float p2 = i + 2 < fend ? __uint_as_float(ew[i + 2]) : 0.f;
-                const float p3 = i + 3 < fend ? __uint_as_float(ew[i + 3]) : 0.f;
-                o += p0;
-                o += p1;
-                o += p2;
-                o += p3;
+#pragma unroll 1
+            for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
+                __syncwarp();
+                chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);  // eg starts at entry nfast
             }
-            i = max(st0, fend);
-            for (; i < s; ++i) {
-                const std::uint32_t e = __ldg(eg + i);
-                o = fmaf(h2f_bits(e & 0xffffu), x_at((e >> 16) & 255u), o);
-            }
-            orow_reg += o;
+            __syncwarp();
+            orow_reg += rs[lane];
+            rs[lane] = 0.f;
         }
 
         __syncwarp();
