@@ -75,16 +75,25 @@ __device__ __forceinline__ float magic_field_rt(std::uint32_t w, int shift, std:
     return __uint_as_float(r);
 }
 
-// Lane statistics field (SB bytes at 2-byte alignment) as two 32-bit words:
+// Lane statistics field (tiled.hpp stat_byte_offset) as two 32-bit words:
 // s = bits [0, 32) (scale codes), z = bits [8*BS, 8*BS + 32) (zero codes).
 template <int BS, int BZ>
-__device__ __forceinline__ void load_stats(const std::uint8_t* p, std::uint32_t& s, std::uint32_t& z) {
-    std::uint64_t v[2];
-    load_stat_bits<BS + BZ>(p, v);
-    s = static_cast<std::uint32_t>(v[0]);
-    const int sh = 8 * BS;  // < 64
-    z = static_cast<std::uint32_t>(v[0] >> sh);
-    if constexpr (8 * BS + 8 * BZ > 64) z |= static_cast<std::uint32_t>(v[1] << (64 - sh));
+__device__ __forceinline__ void load_stats(const std::uint8_t* stats, int lane, std::uint32_t& s, std::uint32_t& z) {
+    constexpr int SB = BS + BZ;
+    if constexpr (SB > 4 && SB < 8) {  // 4-byte plane + (SB-4)-byte plane
+        static_assert(SB == 6, "only 3/3-bit statistics use the split planes on the fast path");
+        const std::uint32_t w0 = reinterpret_cast<const std::uint32_t*>(stats)[lane];
+        const std::uint32_t w1 = reinterpret_cast<const std::uint16_t*>(stats + 128)[lane];
+        s = w0;
+        z = __funnelshift_r(w0, w1, 8 * BS);
+    } else {
+        std::uint64_t v[2];
+        load_stat_bits<SB>(stats + lane * SB, v);
+        s = static_cast<std::uint32_t>(v[0]);
+        const int sh = 8 * BS;  // < 64
+        z = static_cast<std::uint32_t>(v[0] >> sh);
+        if constexpr (8 * BS + 8 * BZ > 64) z |= static_cast<std::uint32_t>(v[1] << (64 - sh));
+    }
 }
 
 template <int BW, int BS, int BZ, bool XLO, int NW, int NSLOT>
@@ -129,53 +138,46 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         return;
     }
 
-    // record byte offsets of 32 consecutive cells at a time across the lanes;
-    // the following window is prefetched one window ahead
-    std::uint32_t off_base = q0;
-    std::uint32_t off_lane = (q0 + lane <= q1) ? __ldg(p.cell_off + q0 + lane) : 0u;
-    std::uint32_t off_next = (q0 + 32 + lane <= q1) ? __ldg(p.cell_off + q0 + 32 + lane) : 0u;
-    auto rec_offset = [&](std::uint32_t q) -> std::uint32_t {  // monotone q, whole warp
-        if (q >= off_base + 32) {
-            off_base += 32;
-            off_lane = off_next;
-            off_next = (off_base + 32 + lane <= q1) ? __ldg(p.cell_off + off_base + 32 + lane) : 0u;
-        }
-        return __shfl_sync(0xffffffffu, off_lane, static_cast<int>(q - off_base));
+    // TMA issue state, lane 0 only: record offsets of the next cell to issue
+    // (r0, r1) and the one after (prefetched a full cell ahead), its panel.
+    const std::uint32_t ncell = q1 - q0;
+    std::uint32_t i_q = q0, i_r0 = 0, i_r1 = 0, i_nx = 0, i_P = 0;
+    std::uint32_t Gc = q0 / p.Pn, P = q0 - Gc * p.Pn;
+    if (lane == 0) {
+        i_r0 = __ldg(p.cell_off + q0);
+        i_r1 = __ldg(p.cell_off + q0 + 1);
+        i_nx = (q0 + 2 <= q1) ? __ldg(p.cell_off + q0 + 2) : 0u;
+        i_P = P;
+    }
+    auto issue_rec = [&](int slot) {  // lane 0: cell i_q -> slot, arms the barrier for record + panel
+        slot_r[warp][slot][0] = i_r0;
+        slot_r[warp][slot][1] = i_r1;
+        const std::uint32_t nb = min(i_r1 - i_r0, p.rec_cap_bytes);
+        std::uint64_t* bar = &bars[warp][slot];
+        mbar_expect_tx(bar, PANEL + nb);
+        bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes + O_REC, p.cells + i_r0, nb, bar);
+        ++i_q;
+        i_r0 = i_r1;
+        i_r1 = i_nx;
+        i_nx = (i_q + 2 <= q1) ? __ldg(p.cell_off + i_q + 2) : 0u;
     };
-    // cell record q -> slot (arms the barrier for record + panel)
-    auto issue_w = [&](std::uint32_t q, int slot) {
-        const std::uint32_t r0 = rec_offset(q), r1 = rec_offset(q + 1);
-        if (lane == 0) {
-            slot_r[warp][slot][0] = r0;
-            slot_r[warp][slot][1] = r1;
-            const std::uint32_t nb = min(r1 - r0, p.rec_cap_bytes);
-            std::uint64_t* bar = &bars[warp][slot];
-            fence_proxy_async();  // the slot's outlier area was rewritten by generic stores
-            mbar_expect_tx(bar, PANEL + nb);
-            bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes + O_REC, p.cells + r0, nb, bar);
-        }
-    };
-    // x operands of panel P (written by the preceding xprep kernel)
-    auto issue_x = [&](std::uint32_t P, int slot) {
-        if (lane == 0)
-            bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes, p.xpanel + PANEL * P, PANEL,
-                     &bars[warp][slot]);
+    auto issue_x = [&](int slot) {  // lane 0: x operands of panel i_P (written by xprep)
+        bulk_g2s(ring + static_cast<std::size_t>(slot) * p.slot_bytes, p.xpanel + PANEL * i_P, PANEL,
+                 &bars[warp][slot]);
+        i_P = (i_P + 1 == p.Pn) ? 0u : i_P + 1;
     };
 
-    const std::uint32_t ncell = q1 - q0;
     // weights stream while the preceding xprep kernel is still running (PDL)
+    if (lane == 0) {
 #pragma unroll 1
-    for (int s = 0; s < NSLOT; ++s)
-        if (static_cast<std::uint32_t>(s) < ncell) issue_w(q0 + s, s);
+        for (int s = 0; s < NSLOT; ++s)
+            if (static_cast<std::uint32_t>(s) < ncell) issue_rec(s);
+    }
     pdl_wait();  // xprep has completed: x panels, partials and y are ours from here on
-    std::uint32_t Gc = q0 / p.Pn, P = q0 - Gc * p.Pn;
-    {
-        std::uint32_t Pi = P;
+    if (lane == 0) {
 #pragma unroll 1
-        for (int s = 0; s < NSLOT; ++s) {
-            if (static_cast<std::uint32_t>(s) < ncell) issue_x(Pi, s);
-            Pi = (Pi + 1 == p.Pn) ? 0u : Pi + 1;
-        }
+        for (int s = 0; s < NSLOT; ++s)
+            if (static_cast<std::uint32_t>(s) < ncell) issue_x(s);
     }
 
     float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
@@ -262,7 +264,6 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
 
 #pragma unroll 1
     for (std::uint32_t it = 0; it < ncell; ++it) {
-        const std::uint32_t q = q0 + it;
         const int slot = static_cast<int>(it % NSLOT);
         const std::uint32_t phase = (it / NSLOT) & 1u;
 
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
                 cw[u][4 * i + 2] = v.z;
                 cw[u][4 * i + 3] = v.w;
             }
-            load_stats<BS, BZ>(unit + CODEB + lane * SB, ss[u], zz[u]);
+            load_stats<BS, BZ>(unit + CODEB, lane, ss[u], zz[u]);
             sc[u][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
             sc[u][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
         }
@@ -457,12 +458,10 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             rs[lane] = 0.f;
         }
 
-        __syncwarp();
-        if (it + NSLOT < ncell) {
-            issue_w(q + NSLOT, slot);
-            std::uint32_t Pn_ = P + NSLOT;
-            while (Pn_ >= p.Pn) Pn_ -= p.Pn;
-            issue_x(Pn_, slot);
+        __syncwarp();  // every lane is done with the slot
+        if (lane == 0 && it + NSLOT < ncell) {
+            issue_rec(slot);
+            issue_x(slot);
         }
         if (++P == p.Pn) {
             flush(Gc, Gc * p.Pn >= q0);

@@ -12,7 +12,7 @@
 //                                       m16n8k16 MMAs of the unit (2 super-
 //                                       tiles x 8 blocks), in "containers"
 //   [stats  : 32 lanes x (BS+BZ) bytes] lane L's 8 scale codes then 8 zero
-//                                       codes, LSB-first
+//                                       codes, LSB-first (stat_byte_offset)
 //   [scalars: 16 blocks x 8 bytes     ]  binary16 {scale_s, scale_z, zero_s, zero_z}
 //
 // unit_bytes = 512*BW + 32*(BS+BZ) + 128 = 16 group records of the stream
@@ -96,6 +96,16 @@ inline constexpr std::uint32_t kPanelScBytes = 128;
 SPQR_HD constexpr std::uint32_t panel_xp_bytes(bool xlo) { return xlo ? 1024u : 512u; }  // f32 / f16 x
 SPQR_HD constexpr std::uint32_t panel_bytes(bool xlo) {
     return kPanelFragBytes + kPanelScBytes + panel_xp_bytes(xlo) + (xlo ? kPanelFragBytes : 0u);
+}
+
+// Byte b of lane L's statistics field inside the unit's stats area.  A
+// 6-byte field (3/3-bit statistics) is split into a 4-byte plane and a 2-byte
+// plane so that a lane reads it with two aligned loads; other widths are
+// lane-contiguous.
+SPQR_HD constexpr std::uint32_t stat_byte_offset(int lane, int b, int sb) {
+    return (sb > 4 && sb < 8)
+               ? (b < 4 ? 4u * lane + b : 128u + static_cast<std::uint32_t>(sb - 4) * lane + (b - 4))
+               : static_cast<std::uint32_t>(sb * lane + b);
 }
 
 // Entry packing of the per-cell outlier lists.

@@ -129,7 +129,7 @@ void pack_unit_stats(const UnitStage& u, int bs, int bz, std::uint8_t* dst) {
             put(8 * bs + eps * bz, bz, u.zcode[blk][row]);
         }
         for (int b = 0; b < sbytes; ++b)
-            dst[L * sbytes + b] = static_cast<std::uint8_t>(bits[b >> 3] >> (8 * (b & 7)));
+            dst[T::stat_byte_offset(L, b, sbytes)] = static_cast<std::uint8_t>(bits[b >> 3] >> (8 * (b & 7)));
     }
 }
 
@@ -139,7 +139,7 @@ void unpack_unit_stats(const std::uint8_t* src, int bs, int bz, UnitStage& u) {
         const int g = L >> 2, t = L & 3;
         std::uint64_t bits[2] = {0, 0};
         for (int b = 0; b < sbytes; ++b)
-            bits[b >> 3] |= static_cast<std::uint64_t>(src[L * sbytes + b]) << (8 * (b & 7));
+            bits[b >> 3] |= static_cast<std::uint64_t>(src[T::stat_byte_offset(L, b, sbytes)]) << (8 * (b & 7));
         auto get = [&](int pos, int nb) {
             std::uint32_t v = 0;
             for (int b = 0; b < nb; ++b, ++pos) v |= static_cast<std::uint32_t>((bits[pos >> 6] >> (pos & 63)) & 1u) << b;
