@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <stdexcept>
@@ -110,6 +111,14 @@ struct spqr_layer {
     std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, grid = 0, n_pad = 0;
     std::uint32_t nwarps[2] = {0, 0};
     std::uint32_t partial_slots[2] = {0, 0};
+    // gemv_cta plan, per x dtype (f16, f32: the panel size differs)
+    struct CtaPlan {
+        std::uint32_t nvcta = 0, grid = 0, nslot_log2 = 0, slot_bytes = 0, rec_cap = 0;
+        std::uint32_t pan_off = 0, part_off = 0, off_off = 0, gd_off = 0, part_cap = 0, smem = 0;
+        bool shared_x = false;  // x panels prepared once per CTA (they fit in shared memory)
+        std::uint32_t* d_start = nullptr;  // [nvcta+1]
+    } cta[2];
+    std::uint32_t pn_magic = 0;
     // own workspace
     mutable std::mutex mu;
     mutable void* d_ws = nullptr;
@@ -123,6 +132,7 @@ struct spqr_layer {
                         static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start[0]),
                         static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
                         static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws,
+                        static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
     }
@@ -145,7 +155,7 @@ spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
 
 // Workspace carve-up (bytes, 256-aligned pieces).
 struct WsLayout {
-    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, total = 0;
+    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, xchg = 0, total = 0;
 };
 std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 WsLayout ws_layout(const spqr_layer* L, int batch) {
@@ -157,6 +167,7 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
         w.panel_stride = static_cast<std::uint64_t>(L->Pn) * spqr_tiled::panel_bytes(true);
         w.panels = o; o += al(b * w.panel_stride);
         w.partial = o; o += al(static_cast<std::uint64_t>(std::max(L->partial_slots[0], L->partial_slots[1])) * 32 * 4);
+        w.xchg = o; o += al(static_cast<std::uint64_t>(L->Gn) * 32 * 8);
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
         w.xp = o; o += al(b * L->info.cols * 4);
@@ -189,6 +200,66 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
     cfg.numAttrs = 1;
     ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemv_tiled");
     ++g_launches;
+}
+
+
+// ---- gemv_cta (v13): producer warp + kNC consumer warps per CTA ----------
+constexpr int kNC = 16;  // 4 warps per SMSP, 128 registers each
+constexpr std::uint32_t kCtaStaticMax = 6144;  // static smem of gemv_cta (checked at first launch)
+
+bool use_legacy_tiled() {
+    static const bool legacy = [] {
+        const char* e = std::getenv("SPQR_KERNEL");
+        return e && std::string(e) == "tiled";
+    }();
+    return legacy;
+}
+
+template <int BW, int BSZ, bool XLO, bool SHX>
+void launch_cta_t(const spqr_dev::CtaParams& p, std::uint32_t grid, std::uint32_t smem, cudaStream_t st) {
+    auto kern = spqr_dev::gemv_cta<BW, BSZ, BSZ, XLO, kNC, SHX>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        cudaFuncAttributes fa{};
+        ck(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes(gemv_cta)");
+        if (fa.sharedSizeBytes > kCtaStaticMax)
+            throw CudaError("gemv_cta: static shared memory exceeds the planned budget");
+        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemLimit - kCtaStaticMax)),
+           "cudaFuncSetAttribute(gemv_cta smem)");
+        attr_set[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNC * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemv_cta");
+    ++g_launches;
+}
+
+void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, cudaStream_t st) {
+    const auto& c = L->cta[xlo ? 1 : 0];
+    const int key = L->info.weight_bits * 1000 + L->info.scale_bits * 100 + (xlo ? 10 : 0) + (c.shared_x ? 1 : 0);
+    switch (key) {
+#define SPQR_CASE(BW, BSZ)                                                                               \
+    case BW * 1000 + BSZ * 100 + 0: launch_cta_t<BW, BSZ, false, false>(p, c.grid, c.smem, st); break; \
+    case BW * 1000 + BSZ * 100 + 1: launch_cta_t<BW, BSZ, false, true>(p, c.grid, c.smem, st); break;  \
+    case BW * 1000 + BSZ * 100 + 10: launch_cta_t<BW, BSZ, true, false>(p, c.grid, c.smem, st); break; \
+    case BW * 1000 + BSZ * 100 + 11: launch_cta_t<BW, BSZ, true, true>(p, c.grid, c.smem, st); break;
+        SPQR_CASE(2, 2) SPQR_CASE(2, 3) SPQR_CASE(2, 4)
+        SPQR_CASE(3, 2) SPQR_CASE(3, 3) SPQR_CASE(3, 4)
+        SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
+#undef SPQR_CASE
+        default: spqr::fail(spqr::Errc::config_invalid, "no gemv_cta kernel instantiated for this layer");
+    }
 }
 
 // x panels for `batch` columns; column b's panels start at b * panel_stride.
@@ -257,6 +328,30 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
+    if (L->fast && !use_legacy_tiled()) {
+        // one fused launch per batch column (x preparation happens inside)
+        if (stage == 1) return;
+        const std::size_t esz = f16 ? 2 : 4;
+        const auto& c = L->cta[f16 ? 0 : 1];
+        for (int b = 0; b < batch; ++b) {
+            spqr_dev::CtaParams p{};
+            p.cells = L->d_cells;
+            p.cell_off = L->d_cell_off;
+            p.cta_start = c.d_start;
+            p.x = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b) * L->info.cols * esz;
+            p.order = static_cast<const std::uint32_t*>(L->d_order);
+            p.y = y + static_cast<std::size_t>(b) * L->info.rows;
+            p.xchg = reinterpret_cast<unsigned long long*>(base + w.xchg);
+            p.m = L->info.rows; p.n = L->info.cols; p.Pn = L->Pn; p.Gn = L->Gn; p.nvcta = c.nvcta;
+            p.pn_magic = L->pn_magic;
+            p.rec_cap = c.rec_cap; p.slot_bytes = c.slot_bytes;
+            p.pan_off = c.pan_off; p.part_off = c.part_off; p.off_off = c.off_off; p.gd_off = c.gd_off;
+            p.part_cap = c.part_cap;
+            p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0) ? 1u : 0u;
+            dispatch_cta(p, L, !f16, st);
+        }
+        return;
+    }
     if (L->fast) {
         auto* panels = base + w.panels;
         if (stage != 2) dispatch_xprep(x, f16, L, batch, panels, w.panel_stride, st);
@@ -363,6 +458,88 @@ void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, in
        "H2D wmap");
 }
 
+
+// gemv_cta partition: contiguous cell ranges balanced by bytes (record bytes +
+// a per-cell fixed cost), one range per CTA -- or several per CTA when the
+// per-range row-sum array would not fit shared memory.  Every range holds at
+// least Pn cells (a row-group pair is shared by at most two ranges; the
+// kernel's pair exchange relies on it); layers with fewer pairs than SMs get
+// one whole pair per range.  Plus the shared-memory plan: two record slots
+// per warp, per-warp x panels, the row-sum array, record offsets, pair counts.
+void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) {
+    auto& c = L->cta[xi];
+    const std::uint32_t Q = t.Gn * t.Pn;
+    const std::uint32_t cellb = t.cell_bytes;
+    const std::uint32_t panel = spqr_tiled::panel_bytes(xi == 1);
+    const std::uint32_t budget = kSmemLimit - kCtaStaticMax;
+    c.shared_x = t.Pn * panel <= 40u * 1024u;
+    const std::uint32_t pan_bytes = c.shared_x ? t.Pn * panel : kNC * panel;
+    constexpr std::uint32_t kPartMax = 48u * 1024u;  // row-sum array cap
+    const std::uint32_t S = static_cast<std::uint32_t>(sms);
+    std::vector<double> pre(Q + 1, 0.0);
+    for (std::uint32_t q = 0; q < Q; ++q) pre[q + 1] = pre[q] + 512.0 + (t.cell_off[q + 1] - t.cell_off[q]);
+    std::vector<std::uint32_t> st;
+    std::uint32_t mc = 0;
+    auto cut = [&](std::uint32_t nv) {  // byte-balanced cut; false if a range is shorter than Pn
+        st.assign(nv + 1, Q);
+        std::uint32_t q = 0;
+        for (std::uint32_t k = 0; k < nv; ++k) {
+            const double target = pre[Q] * k / nv;
+            while (q < Q && pre[q] + 0.5 * (pre[q + 1] - pre[q]) < target) ++q;
+            st[k] = q;
+        }
+        st[nv] = Q;
+        mc = 0;
+        bool ok = true;
+        for (std::uint32_t k = 0; k < nv; ++k) {
+            mc = std::max(mc, st[k + 1] - st[k]);
+            ok = ok && st[k + 1] - st[k] >= t.Pn;
+        }
+        return ok;
+    };
+    std::uint32_t nv = 0;
+    if (t.Gn <= S) {  // one whole pair per range
+        nv = t.Gn;
+        st.resize(nv + 1);
+        for (std::uint32_t k = 0; k <= nv; ++k) st[k] = k * t.Pn;
+        mc = t.Pn;
+    } else {
+        nv = S;
+        while (!cut(nv) && nv > 1) --nv;
+        while (mc * 128u > kPartMax) {  // more ranges than SMs: several per CTA
+            std::uint32_t nn = nv + S;
+            while (!cut(nn) && nn > nv + 1) --nn;
+            nv = nn;
+        }
+    }
+    c.nvcta = nv;
+    c.grid = std::min<std::uint32_t>(nv, S);
+    c.part_cap = std::max<std::uint32_t>(mc, 1);
+    const std::uint32_t part_bytes = (c.part_cap * 128u + 127u) & ~127u;
+    const std::uint32_t off_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
+    const std::uint32_t gd_bytes = off_bytes;
+    const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
+    // two record slots per warp; outliers beyond a slot are read from HBM
+    const std::uint32_t slot = std::min((ring_avail / (2u * kNC)) & ~127u, (cellb + 4096u + 127u) & ~127u);
+    if (slot < cellb + 16u) spqr::fail(spqr::Errc::config_invalid, "gemv_cta: shared memory plan does not fit");
+    c.slot_bytes = slot;
+    c.rec_cap = slot;
+    c.pan_off = slot * 2u * kNC;
+    c.part_off = c.pan_off + pan_bytes;
+    c.off_off = c.part_off + part_bytes;
+    c.gd_off = c.off_off + off_bytes;
+    c.smem = c.gd_off + gd_bytes;
+    c.d_start = dalloc<std::uint32_t>(st.size());
+    ck(cudaMemcpy(c.d_start, st.data(), 4 * st.size(), cudaMemcpyHostToDevice), "H2D cta_start");
+    if (xi == 0) {  // q / Pn as a multiply-high (Pn == 1: the kernel uses q itself)
+        const std::uint64_t mg = t.Pn > 1 ? ((1ull << 32) + t.Pn - 1) / t.Pn : 0;
+        L->pn_magic = static_cast<std::uint32_t>(mg);
+        if (t.Pn > 1)
+            for (std::uint64_t q = 0; q <= Q; ++q)
+                if (((q * mg) >> 32) != q / t.Pn)
+                    spqr::fail(spqr::Errc::config_invalid, "gemv_cta: cell index division out of range");
+    }
+}
 }  // namespace
 
 // ================================================================ C ABI ====
@@ -425,6 +602,8 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
             ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
             plan_partition(L.get(), t, sms, 0);
             plan_partition(L.get(), t, sms, 1);
+            plan_cta(L.get(), t, sms, 0);
+            plan_cta(L.get(), t, sms, 1);
             dev_bytes += t.cells.size() + 4 * t.cell_off.size();
         }
         L->info.fast_path = L->fast;
@@ -567,6 +746,16 @@ int spqr_dense_gemv_f16(const void* w_dev, const void* x_dev, float* y_dev, uint
 }
 
 int spqr_last_launch_count(void) { return g_launches; }
+
+#ifdef SPQR_TIMELINE
+// tools-only: copy the gemv_tiled per-warp timeline (8 x u64 per warp)
+int spqr_debug_timeline(unsigned long long* host, size_t count) {
+    return guard([&] {
+        ck(cudaMemcpyFromSymbol(host, spqr_dev::g_timeline, 8 * std::min<size_t>(count, 148 * 32 * 8)),
+           "timeline");
+    });
+}
+#endif
 
 int spqr_bench_layer(const spqr_layer* L, int repeats, double* ns3) {
     return guard([&] {

@@ -1,0 +1,601 @@
+// gemv_cta.cuh -- the fused SpQR decode-GEMV + CSR outlier merge, v13
+// (sm_100a).  Included by kernels.cuh (inside namespace spqr_dev).
+//
+// Reference semantics: matvec(t, x, plan), kernel.hpp:89-124 (x gather through
+// the permutation :93-98, per-tile dequant :100-111, CSR slices :112-120) --
+//   y[r] = sum_k  s(k,r) * sum_{c in k} (q(r,c) - z(k,r)) * x[c]  +  sum_outliers v * x[col]
+// computed per (row, 16-column block k) as  s*2^(24-e_k) * ( C + z * XX_k ),
+//   C = sum_c (q_c 2^(p_c-24)) (x_c 2^(e_k-p_c))   (m16n8k16 f16 MMA, exact products)
+//   XX_k = -2^-24 sum_c x_c 2^e_k.
+//
+// Structure (one CTA per SM, NC warps):
+//  * the host cuts the cell sequence (row-major 32x256 cells) into per-CTA
+//    contiguous, byte-balanced ranges ("vctas"; more vctas than CTAs only for
+//    layers whose per-CTA partial-sum array would not fit shared memory);
+//  * warps take cells dynamically (a shared ticket counter), so the warps of
+//    an SM finish together whatever their relative speed; each warp holds one
+//    ticket of lookahead and has already issued that cell's record copy
+//    (cp.async.bulk into the warp's second slot, mbarrier completion) while it
+//    computes the current one.  Issue is spread over all warps on purpose: a
+//    single producer thread caps at ~240 cycles per bulk copy (~4.8 TB/s for
+//    4 KB records, tools/tma_bench.cu).  The first records are issued before
+//    the preceding kernel has finished (PDL: weights do not depend on it);
+//  * each consumer prepares its cell's x panel itself (x gather through the
+//    permutation, per-block power-of-two scale, 2^-p column pre-scale, block
+//    sums) -- no separate x-preparation kernel, no x traffic through the ring;
+//  * per cell the warp writes 32 row sums (MMA part + outliers) to a per-CTA
+//    array and counts the cell against its row-group pair; the warp that
+//    completes a pair adds its cells' row sums in cell order and writes y --
+//    during the range, not after it.  A pair shared with a neighbouring range
+//    (ranges hold >= Pn cells, so at most two share a pair) is exchanged
+//    through one 64-bit {value, flag} word per row: the range that starts
+//    inside the pair finishes it first and publishes; the range that ends
+//    inside it adds the published value after its own and resets the word.
+//    No atomics on global memory, no fences, no end-of-kernel barrier.
+// Every reduction order is fixed by the partition, not by the schedule, so y
+// is bitwise reproducible run to run.
+
+struct CtaParams {
+    const std::uint8_t* cells;        // cell records
+    const std::uint32_t* cell_off;    // [ncell+1]
+    const std::uint32_t* cta_start;   // [nvcta+1] first cell of each range
+    const void* x;                    // this batch column, original column order (f16 or f32)
+    const std::uint32_t* order;       // solve position -> source column, or null
+    float* y;                         // [m] this batch column
+    unsigned long long* xchg;         // [Gn][32] {float value, u32 flag}, zero between launches
+    std::uint32_t m, n, Pn, Gn, nvcta;
+    std::uint32_t pn_magic;           // q / Pn == umulhi(q, pn_magic) for every cell index q
+    std::uint32_t rec_cap, slot_bytes;
+    std::uint32_t pan_off, part_off, off_off, gd_off, part_cap;
+    std::uint32_t x_vec;              // x is 16-B aligned and not permuted: vector loads
+};
+
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_sync_named(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ std::uint32_t pack_h2_rn(float lo, float hi) {
+    std::uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// One lane's share of a cell's x panel: columns 8*lane .. 8*lane+7 of panel P
+// (block kk = lane/2, half hf = lane%2).  load_x fetches them (through the
+// permutation, zero beyond n) -- issued one cell ahead; build_panel writes
+// the panel layout of tiled.hpp (panel_bytes): B rows fp16(x 2^(e-p)) [+ low
+// halves for fp32 x], {SC, XX} per block, x in solve order for the outlier
+// merge.  Same values as the v1-v12 xprep_tiled kernel: e = per-block
+// power-of-two scale (max |x| in [2^14, 2^15)), p = the column's code
+// pre-scale, SC = 2^(24-e), XX = -2^-24 sum_c x_c 2^e.
+template <bool XLO>
+struct XLane {
+    std::uint32_t w[XLO ? 8 : 4];  // fp16 pairs, or fp32 bit patterns
+};
+
+template <bool XLO>
+__device__ __forceinline__ XLane<XLO> load_x(const CtaParams& p, std::uint32_t P, int lane) {
+    XLane<XLO> r;
+    const std::uint32_t c0 = 256u * P + 8u * static_cast<std::uint32_t>(lane);
+    if constexpr (!XLO) {
+        if (p.x_vec && c0 + 8u <= p.n) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(p.x) + c0));
+            r.w[0] = v.x; r.w[1] = v.y; r.w[2] = v.z; r.w[3] = v.w;
+        } else {
+            std::uint32_t h[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const std::uint32_t c = c0 + i;
+                h[i] = 0;
+                if (c < p.n) h[i] = __ldg(reinterpret_cast<const unsigned short*>(p.x) + (p.order ? __ldg(p.order + c) : c));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r.w[i] = h[2 * i] | (h[2 * i + 1] << 16);
+        }
+    } else {
+        if (p.x_vec && c0 + 8u <= p.n) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(p.x) + c0));
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(p.x) + c0 + 4));
+            r.w[0] = a.x; r.w[1] = a.y; r.w[2] = a.z; r.w[3] = a.w;
+            r.w[4] = b.x; r.w[5] = b.y; r.w[6] = b.z; r.w[7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const std::uint32_t c = c0 + i;
+                r.w[i] = 0;
+                if (c < p.n) r.w[i] = __ldg(static_cast<const unsigned*>(p.x) + (p.order ? __ldg(p.order + c) : c));
+            }
+        }
+    }
+    return r;
+}
+
+template <int BW, bool XLO>
+__device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int pp, std::uint8_t* pan) {
+    constexpr std::uint32_t O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
+    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
+    float f[8];
+    if constexpr (!XLO) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 v = __half22float2(u32_as_h2(xl.w[i]));
+            f[2 * i] = v.x;
+            f[2 * i + 1] = v.y;
+        }
+        *reinterpret_cast<uint4*>(pan + O_XP + 16u * lane) = make_uint4(xl.w[0], xl.w[1], xl.w[2], xl.w[3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(xl.w[i]);
+        uint4* xp = reinterpret_cast<uint4*>(pan + O_XP + 32u * lane);
+        xp[0] = make_uint4(xl.w[0], xl.w[1], xl.w[2], xl.w[3]);
+        xp[1] = make_uint4(xl.w[4], xl.w[5], xl.w[6], xl.w[7]);
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(f[i]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    int e = 0;
+    if (mx > 0.f && mx < INFINITY) {
+        int E;
+        frexpf(mx, &E);  // mx = m * 2^E, m in [0.5, 1)
+        e = 15 - E;      // mx * 2^e in [2^14, 2^15)
+    }
+    // 2^(e - pp): for fp16 x, e - pp is in [-8, 38] and the scaling is a plain
+    // exact multiply; fp32 x can reach the edges of the exponent range
+    float s[8];
+    if constexpr (XLO) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = ldexpf(f[i], e - pp);
+    } else {
+        const float sc = __uint_as_float(static_cast<std::uint32_t>(127 + e - pp) << 23);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = f[i] * sc;
+    }
+    std::uint32_t hv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hv[i] = pack_h2_rn(s[2 * i], s[2 * i + 1]);
+    *reinterpret_cast<uint4*>(pan + 16u * lane) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    float eff[8];
+    if constexpr (XLO) {
+        std::uint32_t lv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 h = __half22float2(u32_as_h2(hv[i]));
+            lv[i] = pack_h2_rn(s[2 * i] - h.x, s[2 * i + 1] - h.y);
+            const float2 l = __half22float2(u32_as_h2(lv[i]));
+            eff[2 * i] = h.x + l.x;
+            eff[2 * i + 1] = h.y + l.y;
+        }
+        *reinterpret_cast<uint4*>(pan + O_LO + 16u * lane) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 h = __half22float2(u32_as_h2(hv[i]));
+            eff[2 * i] = h.x;
+            eff[2 * i + 1] = h.y;
+        }
+    }
+    float X = ((eff[0] + eff[1]) + (eff[2] + eff[3])) + ((eff[4] + eff[5]) + (eff[6] + eff[7]));
+    X *= __uint_as_float(static_cast<std::uint32_t>(127 + pp) << 23);  // exact: 2^pp
+    X += __shfl_xor_sync(0xffffffffu, X, 1);
+    if ((lane & 1) == 0) {
+        const int kk = lane >> 1;  // block 8h + 2t + bs
+        float* scp = reinterpret_cast<float*>(pan + O_SC) + 4 * (kk >> 1) + (kk & 1);
+        scp[0] = XLO ? ldexpf(1.0f, 24 - e) : __uint_as_float(static_cast<std::uint32_t>(127 + 24 - e) << 23);
+        scp[2] = -X * 5.9604644775390625e-08f;
+    }
+}
+
+// SHX: the CTA prepares all Pn x panels once (shared memory) instead of each
+// warp preparing its cell's panel -- for layers whose panels fit.
+template <int BW, int BS, int BZ, bool XLO, int NC, bool SHX>
+__global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
+    using G = Geo<BW>;
+    constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
+    constexpr std::uint32_t CELL = 2 * UNIT;
+    constexpr std::uint32_t CODEB = T::code_bytes(BW);
+    constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
+    constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
+    constexpr std::uint32_t O_FRAG = 0, O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
+    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
+    constexpr std::uint32_t MASK = (1u << BW) - 1u;
+    constexpr std::uint32_t SMASK = (1u << BS) - 1u, ZMASK = (1u << BZ) - 1u;
+    constexpr float kMagic = 8388608.0f;
+    constexpr int NT = NC * 32;
+
+    extern __shared__ __align__(128) std::uint8_t smem[];
+    __shared__ std::uint64_t full[NC][2];
+    __shared__ std::uint32_t slot_r[NC][2][2];       // record byte range of the slot's cell
+    __shared__ std::uint32_t tick[2];                // per-range ticket counters (by range parity)
+    __shared__ float rowsum[NC][32];                 // outlier row sums of a cell (zero between cells)
+    __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef SPQR_TIMELINE
+    const std::uint32_t wk = blockIdx.x * 16u + static_cast<std::uint32_t>(warp);
+    unsigned long long tl_wait = 0;
+    std::uint32_t tl_cnt = 0;
+#endif
+    SPQR_TL(0)
+
+    if (lane == 0) {
+        mbar_init(&full[warp][0], 1);
+        mbar_init(&full[warp][1], 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x == 0) tick[0] = tick[1] = 0;
+    rowsum[warp][lane] = 0.f;
+    if (lane < 4) zrow[warp][lane] = 0u;
+    std::uint32_t* coff = reinterpret_cast<std::uint32_t*>(smem + p.off_off);  // record offsets of the range
+    std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
+    auto range_setup = [&](std::uint32_t v) {
+        const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
+        for (std::uint32_t i = threadIdx.x; i <= q1 - q0; i += NT) {
+            coff[i] = __ldg(p.cell_off + q0 + i);
+            gdone[i] = 0;
+        }
+    };
+    if (blockIdx.x < p.nvcta) range_setup(blockIdx.x);
+    __syncthreads();
+    // the next kernel in the stream may be scheduled now; it reads what we
+    // write only after this grid has completed (its griddepcontrol.wait)
+    pdl_launch();
+
+    // ----------------------------------------------------------- consumers --
+    const int g = lane >> 2, t = lane & 3;
+    std::uint8_t* const pan_base = smem + p.pan_off;
+    std::uint8_t* pan = SHX ? pan_base : pan_base + static_cast<std::uint32_t>(warp) * PANEL;
+    float* part_base = reinterpret_cast<float*>(smem + p.part_off);
+    // ldmatrix row addresses for the masked B operand: MMA j of a super-tile
+    // routes block j to output column j, so B^T row n is block j's x when
+    // n == j and zero otherwise.  Call c loads MMAs 2c, 2c+1 (x4: k halves).
+    // Lane (lm, lr) addresses row lr of matrix lm; it carries data only in
+    // the call whose MMA j + lm/2 == lr, and then always the same 16 bytes of
+    // the panel (block 8h + lr, k half lm % 2) -- the per-call offset 256h is
+    // an immediate, so the zero row is pre-biased by -256h.
+    const int lm = lane >> 3, lr = lane & 7;
+    const int jact = lr - (lm >> 1);
+    const std::uint32_t lane_off = O_FRAG + 32u * lr + 16u * (lm & 1);
+    const std::uint32_t zero_sa = smem_u32(&zrow[warp][0]);
+    const std::uint32_t zb[2] = {zero_sa, zero_sa - 256u};
+    const std::uint32_t zl[2] = {zero_sa - (O_LO - O_FRAG), zero_sa - 256u - (O_LO - O_FRAG)};
+    const std::uint32_t magic = 0x4B000000u;
+    // this lane's x-preparation columns: block lane/2 of the panel, k half lane%2
+    const int pp = T::column_prescale(BW, static_cast<std::uint32_t>(lane >> 1), 8u * (lane & 1));
+
+    std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes;
+    // lane 0: copy the record of range ticket k into slot sl (offsets from coff)
+    auto issue = [&](std::uint32_t k, std::uint32_t sl) {
+        if (lane == 0) {
+            const std::uint32_t r0 = coff[k], r1 = coff[k + 1];
+            slot_r[warp][sl][0] = r0;
+            slot_r[warp][sl][1] = r1;
+            const std::uint32_t nb = min(r1 - r0, p.rec_cap);
+            mbar_expect_tx(&full[warp][sl], nb);
+            bulk_g2s(ring + sl * p.slot_bytes, p.cells + r0, nb, &full[warp][sl]);
+        }
+    };
+    std::uint32_t nit = 0;  // cells this warp has taken (slot nit & 1, phase (nit >> 1) & 1)
+
+    std::uint32_t it = 0;
+    bool waited = false;
+#pragma unroll 1
+    for (std::uint32_t v = blockIdx.x; v < p.nvcta; v += gridDim.x, ++it) {
+        const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
+        const std::uint32_t nc = q1 - q0;
+        float* part = part_base;
+        const std::uint32_t Ga = p.Pn == 1u ? q0 : __umulhi(q0, p.pn_magic);
+        auto pair_of = [&](std::uint32_t k) {
+            const std::uint32_t q = q0 + k;
+            return p.Pn == 1u ? q : __umulhi(q, p.pn_magic);
+        };
+        auto grab = [&]() {
+            std::uint32_t k = 0;
+            if (lane == 0) k = atomicAdd(&tick[it & 1u], 1u);
+            return __shfl_sync(0xffffffffu, k, 0);
+        };
+        auto panel_of = [&](std::uint32_t k) {
+            const std::uint32_t q = q0 + k;
+            return p.Pn == 1u ? 0u : q - __umulhi(q, p.pn_magic) * p.Pn;
+        };
+        // one ticket of lookahead: the next cell's record copy and x loads are
+        // in flight while this cell computes
+        std::uint32_t tk = grab();
+        if (tk < nc) issue(tk, nit & 1u);
+        if (!waited) {
+            pdl_wait();  // the preceding kernel has completed: x, y and the partial slots are ours
+            waited = true;
+            SPQR_TL(1)
+            if constexpr (SHX) {  // every panel once, for all ranges of this CTA
+#pragma unroll 1
+                for (std::uint32_t P = warp; P < p.Pn; P += NC)
+                    build_panel<BW, XLO>(load_x<XLO>(p, P, lane), lane, pp, pan_base + P * PANEL);
+                bar_sync_named(1, NT);
+            }
+        }
+        XLane<XLO> xl{};
+        if (!SHX && tk < nc) xl = load_x<XLO>(p, panel_of(tk), lane);
+#pragma unroll 1
+        while (tk < nc) {
+            const std::uint32_t tn = grab();
+            XLane<XLO> xn{};
+            if (tn < nc) {
+                issue(tn, (nit + 1u) & 1u);
+                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(tn), lane);
+            }
+            const std::uint32_t slot = nit & 1u;
+
+            if constexpr (SHX) {
+                pan = pan_base + panel_of(tk) * PANEL;
+            } else {
+                build_panel<BW, XLO>(xl, lane, pp, pan);
+                __syncwarp();
+            }
+            const std::uint32_t lane_sa = smem_u32(pan) + lane_off;
+#ifdef SPQR_TIMELINE
+            const unsigned long long tw0 = gtime();
+#endif
+            mbar_wait(&full[warp][slot], (nit >> 1) & 1u);
+#ifdef SPQR_TIMELINE
+            if (tl_cnt == 0) SPQR_TL(2)
+            tl_wait += gtime() - tw0;
+            ++tl_cnt;
+#endif
+            const std::uint8_t* cell = ring + slot * p.slot_bytes;
+            const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
+
+            // x operands of this panel (shared by both units)
+            float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
+#pragma unroll
+            for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(pan + O_SC)[4 * h + t];
+
+            // lane data of both units
+            std::uint32_t cw[2][G::LANE_WORDS];
+            std::uint32_t ss[2], zz[2];
+            uint4 sc[2][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const std::uint8_t* unit = cell + u * UNIT;
+#pragma unroll
+                for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                    const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                    cw[u][4 * i] = w4.x;
+                    cw[u][4 * i + 1] = w4.y;
+                    cw[u][4 * i + 2] = w4.z;
+                    cw[u][4 * i + 3] = w4.w;
+                }
+                load_stats<BS, BZ>(unit + CODEB, lane, ss[u], zz[u]);
+                sc[u][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
+                sc[u][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
+            }
+
+            // 4 independent MMA chains (super-tile h x unit u), interleaved
+            std::uint32_t bfr[2][4], lfr[2][4];
+            float cc[2][2][4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) cc[h][u][i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
+                    std::uint32_t bq[4], lq[4];
+                    if ((j & 1) == 0) {
+                        const bool act = jact == j;
+                        ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bq);
+                        if constexpr (XLO) ldsm_x4((act ? lane_sa : zl[h]) + (256u * h + (O_LO - O_FRAG)), lq);
+                        bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
+                        if constexpr (XLO) {
+                            lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
+                        }
+                    }
+                    const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
+                    std::uint32_t l0 = 0, l1 = 0;
+                    if constexpr (XLO) {
+                        l0 = lfr[h][2 * (j & 1)];
+                        l1 = lfr[h][2 * (j & 1) + 1];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const std::uint32_t* w = cw[u] + G::CW * cidx;
+                        std::uint32_t a[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                            const int i = rho * (G::NP / 2) + qq;
+                            const int B = (BW * i) >> 3, pb = (BW * i) & 7;
+                            a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
+                        }
+                        mma16816(cc[h][u], a, b0, b1);
+                        if constexpr (XLO) mma16816(cc[h][u], a, l0, l1);
+                    }
+                }
+            }
+            float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
+#pragma unroll
+            for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float (&c)[2][4] = cc[h];
+                const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint4 s4 = sc[u][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
+                    const __half2 s0 = u32_as_h2(s4.x), z0 = u32_as_h2(s4.y), s1 = u32_as_h2(s4.z),
+                                  z1 = u32_as_h2(s4.w);
+                    const float2 Ss = make_float2(__low2float(s0), __low2float(s1));
+                    const float2 Zs = make_float2(__high2float(s0), __high2float(s1));
+                    const float2 Sz = make_float2(__low2float(z0), __low2float(z1));
+                    const float2 Zz = make_float2(-__high2float(z0), -__high2float(z1));
+                    const float2 A1 = fmul2(Ss, SC);                         // s_s * 2^(24-e)
+                    const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));  // -s_s z_s 2^(24-e)
+                    const float2 B0 = fmul2(Sz, Zz);                         // -z_s z_z
+#pragma unroll
+                    for (int rho = 0; rho < 2; ++rho) {
+                        const int e0i = 4 * h + rho, e1i = 4 * h + 2 + rho;  // eps of (bs=0, bs=1)
+                        const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss[u], e0i * BS, magic),
+                                                            magic_field_rt<SMASK>(ss[u], e1i * BS, magic)),
+                                                make_float2(-kMagic, -kMagic));
+                        const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz[u], e0i * BZ, magic),
+                                                            magic_field_rt<ZMASK>(zz[u], e1i * BZ, magic)),
+                                                make_float2(-kMagic, -kMagic));
+                        const float2 shat = ffma2(A1, cs, A0);
+                        const float2 zhat = ffma2(Sz, cz, B0);
+                        const float2 tt = ffma2(zhat, XX, make_float2(c[u][2 * rho], c[u][2 * rho + 1]));
+                        acc[u][rho] = ffma2(shat, tt, acc[u][rho]);
+                    }
+                }
+            }
+
+            // outliers: entries (row, col, value) of this cell, sorted by (row,
+            // col), 0xffffffff padding (row 255).  Chunks of 128 entries, 4
+            // consecutive per lane (one 16-byte load): products, a segmented
+            // inclusive scan by row, and the last entry of each row in the
+            // chunk adds the row total to rowsum.  Chunks run in order, so the
+            // sums are deterministic.  Entries beyond the staged part of the
+            // record are read from global memory.
+            const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+            float* rs = rowsum[warp];
+            if (cnt) {
+                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
+                auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
+                    uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
+                    const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                    std::uint32_t k[4];
+                    float sv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        k[j] = e[j] >> 24;
+                        const std::uint32_t c = (e[j] >> 16) & 255u;
+                        float xv;
+                        if constexpr (XLO)
+                            xv = reinterpret_cast<const float*>(pan + O_XP)[c];
+                        else
+                            xv = __half2float(reinterpret_cast<const __half*>(pan + O_XP)[c]);
+                        sv[j] = h2f_bits(e[j] & 0xffffu) * xv;
+                    }
+                    bool same[3];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        same[j] = k[j + 1] == k[j];
+                        if (same[j]) sv[j + 1] += sv[j];
+                    }
+                    const std::uint32_t K = k[3];
+                    const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
+                    const bool head = lane == 0 || pK != K;
+                    const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
+                    const int seg0 = 31 - __clz(heads);
+                    float V = sv[3];
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const float o = __shfl_up_sync(0xffffffffu, V, d);
+                        if (lane - d >= seg0) V += o;
+                    }
+                    float cin = __shfl_up_sync(0xffffffffu, V, 1);
+                    if (lane == 0 || pK != k[0]) cin = 0.f;
+                    const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
+                        if (tail && k[j] < 32u) {
+                            const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
+                            if (first)
+                                rs[k[j]] = tot;
+                            else
+                                rs[k[j]] += tot;
+                        }
+                    }
+                };
+                chunk(es, 4u * lane, nfast, true);
+#pragma unroll 1
+                for (std::uint32_t base = 128; base < nfast; base += 128) {
+                    __syncwarp();
+                    chunk(es, base + 4u * lane, nfast, false);
+                }
+#pragma unroll 1
+                for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
+                    __syncwarp();
+                    chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);
+                }
+            }
+
+            // the cell's 32 row sums: MMA part (lanes t == 0 after the butterfly),
+            // then the outlier part (lane = row)
+            float* prow = part + tk * 32u;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    float a = acc[u][r].x + acc[u][r].y;
+                    a += __shfl_xor_sync(0xffffffffu, a, 1);
+                    a += __shfl_xor_sync(0xffffffffu, a, 2);
+                    if (t == 0) prow[16 * u + 8 * r + g] = a;
+                }
+            __syncwarp();
+            if (cnt) {
+                prow[lane] += rs[lane];
+                rs[lane] = 0.f;
+                __syncwarp();
+            }
+            // count the cell against its pair; the warp that completes the pair
+            // reduces it (row = lane, cells in order) and writes y
+            const std::uint32_t Gq = pair_of(tk);
+            const std::uint32_t cs = Gq * p.Pn, ce = cs + p.Pn;
+            const std::uint32_t a = max(cs, q0), b = min(ce, q1);
+            __threadfence_block();  // this cell's row sums before the count
+            std::uint32_t done = 0;
+            if (lane == 0) done = atomicAdd(&gdone[Gq - Ga], 1u) + 1u;
+            done = __shfl_sync(0xffffffffu, done, 0);
+            if (done == b - a) {
+                __threadfence_block();
+                float sum = 0.f;
+                const float* src = part + (a - q0) * 32u + lane;
+#pragma unroll 4
+                for (std::uint32_t qq = a; qq < b; ++qq, src += 32) sum += *src;
+                const std::uint32_t row = 32u * Gq + lane;
+                unsigned long long* xw = p.xchg + static_cast<std::size_t>(Gq) * 32u + lane;
+                if (a == cs && b == ce) {  // the pair is ours alone
+                    if (row < p.m) p.y[row] = sum;
+                } else if (a != cs) {      // we hold the pair's last cells: publish
+                    const unsigned long long w = (1ull << 32) | __float_as_uint(sum);
+                    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(xw), "l"(w) : "memory");
+                } else {                   // we hold its first cells: add the published rest
+                    unsigned long long w;
+                    do {
+                        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
+                    } while ((w >> 32) == 0ull);
+                    if (row < p.m) p.y[row] = sum + __uint_as_float(static_cast<std::uint32_t>(w));
+                    *xw = 0ull;
+                }
+            }
+            __syncwarp();  // every lane is done with the slot before it is refilled
+            tk = tn;
+            xl = xn;
+            ++nit;
+        }
+        SPQR_TL(3)
+        if (v + gridDim.x < p.nvcta) {  // this CTA has another range
+            bar_sync_named(1, NT);
+            if (threadIdx.x == 0) tick[it & 1u] = 0;
+            range_setup(v + gridDim.x);
+            bar_sync_named(1, NT);
+        }
+    }
+#ifdef SPQR_TIMELINE
+    SPQR_TL(4)
+    if (lane == 0) {
+        g_timeline[8 * wk + 5] = tl_cnt;
+        g_timeline[8 * wk + 6] = tl_wait;
+        g_timeline[8 * wk + 7] = 0;
+    }
+#endif
+}

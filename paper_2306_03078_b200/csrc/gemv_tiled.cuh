@@ -96,6 +96,21 @@ __device__ __forceinline__ void load_stats(const std::uint8_t* stats, int lane, 
     }
 }
 
+#ifdef SPQR_TIMELINE
+// tools-only instrumentation (tools/timeline_dev.py): per warp %globaltimer at
+// entry, after the PDL wait, first cell staged, loop end, exit.
+__device__ unsigned long long g_timeline[148 * 32 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SPQR_TL(k) \
+    if (lane == 0 && wk < 148 * 32) g_timeline[8 * wk + (k)] = gtime();
+#else
+#define SPQR_TL(k)
+#endif
+
 template <int BW, int BS, int BZ, bool XLO, int NW, int NSLOT>
 __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     using G = Geo<BW>;
@@ -123,6 +138,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     const std::uint32_t wk = blockIdx.x * NW + warp;
     const std::uint32_t q0 = p.warp_start[wk], q1 = p.warp_start[wk + 1];
     std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * NSLOT * p.slot_bytes;
+    SPQR_TL(0)
 
     // the next layer's xprep may launch now; it reads x only after this grid
     // has completed (its griddepcontrol.wait), so the tails of consecutive
@@ -174,6 +190,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             if (static_cast<std::uint32_t>(s) < ncell) issue_rec(s);
     }
     pdl_wait();  // xprep has completed: x panels, partials and y are ours from here on
+    SPQR_TL(1)
     if (lane == 0) {
 #pragma unroll 1
         for (int s = 0; s < NSLOT; ++s)
@@ -202,6 +219,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
     if (lane < 4) zrow[warp][lane] = 0u;
     rowsum[warp][lane] = 0.f;
     __syncwarp();
+#ifdef SPQR_TIMELINE
+    std::uint32_t r_last_cnt = 0;
+#endif
     float orow_reg = 0.f;  // outlier sum of local row `lane` (current row-group pair)
 
     auto flush = [&](std::uint32_t Gf, bool whole) {
@@ -268,6 +288,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         const std::uint32_t phase = (it / NSLOT) & 1u;
 
         mbar_wait(&bars[warp][slot], phase);
+#ifdef SPQR_TIMELINE
+        if (it == 0) SPQR_TL(2)
+#endif
         const std::uint8_t* sl = ring + static_cast<std::size_t>(slot) * p.slot_bytes;
         const std::uint8_t* cell = sl + O_REC;
         const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
@@ -387,6 +410,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
         // Chunks run in order, so the sums are deterministic.  Entries beyond
         // the staged part of the record are read from global memory.
         const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+#ifdef SPQR_TIMELINE
+        r_last_cnt += cnt;
+#endif
         if (cnt) {
             const std::uint32_t nfast = (min(r1 - r0, p.rec_cap_bytes) - CELL) / 4u;
             const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);  // in our slot
@@ -469,5 +495,16 @@ __global__ void __launch_bounds__(NW * 32, 1) gemv_tiled(const TiledParams p) {
             ++Gc;
         }
     }
+    SPQR_TL(3)
+#ifdef SPQR_TIMELINE
+    if (lane == 0) {
+        unsigned smid;
+        asm("mov.u32 %0, %smid;" : "=r"(smid));
+        g_timeline[8 * wk + 5] = ncell;
+        g_timeline[8 * wk + 6] = smid;
+        g_timeline[8 * wk + 7] = r_last_cnt;
+    }
+#endif
     if (P != 0) flush(Gc, false);  // range ended inside row-group pair Gc
+    SPQR_TL(4)
 }

@@ -1,0 +1,86 @@
+"""Device-side timeline of one gemv_tiled launch (tools-only build with
+-DSPQR_TIMELINE): per warp %globaltimer at entry, after the PDL wait, first
+cell staged, loop end and exit, relative to the earliest warp entry.
+
+    python tools/timeline_dev.py [MxN ...]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2306_03078_b200 import build as B  # noqa: E402
+
+lib_path = os.path.join(ROOT, "build", "libspqr_tl.so")
+if not os.path.exists(lib_path):
+    B.build(out=lib_path, defines=("SPQR_TIMELINE",))
+os.environ["SPQR_LIB"] = lib_path
+import torch  # noqa: E402
+
+import paper_2306_03078_b200 as P  # noqa: E402
+from paper_2306_03078_b200 import synth  # noqa: E402
+
+P.LIB_PATH = lib_path
+lib = P.lib()
+lib.spqr_debug_timeline.restype = C.c_int
+lib.spqr_debug_timeline.argtypes = [C.c_void_p, C.c_size_t]
+shapes = [tuple(map(int, s.split("x"))) for s in sys.argv[1:]] or [(8192, 8192), (22016, 8192)]
+for m, n in shapes:
+    s = synth.random_stream(m, n, 3, 3, 3, 0.01, seed=5)
+    Ls = [P.Layer(s, device=0) for _ in range(4)]
+    x = torch.randn(n, device="cuda").half()
+    y = torch.empty(m, device="cuda")
+    st = torch.cuda.Stream()
+    for L in Ls:
+        L.matvec(x, y, stream=st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for L in Ls:
+            L.matvec(x, y, stream=st)
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
+    buf = np.zeros(148 * 32 * 8, dtype=np.uint64)
+    assert lib.spqr_debug_timeline(buf.ctypes.data, buf.size) == 0
+    T = buf.reshape(-1, 8).astype(np.int64)
+    if os.environ.get("SPQR_KERNEL") != "tiled":  # gemv_cta: producer rows have no exit stamp
+        prod = T[(T[:, 7] == 1) & (T[:, 3] > 0)]
+        t0p = T[T[:, 0] > 0][:, 0].min()
+        if len(prod): print(f"== {m}x{n} producers: n={len(prod)} done at (us) " +
+              " ".join(f"{v:7.2f}" for v in np.percentile((prod[:, 3] - t0p) / 1e3, [0, 50, 100])) +
+              f"; empty waits/cell {prod[:, 5].mean():.1f}, wait us/producer " +
+              " ".join(f"{v:6.2f}" for v in np.percentile(prod[:, 6] / 1e3, [0, 50, 100])))
+        cons = T[(T[:, 7] == 0) & (T[:, 4] > 0)]
+        print(f"   consumers: full-wait us/warp " +
+              " ".join(f"{v:6.2f}" for v in np.percentile(cons[:, 6] / 1e3, [0, 50, 100])) +
+              f"; cells/warp {cons[:, 5].mean():.2f}")
+        T[:, 5:] = 0
+    t = T[:, :5]
+    meta = T[:, 5:][t[:, 4] > 0]
+    t = t[t[:, 4] > 0]
+    t0 = t[:, 0].min()
+    r = (t - t0) / 1e3  # us
+    print(f"== {m}x{n}: {len(t)} warps, span {r[:, 4].max():.2f} us")
+    for k, name in enumerate(["entry", "pdl_wait", "first_cell", "loop_end", "exit"]):
+        q = np.percentile(r[:, k], [0, 10, 50, 90, 100])
+        print(f"  {name:11s} " + " ".join(f"{v:7.2f}" for v in q))
+    work = r[:, 3] - r[:, 2]
+    print(f"  loop time   " + " ".join(f"{v:7.2f}" for v in np.percentile(work, [0, 10, 50, 90, 100])))
+    ends = np.sort(r[:, 4])
+    for f in (0.5, 0.9, 0.99):
+        print(f"  {int(f * 100)}% of warps done by {ends[int(f * len(ends)) - 1]:.2f} us")
+    order = np.argsort(-work)
+    print("  slowest warps: loop_us cells smid outliers")
+    for i in order[:8]:
+        print(f"    {work[i]:6.2f} {meta[i, 0]:3d} {meta[i, 1]:4d} {meta[i, 2]:5d}")
+    print("  fastest:", [(round(work[i], 2), int(meta[i, 0]), int(meta[i, 2])) for i in order[-4:]])
+    for c in sorted(set(meta[:, 0].tolist())):
+        sel = meta[:, 0] == c
+        print(f"  cells={c}: n={sel.sum()} loop median {np.median(work[sel]):.2f} max {work[sel].max():.2f}")
+    for L in Ls:
+        L.close()
