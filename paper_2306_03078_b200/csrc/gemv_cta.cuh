@@ -310,8 +310,13 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             SPQR_TL(1)
             if constexpr (SHX) {  // every panel once, for all ranges of this CTA
 #pragma unroll 1
-                for (std::uint32_t P = warp; P < p.Pn; P += NC)
-                    build_panel<BW, XLO>(load_x<XLO>(p, P, lane), lane, pp, pan_base + P * PANEL);
+                for (std::uint32_t P = warp; P < p.Pn; P += 2 * NC) {  // two panels' x in flight
+                    const XLane<XLO> xa = load_x<XLO>(p, P, lane);
+                    XLane<XLO> xb{};
+                    if (P + NC < p.Pn) xb = load_x<XLO>(p, P + NC, lane);
+                    build_panel<BW, XLO>(xa, lane, pp, pan_base + P * PANEL);
+                    if (P + NC < p.Pn) build_panel<BW, XLO>(xb, lane, pp, pan_base + (P + NC) * PANEL);
+                }
                 bar_sync_named(1, NT);
             }
         }
@@ -528,18 +533,21 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 }
             }
 
-            // the cell's 32 row sums: MMA part (lanes t == 0 after the butterfly),
-            // then the outlier part (lane = row)
+            // the cell's 32 row sums.  Lane (g, t) holds partials of rows
+            // 16u + 8rho + g (combo c = 2u + rho) over its blocks; a 4x4
+            // transpose-add across the quad leaves lane t with combo c = t.
             float* prow = part + tk * 32u;
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    float a = acc[u][r].x + acc[u][r].y;
-                    a += __shfl_xor_sync(0xffffffffu, a, 1);
-                    a += __shfl_xor_sync(0xffffffffu, a, 2);
-                    if (t == 0) prow[16 * u + 8 * r + g] = a;
-                }
+            {
+                float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
+                float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
+                const bool o1 = t & 1, o2 = t & 2;
+                const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
+                const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
+                const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 1);
+                const float b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 1);
+                const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
+                prow[16 * (t >> 1) + 8 * (t & 1) + g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
             __syncwarp();
             if (cnt) {
                 prow[lane] += rs[lane];
@@ -595,7 +603,9 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if (lane == 0) {
         g_timeline[8 * wk + 5] = tl_cnt;
         g_timeline[8 * wk + 6] = tl_wait;
-        g_timeline[8 * wk + 7] = 0;
+        unsigned smid;
+        asm("mov.u32 %0, %smid;" : "=r"(smid));
+        g_timeline[8 * wk + 7] = 1000u + smid;
     }
 #endif
 }

@@ -2,7 +2,7 @@
 prepared once (stage 1), then the fused kernel (stage 2) once per layer, twice.
 
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        -k regex:gemv_tiled -s 7 -c 7 --csv python tools/profile_block.py
+        -k regex:gemv_cta -s 7 -c 7 --csv python tools/profile_block.py
 """
 import os
 import sys

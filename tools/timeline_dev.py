@@ -55,7 +55,20 @@ for m, n in shapes:
               " ".join(f"{v:7.2f}" for v in np.percentile((prod[:, 3] - t0p) / 1e3, [0, 50, 100])) +
               f"; empty waits/cell {prod[:, 5].mean():.1f}, wait us/producer " +
               " ".join(f"{v:6.2f}" for v in np.percentile(prod[:, 6] / 1e3, [0, 50, 100])))
-        cons = T[(T[:, 7] == 0) & (T[:, 4] > 0)]
+        cons = T[(T[:, 7] >= 1000) & (T[:, 4] > 0)]
+        # per CTA: slowest warp's loop end vs SM id and CTA index
+        t0c = T[T[:, 0] > 0][:, 0].min()
+        per = {}
+        for i, row in enumerate(T):
+            if row[7] >= 1000 and row[4] > 0:
+                b = i // 16
+                per.setdefault(b, [row[7] - 1000, 0])
+                per[b][1] = max(per[b][1], (row[3] - t0c) / 1e3)
+        items = sorted(per.items(), key=lambda kv: kv[1][1])
+        print("   per-CTA last loop end (us): fastest", [(b, sm, round(t, 2)) for b, (sm, t) in items[:5]])
+        print("                               slowest", [(b, sm, round(t, 2)) for b, (sm, t) in items[-8:]])
+        ends = np.array([t for _, (sm, t) in items])
+        print("   per-CTA end percentiles", " ".join(f"{v:6.2f}" for v in np.percentile(ends, [0, 10, 50, 90, 100])))
         print(f"   consumers: full-wait us/warp " +
               " ".join(f"{v:6.2f}" for v in np.percentile(cons[:, 6] / 1e3, [0, 50, 100])) +
               f"; cells/warp {cons[:, 5].mean():.2f}")

@@ -18,7 +18,7 @@ iid = hdr.index("ID")
 per = {}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
 for r in rows[1:]:
-    if "gemv_tiled" not in r[ik]:
+    if "gemv_cta" not in r[ik]:
         continue
     v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1)
     per.setdefault(int(r[iid]), {})[r[im]] = v
@@ -31,7 +31,7 @@ for (name, m, n), a, d in zip(bench.LAYERS, alg, launches):
     items.append({"layer": name, "shape": f"{m}x{n}", "alg_bytes": a, "dram_bytes": int(dram),
                   "dram_over_alg": round(dram / a, 4), "ncu_us": round(d["gpu__time_duration.sum"] / 1e3, 3)})
 res = {"source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                 "--clock-control none -k regex:gemv_tiled (tools/profile_block.py), cold cache per launch",
+                 "--clock-control none -k regex:gemv_cta (tools/profile_block.py), cold cache per launch",
        "dram_bytes_per_launch_avg": int(sum(i["dram_bytes"] for i in items) / len(items)),
        "alg_bytes_per_launch_avg": int(sum(i["alg_bytes"] for i in items) / len(items)),
        "launches": items}
