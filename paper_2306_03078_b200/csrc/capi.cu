@@ -119,6 +119,13 @@ struct spqr_layer {
         std::uint32_t* d_start = nullptr;  // [nvcta+1]
     } cta[2];
     std::uint32_t pn_magic = 0;
+    // gemm_tc plan (batch >= 2): ranges of (128-row tile, panel) units
+    struct TcPlan {
+        std::uint32_t nv = 0, Tn = 0, pslots = 0, slot_bytes = 0;
+        int sigma = 0;
+        std::uint32_t* d_start = nullptr;  // [nv+1]
+        std::uint32_t* d_maps = nullptr;   // gmap [2*Tn] then cmap [2*nv]
+    } tcp;
     // own workspace
     mutable std::mutex mu;
     mutable void* d_ws = nullptr;
@@ -133,6 +140,7 @@ struct spqr_layer {
                         static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
                         static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
+                        static_cast<void*>(tcp.d_start), static_cast<void*>(tcp.d_maps),
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
     }
@@ -155,7 +163,8 @@ spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
 
 // Workspace carve-up (bytes, 256-aligned pieces).
 struct WsLayout {
-    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, xchg = 0, total = 0;
+    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, xchg = 0;
+    std::uint64_t tc_x = 0, tc_part = 0, tc_cnt = 0, total = 0;
 };
 std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 WsLayout ws_layout(const spqr_layer* L, int batch) {
@@ -168,6 +177,11 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
         w.panels = o; o += al(b * w.panel_stride);
         w.partial = o; o += al(static_cast<std::uint64_t>(std::max(L->partial_slots[0], L->partial_slots[1])) * 32 * 4);
         w.xchg = o; o += al(static_cast<std::uint64_t>(L->Gn) * 32 * 8);
+        if (batch >= 2) {  // gemm_tc: x tiles for N <= 128, partial tiles, per-warp tile counters
+            w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
+            w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
+            w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 4 * 4);
+        }
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
         w.xp = o; o += al(b * L->info.cols * 4);
@@ -206,6 +220,14 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
 // ---- gemv_cta (v13): producer warp + kNC consumer warps per CTA ----------
 constexpr int kNC = 16;  // 4 warps per SMSP, 128 registers each
 constexpr std::uint32_t kCtaStaticMax = 6144;  // static smem of gemv_cta (checked at first launch)
+
+bool use_batch_loop() {  // A/B switch: batch >= 2 as repeated batch-1 launches
+    static const bool loop = [] {
+        const char* e = std::getenv("SPQR_BATCH");
+        return e && std::string(e) == "loop";
+    }();
+    return loop;
+}
 
 bool use_legacy_tiled() {
     static const bool legacy = [] {
@@ -259,6 +281,97 @@ void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, c
         SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
 #undef SPQR_CASE
         default: spqr::fail(spqr::Errc::config_invalid, "no gemv_cta kernel instantiated for this layer");
+    }
+}
+
+
+// ---- gemm_tc (batch >= 2): 4 dequant warps + 1 control warp per CTA -------
+constexpr std::uint32_t kTcStaticMax = 2048;
+constexpr std::uint32_t kTcMaxN = 128;  // batch columns per launch
+std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N) {
+    return 2u * 128u * 128u * 2u + 2u * 256u * N + 8u * L->tcp.slot_bytes + 4u * 8192u;
+}
+
+template <int BW, int BSZ>
+void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t st) {
+    auto kern = spqr_dev::gemm_tc<BW, BSZ, BSZ>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        cudaFuncAttributes fa{};
+        ck(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes(gemm_tc)");
+        if (fa.sharedSizeBytes > kTcStaticMax) throw CudaError("gemm_tc: static shared memory exceeds the plan");
+        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemLimit - kTcStaticMax)),
+           "cudaFuncSetAttribute(gemm_tc smem)");
+        attr_set[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.nv);
+    cfg.blockDim = dim3(160);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemm_tc");
+    ++g_launches;
+}
+
+void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
+            cudaStream_t st) {
+    const std::size_t esz = f16 ? 2 : 4;
+    for (int b0 = 0; b0 < batch; b0 += static_cast<int>(kTcMaxN)) {
+        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, static_cast<int>(kTcMaxN)));
+        const std::uint32_t N = (B + 15u) & ~15u;
+        const void* xb = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b0) * L->info.cols * esz;
+        std::uint8_t* xpan = base + w.tc_x;
+        {
+            const std::uint32_t total = 2u * L->Pn * N * 16u;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((total + 255u) / 256u);
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_tc, xb, f16, L->info.cols, B, N, L->Pn,
+                                  static_cast<const std::uint32_t*>(L->d_order), xpan),
+               "launch xprep_tc");
+            ++g_launches;
+        }
+        spqr_dev::TcParams p{};
+        p.cells = L->d_cells;
+        p.cell_off = L->d_cell_off;
+        p.cta_start = L->tcp.d_start;
+        p.gmap = L->tcp.d_maps;
+        p.cmap = L->tcp.d_maps + 2 * L->tcp.Tn;
+        p.xpanels = xpan;
+        p.y = y + static_cast<std::size_t>(b0) * L->info.rows;
+        p.partial = reinterpret_cast<float*>(base + w.tc_part);
+        p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
+        p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
+        p.rec_cap = L->tcp.slot_bytes; p.slot_bytes = L->tcp.slot_bytes;
+        p.sigma = L->tcp.sigma;
+        p.out_scale = std::ldexp(1.0f, L->tcp.sigma);
+        const std::uint32_t smem = tc_smem(L, N);
+        switch (L->info.weight_bits * 10 + L->info.scale_bits) {
+            case 22: launch_tc_t<2, 2>(p, smem, st); break;
+            case 23: launch_tc_t<2, 3>(p, smem, st); break;
+            case 24: launch_tc_t<2, 4>(p, smem, st); break;
+            case 32: launch_tc_t<3, 2>(p, smem, st); break;
+            case 33: launch_tc_t<3, 3>(p, smem, st); break;
+            case 34: launch_tc_t<3, 4>(p, smem, st); break;
+            case 42: launch_tc_t<4, 2>(p, smem, st); break;
+            case 43: launch_tc_t<4, 3>(p, smem, st); break;
+            case 44: launch_tc_t<4, 4>(p, smem, st); break;
+            default: spqr::fail(spqr::Errc::config_invalid, "no gemm_tc kernel instantiated for this layer");
+        }
     }
 }
 
@@ -328,6 +441,11 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
+    if (L->fast && !use_legacy_tiled() && batch >= 2 && !use_batch_loop()) {
+        if (stage == 1) return;
+        run_tc(L, x, f16, y, batch, base, w, st);
+        return;
+    }
     if (L->fast && !use_legacy_tiled()) {
         // one fused launch per batch column (x preparation happens inside)
         if (stage == 1) return;
@@ -540,6 +658,74 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
                     spqr::fail(spqr::Errc::config_invalid, "gemv_cta: cell index division out of range");
     }
 }
+
+// gemm_tc partition: units (128-row tile T, panel P), T-major, cut into
+// byte-balanced contiguous ranges (one per CTA); tiles shared by several
+// ranges are reduced through partial slots in range order.  sigma: the
+// per-layer power of two that keeps s * 2^(24 - p - sigma) < 2^15 for every
+// first-level scale s (binary16 range of the dequantization multiplier).
+void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const spqr::detail::StreamView& v, int sms) {
+    auto& c = L->tcp;
+    c.Tn = (t.Gn + 3u) / 4u;
+    const std::uint32_t U = c.Tn * t.Pn;
+    std::vector<double> pre(U + 1, 0.0);
+    for (std::uint32_t u = 0; u < U; ++u) {
+        const std::uint32_t T_ = u / t.Pn, P = u % t.Pn;
+        double b = 2048.0;
+        for (std::uint32_t i = 0; i < 4; ++i) {
+            const std::uint32_t G = 4 * T_ + i;
+            if (G < t.Gn) b += t.cell_off[G * t.Pn + P + 1] - t.cell_off[G * t.Pn + P];
+        }
+        pre[u + 1] = pre[u] + b;
+    }
+    const std::uint32_t nv = std::max<std::uint32_t>(1, std::min<std::uint32_t>(static_cast<std::uint32_t>(sms), U));
+    std::vector<std::uint32_t> st(nv + 1, U);
+    std::uint32_t q = 0;
+    for (std::uint32_t k = 0; k < nv; ++k) {
+        const double target = pre[U] * k / nv;
+        while (q < U && pre[q] + 0.5 * (pre[q + 1] - pre[q]) < target) ++q;
+        st[k] = q;
+    }
+    st[nv] = U;
+    c.nv = nv;
+    std::vector<std::uint32_t> gmap(2ull * c.Tn, 0), cmap(2ull * nv, 0);
+    for (std::uint32_t k = 0; k < nv; ++k) {
+        const std::uint32_t a = st[k], b = st[k + 1];
+        if (a >= b) continue;
+        const std::uint32_t ta = a / t.Pn, tb = (b - 1) / t.Pn;
+        const bool whole_a = a == ta * t.Pn && (tb != ta || b == (ta + 1) * t.Pn);
+        if (!whole_a) cmap[2 * k] = gmap[2 * ta + 1]++;
+        if (tb != ta && b != (tb + 1) * t.Pn) cmap[2 * k + 1] = gmap[2 * tb + 1]++;
+    }
+    std::uint32_t slots = 0;
+    for (std::uint32_t T_ = 0; T_ < c.Tn; ++T_) {
+        gmap[2 * T_] = slots;
+        slots += gmap[2 * T_ + 1];
+    }
+    c.pslots = slots;
+    c.slot_bytes = (t.cell_bytes + 2048u + 127u) & ~127u;
+    const std::uint32_t need = 2u * 128u * 128u * 2u + 2u * 256u * kTcMaxN + 8u * c.slot_bytes + 4u * 8192u;
+    if (need + kTcStaticMax > kSmemLimit)
+        c.slot_bytes = ((kSmemLimit - kTcStaticMax - (need - 8u * c.slot_bytes)) / 8u) & ~127u;
+    if (c.slot_bytes < t.cell_bytes + 16u) spqr::fail(spqr::Errc::config_invalid, "gemm_tc: shared memory plan");
+    // sigma from the first-level scale bound
+    double smax = 0.0;
+    const int top = (1 << v.sb) - 1;
+    for (std::uint32_t k = 0; k < v.nblocks; ++k)
+        for (std::uint32_t g = 0; g < v.ngroups; ++g) {
+            const std::size_t o = v.record_offset(k, g);
+            const double S = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o));
+            const double Z = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o + 2));
+            smax = std::max({smax, std::fabs(S * (0 - Z)), std::fabs(S * (top - Z))});
+        }
+    c.sigma = 0;
+    if (smax > 0 && std::isfinite(smax)) c.sigma = std::clamp(static_cast<int>(std::ceil(std::log2(smax))) + 9, -90, 90);
+    c.d_start = dalloc<std::uint32_t>(st.size());
+    c.d_maps = dalloc<std::uint32_t>(gmap.size() + cmap.size());
+    ck(cudaMemcpy(c.d_start, st.data(), 4 * st.size(), cudaMemcpyHostToDevice), "H2D tc start");
+    ck(cudaMemcpy(c.d_maps, gmap.data(), 4 * gmap.size(), cudaMemcpyHostToDevice), "H2D tc gmap");
+    ck(cudaMemcpy(c.d_maps + gmap.size(), cmap.data(), 4 * cmap.size(), cudaMemcpyHostToDevice), "H2D tc cmap");
+}
 }  // namespace
 
 // ================================================================ C ABI ====
@@ -604,6 +790,7 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
             plan_partition(L.get(), t, sms, 1);
             plan_cta(L.get(), t, sms, 0);
             plan_cta(L.get(), t, sms, 1);
+            plan_tc(L.get(), t, v, sms);
             dev_bytes += t.cells.size() + 4 * t.cell_off.size();
         }
         L->info.fast_path = L->fast;

@@ -1,0 +1,470 @@
+// gemm_tc.cuh -- batched SpQR decode (batch >= 2): dequantize to fp16 in
+// shared memory, then tcgen05.mma (sm_100a 5th-generation tensor cores, fp32
+// accumulators in TMEM).  Included by kernels.cuh (namespace spqr_dev).
+//
+// Reference semantics: matvec(t, x, plan) (kernel.hpp:89-124) applied to each
+// of the B batch columns; the weights are dequantize_full's (kernel.hpp:17-25,
+// solver.hpp:345-362: s*(q - z), then + fp16 outlier), rounded once to fp16
+// (scaled by 2^-sigma, an exact per-layer power of two that keeps every
+// operand in fp16 range), which is what makes the product a dense
+// contraction the tensor cores can run (BASELINE north star: "dequant-then-
+// mma path for batch >= 16").  Accumulation is fp32 in TMEM; the tolerance is
+// the north star's 1e-3 relative (fp16 weight rounding costs ~1e-4).
+//
+// Tiles: 128 rows (four 32-row cell rows) x 128 columns (half a 256-column
+// panel) per MMA stage, N = batch padded to 16 (<= 128 per launch).
+//   * warps 0-3 ("dequant warps"): warp i streams the cells of row-group pair
+//     4T+i (cp.async.bulk, two record slots, one cell of lookahead), decodes
+//     the bilevel statistics into a per-(row, block) fp16 table
+//     {s 2^(24-p-sigma) for both column halves, -s z 2^-sigma}, turns every
+//     A-fragment register of codes (the batch-1 layout: codes as binary16
+//     subnormals code*2^(p-24), ONE LOP3) into weights with ONE HFMA2, writes
+//     them with stmatrix into the UMMA K-major core-matrix layout, adds the
+//     cell's outliers in place, and after the tile's last stage reads the
+//     accumulator back (tcgen05.ld) and writes y;
+//   * warp 4 ("control"): allocates TMEM (two accumulators of N columns),
+//     copies each stage's x tile (prepared by xprep_tc in the same layout),
+//     issues the 8 tcgen05.mma of a stage and commits them to mbarriers.
+// A and x tiles are double-buffered; accumulators are double-buffered across
+// 128-row tiles so the epilogue of one tile overlaps the next tile's MMAs.
+// Split-K across CTAs: each CTA owns a contiguous, byte-balanced range of
+// (tile, panel) units; partial tiles go through partial slots and a per-warp
+// acq_rel counter, the last contributor adding them in range order.
+
+struct TcParams {
+    const std::uint8_t* cells;        // cell records (batch-1 layout)
+    const std::uint32_t* cell_off;    // [ncell+1]
+    const std::uint32_t* cta_start;   // [nv+1] first unit (T * Pn + P) of each range
+    const std::uint32_t* gmap;        // [Tn][2] {partial slot base, contributing ranges}
+    const std::uint32_t* cmap;        // [nv][2] ordinal of the range in its first / last tile
+    const std::uint8_t* xpanels;      // [2*Pn][N x 128 fp16] x tiles (xprep_tc)
+    float* y;                         // [B][m]
+    float* partial;                   // [slots][N][128]
+    std::uint32_t* counters;          // [Tn][4], zero between launches
+    std::uint32_t m, Pn, Gn, Tn, nv, B, N;
+    std::uint32_t rec_cap, slot_bytes;
+    float out_scale;                  // 2^sigma
+    int sigma;
+};
+
+namespace tc {
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t addr, std::uint32_t lbo, std::uint32_t sbo) {
+    // K-major, no swizzle: core matrices of 8 rows x 16 B; lbo = stride between
+    // the two K core matrices of an MMA, sbo = stride between 8-row groups
+    return static_cast<std::uint64_t>((addr >> 4) & 0x3FFFu) |
+           (static_cast<std::uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+           (static_cast<std::uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1 (sm_100)
+}
+__device__ __forceinline__ void mma_f16(std::uint32_t d_tmem, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                        std::uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void commit(std::uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void ld16(std::uint32_t taddr, float (&v)[16]) {
+    std::uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void stsm_x4(std::uint32_t addr, std::uint32_t a0, std::uint32_t a1, std::uint32_t a2,
+                                        std::uint32_t a3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a0), "r"(a1),
+                 "r"(a2), "r"(a3)
+                 : "memory");
+}
+// (a - (z, z)) * (s, s) + (c, c) per f16 lane; z, s, c are the low (HI=false)
+// or high (HI=true) halves of their registers.  a - z is exact (both are
+// integers times the same power of two), so the weight is rounded once.
+template <bool HI>
+__device__ __forceinline__ std::uint32_t deq2(std::uint32_t a, std::uint32_t z, std::uint32_t s, std::uint32_t c) {
+    std::uint32_t d;
+    if constexpr (HI)
+        asm("{\n\t.reg .b16 zl, zh, sl, sh, cl, ch;\n\t.reg .b32 z2, s2, c2, t;\n\t"
+            "mov.b32 {zl, zh}, %2;\n\tmov.b32 z2, {zh, zh};\n\t"
+            "mov.b32 {sl, sh}, %3;\n\tmov.b32 s2, {sh, sh};\n\t"
+            "mov.b32 {cl, ch}, %4;\n\tmov.b32 c2, {cl, cl};\n\t"
+            "sub.rn.f16x2 t, %1, z2;\n\tfma.rn.f16x2 %0, t, s2, c2;\n\t}"
+            : "=r"(d)
+            : "r"(a), "r"(z), "r"(s), "r"(c));
+    else
+        asm("{\n\t.reg .b16 zl, zh, sl, sh, cl, ch;\n\t.reg .b32 z2, s2, c2, t;\n\t"
+            "mov.b32 {zl, zh}, %2;\n\tmov.b32 z2, {zl, zl};\n\t"
+            "mov.b32 {sl, sh}, %3;\n\tmov.b32 s2, {sl, sl};\n\t"
+            "mov.b32 {cl, ch}, %4;\n\tmov.b32 c2, {cl, cl};\n\t"
+            "sub.rn.f16x2 t, %1, z2;\n\tfma.rn.f16x2 %0, t, s2, c2;\n\t}"
+            : "=r"(d)
+            : "r"(a), "r"(z), "r"(s), "r"(c));
+    return d;
+}
+}  // namespace tc
+
+// x tiles for the tensor cores: stage (P, h) holds columns 256P + 128h + k,
+// k < 128, of every batch column n < N (zero for n >= B or beyond the layer)
+// as fp16, K-major core matrices: byte (k/8)*16N + (n/8)*128 + (n%8)*16 + (k%8)*2.
+__global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int x_f16, std::uint32_t n,
+                                                std::uint32_t B, std::uint32_t N, std::uint32_t Pn,
+                                                const std::uint32_t* __restrict__ order, std::uint8_t* __restrict__ out) {
+    pdl_launch();
+    const std::uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // (stage, n, k core)
+    const std::uint32_t total = 2u * Pn * N * 16u;
+    pdl_wait();
+    if (idx >= total) return;
+    const std::uint32_t kc = idx & 15u, nn = (idx >> 4) % N, st = idx / (16u * N);
+    const std::uint32_t c0 = 128u * st + 8u * kc;  // st = 2P + h
+    std::uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        float v2[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const std::uint32_t c = c0 + 2 * e + q;
+            float v = 0.f;
+            if (nn < B && c < n) {
+                const std::uint32_t src = order ? __ldg(order + c) : c;
+                const std::size_t off = static_cast<std::size_t>(nn) * n + src;
+                v = x_f16 ? __half2float(static_cast<const __half*>(x)[off]) : static_cast<const float*>(x)[off];
+            }
+            v2[q] = v;
+        }
+        w[e] = pack_h2_rn(v2[0], v2[1]);
+    }
+    std::uint8_t* dst = out + static_cast<std::size_t>(st) * 256u * N + kc * 16u * N + (nn >> 3) * 128u + (nn & 7u) * 16u;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int BW, int BS, int BZ>
+__global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
+    using G = Geo<BW>;
+    constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
+    constexpr std::uint32_t CELL = 2 * UNIT;
+    constexpr std::uint32_t CODEB = T::code_bytes(BW);
+    constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
+    constexpr std::uint32_t MASK = (1u << BW) - 1u;
+    constexpr std::uint32_t SMASK = (1u << BS) - 1u, ZMASK = (1u << BZ) - 1u;
+    constexpr float kMagic = 8388608.0f;
+    constexpr std::uint32_t A_STAGE = 128u * 128u * 2u;  // 32 KB
+    constexpr std::uint32_t KC_A = 2048u;                // A: bytes between k core matrices (16 row groups)
+
+    extern __shared__ __align__(128) std::uint8_t smem[];
+    __shared__ std::uint64_t rec_full[4][2], a_full[2], a_free[2], b_full[2], d_full[2], d_free[2];
+    __shared__ std::uint32_t slot_r[4][2][2];
+    __shared__ std::uint32_t tmem_base;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const std::uint32_t N = p.N;
+    const std::uint32_t B_STAGE = 256u * N;
+    std::uint8_t* abuf = smem;                                  // [2][A_STAGE]
+    std::uint8_t* bbuf = smem + 2 * A_STAGE;                    // [2][B_STAGE]
+    std::uint8_t* recs = bbuf + 2 * B_STAGE;                    // [4][2][slot_bytes]
+    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [4][2 units][16 rows][16 blocks] x 16 B
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&rec_full[i][0], 1);
+            mbar_init(&rec_full[i][1], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&a_full[b], 4);
+            mbar_init(&a_free[b], 1);
+            mbar_init(&b_full[b], 1);
+            mbar_init(&d_full[b], 1);
+            mbar_init(&d_free[b], 4);
+        }
+        fence_mbar_init();
+    }
+    // zero both A stages once: rows of missing row-group pairs (the layer's last
+    // tile) then contribute 0 instead of whatever shared memory held
+    for (std::uint32_t i = threadIdx.x; i < 2u * A_STAGE / 16u; i += blockDim.x)
+        reinterpret_cast<uint4*>(abuf)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    if (warp == 4) {  // two accumulators of N fp32 columns each
+        const std::uint32_t cols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    pdl_launch();
+    const std::uint32_t tmem = tmem_base;
+    const std::uint32_t v = blockIdx.x;
+    const std::uint32_t u0 = __ldg(p.cta_start + v), u1 = __ldg(p.cta_start + v + 1);
+    const std::uint32_t nst = 2u * (u1 - u0);  // MMA stages of this range
+
+    if (warp == 4) {
+        // ------------------------------------------------------- control --
+        if (lane == 0) {
+            pdl_wait();  // xprep_tc has completed
+            const std::uint32_t idesc = (1u << 4) | ((N >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32, K-major
+            auto issue_b = [&](std::uint32_t s) {
+                const std::uint32_t u = u0 + (s >> 1), P = u % p.Pn;
+                const std::uint32_t b = s & 1u;
+                if (s >= 2) mbar_wait(&a_free[b], ((s >> 1) - 1u) & 1u);
+                mbar_expect_tx(&b_full[b], B_STAGE);
+                bulk_g2s(bbuf + b * B_STAGE, p.xpanels + static_cast<std::size_t>(2u * P + (s & 1u)) * B_STAGE, B_STAGE,
+                         &b_full[b]);
+            };
+            if (nst > 0) issue_b(0);
+            std::uint32_t tile_i = 0;  // tiles started in this range
+#pragma unroll 1
+            for (std::uint32_t s = 0; s < nst; ++s) {
+                const std::uint32_t u = u0 + (s >> 1), P = u % p.Pn;
+                const bool first = (s & 1u) == 0 && ((s >> 1) == 0 || P == 0);  // first stage of a tile
+                const bool last = (s & 1u) && (u + 1 == u1 || P + 1 == p.Pn);
+                if (first && tile_i >= 2) mbar_wait(&d_free[tile_i & 1u], ((tile_i >> 1) - 1u) & 1u);
+                if (s + 1 < nst) issue_b(s + 1);
+                const std::uint32_t b = s & 1u;
+                mbar_wait(&a_full[b], (s >> 1) & 1u);
+                mbar_wait(&b_full[b], (s >> 1) & 1u);
+                tc::fence_after();
+                const std::uint32_t d = tmem + (tile_i & 1u) * N;
+                const std::uint32_t a_sa = smem_u32(abuf + b * A_STAGE), b_sa = smem_u32(bbuf + b * B_STAGE);
+#pragma unroll
+                for (std::uint32_t kk = 0; kk < 8; ++kk)
+                    tc::mma_f16(d, tc::smem_desc(a_sa + kk * 2u * KC_A, KC_A, 128u),
+                                tc::smem_desc(b_sa + kk * 2u * 16u * N, 16u * N, 128u), idesc,
+                                (first && kk == 0) ? 0u : 1u);
+                tc::commit(&a_free[b]);  // A and x buffers b are free once these MMAs finish
+                if (last) {
+                    tc::commit(&d_full[tile_i & 1u]);
+                    ++tile_i;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------- dequant --
+        const int g = lane >> 2, t = lane & 3;
+        std::uint8_t* ring = recs + static_cast<std::uint32_t>(warp) * 2u * p.slot_bytes;
+        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 8192u;
+        const std::uint32_t magic = 0x4B000000u;
+        // cell of unit u for this warp (row-group pair 4T + warp), or none
+        auto cell_of = [&](std::uint32_t u, std::uint32_t& q) {
+            const std::uint32_t T_ = u / p.Pn, P = u - T_ * p.Pn;
+            const std::uint32_t Gq = 4u * T_ + static_cast<std::uint32_t>(warp);
+            q = Gq * p.Pn + P;
+            return Gq < p.Gn;
+        };
+        auto issue = [&](std::uint32_t u, std::uint32_t sl) {
+            std::uint32_t q;
+            if (lane == 0 && cell_of(u, q)) {
+                const std::uint32_t r0 = __ldg(p.cell_off + q), r1 = __ldg(p.cell_off + q + 1);
+                slot_r[warp][sl][0] = r0;
+                slot_r[warp][sl][1] = r1;
+                const std::uint32_t nb = min(r1 - r0, p.rec_cap);
+                mbar_expect_tx(&rec_full[warp][sl], nb);
+                bulk_g2s(ring + sl * p.slot_bytes, p.cells + r0, nb, &rec_full[warp][sl]);
+            }
+        };
+        const float sig_scale = __uint_as_float(static_cast<std::uint32_t>(127 - p.sigma) << 23);  // 2^-sigma
+        if (u0 < u1) issue(u0, 0);
+        pdl_wait();
+        std::uint32_t tile_i = 0;
+#pragma unroll 1
+        for (std::uint32_t u = u0; u < u1; ++u) {
+            const std::uint32_t it = u - u0;
+            if (u + 1 < u1) issue(u + 1, (it + 1) & 1u);
+            std::uint32_t q;
+            const bool have = cell_of(u, q);
+            const std::uint32_t sl = it & 1u;
+            const std::uint8_t* cell = ring + sl * p.slot_bytes;
+            std::uint32_t r0 = 0, r1 = 0;
+            if (have) {
+                mbar_wait(&rec_full[warp][sl], (it >> 1) & 1u);
+                r0 = slot_r[warp][sl][0];
+                r1 = slot_r[warp][sl][1];
+                // statistics table: lane owns (row g + 8rho, block 8h + 2t + bs) of both units
+#pragma unroll
+                for (int uu = 0; uu < 2; ++uu) {
+                    const std::uint8_t* unit = cell + uu * UNIT;
+                    std::uint32_t ss, zz;
+                    load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * h + 2 * t) * 8);
+                        const std::uint32_t sw[2] = {s4.x, s4.z}, zw[2] = {s4.y, s4.w};
+#pragma unroll
+                        for (int bs = 0; bs < 2; ++bs) {
+                            const __half2 sh = u32_as_h2(sw[bs]), zh = u32_as_h2(zw[bs]);
+                            const float Ss = __low2float(sh), Zs = __high2float(sh);
+                            const float Sz = __low2float(zh), Zz = __high2float(zh);
+                            const int blk = 8 * h + 2 * t + bs;
+                            const int mm = blk % G::MPC;
+                            const float f0 = __uint_as_float(static_cast<std::uint32_t>(
+                                127 + 24 - T::prescale_p(BW, 2 * mm) - p.sigma) << 23);
+                            const float f1 = __uint_as_float(static_cast<std::uint32_t>(
+                                127 + 24 - T::prescale_p(BW, 2 * mm + 1) - p.sigma) << 23);
+                            // the codes' binary16 scale 2^(p-24) for both column halves
+                            const float g0 = __uint_as_float(static_cast<std::uint32_t>(
+                                127 - 24 + T::prescale_p(BW, 2 * mm)) << 23);
+                            const float g1 = __uint_as_float(static_cast<std::uint32_t>(
+                                127 - 24 + T::prescale_p(BW, 2 * mm + 1)) << 23);
+#pragma unroll
+                            for (int rho = 0; rho < 2; ++rho) {
+                                const int eps = 4 * h + 2 * bs + rho;
+                                const float cs = magic_field_rt<SMASK>(ss, eps * BS, magic) - kMagic;
+                                const float cz = magic_field_rt<ZMASK>(zz, eps * BZ, magic) - kMagic;
+                                const float shat = Ss * (cs - Zs);
+                                const float zhat = Sz * (cz - Zz);
+                                // integer part of the zero goes into the codes exactly; the
+                                // fraction (|.| <= 1/2) is the fp16 addend
+                                const float zi = fminf(fmaxf(rintf(zhat), -1000.f), 1000.f);
+                                const std::uint32_t s01 = pack_h2_rn(shat * f0, shat * f1);
+                                const std::uint32_t z01 = pack_h2_rn(zi * g0, zi * g1);
+                                const std::uint32_t c = pack_h2_rn(-(shat * (zhat - zi)) * sig_scale, 0.f);
+                                *reinterpret_cast<uint4*>(tab + ((uu * 16 + g + 8 * rho) * 16 + blk) * 16) =
+                                    make_uint4(s01, z01, c, 0u);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+#pragma unroll 1
+            for (std::uint32_t h = 0; h < 2; ++h) {
+                const std::uint32_t s = 2u * it + h, b = s & 1u;
+                if (s >= 2) mbar_wait(&a_free[b], ((s >> 1) - 1u) & 1u);
+                std::uint8_t* A = abuf + b * A_STAGE;
+                if (have) {
+#pragma unroll
+                    for (int uu = 0; uu < 2; ++uu) {
+                        const std::uint8_t* unit = cell + uu * UNIT;
+                        std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+                        for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                            const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                            cw[4 * i] = w4.x;
+                            cw[4 * i + 1] = w4.y;
+                            cw[4 * i + 2] = w4.z;
+                            cw[4 * i + 3] = w4.w;
+                        }
+                        // stmatrix row address of this lane: matrix lane/8 = (row half, k half)
+                        const std::uint32_t mq = static_cast<std::uint32_t>(lane >> 3);
+                        const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
+                                                     (4u * warp + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
+                        auto do_half = [&](auto HH) {
+                            constexpr int hh = decltype(HH)::value;
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) {
+                                const int mu = 8 * hh + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
+                                const std::uint32_t* w = cw + G::CW * cidx;
+                                const uint4 e0 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g) * 16 + mu) * 16);
+                                const uint4 e1 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g + 8) * 16 + mu) * 16);
+                                std::uint32_t a[4];
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) {
+                                    const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                                    const int i = rho * (G::NP / 2) + qq;
+                                    const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
+                                    const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                                    const uint4 e = rho ? e1 : e0;
+                                    a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
+                                }
+                                tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
+                            }
+                        };
+                        if (h == 0)
+                            do_half(std::integral_constant<int, 0>{});
+                        else
+                            do_half(std::integral_constant<int, 1>{});
+                    }
+                    __syncwarp();
+                    // outliers of this half: w += v (fp16, scaled by 2^-sigma)
+                    const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+#pragma unroll 1
+                    for (std::uint32_t i = lane; i < cnt; i += 32) {
+                        const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
+                        const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
+                        if (row >= 32u || (col >> 7) != h) continue;  // 0xffffffff = record padding
+                        const std::uint32_t k = col & 127u, rr = 32u * warp + row;
+                        __half* wp = reinterpret_cast<__half*>(A + (k >> 3) * KC_A + (rr >> 3) * 128u + (rr & 7u) * 16u +
+                                                               (k & 7u) * 2u);
+                        *wp = __float2half_rn(__half2float(*wp) + h2f_bits(e & 0xffffu) * sig_scale);
+                    }
+                }
+                fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[b]);
+            }
+            // epilogue after the tile's last unit in this range
+            const std::uint32_t P = u % p.Pn;
+            if (u + 1 == u1 || P + 1 == p.Pn) {
+                const std::uint32_t T_ = u / p.Pn;
+                const std::uint32_t db = tile_i & 1u;
+                mbar_wait(&d_full[db], (tile_i >> 1) & 1u);
+                tc::fence_after();
+                const std::uint32_t row = 128u * T_ + 32u * warp + lane;
+                const std::uint32_t ta = tmem + ((32u * warp) << 16) + db * N;
+                const std::uint32_t ua = u0 > T_ * p.Pn ? u0 : T_ * p.Pn;  // this range's units of tile T
+                const bool whole = ua == T_ * p.Pn && u + 1 == (T_ + 1) * p.Pn;
+                const uint2 gm = whole ? make_uint2(0, 0) : __ldg(reinterpret_cast<const uint2*>(p.gmap) + T_);
+                const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == u0 / p.Pn ? 0u : 1u));
+#pragma unroll 1
+                for (std::uint32_t c0 = 0; c0 < N; c0 += 16) {
+                    float vv[16];
+                    tc::ld16(ta + c0, vv);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const std::uint32_t bcol = c0 + j;
+                        if (whole) {
+                            if (bcol < p.B && row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = vv[j] * p.out_scale;
+                        } else {
+                            __stcg(p.partial + (static_cast<std::size_t>(gm.x + ord) * N + bcol) * 128u + 32u * warp + lane,
+                                   vv[j]);
+                        }
+                    }
+                }
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&d_free[db]);
+                if (!whole) {  // last contributor adds the partial tiles in range order
+                    std::uint32_t prev = 0;
+                    if (lane == 0)
+                        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;"
+                                     : "=r"(prev)
+                                     : "l"(p.counters + 4u * T_ + warp)
+                                     : "memory");
+                    prev = __shfl_sync(0xffffffffu, prev, 0);
+                    __syncwarp();
+                    if (prev == gm.y - 1u) {
+#pragma unroll 1
+                        for (std::uint32_t bcol = 0; bcol < p.B; ++bcol) {
+                            float sum = 0.f;
+                            for (std::uint32_t j = 0; j < gm.y; ++j)
+                                sum += __ldcg(p.partial + (static_cast<std::size_t>(gm.x + j) * N + bcol) * 128u +
+                                              32u * warp + lane);
+                            if (row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = sum * p.out_scale;
+                        }
+                        if (lane == 0) p.counters[4u * T_ + warp] = 0;
+                    }
+                }
+                ++tile_i;
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc::fence_after();
+        const std::uint32_t cols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+    }
+}

@@ -18,6 +18,7 @@
 
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "tiled.hpp"
 
@@ -158,6 +159,7 @@ __device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int 
 
 #include "gemv_tiled.cuh"
 #include "gemv_cta.cuh"
+#include "gemm_tc.cuh"
 
 // x preparation for the tiled path: one thread per (column, batch column);
 // the 16 lanes of a half-warp form one 16-column block.  Writes the panel

@@ -131,10 +131,13 @@ def test_batch_and_host_api(cuda, oracle_c):
         Y = cuda.empty((3, 128), device="cuda")
         L.matvec(_dev(cuda, X), Y, batch=3)
         Yh = L.matvec_host(X)
+        # batch >= 2 on the fast path is the tcgen05 dequant-then-MMA kernel
+        # (fp16 weights: the north star's 1e-3); the generic path stays fp32
+        tol = 1e-5 if generic else TOL
         for b in range(3):
             ref = t.matvec(X[b])
-            assert relative_l2(Y[b].cpu().numpy(), ref) < 1e-5
-            assert relative_l2(Yh[b], ref) < 1e-5
+            assert relative_l2(Y[b].cpu().numpy(), ref) < tol
+            assert relative_l2(Yh[b], ref) < tol
 
 
 def test_deterministic_and_workspace(cuda):
