@@ -180,7 +180,7 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
         if (batch >= 2) {  // gemm_tc: x tiles for N <= 128, partial tiles, per-warp tile counters
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
-            w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 4 * 4);
+            w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 8 * 4);
         }
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
@@ -288,8 +288,11 @@ void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, c
 // ---- gemm_tc (batch >= 2): 4 dequant warps + 1 control warp per CTA -------
 constexpr std::uint32_t kTcStaticMax = 2048;
 constexpr std::uint32_t kTcMaxN = 128;  // batch columns per launch
+// below this batch, repeated gemv_cta launches beat the dequant-then-MMA
+// kernel (tools/batch_sweep.py: 2 x 30 us vs 122 us at batch 2 on 8192x22016)
+constexpr int kTcMinBatch = 5;
 std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N) {
-    return 2u * 128u * 128u * 2u + 2u * 256u * N + 8u * L->tcp.slot_bytes + 4u * 8192u;
+    return 2u * 128u * 128u * 2u + 2u * 256u * N + 8u * L->tcp.slot_bytes + 8u * 4096u;
 }
 
 template <int BW, int BSZ>
@@ -309,7 +312,7 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nv);
-    cfg.blockDim = dim3(160);
+    cfg.blockDim = dim3(288);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -441,7 +444,7 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
-    if (L->fast && !use_legacy_tiled() && batch >= 2 && !use_batch_loop()) {
+    if (L->fast && !use_legacy_tiled() && batch >= kTcMinBatch && !use_batch_loop()) {
         if (stage == 1) return;
         run_tc(L, x, f16, y, batch, base, w, st);
         return;
@@ -704,7 +707,7 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const spqr::detail
     }
     c.pslots = slots;
     c.slot_bytes = (t.cell_bytes + 2048u + 127u) & ~127u;
-    const std::uint32_t need = 2u * 128u * 128u * 2u + 2u * 256u * kTcMaxN + 8u * c.slot_bytes + 4u * 8192u;
+    const std::uint32_t need = 2u * 128u * 128u * 2u + 2u * 256u * kTcMaxN + 8u * c.slot_bytes + 8u * 4096u;
     if (need + kTcStaticMax > kSmemLimit)
         c.slot_bytes = ((kSmemLimit - kTcStaticMax - (need - 8u * c.slot_bytes)) / 8u) & ~127u;
     if (c.slot_bytes < t.cell_bytes + 16u) spqr::fail(spqr::Errc::config_invalid, "gemm_tc: shared memory plan");

@@ -40,7 +40,7 @@ struct TcParams {
     const std::uint8_t* xpanels;      // [2*Pn][N x 128 fp16] x tiles (xprep_tc)
     float* y;                         // [B][m]
     float* partial;                   // [slots][N][128]
-    std::uint32_t* counters;          // [Tn][4], zero between launches
+    std::uint32_t* counters;          // [Tn][8] (per dequant warp), zero between launches
     std::uint32_t m, Pn, Gn, Tn, nv, B, N;
     std::uint32_t rec_cap, slot_bytes;
     float out_scale;                  // 2^sigma
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int 
 }
 
 template <int BW, int BS, int BZ>
-__global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
+__global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
@@ -158,31 +158,34 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
     constexpr float kMagic = 8388608.0f;
     constexpr std::uint32_t A_STAGE = 128u * 128u * 2u;  // 32 KB
     constexpr std::uint32_t KC_A = 2048u;                // A: bytes between k core matrices (16 row groups)
+    constexpr int CTRL = 8;                              // control warp
 
     extern __shared__ __align__(128) std::uint8_t smem[];
-    __shared__ std::uint64_t rec_full[4][2], a_full[2], a_free[2], b_full[2], d_full[2], d_free[2];
+    __shared__ std::uint64_t rec_full[4][2], rec_empty[4][2], a_full[2], a_free[2], b_full[2], d_full[2], d_free[2];
     __shared__ std::uint32_t slot_r[4][2][2];
     __shared__ std::uint32_t tmem_base;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::uint32_t N = p.N;
     const std::uint32_t B_STAGE = 256u * N;
-    std::uint8_t* abuf = smem;                                  // [2][A_STAGE]
+    const std::uint32_t tcols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
+    std::uint8_t* abuf = smem;                                  // [2][A_STAGE]: stage half h in buffer h
     std::uint8_t* bbuf = smem + 2 * A_STAGE;                    // [2][B_STAGE]
-    std::uint8_t* recs = bbuf + 2 * B_STAGE;                    // [4][2][slot_bytes]
-    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [4][2 units][16 rows][16 blocks] x 16 B
+    std::uint8_t* recs = bbuf + 2 * B_STAGE;                    // [4 cell rows][2][slot_bytes]
+    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [8 warps][2 units][16 rows][8 blocks] x 16 B
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&rec_full[i][0], 1);
-            mbar_init(&rec_full[i][1], 1);
-        }
+        for (int i = 0; i < 4; ++i)
+            for (int k = 0; k < 2; ++k) {
+                mbar_init(&rec_full[i][k], 1);
+                mbar_init(&rec_empty[i][k], 2);  // both half-warps of the cell row
+            }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&a_full[b], 4);
             mbar_init(&a_free[b], 1);
             mbar_init(&b_full[b], 1);
             mbar_init(&d_full[b], 1);
-            mbar_init(&d_free[b], 4);
+            mbar_init(&d_free[b], 8);
         }
         fence_mbar_init();
     }
@@ -191,10 +194,9 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
     for (std::uint32_t i = threadIdx.x; i < 2u * A_STAGE / 16u; i += blockDim.x)
         reinterpret_cast<uint4*>(abuf)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
-    if (warp == 4) {  // two accumulators of N fp32 columns each
-        const std::uint32_t cols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
+    if (warp == CTRL) {  // two accumulators of N fp32 columns each
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                     "r"(cols));
+                     "r"(tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc::fence_before();
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
     const std::uint32_t u0 = __ldg(p.cta_start + v), u1 = __ldg(p.cta_start + v + 1);
     const std::uint32_t nst = 2u * (u1 - u0);  // MMA stages of this range
 
-    if (warp == 4) {
+    if (warp == CTRL) {
         // ------------------------------------------------------- control --
         if (lane == 0) {
             pdl_wait();  // xprep_tc has completed
@@ -249,176 +251,179 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
         __syncwarp();
     } else {
         // ------------------------------------------------------- dequant --
+        // warp = 4 hh + ci: cell row ci (row-group pair 4T + ci) of every tile,
+        // column half hh (blocks 8hh .. 8hh+7) of every panel
+        const int ci = warp & 3, hh = warp >> 2;
         const int g = lane >> 2, t = lane & 3;
-        std::uint8_t* ring = recs + static_cast<std::uint32_t>(warp) * 2u * p.slot_bytes;
-        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 8192u;
+        std::uint8_t* ring = recs + static_cast<std::uint32_t>(ci) * 2u * p.slot_bytes;
+        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 4096u;
         const std::uint32_t magic = 0x4B000000u;
-        // cell of unit u for this warp (row-group pair 4T + warp), or none
         auto cell_of = [&](std::uint32_t u, std::uint32_t& q) {
             const std::uint32_t T_ = u / p.Pn, P = u - T_ * p.Pn;
-            const std::uint32_t Gq = 4u * T_ + static_cast<std::uint32_t>(warp);
+            const std::uint32_t Gq = 4u * T_ + static_cast<std::uint32_t>(ci);
             q = Gq * p.Pn + P;
             return Gq < p.Gn;
         };
-        auto issue = [&](std::uint32_t u, std::uint32_t sl) {
+        // record k of this cell row goes to slot k & 1; half 0 issues it once
+        // both halves released the slot's previous record
+        auto issue = [&](std::uint32_t u, std::uint32_t k) {
             std::uint32_t q;
-            if (lane == 0 && cell_of(u, q)) {
+            if (hh == 0 && lane == 0 && cell_of(u, q)) {
+                const std::uint32_t sl = k & 1u;
+                if (k >= 2) mbar_wait(&rec_empty[ci][sl], ((k >> 1) - 1u) & 1u);
                 const std::uint32_t r0 = __ldg(p.cell_off + q), r1 = __ldg(p.cell_off + q + 1);
-                slot_r[warp][sl][0] = r0;
-                slot_r[warp][sl][1] = r1;
+                slot_r[ci][sl][0] = r0;
+                slot_r[ci][sl][1] = r1;
                 const std::uint32_t nb = min(r1 - r0, p.rec_cap);
-                mbar_expect_tx(&rec_full[warp][sl], nb);
-                bulk_g2s(ring + sl * p.slot_bytes, p.cells + r0, nb, &rec_full[warp][sl]);
+                mbar_expect_tx(&rec_full[ci][sl], nb);
+                bulk_g2s(ring + sl * p.slot_bytes, p.cells + r0, nb, &rec_full[ci][sl]);
             }
         };
         const float sig_scale = __uint_as_float(static_cast<std::uint32_t>(127 - p.sigma) << 23);  // 2^-sigma
+        std::uint32_t k = 0;  // records of this cell row consumed so far
         if (u0 < u1) issue(u0, 0);
         pdl_wait();
         std::uint32_t tile_i = 0;
+        // stmatrix row address of this lane: matrix lane/8 = (row half, k half)
+        const std::uint32_t mq = static_cast<std::uint32_t>(lane >> 3);
 #pragma unroll 1
         for (std::uint32_t u = u0; u < u1; ++u) {
             const std::uint32_t it = u - u0;
-            if (u + 1 < u1) issue(u + 1, (it + 1) & 1u);
             std::uint32_t q;
             const bool have = cell_of(u, q);
-            const std::uint32_t sl = it & 1u;
+            if (have && u + 1 < u1) issue(u + 1, k + 1);
+            const std::uint32_t sl = k & 1u;
             const std::uint8_t* cell = ring + sl * p.slot_bytes;
             std::uint32_t r0 = 0, r1 = 0;
             if (have) {
-                mbar_wait(&rec_full[warp][sl], (it >> 1) & 1u);
-                r0 = slot_r[warp][sl][0];
-                r1 = slot_r[warp][sl][1];
-                // statistics table: lane owns (row g + 8rho, block 8h + 2t + bs) of both units
+                mbar_wait(&rec_full[ci][sl], (k >> 1) & 1u);
+                r0 = slot_r[ci][sl][0];
+                r1 = slot_r[ci][sl][1];
+                // statistics of this half: lane owns (row g + 8rho, block 8hh + 2t + bs) of both units
 #pragma unroll
                 for (int uu = 0; uu < 2; ++uu) {
                     const std::uint8_t* unit = cell + uu * UNIT;
                     std::uint32_t ss, zz;
                     load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
+                    const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * hh + 2 * t) * 8);
+                    const std::uint32_t sw[2] = {s4.x, s4.z}, zw[2] = {s4.y, s4.w};
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * h + 2 * t) * 8);
-                        const std::uint32_t sw[2] = {s4.x, s4.z}, zw[2] = {s4.y, s4.w};
+                    for (int bs = 0; bs < 2; ++bs) {
+                        const __half2 sh = u32_as_h2(sw[bs]), zh = u32_as_h2(zw[bs]);
+                        const float Ss = __low2float(sh), Zs = __high2float(sh);
+                        const float Sz = __low2float(zh), Zz = __high2float(zh);
+                        const int mm = (2 * t + bs) % G::MPC;  // block 8hh + 2t + bs, 8 % MPC == 0
+                        const int p0 = T::prescale_p(BW, 2 * mm), p1 = T::prescale_p(BW, 2 * mm + 1);
+                        const float f0 = __uint_as_float(static_cast<std::uint32_t>(127 + 24 - p0 - p.sigma) << 23);
+                        const float f1 = __uint_as_float(static_cast<std::uint32_t>(127 + 24 - p1 - p.sigma) << 23);
+                        const float g0 = __uint_as_float(static_cast<std::uint32_t>(127 - 24 + p0) << 23);
+                        const float g1 = __uint_as_float(static_cast<std::uint32_t>(127 - 24 + p1) << 23);
 #pragma unroll
-                        for (int bs = 0; bs < 2; ++bs) {
-                            const __half2 sh = u32_as_h2(sw[bs]), zh = u32_as_h2(zw[bs]);
-                            const float Ss = __low2float(sh), Zs = __high2float(sh);
-                            const float Sz = __low2float(zh), Zz = __high2float(zh);
-                            const int blk = 8 * h + 2 * t + bs;
-                            const int mm = blk % G::MPC;
-                            const float f0 = __uint_as_float(static_cast<std::uint32_t>(
-                                127 + 24 - T::prescale_p(BW, 2 * mm) - p.sigma) << 23);
-                            const float f1 = __uint_as_float(static_cast<std::uint32_t>(
-                                127 + 24 - T::prescale_p(BW, 2 * mm + 1) - p.sigma) << 23);
-                            // the codes' binary16 scale 2^(p-24) for both column halves
-                            const float g0 = __uint_as_float(static_cast<std::uint32_t>(
-                                127 - 24 + T::prescale_p(BW, 2 * mm)) << 23);
-                            const float g1 = __uint_as_float(static_cast<std::uint32_t>(
-                                127 - 24 + T::prescale_p(BW, 2 * mm + 1)) << 23);
-#pragma unroll
-                            for (int rho = 0; rho < 2; ++rho) {
-                                const int eps = 4 * h + 2 * bs + rho;
-                                const float cs = magic_field_rt<SMASK>(ss, eps * BS, magic) - kMagic;
-                                const float cz = magic_field_rt<ZMASK>(zz, eps * BZ, magic) - kMagic;
-                                const float shat = Ss * (cs - Zs);
-                                const float zhat = Sz * (cz - Zz);
-                                // integer part of the zero goes into the codes exactly; the
-                                // fraction (|.| <= 1/2) is the fp16 addend
-                                const float zi = fminf(fmaxf(rintf(zhat), -1000.f), 1000.f);
-                                const std::uint32_t s01 = pack_h2_rn(shat * f0, shat * f1);
-                                const std::uint32_t z01 = pack_h2_rn(zi * g0, zi * g1);
-                                const std::uint32_t c = pack_h2_rn(-(shat * (zhat - zi)) * sig_scale, 0.f);
-                                *reinterpret_cast<uint4*>(tab + ((uu * 16 + g + 8 * rho) * 16 + blk) * 16) =
-                                    make_uint4(s01, z01, c, 0u);
-                            }
+                        for (int rho = 0; rho < 2; ++rho) {
+                            const int eps = 4 * hh + 2 * bs + rho;
+                            const float cs = magic_field_rt<SMASK>(ss, eps * BS, magic) - kMagic;
+                            const float cz = magic_field_rt<ZMASK>(zz, eps * BZ, magic) - kMagic;
+                            const float shat = Ss * (cs - Zs);
+                            const float zhat = Sz * (cz - Zz);
+                            // integer part of the zero goes into the codes exactly; the
+                            // fraction (|.| <= 1/2) is the fp16 addend
+                            const float zi = fminf(fmaxf(rintf(zhat), -1000.f), 1000.f);
+                            const std::uint32_t s01 = pack_h2_rn(shat * f0, shat * f1);
+                            const std::uint32_t z01 = pack_h2_rn(zi * g0, zi * g1);
+                            const std::uint32_t c = pack_h2_rn(-(shat * (zhat - zi)) * sig_scale, 0.f);
+                            *reinterpret_cast<uint4*>(tab + ((uu * 16 + g + 8 * rho) * 8 + 2 * t + bs) * 16) =
+                                make_uint4(s01, z01, c, 0u);
                         }
                     }
                 }
                 __syncwarp();
             }
-#pragma unroll 1
-            for (std::uint32_t h = 0; h < 2; ++h) {
-                const std::uint32_t s = 2u * it + h, b = s & 1u;
-                if (s >= 2) mbar_wait(&a_free[b], ((s >> 1) - 1u) & 1u);
-                std::uint8_t* A = abuf + b * A_STAGE;
-                if (have) {
+            const std::uint32_t s = 2u * it + static_cast<std::uint32_t>(hh);
+            if (it >= 1) mbar_wait(&a_free[hh], (it - 1u) & 1u);
+            std::uint8_t* A = abuf + static_cast<std::uint32_t>(hh) * A_STAGE;
+            if (have) {
 #pragma unroll
-                    for (int uu = 0; uu < 2; ++uu) {
-                        const std::uint8_t* unit = cell + uu * UNIT;
-                        std::uint32_t cw[G::LANE_WORDS];
+                for (int uu = 0; uu < 2; ++uu) {
+                    const std::uint8_t* unit = cell + uu * UNIT;
+                    std::uint32_t cw[G::LANE_WORDS];
 #pragma unroll
-                        for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                            const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                            cw[4 * i] = w4.x;
-                            cw[4 * i + 1] = w4.y;
-                            cw[4 * i + 2] = w4.z;
-                            cw[4 * i + 3] = w4.w;
-                        }
-                        // stmatrix row address of this lane: matrix lane/8 = (row half, k half)
-                        const std::uint32_t mq = static_cast<std::uint32_t>(lane >> 3);
-                        const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
-                                                     (4u * warp + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
-                        auto do_half = [&](auto HH) {
-                            constexpr int hh = decltype(HH)::value;
-#pragma unroll
-                            for (int jj = 0; jj < 8; ++jj) {
-                                const int mu = 8 * hh + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
-                                const std::uint32_t* w = cw + G::CW * cidx;
-                                const uint4 e0 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g) * 16 + mu) * 16);
-                                const uint4 e1 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g + 8) * 16 + mu) * 16);
-                                std::uint32_t a[4];
-#pragma unroll
-                                for (int r = 0; r < 4; ++r) {
-                                    const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                                    const int i = rho * (G::NP / 2) + qq;
-                                    const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                                    const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
-                                    const uint4 e = rho ? e1 : e0;
-                                    a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
-                                }
-                                tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
-                            }
-                        };
-                        if (h == 0)
-                            do_half(std::integral_constant<int, 0>{});
-                        else
-                            do_half(std::integral_constant<int, 1>{});
+                    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                        const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                        cw[4 * i] = w4.x;
+                        cw[4 * i + 1] = w4.y;
+                        cw[4 * i + 2] = w4.z;
+                        cw[4 * i + 3] = w4.w;
                     }
-                    __syncwarp();
-                    // outliers of this half: w += v (fp16, scaled by 2^-sigma)
-                    const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
-                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
-                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+                    const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
+                                                 (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
+                    auto do_half = [&](auto HH) {
+                        constexpr int h_ = decltype(HH)::value;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
+                            const std::uint32_t* w = cw + G::CW * cidx;
+                            const uint4 e0 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g) * 8 + jj) * 16);
+                            const uint4 e1 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g + 8) * 8 + jj) * 16);
+                            std::uint32_t a[4];
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                                const int i = rho * (G::NP / 2) + qq;
+                                const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
+                                const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                                const uint4 e = rho ? e1 : e0;
+                                a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
+                            }
+                            tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
+                        }
+                    };
+                    if (hh == 0)
+                        do_half(std::integral_constant<int, 0>{});
+                    else
+                        do_half(std::integral_constant<int, 1>{});
+                }
+                __syncwarp();
+                // outliers of this half: w += v (fp16, scaled by 2^-sigma)
+                const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
 #pragma unroll 1
-                    for (std::uint32_t i = lane; i < cnt; i += 32) {
-                        const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
-                        const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
-                        if (row >= 32u || (col >> 7) != h) continue;  // 0xffffffff = record padding
-                        const std::uint32_t k = col & 127u, rr = 32u * warp + row;
-                        __half* wp = reinterpret_cast<__half*>(A + (k >> 3) * KC_A + (rr >> 3) * 128u + (rr & 7u) * 16u +
-                                                               (k & 7u) * 2u);
+                for (std::uint32_t i = lane; i < cnt; i += 32) {
+                    const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
+                    const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
+                    if (row < 32u && (col >> 7) == static_cast<std::uint32_t>(hh)) {  // 0xffffffff = padding
+                        const std::uint32_t kq = col & 127u, rr = 32u * ci + row;
+                        __half* wp = reinterpret_cast<__half*>(A + (kq >> 3) * KC_A + (rr >> 3) * 128u +
+                                                               (rr & 7u) * 16u + (kq & 7u) * 2u);
                         *wp = __float2half_rn(__half2float(*wp) + h2f_bits(e & 0xffffu) * sig_scale);
                     }
                 }
-                fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a_full[b]);
             }
-            // epilogue after the tile's last unit in this range
+            fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_full[hh]);
+            if (have) {
+                if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);  // this half is done with the record
+                ++k;
+            }
+            (void)s;
+            // epilogue after the tile's last unit in this range: the two halves
+            // of a cell row split the accumulator's 16-column chunks
             const std::uint32_t P = u % p.Pn;
             if (u + 1 == u1 || P + 1 == p.Pn) {
                 const std::uint32_t T_ = u / p.Pn;
                 const std::uint32_t db = tile_i & 1u;
                 mbar_wait(&d_full[db], (tile_i >> 1) & 1u);
                 tc::fence_after();
-                const std::uint32_t row = 128u * T_ + 32u * warp + lane;
-                const std::uint32_t ta = tmem + ((32u * warp) << 16) + db * N;
+                const std::uint32_t row = 128u * T_ + 32u * ci + lane;
+                const std::uint32_t ta = tmem + ((32u * ci) << 16) + db * N;
                 const std::uint32_t ua = u0 > T_ * p.Pn ? u0 : T_ * p.Pn;  // this range's units of tile T
                 const bool whole = ua == T_ * p.Pn && u + 1 == (T_ + 1) * p.Pn;
                 const uint2 gm = whole ? make_uint2(0, 0) : __ldg(reinterpret_cast<const uint2*>(p.gmap) + T_);
                 const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == u0 / p.Pn ? 0u : 1u));
 #pragma unroll 1
-                for (std::uint32_t c0 = 0; c0 < N; c0 += 16) {
+                for (std::uint32_t c0 = 16u * hh; c0 < N; c0 += 32) {
                     float vv[16];
                     tc::ld16(ta + c0, vv);
 #pragma unroll
@@ -427,7 +432,7 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
                         if (whole) {
                             if (bcol < p.B && row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = vv[j] * p.out_scale;
                         } else {
-                            __stcg(p.partial + (static_cast<std::size_t>(gm.x + ord) * N + bcol) * 128u + 32u * warp + lane,
+                            __stcg(p.partial + (static_cast<std::size_t>(gm.x + ord) * N + bcol) * 128u + 32u * ci + lane,
                                    vv[j]);
                         }
                     }
@@ -440,20 +445,21 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
                     if (lane == 0)
                         asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;"
                                      : "=r"(prev)
-                                     : "l"(p.counters + 4u * T_ + warp)
+                                     : "l"(p.counters + 8u * T_ + warp)
                                      : "memory");
                     prev = __shfl_sync(0xffffffffu, prev, 0);
                     __syncwarp();
                     if (prev == gm.y - 1u) {
 #pragma unroll 1
-                        for (std::uint32_t bcol = 0; bcol < p.B; ++bcol) {
-                            float sum = 0.f;
-                            for (std::uint32_t j = 0; j < gm.y; ++j)
-                                sum += __ldcg(p.partial + (static_cast<std::size_t>(gm.x + j) * N + bcol) * 128u +
-                                              32u * warp + lane);
-                            if (row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = sum * p.out_scale;
-                        }
-                        if (lane == 0) p.counters[4u * T_ + warp] = 0;
+                        for (std::uint32_t c0 = 16u * hh; c0 < N; c0 += 32)
+                            for (std::uint32_t bcol = c0; bcol < c0 + 16u && bcol < p.B; ++bcol) {
+                                float sum = 0.f;
+                                for (std::uint32_t j = 0; j < gm.y; ++j)
+                                    sum += __ldcg(p.partial + (static_cast<std::size_t>(gm.x + j) * N + bcol) * 128u +
+                                                  32u * ci + lane);
+                                if (row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = sum * p.out_scale;
+                            }
+                        if (lane == 0) p.counters[8u * T_ + warp] = 0;
                     }
                 }
                 ++tile_i;
@@ -462,9 +468,8 @@ __global__ void __launch_bounds__(160, 1) gemm_tc(const TcParams p) {
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == CTRL) {
         tc::fence_after();
-        const std::uint32_t cols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
     }
 }
