@@ -218,7 +218,10 @@ void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::siz
 
 
 // ---- gemv_cta (v13): producer warp + kNC consumer warps per CTA ----------
-constexpr int kNC = 16;  // 4 warps per SMSP, 128 registers each
+#ifndef SPQR_NC
+#define SPQR_NC 16
+#endif
+constexpr int kNC = SPQR_NC;  // 16: 4 warps per SMSP, up to 128 registers each
 constexpr std::uint32_t kCtaStaticMax = 6144;  // static smem of gemv_cta (checked at first launch)
 
 bool use_batch_loop() {  // A/B switch: batch >= 2 as repeated batch-1 launches

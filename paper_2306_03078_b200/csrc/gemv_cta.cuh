@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ std::uint64_t full[NC][2];
     __shared__ std::uint32_t slot_r[NC][2][2];       // record byte range of the slot's cell
     __shared__ std::uint32_t tick[2];                // per-range ticket counters (by range parity)
+    __shared__ volatile std::uint32_t pflag[64];     // SHX: x panel built
     __shared__ float rowsum[NC][32];                 // outlier row sums of a cell (zero between cells)
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
@@ -225,9 +226,23 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         mbar_init(&full[warp][1], 1);
         fence_mbar_init();
     }
-    if (threadIdx.x == 0) tick[0] = tick[1] = 0;
+    if (threadIdx.x == 0) tick[0] = tick[1] = NC;  // ticket w < NC is warp w's first cell
+    if (threadIdx.x < 64) pflag[threadIdx.x] = 0u;
     rowsum[warp][lane] = 0.f;
     if (lane < 4) zrow[warp][lane] = 0u;
+    // the first record of this warp's first ticket goes out before anything
+    // else, from the global offsets (the range's offset table loads meanwhile)
+    if (blockIdx.x < p.nvcta && lane == 0) {
+        const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
+        if (static_cast<std::uint32_t>(warp) < q1 - q0) {
+            const std::uint32_t r0 = __ldg(p.cell_off + q0 + warp), r1 = __ldg(p.cell_off + q0 + warp + 1);
+            slot_r[warp][0][0] = r0;
+            slot_r[warp][0][1] = r1;
+            const std::uint32_t nb = min(r1 - r0, p.rec_cap);
+            mbar_expect_tx(&full[warp][0], nb);
+            bulk_g2s(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, p.cells + r0, nb, &full[warp][0]);
+        }
+    }
     std::uint32_t* coff = reinterpret_cast<std::uint32_t*>(smem + p.off_off);  // record offsets of the range
     std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
     auto range_setup = [&](std::uint32_t v) {
@@ -301,23 +316,29 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             return p.Pn == 1u ? 0u : q - __umulhi(q, p.pn_magic) * p.Pn;
         };
         // one ticket of lookahead: the next cell's record copy and x loads are
-        // in flight while this cell computes
-        std::uint32_t tk = grab();
-        if (tk < nc) issue(tk, nit & 1u);
+        // in flight while this cell computes.  Warp w's first ticket is w.
+        std::uint32_t tk = static_cast<std::uint32_t>(warp);
+        if (tk < nc && waited) issue(tk, nit & 1u);  // (the first range's went out in the prologue)
+        // SHX: panel index i = warp + NC j covers panel (P0 + i) mod Pn; j = 0 is the
+        // panel of this warp's first cell.  Each warp builds its panels right
+        // after the PDL wait; readers check pflag instead of a CTA barrier.
+        const std::uint32_t P0 = panel_of(0);
+        auto build_shared = [&](std::uint32_t i) {
+            std::uint32_t P = P0 + i;
+            if (P >= p.Pn) P -= p.Pn;
+            build_panel<BW, XLO>(load_x<XLO>(p, P, lane), lane, pp, pan_base + P * PANEL);
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) pflag[P] = 1u;
+        };
+        bool rest_pending = false;
         if (!waited) {
             pdl_wait();  // the preceding kernel has completed: x, y and the partial slots are ours
             waited = true;
             SPQR_TL(1)
-            if constexpr (SHX) {  // every panel once, for all ranges of this CTA
+            if constexpr (SHX) {  // own panels, the first cell's first; no CTA barrier
 #pragma unroll 1
-                for (std::uint32_t P = warp; P < p.Pn; P += 2 * NC) {  // two panels' x in flight
-                    const XLane<XLO> xa = load_x<XLO>(p, P, lane);
-                    XLane<XLO> xb{};
-                    if (P + NC < p.Pn) xb = load_x<XLO>(p, P + NC, lane);
-                    build_panel<BW, XLO>(xa, lane, pp, pan_base + P * PANEL);
-                    if (P + NC < p.Pn) build_panel<BW, XLO>(xb, lane, pp, pan_base + (P + NC) * PANEL);
-                }
-                bar_sync_named(1, NT);
+                for (std::uint32_t i = warp; i < p.Pn; i += NC) build_shared(i);
             }
         }
         XLane<XLO> xl{};
@@ -333,7 +354,13 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             const std::uint32_t slot = nit & 1u;
 
             if constexpr (SHX) {
-                pan = pan_base + panel_of(tk) * PANEL;
+                const std::uint32_t P = panel_of(tk);
+                pan = pan_base + P * PANEL;
+                if (pflag[P] == 0u) {
+                    while (pflag[P] == 0u) {
+                    }
+                }
+                __threadfence_block();
             } else {
                 build_panel<BW, XLO>(xl, lane, pp, pan);
                 __syncwarp();
@@ -589,11 +616,25 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             tk = tn;
             xl = xn;
             ++nit;
+            if constexpr (SHX) {
+                if (rest_pending) {  // the remaining panels of this warp
+                    rest_pending = false;
+#pragma unroll 1
+                    for (std::uint32_t i = warp + NC; i < p.Pn; i += NC) build_shared(i);
+                }
+            }
+        }
+        if constexpr (SHX) {  // a warp without cells in this range still builds its panels
+            if (rest_pending) {
+                rest_pending = false;
+#pragma unroll 1
+                for (std::uint32_t i = warp + NC; i < p.Pn; i += NC) build_shared(i);
+            }
         }
         SPQR_TL(3)
         if (v + gridDim.x < p.nvcta) {  // this CTA has another range
             bar_sync_named(1, NT);
-            if (threadIdx.x == 0) tick[it & 1u] = 0;
+            if (threadIdx.x == 0) tick[it & 1u] = NC;
             range_setup(v + gridDim.x);
             bar_sync_named(1, NT);
         }

@@ -68,6 +68,19 @@ for m, n in shapes:
         print("   per-CTA last loop end (us): fastest", [(b, sm, round(t, 2)) for b, (sm, t) in items[:5]])
         print("                               slowest", [(b, sm, round(t, 2)) for b, (sm, t) in items[-8:]])
         ends = np.array([t for _, (sm, t) in items])
+        ent = {}
+        for i, row in enumerate(T):
+            if row[7] >= 1000 and row[0] > 0:
+                ent.setdefault(i // 16, []).append((row[0] - t0c) / 1e3)
+        q4 = [np.mean([np.mean(ent[b]) for b in ent if lo <= b < lo + 37]) for lo in (0, 37, 74, 111)]
+        e4 = [np.mean([per[b][1] for b in per if lo <= b < lo + 37]) for lo in (0, 37, 74, 111)]
+        for b, (sm, tend) in items[-4:] + items[len(items) // 2:len(items) // 2 + 1]:
+            rows_b = T[16 * b:16 * b + 16]
+            rel = lambda k: (rows_b[:, k][rows_b[:, k] > 0] - t0c) / 1e3
+            print(f"   CTA {b:3d} sm {sm:3d}: entry {rel(0).min():6.2f} pdl {rel(1).min():6.2f} first {rel(2).min():6.2f}"
+                  f"..{rel(2).max():6.2f} loop_end {rel(3).min():6.2f}..{rel(3).max():6.2f} cells/warp "
+                  f"{rows_b[:, 5].tolist()}")
+        print("   mean CTA entry by blockIdx quarter", [round(x, 2) for x in q4], "mean loop end", [round(x, 2) for x in e4])
         print("   per-CTA end percentiles", " ".join(f"{v:6.2f}" for v in np.percentile(ends, [0, 10, 50, 90, 100])))
         print(f"   consumers: full-wait us/warp " +
               " ".join(f"{v:6.2f}" for v in np.percentile(cons[:, 6] / 1e3, [0, 50, 100])) +
