@@ -41,6 +41,8 @@ METRIC = "SpQR matvec µs/layer & HBM GB/s vs roofline (LLaMA shapes) vs fp16 GE
 LAYERS = [("q_proj", 8192, 8192), ("k_proj", 8192, 8192), ("v_proj", 8192, 8192),
           ("o_proj", 8192, 8192), ("gate_proj", 22016, 8192), ("up_proj", 22016, 8192),
           ("down_proj", 8192, 22016)]
+# launch groups of a decoder block: layers sharing their input are stacked
+GROUPS = [("qkv", [0, 1, 2]), ("o", [3]), ("gate_up", [4, 5]), ("down", [6])]
 BITS, RATE = 3, 0.01
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -53,6 +55,7 @@ def workload_config(n_gpus: int) -> dict:
         "weight_bits": BITS, "stat_bits": 3, "beta1": 16, "beta2": 16, "outlier_rate": RATE,
         "batch": 1, "x_dtype": "f16", "layers": len(LAYERS),
         "l2": "weights 400 MB per step > 126 MB L2: inputs larger than L2, no flush",
+        "launches": "4 per step: q/k/v stacked (fused QKV), o, gate/up stacked, down; x shared within a group",
         "parallelism": f"row-shard x{n_gpus} + NCCL all-gather of y" if n_gpus > 1 else "single GPU",
     }
 
@@ -237,30 +240,49 @@ def run_ours(args) -> None:
     streams = make_streams()
     from paper_2306_03078_b200.sharded import gather_rows, row_bands
 
-    layers, xs, ys, yfull, xs32, bands = [], [], [], [], [], []
+    # One decoder block as a serving stack runs it: q/k/v share x (one stacked
+    # handle = fused QKV), gate/up share x (stacked), o and down alone -> four
+    # launches per step over the same seven layers' bytes.  N > 1: each rank
+    # holds the same row band of every member layer (stacked), and the bands
+    # are all-gathered (rank-major) after every launch.
+    groups = []
     bytes_step = 0  # whole-job algorithmic bytes per step
     gen = torch.Generator(device="cpu").manual_seed(2)
-    for (name, m, n), s in zip(LAYERS, streams):
-        bands.append(row_bands(m, world))
-        r0, r1 = bands[-1][rank]
-        L = P.Layer(s, device=dev.index, rows=(r0, r1) if world > 1 else None)
-        assert L.info["fast_path"] == 1
-        layers.append(L)
+    for gname, members in GROUPS:
+        n = LAYERS[members[0]][2]
+        parts, rows_local, bands = [], 0, []
+        for i in members:
+            m = LAYERS[i][1]
+            bd = row_bands(m, world)
+            bands.append(bd)
+            r0, r1 = bd[rank]
+            parts.append(streams[i] if world == 1 else P.slice_rows(streams[i], r0, r1))
+            rows_local += r1 - r0
+            bytes_step += alg_bytes(len(streams[i]) - 48, m, n) + 2 * n * (world - 1)
+        L = P.Layer(parts[0], device=dev.index) if len(parts) == 1 else P.Layer.stacked(parts, device=dev.index)
+        assert L.info["fast_path"] == 1 and L.rows == rows_local
         x = torch.randn(n, generator=gen).to(torch.float16)
-        xs.append(x.to(dev))
-        xs32.append(x.float().pin_memory())
-        ys.append(torch.empty(r1 - r0, device=dev))
-        yfull.append(torch.empty(world * max(b - a for a, b in bands[-1]), device=dev) if world > 1 else None)
-        bytes_step += alg_bytes(len(s) - 48, m, n) + 2 * n * (world - 1)
+        m_total = sum(LAYERS[i][1] for i in members)
+        per_rank = max(sum(bd[r][1] - bd[r][0] for bd in bands) for r in range(world))
+        groups.append({
+            "name": gname, "members": members, "m": m_total, "n": n, "L": L, "x": x.to(dev),
+            "x32": x.float().pin_memory(), "y": torch.empty(rows_local, device=dev),
+            "band": (0, rows_local), "yfull": torch.empty(world * per_rank, device=dev) if world > 1 else None,
+            "bands": [(r * per_rank, r * per_rank + per_rank) for r in range(world)],
+        })
     payload_step = sum(len(s) - 48 for s in streams)
 
     stream = torch.cuda.Stream(device=dev)
 
+    def gather(gp):  # equal-size rank bands (every member's band is 32-row aligned)
+        gather_rows(torch.nn.functional.pad(gp["y"], (0, gp["bands"][0][1] - gp["y"].numel())), gp["bands"],
+                    out=gp["yfull"])
+
     def step():
-        for i, L in enumerate(layers):
-            L.matvec(xs[i], ys[i], stream=stream)
+        for gp in groups:
+            gp["L"].matvec(gp["x"], gp["y"], stream=stream)
             if world > 1:
-                gather_rows(ys[i], bands[i], out=yfull[i])
+                gather(gp)
 
     with torch.cuda.stream(stream):
         for _ in range(3):
@@ -302,39 +324,41 @@ def run_ours(args) -> None:
     ms_per_step = ms / args.steps
     value = bytes_step / (ms_per_step * 1e-3) / 1e9
 
-    # launches of our kernels per step, counted by the library (one C-ABI call per layer)
+    # launches of our kernels per step, counted by the library (one C-ABI call per group)
     launches_per_step = 0
     with torch.cuda.stream(stream):
-        for i, L in enumerate(layers):
-            L.matvec(xs[i], ys[i], stream=stream)
+        for gp in groups:
+            gp["L"].matvec(gp["x"], gp["y"], stream=stream)
             launches_per_step += P.last_launch_count()
     torch.cuda.synchronize()
 
-    # ---- dominant kernel alone: the fused GEMV, cycling all seven layers ----
-    for i, L in enumerate(layers):
-        L.matvec_stage(xs[i], ys[i], stage=1, stream=stream)
-    torch.cuda.synchronize()
-    kgraph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(kgraph, stream=stream):
-        for i, L in enumerate(layers):
-            L.matvec_stage(xs[i], ys[i], stage=2, stream=stream)
-    reps = max(20, args.steps // 5)
-    with torch.cuda.stream(stream):
-        for _ in range(5):
-            kgraph.replay()
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(reps):
-            kgraph.replay()
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kms = k0.elapsed_time(k1) / reps  # one cycle = 7 launches
-    kbytes = sum(alg_bytes(L.info["payload_bytes"], L.rows, L.cols) for L in layers)  # this rank
+    # ---- dominant kernel alone (no all-gather), per group and over the block ----
+    def graph_time(fn, reps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                g.replay()
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                g.replay()
+        b_.record(stream)
+        torch.cuda.synchronize()
+        return a_.elapsed_time(b_) / reps
+
+    kms = graph_time(lambda: [gp["L"].matvec(gp["x"], gp["y"], stream=stream) for gp in groups],
+                     max(20, args.steps // 5))
+    kbytes = sum(alg_bytes(gp["L"].info["payload_bytes"], gp["L"].rows, gp["n"]) for gp in groups)  # this rank
     peak, peak_kind = load_peaks()
     achieved = kbytes / (kms * 1e-3) / 1e9
-    traffic = None  # ncu dram__bytes_read+write per launch, averaged over the 7 launches
+    traffic = None  # ncu dram__bytes_read+write per launch, averaged over the block's launches
     tf = os.path.join(ROOT, "profiles", "gemv_traffic.json")
     if os.path.exists(tf) and world == 1:
         try:
@@ -344,87 +368,55 @@ def run_ours(args) -> None:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "gemv_cta (fused x preparation + decode-GEMV + CSR merge, one launch per layer)",
-                "us_per_launch": round(1e3 * kms / len(layers), 3),
-                "alg_bytes_per_launch": kbytes // len(layers)}
+                "kernel": "gemv_cta (fused x preparation + decode-GEMV + CSR merge, one launch per group)",
+                "us_per_launch": round(1e3 * kms / len(groups), 3),
+                "alg_bytes_per_launch": kbytes // len(groups)}
 
-    # ---- per-shape microseconds (full matvec incl. x preparation) ----
+    # ---- per group: us per launch (L2-defeating copies are not needed: every
+    # group is >= 33 MB and the four groups cycle through 400 MB) ----
     per_layer = {}
-    for i, (name, m, n) in enumerate(LAYERS):
-        shape = f"{m}x{n}"
-        if shape in per_layer:
-            continue
-        same = [j for j, l in enumerate(LAYERS) if f"{l[1]}x{l[2]}" == shape]
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for j in same:
-                layers[j].matvec(xs[j], ys[j], stream=stream)
-        with torch.cuda.stream(stream):
-            for _ in range(3):
-                g.replay()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        r = 50
-        a.record(stream)
-        with torch.cuda.stream(stream):
-            for _ in range(r):
-                g.replay()
-        b.record(stream)
-        torch.cuda.synchronize()
-        us = 1e3 * a.elapsed_time(b) / (r * len(same))
-        pb = layers[i].info["payload_bytes"]
-        per_layer[shape] = {"us": round(us, 3), "GB/s": round(alg_bytes(pb, layers[i].rows, n) / (us * 1e-6) / 1e9, 1),
-                            "copies_cycled": len(same),
-                            "l2_resident_risk": len(same) * pb < 126e6}
+    for gp in groups:
+        us = 1e3 * graph_time(lambda gp=gp: gp["L"].matvec(gp["x"], gp["y"], stream=stream), 50)
+        pb = gp["L"].info["payload_bytes"]
+        per_layer[f"{gp['name']} {gp['L'].rows}x{gp['n']}"] = {
+            "us": round(us, 3), "us_per_member_layer": round(us / len(gp["members"]), 3),
+            "GB/s": round(alg_bytes(pb, gp["L"].rows, gp["n"]) / (us * 1e-6) / 1e9, 1),
+            "l2_resident_risk": pb < 126e6}
 
-    # ---- dense fp16 GEMV comparator (ours and cuBLAS), same shapes ----
+    # ---- dense fp16 GEMV comparator (ours and cuBLAS), same stacked shapes ----
     dense = {}
     if world == 1:
-        W16 = [torch.randn(m, n, device=dev, dtype=torch.float16) * 0.02 for _, m, n in LAYERS]
-        yd = [torch.empty(m, device=dev) for _, m, _ in LAYERS]
-        for label, fn in (("ours", lambda i: P.dense_gemv_f16(W16[i], xs[i], yd[i], LAYERS[i][1], LAYERS[i][2],
-                                                               stream=stream)),
-                          ("cublas", lambda i: torch.mv(W16[i], xs[i]))):
+        W16 = [torch.randn(gp["m"], gp["n"], device=dev, dtype=torch.float16) * 0.02 for gp in groups]
+        yd = [torch.empty(gp["m"], device=dev) for gp in groups]
+        for label, fn in (("ours", lambda i: P.dense_gemv_f16(W16[i], groups[i]["x"], yd[i], groups[i]["m"],
+                                                               groups[i]["n"], stream=stream)),
+                          ("cublas", lambda i: torch.mv(W16[i], groups[i]["x"]))):
             with torch.cuda.stream(stream):
-                for i in range(len(LAYERS)):  # eager warm-up (creates the cuBLAS handle)
+                for i in range(len(groups)):  # eager warm-up (creates the cuBLAS handle)
                     fn(i)
             torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(len(LAYERS)):
-                    fn(i)
-            with torch.cuda.stream(stream):
-                for _ in range(3):
-                    g.replay()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            with torch.cuda.stream(stream):
-                for _ in range(20):
-                    g.replay()
-            b.record(stream)
-            torch.cuda.synchronize()
-            dense[label] = a.elapsed_time(b) / 20
+            dense[label] = graph_time(lambda: [fn(i) for i in range(len(groups))], 20)
         best = min(dense.values())
         dense = {"ms_per_step_ours": round(dense["ours"], 4), "ms_per_step_cublas": round(dense["cublas"], 4),
-                 "dense_bytes_per_step": sum(2 * m * n + 2 * n + 4 * m for _, m, n in LAYERS),
-                 "speedup_spqr_vs_best_dense": round(best / ms_per_step, 3)}
+                 "dense_bytes_per_step": sum(2 * gp["m"] * gp["n"] + 2 * gp["n"] + 4 * gp["m"] for gp in groups),
+                 "speedup_spqr_vs_best_dense": round(best / ms_per_step, 3),
+                 "shapes": "same stacked groups as ours (fused QKV, fused gate/up, o, down)"}
         del W16, yd
 
     # ---- end to end through the public API with host buffers ----
     e2e_steps = max(5, min(args.steps, 50))
-    ys_h = [torch.empty(m, dtype=torch.float32).pin_memory() for _, m, _ in LAYERS]
-    xd32 = [torch.empty(n, device=dev, dtype=torch.float32) for _, _, n in LAYERS]
+    ys_h = [torch.empty(gp["m"], dtype=torch.float32).pin_memory() for gp in groups]
+    xd32 = [torch.empty(gp["n"], device=dev, dtype=torch.float32) for gp in groups]
 
     def e2e_step():
-        for i, L in enumerate(layers):
+        for i, gp in enumerate(groups):
             if world == 1:
-                ys_h[i].numpy()[:] = L.matvec_host(xs32[i].numpy())
+                ys_h[i].numpy()[:] = gp["L"].matvec_host(gp["x32"].numpy())
             else:
-                xd32[i].copy_(xs32[i], non_blocking=True)
-                L.matvec(xd32[i], ys[i], stream=torch.cuda.current_stream())
-                gather_rows(ys[i], bands[i], out=yfull[i])
-                ys_h[i].copy_(yfull[i][: LAYERS[i][1]], non_blocking=True)
+                xd32[i].copy_(gp["x32"], non_blocking=True)
+                gp["L"].matvec(xd32[i], gp["y"], stream=torch.cuda.current_stream())
+                gather(gp)
+                ys_h[i].copy_(gp["yfull"][: gp["m"]], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
 
     for _ in range(2):
@@ -442,11 +434,11 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": round(bytes_step * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": sum(4 * n for _, _, n in LAYERS),
-           "d2h_bytes_per_step": sum(4 * m for _, m, _ in LAYERS),
+           "h2d_bytes_per_step": sum(4 * gp["n"] for gp in groups),
+           "d2h_bytes_per_step": sum(4 * gp["m"] for gp in groups),
            "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3),
-           "path": "spqr_matvec_host (C ABI: H2D fp32 x, fused kernels, D2H y, sync) per layer"
-                   if world == 1 else "H2D x, spqr_matvec, NCCL all-gather, D2H y per layer"}
+           "path": "spqr_matvec_host (C ABI: H2D fp32 x, fused kernels, D2H y, sync) per group"
+                   if world == 1 else "H2D x, spqr_matvec, NCCL all-gather, D2H y per group"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -170,6 +170,14 @@ int spqr_debug_tiled_host(const uint8_t* stream, size_t nbytes, uint32_t* dims4,
  * validates exactly like decode, transcodes to the HBM layout, uploads once. */
 int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opts* opts,
                       spqr_layer** out);
+/* Extension (no reference counterpart; the reference decodes one tensor at a
+ * time): layers sharing their input -- q/k/v, gate/up -- stacked row-wise in
+ * one handle, so one launch writes all outputs (layer i's rows follow layer
+ * i-1's in y).  Same columns, widths, group sizes and permutation required;
+ * rows % 32 == 0 for all but the last.  matvec / matvec_ws / matvec_host only
+ * (dequantize and export return SPQR_E_CONFIG_INVALID). */
+int spqr_layer_create_stacked(const uint8_t* const* streams, const size_t* sizes, int count,
+                              const spqr_layer_opts* opts, spqr_layer** out);
 void spqr_layer_destroy(spqr_layer* layer);
 int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info);
 

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
         "spqr_transcode_roundtrip_host": (i32, [vp, sz, vp, sz, C.POINTER(C.c_size_t)]),
         "spqr_layer_create": (i32, [vp, sz, C.POINTER(LayerOpts), C.POINTER(vp)]),
         "spqr_layer_destroy": (None, [vp]),
+        "spqr_layer_create_stacked": (i32, [C.POINTER(vp), C.POINTER(sz), i32, C.POINTER(LayerOpts), C.POINTER(vp)]),
         "spqr_layer_get_info": (i32, [vp, C.POINTER(LayerInfo)]),
         "spqr_layer_export_stream": (i32, [vp, vp, sz, C.POINTER(C.c_size_t)]),
         "spqr_dequantize": (i32, [vp, vp, vp]),
@@ -319,6 +320,24 @@ class Layer:
         _check(lib().spqr_layer_get_info(h, C.byref(info)))
         self.info = info.as_dict()
         self.rows, self.cols = self.info["rows"], self.info["cols"]
+
+    @classmethod
+    def stacked(cls, streams: list, device: int = -1) -> "Layer":
+        """Several layers sharing their input (q/k/v, gate/up) stacked row-wise
+        in one handle (spqr_layer_create_stacked): one launch, y = [y_0; y_1; ...]."""
+        bufs = [_buf(s) for s in streams]
+        ptrs = (C.c_void_p * len(bufs))(*[b[1] for b in bufs])
+        sizes = (C.c_size_t * len(bufs))(*[b[2] for b in bufs])
+        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0)
+        h = C.c_void_p()
+        _check(lib().spqr_layer_create_stacked(ptrs, sizes, len(bufs), C.byref(opts), C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        info = LayerInfo()
+        _check(lib().spqr_layer_get_info(h, C.byref(info)))
+        self.info = info.as_dict()
+        self.rows, self.cols = self.info["rows"], self.info["cols"]
+        return self
 
     def close(self):
         if getattr(self, "_h", None):

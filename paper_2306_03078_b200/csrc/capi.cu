@@ -103,6 +103,7 @@ struct spqr_layer {
     std::uint32_t* d_order = nullptr;  // solve position -> source column, or null
     // tiled fast path
     bool fast = false;
+    bool stacked = false;  // several streams stacked row-wise (matvec only)
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
     std::uint32_t* d_warp_start[2] = {nullptr, nullptr};  // per x dtype (f16, f32): warp count differs
@@ -670,7 +671,8 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
 // ranges are reduced through partial slots in range order.  sigma: the
 // per-layer power of two that keeps s * 2^(24 - p - sigma) < 2^15 for every
 // first-level scale s (binary16 range of the dequantization multiplier).
-void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const spqr::detail::StreamView& v, int sms) {
+void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<spqr::detail::StreamView>& views,
+             int sms) {
     auto& c = L->tcp;
     c.Tn = (t.Gn + 3u) / 4u;
     const std::uint32_t U = c.Tn * t.Pn;
@@ -716,14 +718,16 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const spqr::detail
     if (c.slot_bytes < t.cell_bytes + 16u) spqr::fail(spqr::Errc::config_invalid, "gemm_tc: shared memory plan");
     // sigma from the first-level scale bound
     double smax = 0.0;
-    const int top = (1 << v.sb) - 1;
-    for (std::uint32_t k = 0; k < v.nblocks; ++k)
-        for (std::uint32_t g = 0; g < v.ngroups; ++g) {
-            const std::size_t o = v.record_offset(k, g);
-            const double S = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o));
-            const double Z = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o + 2));
-            smax = std::max({smax, std::fabs(S * (0 - Z)), std::fabs(S * (top - Z))});
-        }
+    for (const auto& v : views) {
+        const int top = (1 << v.sb) - 1;
+        for (std::uint32_t k = 0; k < v.nblocks; ++k)
+            for (std::uint32_t g = 0; g < v.ngroups; ++g) {
+                const std::size_t o = v.record_offset(k, g);
+                const double S = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o));
+                const double Z = spqr::fp16_to_float(spqr::detail::StreamView::load_u16(v.base + o + 2));
+                smax = std::max({smax, std::fabs(S * (0 - Z)), std::fabs(S * (top - Z))});
+            }
+    }
     c.sigma = 0;
     if (smax > 0 && std::isfinite(smax)) c.sigma = std::clamp(static_cast<int>(std::ceil(std::log2(smax))) + 9, -90, 90);
     c.d_start = dalloc<std::uint32_t>(st.size());
@@ -731,6 +735,24 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const spqr::detail
     ck(cudaMemcpy(c.d_start, st.data(), 4 * st.size(), cudaMemcpyHostToDevice), "H2D tc start");
     ck(cudaMemcpy(c.d_maps, gmap.data(), 4 * gmap.size(), cudaMemcpyHostToDevice), "H2D tc gmap");
     ck(cudaMemcpy(c.d_maps + gmap.size(), cmap.data(), 4 * cmap.size(), cudaMemcpyHostToDevice), "H2D tc cmap");
+}
+
+// Device copy of a tiled layer + every launch plan; returns device bytes.
+std::uint64_t upload_tiled(spqr_layer* L, const spqr::detail::TiledHost& t,
+                           const std::vector<spqr::detail::StreamView>& views) {
+    L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
+    L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
+    ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
+    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size());
+    ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice), "H2D cell_off");
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
+    plan_partition(L, t, sms, 0);
+    plan_partition(L, t, sms, 1);
+    plan_cta(L, t, sms, 0);
+    plan_cta(L, t, sms, 1);
+    plan_tc(L, t, views, sms);
+    return t.cells.size() + 4 * t.cell_off.size();
 }
 }  // namespace
 
@@ -782,24 +804,91 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
             ck(cudaMemcpy(L->d_stream, s, n, cudaMemcpyHostToDevice), "H2D stream");
             dev_bytes += n;
         }
-        if (L->fast) {
-            const spqr::detail::TiledHost t = spqr::detail::transcode_to_tiled(v, 0);
-            L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
-            L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
-            ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
-            L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size());
-            ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice),
-               "H2D cell_off");
-            int sms = 0;
-            ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
-            plan_partition(L.get(), t, sms, 0);
-            plan_partition(L.get(), t, sms, 1);
-            plan_cta(L.get(), t, sms, 0);
-            plan_cta(L.get(), t, sms, 1);
-            plan_tc(L.get(), t, v, sms);
-            dev_bytes += t.cells.size() + 4 * t.cell_off.size();
-        }
+        if (L->fast) dev_bytes += upload_tiled(L.get(), spqr::detail::transcode_to_tiled(v, 0), {v});
         L->info.fast_path = L->fast;
+        ensure_own_ws(L.get(), 1);
+        dev_bytes += L->ws_bytes;
+        L->info.device_bytes = dev_bytes;
+        *out = L.release();
+    });
+}
+
+// Extension (no reference counterpart: the reference decodes one tensor at a
+// time): several layers with the same input -- q/k/v, or gate/up -- stacked
+// row-wise into one handle, so one launch computes all their outputs (rows of
+// layer i follow those of layer i-1 in y).  Every stream must be on the fast
+// path with identical columns, widths, group sizes and permutation, and all
+// but the last must have rows % 32 == 0.  matvec only: dequantize / export
+// on a stacked handle return SPQR_E_CONFIG_INVALID.
+int spqr_layer_create_stacked(const uint8_t* const* streams, const size_t* sizes, int count,
+                              const spqr_layer_opts* opts, spqr_layer** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (count < 1 || !streams || !sizes) spqr::fail(spqr::Errc::config_invalid, "stacked: no layers");
+        spqr_layer_opts o{};
+        o.device = -1;
+        if (opts) o = *opts;
+        if (o.row_end > o.row_begin || o.force_generic)
+            spqr::fail(spqr::Errc::config_invalid, "stacked: row bands / generic path not supported");
+        std::vector<spqr::detail::StreamView> views;
+        for (int i = 0; i < count; ++i) views.push_back(spqr::detail::parse_stream(streams[i], sizes[i]));
+        const auto& v0 = views[0];
+        for (int i = 0; i < count; ++i) {
+            const auto& v = views[i];
+            if (!spqr::detail::tiled_supported(v))
+                spqr::fail(spqr::Errc::config_invalid, "stacked: layer outside the tiled geometry");
+            if (v.cols != v0.cols || v.wb != v0.wb || v.sb != v0.sb || v.zb != v0.zb || v.b1 != v0.b1 ||
+                v.b2 != v0.b2 || v.has_permutation != v0.has_permutation)
+                spqr::fail(spqr::Errc::shape_mismatch, "stacked: layers differ in columns, widths or groups");
+            if (i + 1 < count && v.rows % 32 != 0)
+                spqr::fail(spqr::Errc::shape_mismatch, "stacked: rows of all but the last layer must be a multiple of 32");
+            if (v.has_permutation)
+                for (std::uint32_t k = 0; k < v.cols; ++k)
+                    if (v.order(k) != v0.order(k)) spqr::fail(spqr::Errc::shape_mismatch, "stacked: permutations differ");
+        }
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (ndev == 0) throw CudaError("CUDA: no device");
+        DevGuard dg(o.device);
+        auto L = std::make_unique<spqr_layer>();
+        ck(cudaGetDevice(&L->device), "cudaGetDevice");
+        L->stacked = true;
+        L->prefix.assign(streams[0], streams[0] + v0.rec_off);
+        L->geo = spqr::detail::geometry_from_prefix(L->prefix.data(), L->prefix.size());
+        std::memset(&L->info, 0, sizeof(L->info));
+        L->info.cols = v0.cols; L->info.weight_bits = v0.wb; L->info.scale_bits = v0.sb; L->info.zero_bits = v0.zb;
+        L->info.beta1 = v0.b1; L->info.beta2 = v0.b2; L->info.flags = v0.flags;
+        L->info.has_permutation = v0.has_permutation; L->info.tau = v0.tau; L->info.lambda_rel = v0.lambda_rel;
+        L->info.device = L->device;
+        spqr::detail::TiledHost t;
+        for (int i = 0; i < count; ++i) {
+            const spqr::detail::TiledHost ti = spqr::detail::transcode_to_tiled(views[i], 0);
+            const std::uint64_t base = t.cells.size();
+            if (base + ti.cells.size() > 0xfffffff0ull) spqr::fail(spqr::Errc::config_invalid, "stacked: too large");
+            if (i == 0) {
+                t.Pn = ti.Pn;
+                t.cell_bytes = ti.cell_bytes;
+                t.prefix = ti.prefix;
+            }
+            t.Gn += ti.Gn;
+            t.cells.insert(t.cells.end(), ti.cells.begin(), ti.cells.end());
+            if (!t.cell_off.empty()) t.cell_off.pop_back();
+            for (std::uint32_t off : ti.cell_off) t.cell_off.push_back(static_cast<std::uint32_t>(base + off));
+            L->info.rows += views[i].rows;
+            L->info.outlier_count += views[i].nnz;
+            L->info.payload_bytes += sizes[i] - spqr::kSpqrHeaderBytes;
+        }
+        std::uint64_t dev_bytes = 0;
+        if (v0.has_permutation) {
+            std::vector<std::uint32_t> ord(v0.cols);
+            for (std::uint32_t k = 0; k < v0.cols; ++k) ord[k] = v0.order(k);
+            L->d_order = dalloc<std::uint32_t>(v0.cols);
+            ck(cudaMemcpy(L->d_order, ord.data(), 4ull * v0.cols, cudaMemcpyHostToDevice), "H2D order");
+            dev_bytes += 4ull * v0.cols;
+        }
+        L->fast = true;
+        dev_bytes += upload_tiled(L.get(), t, views);
+        L->info.fast_path = 1;
         ensure_own_ws(L.get(), 1);
         dev_bytes += L->ws_bytes;
         L->info.device_bytes = dev_bytes;
@@ -820,6 +909,7 @@ int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info) {
 int spqr_layer_export_stream(const spqr_layer* L, uint8_t* out, size_t cap, size_t* len) {
     int rc = SPQR_OK;
     const int g = guard([&] {
+        if (L->stacked) spqr::fail(spqr::Errc::config_invalid, "export of a stacked layer handle");
         DevGuard dg(L->device);
         std::vector<std::uint8_t> bytes;
         if (L->fast) {
@@ -848,6 +938,7 @@ int spqr_layer_export_stream(const spqr_layer* L, uint8_t* out, size_t cap, size
 
 int spqr_dequantize(const spqr_layer* L, float* w_dev, void* cuda_stream) {
     return guard([&] {
+        if (L->stacked) spqr::fail(spqr::Errc::config_invalid, "dequantize of a stacked layer handle");
         DevGuard dg(L->device);
         auto st = static_cast<cudaStream_t>(cuda_stream);
         g_launches = 0;

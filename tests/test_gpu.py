@@ -214,3 +214,27 @@ def test_errors_surface(cuda):
     with pytest.raises(P.SpqrError) as ei:
         P.Layer(s[:-3])
     assert ei.value.errc == "malformed_stream"
+
+
+def test_stacked_layers_match_separate(cuda, oracle_c):
+    """spqr_layer_create_stacked: q/k/v-style layers sharing x in one handle;
+    y is the row-wise concatenation of the separate products."""
+    streams = [P.encode_arrays(synth.make_layer(m, 768, seed=20 + i, outlier_rate=0.02)) for i, m in
+               enumerate((96, 64, 50))]
+    L = P.Layer.stacked(streams)
+    assert L.rows == 96 + 64 + 50 and L.info["fast_path"] == 1
+    refs = [oracle_c.decode(s) for s in streams]
+    rng = np.random.default_rng(4)
+    for batch, dt, tol in ((1, np.float16, 1e-5), (1, np.float32, 1e-5), (8, np.float16, TOL)):
+        X = rng.standard_normal((batch, 768)).astype(dt)
+        Y = cuda.empty((batch, L.rows), device="cuda")
+        L.matvec(_dev(cuda, X), Y, batch=batch)
+        got = Y.cpu().numpy()
+        for b in range(batch):
+            ref = np.concatenate([t.matvec(X[b].astype(np.float32)) for t in refs])
+            assert relative_l2(got[b], ref) < tol, (batch, dt)
+    with pytest.raises(P.SpqrError):
+        L.dequantize(cuda.empty((L.rows, 768), device="cuda"))
+    bad = P.encode_arrays(synth.make_layer(64, 512, seed=1))
+    with pytest.raises(P.SpqrError):
+        P.Layer.stacked([streams[0], bad])

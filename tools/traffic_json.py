@@ -24,11 +24,12 @@ for r in rows[1:]:
     per.setdefault(int(r[iid]), {})[r[im]] = v
 alg = [int(m.group(1)) for m in re.finditer(r"alg_bytes (\d+)", open(log_path).read())]
 launches = [per[k] for k in sorted(per)]
-assert len(launches) == len(alg) == len(bench.LAYERS), (len(launches), len(alg))
+assert len(launches) == len(alg) == len(bench.GROUPS), (len(launches), len(alg))
 items = []
-for (name, m, n), a, d in zip(bench.LAYERS, alg, launches):
+shapes = re.findall(r"^(\S+) (\d+x\d+) alg_bytes", open(log_path).read(), re.M)
+for (name, shape), a, d in zip(shapes, alg, launches):
     dram = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
-    items.append({"layer": name, "shape": f"{m}x{n}", "alg_bytes": a, "dram_bytes": int(dram),
+    items.append({"layer": name, "shape": shape, "alg_bytes": a, "dram_bytes": int(dram),
                   "dram_over_alg": round(dram / a, 4), "ncu_us": round(d["gpu__time_duration.sum"] / 1e3, 3)})
 res = {"source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
                  "--clock-control none -k regex:gemv_cta (tools/profile_block.py), cold cache per launch",
