@@ -196,15 +196,20 @@ uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
  * x: batch x cols (f16 or f32, original column order), y: batch x rows fp32.
  * Asynchronous on cuda_stream; allocates nothing.  spqr_matvec uses the
  * layer's own workspace (one stream at a time); spqr_matvec_ws takes a caller
- * workspace (concurrent streams). */
+ * workspace (concurrent streams; size from spqr_workspace_bytes(layer, batch)).
+ * Fast-path layers: batch 1-4 run one fused gemv_cta launch per column
+ * (exact codes, fp32 accumulation: ~1e-7 relative to the reference);
+ * batch >= 5 run xprep_tc + gemm_tc per 128 columns (weights rounded to fp16,
+ * tcgen05 tensor cores: <= 1e-3 relative, the north star's bar). */
 int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                 void* cuda_stream);
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,
                    int batch, void* workspace, uint64_t ws_bytes, void* cuda_stream);
 
-/* The two launches of spqr_matvec separately (profiling): stage 1 = x
- * preparation only (gather + scaling into the layer workspace), stage 2 = the
- * fused product only (reuses the last stage-1 preparation), 0 = both. */
+/* Profiling split of spqr_matvec: stage 1 = x preparation only, stage 2 = the
+ * product only, 0 = both.  On the fast path x preparation is fused into the
+ * product kernel, so stage 1 launches nothing and stage 2 equals stage 0;
+ * the generic (raw-stream) path still has two kernels. */
 int spqr_matvec_stage(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                       int stage, void* cuda_stream);
 
