@@ -231,9 +231,17 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: SPQR_BENCH_SHARE_GPU=1 runs every rank on cuda:0 over gloo, so
+    # the N > 1 code path can be exercised on a one-GPU box (not a bench number)
+    share = os.environ.get("SPQR_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
@@ -288,15 +296,20 @@ def run_ours(args) -> None:
         for _ in range(3):
             step()
     torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        step()
-    torch.cuda.synchronize()
+    graph = None
+    if not share:  # gloo collectives (the shared-GPU test hook) cannot be captured
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        torch.cuda.synchronize()
 
     def replay(n):
         with torch.cuda.stream(stream):
             for _ in range(n):
-                graph.replay()
+                if graph is None:
+                    step()
+                else:
+                    graph.replay()
 
     # clocks: sample through a ~1.5 s soak plus the timed region
     with ClockSampler(dev.index) as clk:
