@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #ifdef SPQR_TIMELINE
     const std::uint32_t wk = blockIdx.x * 16u + static_cast<std::uint32_t>(warp);
-    unsigned long long tl_wait = 0;
+    unsigned long long tl_wait = 0, tl_panels = 0;
     std::uint32_t tl_cnt = 0;
 #endif
     SPQR_TL(0)
@@ -323,23 +323,36 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         // panel of this warp's first cell.  Each warp builds its panels right
         // after the PDL wait; readers check pflag instead of a CTA barrier.
         const std::uint32_t P0 = panel_of(0);
-        auto build_shared = [&](std::uint32_t i) {
+        auto panel_at = [&](std::uint32_t i) {
             std::uint32_t P = P0 + i;
-            if (P >= p.Pn) P -= p.Pn;
-            build_panel<BW, XLO>(load_x<XLO>(p, P, lane), lane, pp, pan_base + P * PANEL);
+            return P >= p.Pn ? P - p.Pn : P;
+        };
+        auto publish = [&](std::uint32_t P, const XLane<XLO>& xv) {
+            build_panel<BW, XLO>(xv, lane, pp, pan_base + P * PANEL);
             __syncwarp();
             __threadfence_block();
             if (lane == 0) pflag[P] = 1u;
         };
-        bool rest_pending = false;
         if (!waited) {
             pdl_wait();  // the preceding kernel has completed: x, y and the partial slots are ours
             waited = true;
             SPQR_TL(1)
-            if constexpr (SHX) {  // own panels, the first cell's first; no CTA barrier
+            if constexpr (SHX) {  // own panels (<= 3), the first cell's first; every x load
+                                  // is in flight before the first build; no CTA barrier
+                const std::uint32_t i0 = warp, i1 = warp + NC, i2 = warp + 2 * NC;
+                XLane<XLO> xa{}, xb{}, xc{};
+                if (i0 < p.Pn) xa = load_x<XLO>(p, panel_at(i0), lane);
+                if (i1 < p.Pn) xb = load_x<XLO>(p, panel_at(i1), lane);
+                if (i2 < p.Pn) xc = load_x<XLO>(p, panel_at(i2), lane);
+                if (i0 < p.Pn) publish(panel_at(i0), xa);
+                if (i1 < p.Pn) publish(panel_at(i1), xb);
+                if (i2 < p.Pn) publish(panel_at(i2), xc);
 #pragma unroll 1
-                for (std::uint32_t i = warp; i < p.Pn; i += NC) build_shared(i);
+                for (std::uint32_t i = warp + 3 * NC; i < p.Pn; i += NC) publish(panel_at(i), load_x<XLO>(p, panel_at(i), lane));
             }
+#ifdef SPQR_TIMELINE
+            tl_panels = gtime();
+#endif
         }
         XLane<XLO> xl{};
         if (!SHX && tk < nc) xl = load_x<XLO>(p, panel_of(tk), lane);
@@ -616,20 +629,6 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             tk = tn;
             xl = xn;
             ++nit;
-            if constexpr (SHX) {
-                if (rest_pending) {  // the remaining panels of this warp
-                    rest_pending = false;
-#pragma unroll 1
-                    for (std::uint32_t i = warp + NC; i < p.Pn; i += NC) build_shared(i);
-                }
-            }
-        }
-        if constexpr (SHX) {  // a warp without cells in this range still builds its panels
-            if (rest_pending) {
-                rest_pending = false;
-#pragma unroll 1
-                for (std::uint32_t i = warp + NC; i < p.Pn; i += NC) build_shared(i);
-            }
         }
         SPQR_TL(3)
         if (v + gridDim.x < p.nvcta) {  // this CTA has another range
@@ -642,7 +641,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 #ifdef SPQR_TIMELINE
     SPQR_TL(4)
     if (lane == 0) {
-        g_timeline[8 * wk + 5] = tl_cnt;
+        g_timeline[8 * wk + 5] = tl_panels;
         g_timeline[8 * wk + 6] = tl_wait;
         unsigned smid;
         asm("mov.u32 %0, %smid;" : "=r"(smid));

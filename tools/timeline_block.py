@@ -1,0 +1,71 @@
+"""Device timeline of one launch inside the bench's block sequence (-DSPQR_TIMELINE
+build): the four groups run back to back in a CUDA graph, then the sequence
+up to the chosen group is replayed once more so the timeline buffer holds that
+group's launch with its real predecessor.
+
+    python tools/timeline_block.py [qkv|o|gate_up|down]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2306_03078_b200 import build as B  # noqa: E402
+
+lib_path = os.path.join(ROOT, "build", "libspqr_tl.so")
+if not os.path.exists(lib_path):
+    B.build(out=lib_path, defines=("SPQR_TIMELINE",))
+os.environ["SPQR_LIB"] = lib_path
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2306_03078_b200 as P  # noqa: E402
+
+P.LIB_PATH = lib_path
+lib = P.lib()
+lib.spqr_debug_timeline.restype = C.c_int
+lib.spqr_debug_timeline.argtypes = [C.c_void_p, C.c_size_t]
+target = sys.argv[1] if len(sys.argv) > 1 else "o"
+streams = bench.make_streams()
+groups = []
+for gname, members in bench.GROUPS:
+    parts = [streams[i] for i in members]
+    L = P.Layer(parts[0]) if len(parts) == 1 else P.Layer.stacked(parts)
+    groups.append((gname, L, torch.randn(L.cols, device="cuda").half(), torch.empty(L.rows, device="cuda")))
+st = torch.cuda.Stream()
+upto = [g[0] for g in groups].index(target)
+
+
+def run(seq):
+    for gname, L, x, y in seq:
+        L.matvec(x, y, stream=st)
+
+
+with torch.cuda.stream(st):
+    run(groups)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    run(groups)
+    run(groups[: upto + 1])
+with torch.cuda.stream(st):
+    for _ in range(3):
+        g.replay()
+torch.cuda.synchronize()
+buf = np.zeros(148 * 32 * 8, dtype=np.uint64)
+assert lib.spqr_debug_timeline(buf.ctypes.data, buf.size) == 0
+T = buf.reshape(-1, 8).astype(np.int64)
+T = T[(T[:, 4] > 0) & (T[:, 7] >= 1000)]
+t0 = T[:, 0].min()
+r = (T[:, :5] - t0) / 1e3
+print(f"== {target} (after {groups[upto - 1][0] if upto else groups[-1][0]}): span {r[:, 4].max():.2f} us")
+for k, name in enumerate(["entry", "pdl_wait", "first_cell", "loop_end", "exit"]):
+    q = np.percentile(r[:, k], [0, 10, 50, 90, 100])
+    print(f"  {name:11s} " + " ".join(f"{v:7.2f}" for v in q))
+if T[:, 5].max() > 1e12:  # panels-built stamp (SHX layers)
+    q = np.percentile((T[:, 5] - t0) / 1e3, [0, 10, 50, 90, 100])
+    print(f"  {'panels':11s} " + " ".join(f"{v:7.2f}" for v in q))
+print(f"  full-wait us per warp (median) {np.median(T[:, 6]) / 1e3:.2f}")
