@@ -181,7 +181,7 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
         if (batch >= 2) {  // gemm_tc: x tiles for N <= 128, partial tiles, per-warp tile counters
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
-            w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 8 * 4);
+            w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 16 * 4);
         }
         w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
@@ -291,12 +291,12 @@ void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, c
 
 // ---- gemm_tc (batch >= 2): 4 dequant warps + 1 control warp per CTA -------
 constexpr std::uint32_t kTcStaticMax = 2048;
-constexpr std::uint32_t kTcMaxN = 128;  // batch columns per launch
+constexpr std::uint32_t kTcMaxN = 64;  // batch columns per launch
 // below this batch, repeated gemv_cta launches beat the dequant-then-MMA
 // kernel (tools/batch_sweep.py: 2 x 30 us vs 122 us at batch 2 on 8192x22016)
 constexpr int kTcMinBatch = 5;
 std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N) {
-    return 2u * 128u * 128u * 2u + 2u * 256u * N + 8u * L->tcp.slot_bytes + 8u * 4096u;
+    return 3u * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + 16u * 2304u;
 }
 
 template <int BW, int BSZ>
@@ -316,7 +316,7 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nv);
-    cfg.blockDim = dim3(288);
+    cfg.blockDim = dim3(544);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -363,7 +363,7 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
         p.partial = reinterpret_cast<float*>(base + w.tc_part);
         p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
         p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
-        p.rec_cap = L->tcp.slot_bytes; p.slot_bytes = L->tcp.slot_bytes;
+        p.rec_cap = L->tcp.slot_bytes; p.slot_bytes = L->tcp.slot_bytes; p.pn_magic = L->pn_magic;
         p.sigma = L->tcp.sigma;
         p.out_scale = std::ldexp(1.0f, L->tcp.sigma);
         const std::uint32_t smem = tc_smem(L, N);
@@ -711,8 +711,8 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
         slots += gmap[2 * T_ + 1];
     }
     c.pslots = slots;
-    c.slot_bytes = (t.cell_bytes + 2048u + 127u) & ~127u;
-    const std::uint32_t need = 2u * 128u * 128u * 2u + 2u * 256u * kTcMaxN + 8u * c.slot_bytes + 8u * 4096u;
+    c.slot_bytes = (t.cell_bytes + 512u + 127u) & ~127u;  // outliers beyond a slot are read from HBM
+    const std::uint32_t need = 3u * 128u * 128u * 2u + 3u * 256u * kTcMaxN + 8u * c.slot_bytes + 16u * 2304u;
     if (need + kTcStaticMax > kSmemLimit)
         c.slot_bytes = ((kSmemLimit - kTcStaticMax - (need - 8u * c.slot_bytes)) / 8u) & ~127u;
     if (c.slot_bytes < t.cell_bytes + 16u) spqr::fail(spqr::Errc::config_invalid, "gemm_tc: shared memory plan");

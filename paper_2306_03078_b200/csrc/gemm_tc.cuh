@@ -12,7 +12,7 @@
 // the north star's 1e-3 relative (fp16 weight rounding costs ~1e-4).
 //
 // Tiles: 128 rows (four 32-row cell rows) x 128 columns (half a 256-column
-// panel) per MMA stage, N = batch padded to 16 (<= 128 per launch).
+// panel) per MMA stage, N = batch padded to 16 (<= 64 per launch).
 //   * warps 0-3 ("dequant warps"): warp i streams the cells of row-group pair
 //     4T+i (cp.async.bulk, two record slots, one cell of lookahead), decodes
 //     the bilevel statistics into a per-(row, block) fp16 table
@@ -40,9 +40,10 @@ struct TcParams {
     const std::uint8_t* xpanels;      // [2*Pn][N x 128 fp16] x tiles (xprep_tc)
     float* y;                         // [B][m]
     float* partial;                   // [slots][N][128]
-    std::uint32_t* counters;          // [Tn][8] (per dequant warp), zero between launches
+    std::uint32_t* counters;          // [Tn][16] (per dequant warp), zero between launches
     std::uint32_t m, Pn, Gn, Tn, nv, B, N;
     std::uint32_t rec_cap, slot_bytes;
+    std::uint32_t pn_magic;           // u / Pn == umulhi(u, pn_magic) (Pn > 1)
     float out_scale;                  // 2^sigma
     int sigma;
 };
@@ -82,9 +83,11 @@ __device__ __forceinline__ void ld16(std::uint32_t taddr, float (&v)[16]) {
 }
 __device__ __forceinline__ void stsm_x4(std::uint32_t addr, std::uint32_t a0, std::uint32_t a1, std::uint32_t a2,
                                         std::uint32_t a3) {
+    // no "memory" clobber: the A stage is only read by the tensor core after the
+    // (volatile, clobbering) proxy fence + mbarrier arrive, which stay ordered
+    // after this volatile asm; the table loads may be scheduled across it
     asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a0), "r"(a1),
-                 "r"(a2), "r"(a3)
-                 : "memory");
+                 "r"(a2), "r"(a3));
 }
 // (a - (z, z)) * (s, s) + (c, c) per f16 lane; z, s, c are the low (HI=false)
 // or high (HI=true) halves of their registers.  a - z is exact (both are
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int 
 }
 
 template <int BW, int BS, int BZ>
-__global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
+__global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
@@ -158,40 +161,57 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
     constexpr float kMagic = 8388608.0f;
     constexpr std::uint32_t A_STAGE = 128u * 128u * 2u;  // 32 KB
     constexpr std::uint32_t KC_A = 2048u;                // A: bytes between k core matrices (16 row groups)
-    constexpr int CTRL = 8;                              // control warp
+    constexpr int ND = 16;                               // dequant warps
+    constexpr int CTRL = ND;                             // control warp
 
     extern __shared__ __align__(128) std::uint8_t smem[];
-    __shared__ std::uint64_t rec_full[4][2], rec_empty[4][2], a_full[2], a_free[2], b_full[2], d_full[2], d_free[2];
+    __shared__ std::uint64_t rec_full[4][2], rec_empty[4][2], a_full[3], a_free[3], b_full[3], b_free[3], d_full[2],
+        d_free[2];
     __shared__ std::uint32_t slot_r[4][2][2];
     __shared__ std::uint32_t tmem_base;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::uint32_t N = p.N;
     const std::uint32_t B_STAGE = 256u * N;
+#ifdef SPQR_TIMELINE
+    unsigned long long tw[4] = {0, 0, 0, 0};
+    const unsigned long long t_start = gtime();
+#define TC_WAIT(i, expr)                      \
+    {                                         \
+        const unsigned long long t0_ = gtime(); \
+        expr;                                 \
+        tw[i] += gtime() - t0_;               \
+    }
+#else
+#define TC_WAIT(i, expr) expr;
+#endif
     const std::uint32_t tcols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
-    std::uint8_t* abuf = smem;                                  // [2][A_STAGE]: stage half h in buffer h
-    std::uint8_t* bbuf = smem + 2 * A_STAGE;                    // [2][B_STAGE]
-    std::uint8_t* recs = bbuf + 2 * B_STAGE;                    // [4 cell rows][2][slot_bytes]
-    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [8 warps][2 units][16 rows][8 blocks] x 16 B
+    std::uint8_t* abuf = smem;                                  // [3][A_STAGE]: stage s in buffer s % 3
+    std::uint8_t* bbuf = smem + 3 * A_STAGE;                    // [3][B_STAGE]: x tiles, 2 stages of lookahead
+    std::uint8_t* recs = bbuf + 3 * B_STAGE;                    // [4 cell rows][2][slot_bytes]
+    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [16 warps][16 rows][144 B: 8 blocks x 16 B + pad]
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i)
             for (int k = 0; k < 2; ++k) {
                 mbar_init(&rec_full[i][k], 1);
-                mbar_init(&rec_empty[i][k], 2);  // both half-warps of the cell row
+                mbar_init(&rec_empty[i][k], 4);  // the four (unit, half) warps of the cell row
             }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&a_full[b], 4);
+        for (int b = 0; b < 3; ++b) {
+            mbar_init(&a_full[b], 8);  // 4 cell rows x 2 units write a half stage
             mbar_init(&a_free[b], 1);
             mbar_init(&b_full[b], 1);
+            mbar_init(&b_free[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], 1);
-            mbar_init(&d_free[b], 8);
+            mbar_init(&d_free[b], ND);
         }
         fence_mbar_init();
     }
     // zero both A stages once: rows of missing row-group pairs (the layer's last
     // tile) then contribute 0 instead of whatever shared memory held
-    for (std::uint32_t i = threadIdx.x; i < 2u * A_STAGE / 16u; i += blockDim.x)
+    for (std::uint32_t i = threadIdx.x; i < 3u * A_STAGE / 16u; i += blockDim.x)
         reinterpret_cast<uint4*>(abuf)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
     if (warp == CTRL) {  // two accumulators of N fp32 columns each
@@ -213,35 +233,37 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
         if (lane == 0) {
             pdl_wait();  // xprep_tc has completed
             const std::uint32_t idesc = (1u << 4) | ((N >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32, K-major
-            auto issue_b = [&](std::uint32_t s) {
-                const std::uint32_t u = u0 + (s >> 1), P = u % p.Pn;
-                const std::uint32_t b = s & 1u;
-                if (s >= 2) mbar_wait(&a_free[b], ((s >> 1) - 1u) & 1u);
+            auto pan = [&](std::uint32_t u) { return p.Pn == 1u ? 0u : u - __umulhi(u, p.pn_magic) * p.Pn; };
+            auto issue_b = [&](std::uint32_t s) {  // x tile of stage s into buffer s % 3
+                const std::uint32_t u = u0 + (s >> 1), P = pan(u);
+                const std::uint32_t b = s % 3u;
+                if (s >= 3) mbar_wait(&b_free[b], ((s / 3u) - 1u) & 1u);
                 mbar_expect_tx(&b_full[b], B_STAGE);
                 bulk_g2s(bbuf + b * B_STAGE, p.xpanels + static_cast<std::size_t>(2u * P + (s & 1u)) * B_STAGE, B_STAGE,
                          &b_full[b]);
             };
-            if (nst > 0) issue_b(0);
+            for (std::uint32_t s = 0; s < 2 && s < nst; ++s) issue_b(s);
             std::uint32_t tile_i = 0;  // tiles started in this range
 #pragma unroll 1
             for (std::uint32_t s = 0; s < nst; ++s) {
-                const std::uint32_t u = u0 + (s >> 1), P = u % p.Pn;
+                const std::uint32_t u = u0 + (s >> 1), P = pan(u);
                 const bool first = (s & 1u) == 0 && ((s >> 1) == 0 || P == 0);  // first stage of a tile
                 const bool last = (s & 1u) && (u + 1 == u1 || P + 1 == p.Pn);
-                if (first && tile_i >= 2) mbar_wait(&d_free[tile_i & 1u], ((tile_i >> 1) - 1u) & 1u);
-                if (s + 1 < nst) issue_b(s + 1);
-                const std::uint32_t b = s & 1u;
-                mbar_wait(&a_full[b], (s >> 1) & 1u);
-                mbar_wait(&b_full[b], (s >> 1) & 1u);
+                if (first && tile_i >= 2) TC_WAIT(2, mbar_wait(&d_free[tile_i & 1u], ((tile_i >> 1) - 1u) & 1u))
+                if (s + 2 < nst) issue_b(s + 2);
+                const std::uint32_t b = s % 3u, bb = b;
+                TC_WAIT(0, mbar_wait(&a_full[b], (s / 3u) & 1u))
+                TC_WAIT(1, mbar_wait(&b_full[bb], (s / 3u) & 1u))
                 tc::fence_after();
                 const std::uint32_t d = tmem + (tile_i & 1u) * N;
-                const std::uint32_t a_sa = smem_u32(abuf + b * A_STAGE), b_sa = smem_u32(bbuf + b * B_STAGE);
+                const std::uint32_t a_sa = smem_u32(abuf + b * A_STAGE), b_sa = smem_u32(bbuf + bb * B_STAGE);
 #pragma unroll
                 for (std::uint32_t kk = 0; kk < 8; ++kk)
                     tc::mma_f16(d, tc::smem_desc(a_sa + kk * 2u * KC_A, KC_A, 128u),
                                 tc::smem_desc(b_sa + kk * 2u * 16u * N, 16u * N, 128u), idesc,
                                 (first && kk == 0) ? 0u : 1u);
-                tc::commit(&a_free[b]);  // A and x buffers b are free once these MMAs finish
+                tc::commit(&a_free[b]);   // A buffer b and x buffer bb are free once these MMAs finish
+                tc::commit(&b_free[bb]);
                 if (last) {
                     tc::commit(&d_full[tile_i & 1u]);
                     ++tile_i;
@@ -251,24 +273,26 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
         __syncwarp();
     } else {
         // ------------------------------------------------------- dequant --
-        // warp = 4 hh + ci: cell row ci (row-group pair 4T + ci) of every tile,
-        // column half hh (blocks 8hh .. 8hh+7) of every panel
-        const int ci = warp & 3, hh = warp >> 2;
+        // warp = 8 uu + 4 hh + ci: cell row ci (row-group pair 4T + ci), column
+        // half hh (blocks 8hh .. 8hh+7) and unit uu (rows 16uu .. 16uu+15) of
+        // every cell; warp % 4 == ci, the TMEM lane quarter the epilogue reads
+        const int ci = warp & 3, hh = (warp >> 2) & 1, uu = warp >> 3;
         const int g = lane >> 2, t = lane & 3;
         std::uint8_t* ring = recs + static_cast<std::uint32_t>(ci) * 2u * p.slot_bytes;
-        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 4096u;
+        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 2304u;  // 16 rows x 144 B (padded: no bank conflicts)
         const std::uint32_t magic = 0x4B000000u;
+        auto tile_of = [&](std::uint32_t u) { return p.Pn == 1u ? u : __umulhi(u, p.pn_magic); };
         auto cell_of = [&](std::uint32_t u, std::uint32_t& q) {
-            const std::uint32_t T_ = u / p.Pn, P = u - T_ * p.Pn;
+            const std::uint32_t T_ = tile_of(u), P = u - T_ * p.Pn;
             const std::uint32_t Gq = 4u * T_ + static_cast<std::uint32_t>(ci);
             q = Gq * p.Pn + P;
             return Gq < p.Gn;
         };
-        // record k of this cell row goes to slot k & 1; half 0 issues it once
-        // both halves released the slot's previous record
+        // record k of this cell row goes to slot k & 1; warp (ci, 0, 0) issues it
+        // once all four warps of the row released the slot's previous record
         auto issue = [&](std::uint32_t u, std::uint32_t k) {
             std::uint32_t q;
-            if (hh == 0 && lane == 0 && cell_of(u, q)) {
+            if (warp == ci && lane == 0 && cell_of(u, q)) {
                 const std::uint32_t sl = k & 1u;
                 if (k >= 2) mbar_wait(&rec_empty[ci][sl], ((k >> 1) - 1u) & 1u);
                 const std::uint32_t r0 = __ldg(p.cell_off + q), r1 = __ldg(p.cell_off + q + 1);
@@ -280,6 +304,17 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
             }
         };
         const float sig_scale = __uint_as_float(static_cast<std::uint32_t>(127 - p.sigma) << 23);  // 2^-sigma
+        // per-lane constants of the statistics: blocks 8hh + 2t + bs, bs = 0, 1
+        float2 f0, f1, g0, g1;  // s multipliers 2^(24-p-sigma) and code scales 2^(p-24), column halves 0 / 1
+        {
+            const int mm0 = (2 * t) % G::MPC, mm1 = (2 * t + 1) % G::MPC;
+            auto pw = [](int e) { return __uint_as_float(static_cast<std::uint32_t>(127 + e) << 23); };
+            f0 = make_float2(pw(24 - T::prescale_p(BW, 2 * mm0) - p.sigma), pw(24 - T::prescale_p(BW, 2 * mm1) - p.sigma));
+            f1 = make_float2(pw(24 - T::prescale_p(BW, 2 * mm0 + 1) - p.sigma),
+                             pw(24 - T::prescale_p(BW, 2 * mm1 + 1) - p.sigma));
+            g0 = make_float2(pw(T::prescale_p(BW, 2 * mm0) - 24), pw(T::prescale_p(BW, 2 * mm1) - 24));
+            g1 = make_float2(pw(T::prescale_p(BW, 2 * mm0 + 1) - 24), pw(T::prescale_p(BW, 2 * mm1 + 1) - 24));
+        }
         std::uint32_t k = 0;  // records of this cell row consumed so far
         if (u0 < u1) issue(u0, 0);
         pdl_wait();
@@ -294,136 +329,156 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
             if (have && u + 1 < u1) issue(u + 1, k + 1);
             const std::uint32_t sl = k & 1u;
             const std::uint8_t* cell = ring + sl * p.slot_bytes;
+            const std::uint8_t* unit = cell + uu * UNIT;
             std::uint32_t r0 = 0, r1 = 0;
             if (have) {
-                mbar_wait(&rec_full[ci][sl], (k >> 1) & 1u);
+                TC_WAIT(0, mbar_wait(&rec_full[ci][sl], (k >> 1) & 1u))
                 r0 = slot_r[ci][sl][0];
                 r1 = slot_r[ci][sl][1];
-                // statistics of this half: lane owns (row g + 8rho, block 8hh + 2t + bs) of both units
+                // statistics: lane owns (row g + 8rho, block 8hh + 2t + bs) of unit uu;
+                // the two blocks bs = 0, 1 ride in the halves of packed f32x2 math
+                std::uint32_t ss, zz;
+                load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
+                const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * hh + 2 * t) * 8);
+                const __half2 sh0 = u32_as_h2(s4.x), zh0 = u32_as_h2(s4.y), sh1 = u32_as_h2(s4.z), zh1 = u32_as_h2(s4.w);
+                const float2 Ss = make_float2(__low2float(sh0), __low2float(sh1));
+                const float2 Zs = make_float2(-__high2float(sh0), -__high2float(sh1));
+                const float2 Sz = make_float2(__low2float(zh0), __low2float(zh1));
+                const float2 Zz = make_float2(-__high2float(zh0), -__high2float(zh1));
 #pragma unroll
-                for (int uu = 0; uu < 2; ++uu) {
-                    const std::uint8_t* unit = cell + uu * UNIT;
-                    std::uint32_t ss, zz;
-                    load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
-                    const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * hh + 2 * t) * 8);
-                    const std::uint32_t sw[2] = {s4.x, s4.z}, zw[2] = {s4.y, s4.w};
-#pragma unroll
-                    for (int bs = 0; bs < 2; ++bs) {
-                        const __half2 sh = u32_as_h2(sw[bs]), zh = u32_as_h2(zw[bs]);
-                        const float Ss = __low2float(sh), Zs = __high2float(sh);
-                        const float Sz = __low2float(zh), Zz = __high2float(zh);
-                        const int mm = (2 * t + bs) % G::MPC;  // block 8hh + 2t + bs, 8 % MPC == 0
-                        const int p0 = T::prescale_p(BW, 2 * mm), p1 = T::prescale_p(BW, 2 * mm + 1);
-                        const float f0 = __uint_as_float(static_cast<std::uint32_t>(127 + 24 - p0 - p.sigma) << 23);
-                        const float f1 = __uint_as_float(static_cast<std::uint32_t>(127 + 24 - p1 - p.sigma) << 23);
-                        const float g0 = __uint_as_float(static_cast<std::uint32_t>(127 - 24 + p0) << 23);
-                        const float g1 = __uint_as_float(static_cast<std::uint32_t>(127 - 24 + p1) << 23);
-#pragma unroll
-                        for (int rho = 0; rho < 2; ++rho) {
-                            const int eps = 4 * hh + 2 * bs + rho;
-                            const float cs = magic_field_rt<SMASK>(ss, eps * BS, magic) - kMagic;
-                            const float cz = magic_field_rt<ZMASK>(zz, eps * BZ, magic) - kMagic;
-                            const float shat = Ss * (cs - Zs);
-                            const float zhat = Sz * (cz - Zz);
-                            // integer part of the zero goes into the codes exactly; the
-                            // fraction (|.| <= 1/2) is the fp16 addend
-                            const float zi = fminf(fmaxf(rintf(zhat), -1000.f), 1000.f);
-                            const std::uint32_t s01 = pack_h2_rn(shat * f0, shat * f1);
-                            const std::uint32_t z01 = pack_h2_rn(zi * g0, zi * g1);
-                            const std::uint32_t c = pack_h2_rn(-(shat * (zhat - zi)) * sig_scale, 0.f);
-                            *reinterpret_cast<uint4*>(tab + ((uu * 16 + g + 8 * rho) * 8 + 2 * t + bs) * 16) =
-                                make_uint4(s01, z01, c, 0u);
-                        }
-                    }
+                for (int rho = 0; rho < 2; ++rho) {
+                    const int e0 = 4 * hh + rho, e1 = 4 * hh + 2 + rho;  // eps of bs = 0, 1
+                    const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss, e0 * BS, magic),
+                                                        magic_field_rt<SMASK>(ss, e1 * BS, magic)),
+                                            make_float2(-kMagic, -kMagic));
+                    const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz, e0 * BZ, magic),
+                                                        magic_field_rt<ZMASK>(zz, e1 * BZ, magic)),
+                                            make_float2(-kMagic, -kMagic));
+                    const float2 shat = fmul2(Ss, fadd2(cs, Zs));
+                    const float2 zhat = fmul2(Sz, fadd2(cz, Zz));
+                    // integer part of the zero goes into the codes exactly; the
+                    // fraction (|.| <= 1/2) is the fp16 addend
+                    const float2 zi = make_float2(fminf(fmaxf(rintf(zhat.x), -1000.f), 1000.f),
+                                                  fminf(fmaxf(rintf(zhat.y), -1000.f), 1000.f));
+                    const float2 S0 = fmul2(shat, f0), S1 = fmul2(shat, f1);
+                    const float2 Z0 = fmul2(zi, g0), Z1 = fmul2(zi, g1);
+                    const float2 C = fmul2(fmul2(shat, fadd2(zi, make_float2(-zhat.x, -zhat.y))),
+                                           make_float2(sig_scale, sig_scale));
+                    const int row = g + 8 * rho;
+                    *reinterpret_cast<uint4*>(tab + row * 144 + (2 * t) * 16) =
+                        make_uint4(pack_h2_rn(S0.x, S1.x), pack_h2_rn(Z0.x, Z1.x), pack_h2_rn(C.x, 0.f), 0u);
+                    *reinterpret_cast<uint4*>(tab + row * 144 + (2 * t + 1) * 16) =
+                        make_uint4(pack_h2_rn(S0.y, S1.y), pack_h2_rn(Z0.y, Z1.y), pack_h2_rn(C.y, 0.f), 0u);
                 }
                 __syncwarp();
             }
-            const std::uint32_t s = 2u * it + static_cast<std::uint32_t>(hh);
-            if (it >= 1) mbar_wait(&a_free[hh], (it - 1u) & 1u);
-            std::uint8_t* A = abuf + static_cast<std::uint32_t>(hh) * A_STAGE;
+            const std::uint32_t st_ = 2u * it + static_cast<std::uint32_t>(hh), ab = st_ % 3u;
+            if (st_ >= 3) TC_WAIT(1, mbar_wait(&a_free[ab], ((st_ / 3u) - 1u) & 1u))
+            std::uint8_t* A = abuf + ab * A_STAGE;
             if (have) {
+                std::uint32_t cw[G::LANE_WORDS];
 #pragma unroll
-                for (int uu = 0; uu < 2; ++uu) {
-                    const std::uint8_t* unit = cell + uu * UNIT;
-                    std::uint32_t cw[G::LANE_WORDS];
-#pragma unroll
-                    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                        const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                        cw[4 * i] = w4.x;
-                        cw[4 * i + 1] = w4.y;
-                        cw[4 * i + 2] = w4.z;
-                        cw[4 * i + 3] = w4.w;
-                    }
-                    const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
-                                                 (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
-                    auto do_half = [&](auto HH) {
-                        constexpr int h_ = decltype(HH)::value;
-#pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) {
-                            const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
-                            const std::uint32_t* w = cw + G::CW * cidx;
-                            const uint4 e0 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g) * 8 + jj) * 16);
-                            const uint4 e1 = *reinterpret_cast<const uint4*>(tab + ((uu * 16 + g + 8) * 8 + jj) * 16);
-                            std::uint32_t a[4];
-#pragma unroll
-                            for (int r = 0; r < 4; ++r) {
-                                const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                                const int i = rho * (G::NP / 2) + qq;
-                                const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                                const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
-                                const uint4 e = rho ? e1 : e0;
-                                a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
-                            }
-                            tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
-                        }
-                    };
-                    if (hh == 0)
-                        do_half(std::integral_constant<int, 0>{});
-                    else
-                        do_half(std::integral_constant<int, 1>{});
+                for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                    const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                    cw[4 * i] = w4.x;
+                    cw[4 * i + 1] = w4.y;
+                    cw[4 * i + 2] = w4.z;
+                    cw[4 * i + 3] = w4.w;
                 }
+                const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
+                                             (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
+                auto do_half = [&](auto HH) {
+                    constexpr int h_ = decltype(HH)::value;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
+                        const std::uint32_t* w = cw + G::CW * cidx;
+                        const uint4 e0 = *reinterpret_cast<const uint4*>(tab + g * 144 + jj * 16);
+                        const uint4 e1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144 + jj * 16);
+                        std::uint32_t a[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                            const int i = rho * (G::NP / 2) + qq;
+                            const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
+                            const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                            const uint4 e = rho ? e1 : e0;
+                            a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
+                        }
+                        tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
+                    }
+                };
+                if (hh == 0)
+                    do_half(std::integral_constant<int, 0>{});
+                else
+                    do_half(std::integral_constant<int, 1>{});
                 __syncwarp();
-                // outliers of this half: w += v (fp16, scaled by 2^-sigma)
+                // outliers of this (unit, half): w += v (fp16, scaled by 2^-sigma).
+                // Entries are sorted by (row, col): unit 0's rows come first, so
+                // this warp's unit is one contiguous run [ia, ib) of the list
                 const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
-                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
-                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+                if (cnt) {
+                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+                    auto entry = [&](std::uint32_t i) { return i < nfast ? es[i] : __ldg(eg + i); };
+                    // n0 = entries of rows 0..15 = first index whose row is >= 16
+                    // (padding sorts last: row 255): two rounds of 32 probes
+                    std::uint32_t lo = 0, span = cnt;  // the boundary lies in [lo, lo + span]
 #pragma unroll 1
-                for (std::uint32_t i = lane; i < cnt; i += 32) {
-                    const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
-                    const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
-                    if (row < 32u && (col >> 7) == static_cast<std::uint32_t>(hh)) {  // 0xffffffff = padding
-                        const std::uint32_t kq = col & 127u, rr = 32u * ci + row;
-                        __half* wp = reinterpret_cast<__half*>(A + (kq >> 3) * KC_A + (rr >> 3) * 128u +
-                                                               (rr & 7u) * 16u + (kq & 7u) * 2u);
-                        *wp = __float2half_rn(__half2float(*wp) + h2f_bits(e & 0xffffu) * sig_scale);
+                    while (span > 32) {
+                        const std::uint32_t step = (span + 31) / 32;
+                        const std::uint32_t i = lo + lane * step;  // probe: is entry i still unit 0?
+                        const bool below = i < cnt && (entry(i) >> 24) < 16u;
+                        const std::uint32_t nb = __popc(__ballot_sync(0xffffffffu, below));  // probes below
+                        if (nb == 0) break;  // boundary at lo
+                        lo += (nb - 1) * step + 1;
+                        span = step - 1;
+                    }
+                    const bool below = lane < span && lo + lane < cnt && (entry(lo + lane) >> 24) < 16u;
+                    const std::uint32_t n0 = lo + __popc(__ballot_sync(0xffffffffu, below));
+                    const std::uint32_t ia = uu ? n0 : 0u, ib = uu ? cnt : n0;
+                    const std::uint32_t a_row0 = smem_u32(A) + (4u * ci) * 128u;
+#pragma unroll 1
+                    for (std::uint32_t i = ia + lane; i < ib; i += 32) {
+                        const std::uint32_t e = entry(i);
+                        const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
+                        if (row < 32u && (col >> 7) == static_cast<std::uint32_t>(hh)) {
+                            const std::uint32_t kq = col & 127u;
+                            const std::uint32_t sa = a_row0 + (kq >> 3) * KC_A + (row >> 3) * 128u + (row & 7u) * 16u +
+                                                     (kq & 7u) * 2u;
+                            unsigned short hb;
+                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hb) : "r"(sa));
+                            const float wv = __half2float(__ushort_as_half(hb)) + h2f_bits(e & 0xffffu) * sig_scale;
+                            hb = __half_as_ushort(__float2half_rn(wv));
+                            asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa), "h"(hb));
+                        }
                     }
                 }
             }
             fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
             __syncwarp();
-            if (lane == 0) mbar_arrive(&a_full[hh]);
+            if (lane == 0) mbar_arrive(&a_full[ab]);
             if (have) {
-                if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);  // this half is done with the record
+                if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);  // this warp is done with the record
                 ++k;
             }
-            (void)s;
-            // epilogue after the tile's last unit in this range: the two halves
+            // epilogue after the tile's last unit in this range: the four warps
             // of a cell row split the accumulator's 16-column chunks
-            const std::uint32_t P = u % p.Pn;
+            const std::uint32_t T_ = tile_of(u), P = u - T_ * p.Pn;
             if (u + 1 == u1 || P + 1 == p.Pn) {
-                const std::uint32_t T_ = u / p.Pn;
                 const std::uint32_t db = tile_i & 1u;
-                mbar_wait(&d_full[db], (tile_i >> 1) & 1u);
+                const std::uint32_t part4 = static_cast<std::uint32_t>(warp >> 2);  // 0..3
+                TC_WAIT(2, mbar_wait(&d_full[db], (tile_i >> 1) & 1u))
                 tc::fence_after();
                 const std::uint32_t row = 128u * T_ + 32u * ci + lane;
                 const std::uint32_t ta = tmem + ((32u * ci) << 16) + db * N;
                 const std::uint32_t ua = u0 > T_ * p.Pn ? u0 : T_ * p.Pn;  // this range's units of tile T
                 const bool whole = ua == T_ * p.Pn && u + 1 == (T_ + 1) * p.Pn;
                 const uint2 gm = whole ? make_uint2(0, 0) : __ldg(reinterpret_cast<const uint2*>(p.gmap) + T_);
-                const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == u0 / p.Pn ? 0u : 1u));
+                const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == tile_of(u0) ? 0u : 1u));
 #pragma unroll 1
-                for (std::uint32_t c0 = 16u * hh; c0 < N; c0 += 32) {
+                for (std::uint32_t c0 = 16u * part4; c0 < N; c0 += 64) {
                     float vv[16];
                     tc::ld16(ta + c0, vv);
 #pragma unroll
@@ -445,13 +500,13 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
                     if (lane == 0)
                         asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;"
                                      : "=r"(prev)
-                                     : "l"(p.counters + 8u * T_ + warp)
+                                     : "l"(p.counters + 16u * T_ + warp)
                                      : "memory");
                     prev = __shfl_sync(0xffffffffu, prev, 0);
                     __syncwarp();
                     if (prev == gm.y - 1u) {
 #pragma unroll 1
-                        for (std::uint32_t c0 = 16u * hh; c0 < N; c0 += 32)
+                        for (std::uint32_t c0 = 16u * part4; c0 < N; c0 += 64)
                             for (std::uint32_t bcol = c0; bcol < c0 + 16u && bcol < p.B; ++bcol) {
                                 float sum = 0.f;
                                 for (std::uint32_t j = 0; j < gm.y; ++j)
@@ -459,13 +514,26 @@ __global__ void __launch_bounds__(288, 1) gemm_tc(const TcParams p) {
                                                   32u * ci + lane);
                                 if (row < p.m) p.y[static_cast<std::size_t>(bcol) * p.m + row] = sum * p.out_scale;
                             }
-                        if (lane == 0) p.counters[8u * T_ + warp] = 0;
+                        if (lane == 0) p.counters[16u * T_ + warp] = 0;
                     }
                 }
                 ++tile_i;
             }
         }
     }
+#ifdef SPQR_TIMELINE
+    if (lane == 0 && blockIdx.x < 148) {
+        const std::uint32_t wk = blockIdx.x * 32u + warp;
+        g_timeline[8 * wk + 0] = t_start;
+        g_timeline[8 * wk + 1] = gtime();
+        g_timeline[8 * wk + 2] = tw[0];
+        g_timeline[8 * wk + 3] = tw[1];
+        g_timeline[8 * wk + 4] = tw[2];
+        g_timeline[8 * wk + 5] = u1 - u0;
+        g_timeline[8 * wk + 6] = warp;
+        g_timeline[8 * wk + 7] = 7;
+    }
+#endif
     tc::fence_before();
     __syncthreads();
     if (warp == CTRL) {
