@@ -293,8 +293,8 @@ void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, c
 constexpr std::uint32_t kTcStaticMax = 2048;
 constexpr std::uint32_t kTcMaxN = 64;  // batch columns per launch
 // below this batch, repeated gemv_cta launches beat the dequant-then-MMA
-// kernel (tools/batch_sweep.py: 2 x 30 us vs 122 us at batch 2 on 8192x22016)
-constexpr int kTcMinBatch = 5;
+// kernel (tools/batch_sweep.py, 8192x22016: 3 x 29 us < ~93 us < 4 x 29 us)
+constexpr int kTcMinBatch = 4;
 std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N) {
     return 3u * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + 16u * 2304u;
 }
