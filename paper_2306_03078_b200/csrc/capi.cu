@@ -641,8 +641,8 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     c.grid = std::min<std::uint32_t>(nv, S);
     c.part_cap = std::max<std::uint32_t>(mc, 1);
     const std::uint32_t part_bytes = (c.part_cap * 128u + 127u) & ~127u;
-    const std::uint32_t off_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
-    const std::uint32_t gd_bytes = off_bytes;
+    const std::uint32_t off_bytes = ((c.part_cap + 9u) * 4u + 127u) & ~127u;  // 16-B aligned superset
+    const std::uint32_t gd_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
     const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
     // two record slots per warp; outliers beyond a slot are read from HBM
     const std::uint32_t slot = std::min((ring_avail / (2u * kNC)) & ~127u, (cellb + 4096u + 127u) & ~127u);
@@ -743,7 +743,7 @@ std::uint64_t upload_tiled(spqr_layer* L, const spqr::detail::TiledHost& t,
     L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
     L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
     ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
-    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size());
+    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size() + 4);  // + 4: gemv_cta copies 16-B aligned supersets
     ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice), "H2D cell_off");
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 
     extern __shared__ __align__(128) std::uint8_t smem[];
     __shared__ std::uint64_t full[NC][2];
+    __shared__ std::uint64_t coff_bar;               // the first range's record offsets have landed
     __shared__ std::uint32_t slot_r[NC][2][2];       // record byte range of the slot's cell
     __shared__ std::uint32_t tick[2];                // per-range ticket counters (by range parity)
     __shared__ volatile std::uint32_t pflag[64];     // SHX: x panel built
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if (lane == 0) {
         mbar_init(&full[warp][0], 1);
         mbar_init(&full[warp][1], 1);
+        if (warp == 0) mbar_init(&coff_bar, 1);
         fence_mbar_init();
     }
     if (threadIdx.x == 0) tick[0] = tick[1] = NC;  // ticket w < NC is warp w's first cell
@@ -243,16 +245,30 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             bulk_g2s(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, p.cells + r0, nb, &full[warp][0]);
         }
     }
-    std::uint32_t* coff = reinterpret_cast<std::uint32_t*>(smem + p.off_off);  // record offsets of the range
+    // record offsets of the range: the first range's arrive by one bulk copy
+    // (16-B aligned superset; cell_off is padded), so nothing before the PDL
+    // wait waits on a global load; later ranges load them after a barrier
+    std::uint32_t* const coff_base = reinterpret_cast<std::uint32_t*>(smem + p.off_off);
+    std::uint32_t* coff = coff_base;
     std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
     auto range_setup = [&](std::uint32_t v) {
         const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
+        coff = coff_base;
         for (std::uint32_t i = threadIdx.x; i <= q1 - q0; i += NT) {
             coff[i] = __ldg(p.cell_off + q0 + i);
             gdone[i] = 0;
         }
     };
-    if (blockIdx.x < p.nvcta) range_setup(blockIdx.x);
+    if (blockIdx.x < p.nvcta) {
+        const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
+        const std::uint32_t qa = q0 & ~3u, qb = (q1 + 4u) & ~3u;
+        coff = coff_base + (q0 - qa);
+        for (std::uint32_t i = threadIdx.x; i <= q1 - q0; i += NT) gdone[i] = 0;
+        if (threadIdx.x == 0) {  // the thread that initialised coff_bar
+            mbar_expect_tx(&coff_bar, 4u * (qb - qa));
+            bulk_g2s(coff_base, p.cell_off + qa, 4u * (qb - qa), &coff_bar);
+        }
+    }
     __syncthreads();
     // the next kernel in the stream may be scheduled now; it reads what we
     // write only after this grid has completed (its griddepcontrol.wait)
@@ -284,6 +300,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     // lane 0: copy the record of range ticket k into slot sl (offsets from coff)
     auto issue = [&](std::uint32_t k, std::uint32_t sl) {
         if (lane == 0) {
+            mbar_wait(&coff_bar, 0);  // immediate after the first range's offsets landed
             const std::uint32_t r0 = coff[k], r1 = coff[k + 1];
             slot_r[warp][sl][0] = r0;
             slot_r[warp][sl][1] = r1;
