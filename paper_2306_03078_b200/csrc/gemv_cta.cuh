@@ -35,6 +35,13 @@
 // Every reduction order is fixed by the partition, not by the schedule, so y
 // is bitwise reproducible run to run.
 
+// Cells of a range split into two half tickets at its end (see decode()):
+// measured slower than whole cells (a half ticket costs ~2/3 of a cell), so
+// off by default; -DSPQR_SPLIT_CELLS_FN='min(NC / 2u, nc / 2u)' turns it on.
+#ifndef SPQR_SPLIT_CELLS_FN
+#define SPQR_SPLIT_CELLS_FN 0u
+#endif
+
 struct CtaParams {
     const std::uint8_t* cells;        // cell records
     const std::uint32_t* cell_off;    // [ncell+1]
@@ -232,17 +239,45 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if (threadIdx.x < 64) pflag[threadIdx.x] = 0u;
     rowsum[warp][lane] = 0.f;
     if (lane < 4) zrow[warp][lane] = 0u;
+    // Tickets of a range of nc cells: the first nc - S are whole cells, the
+    // last S cells are split into two half tickets (one 16-row unit each) so
+    // the range's final round is half as long.  Ticket -> (cell, unit or -1).
+    auto split_of = [](std::uint32_t nc) -> std::uint32_t { return SPQR_SPLIT_CELLS_FN; };
+    auto decode = [](std::uint32_t tkt, std::uint32_t nc, std::uint32_t S, int& uo) {
+        const std::uint32_t f = nc - S;
+        if (tkt < f) {
+            uo = -1;
+            return tkt;
+        }
+        uo = static_cast<int>((tkt - f) & 1u);
+        return f + ((tkt - f) >> 1);
+    };
+    // lane 0: bulk copies of a ticket's record bytes into a slot -- the whole
+    // record, or for a half ticket its unit plus the cell's outlier entries
+    auto copy_rec = [&](std::uint8_t* dst, std::uint32_t r0, std::uint32_t r1, int uo, std::uint64_t* bar) {
+        const std::uint32_t nb = min(r1 - r0, p.rec_cap);
+        if (uo < 0) {
+            mbar_expect_tx(bar, nb);
+            bulk_g2s(dst, p.cells + r0, nb, bar);
+        } else {
+            const std::uint32_t ol = nb - CELL;
+            mbar_expect_tx(bar, UNIT + ol);
+            bulk_g2s(dst + uo * UNIT, p.cells + r0 + uo * UNIT, UNIT, bar);
+            if (ol) bulk_g2s(dst + CELL, p.cells + r0 + CELL, ol, bar);
+        }
+    };
     // the first record of this warp's first ticket goes out before anything
     // else, from the global offsets (the range's offset table loads meanwhile)
     if (blockIdx.x < p.nvcta && lane == 0) {
         const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
-        if (static_cast<std::uint32_t>(warp) < q1 - q0) {
-            const std::uint32_t r0 = __ldg(p.cell_off + q0 + warp), r1 = __ldg(p.cell_off + q0 + warp + 1);
+        const std::uint32_t S0 = split_of(q1 - q0);
+        if (static_cast<std::uint32_t>(warp) < q1 - q0 + S0) {
+            int uo;
+            const std::uint32_t c = decode(warp, q1 - q0, S0, uo);
+            const std::uint32_t r0 = __ldg(p.cell_off + q0 + c), r1 = __ldg(p.cell_off + q0 + c + 1);
             slot_r[warp][0][0] = r0;
             slot_r[warp][0][1] = r1;
-            const std::uint32_t nb = min(r1 - r0, p.rec_cap);
-            mbar_expect_tx(&full[warp][0], nb);
-            bulk_g2s(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, p.cells + r0, nb, &full[warp][0]);
+            copy_rec(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, r0, r1, uo, &full[warp][0]);
         }
     }
     // record offsets of the range: the first range's arrive by one bulk copy
@@ -297,16 +332,14 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     const int pp = T::column_prescale(BW, static_cast<std::uint32_t>(lane >> 1), 8u * (lane & 1));
 
     std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes;
-    // lane 0: copy the record of range ticket k into slot sl (offsets from coff)
-    auto issue = [&](std::uint32_t k, std::uint32_t sl) {
+    // lane 0: copy the record of cell k (unit uo, or whole) into slot sl (offsets from coff)
+    auto issue = [&](std::uint32_t k, int uo, std::uint32_t sl) {
         if (lane == 0) {
             mbar_wait(&coff_bar, 0);  // immediate after the first range's offsets landed
             const std::uint32_t r0 = coff[k], r1 = coff[k + 1];
             slot_r[warp][sl][0] = r0;
             slot_r[warp][sl][1] = r1;
-            const std::uint32_t nb = min(r1 - r0, p.rec_cap);
-            mbar_expect_tx(&full[warp][sl], nb);
-            bulk_g2s(ring + sl * p.slot_bytes, p.cells + r0, nb, &full[warp][sl]);
+            copy_rec(ring + sl * p.slot_bytes, r0, r1, uo, &full[warp][sl]);
         }
     };
     std::uint32_t nit = 0;  // cells this warp has taken (slot nit & 1, phase (nit >> 1) & 1)
@@ -317,6 +350,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     for (std::uint32_t v = blockIdx.x; v < p.nvcta; v += gridDim.x, ++it) {
         const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
         const std::uint32_t nc = q1 - q0;
+        const std::uint32_t S = split_of(nc), nt = nc + S;  // tickets
         float* part = part_base;
         const std::uint32_t Ga = p.Pn == 1u ? q0 : __umulhi(q0, p.pn_magic);
         auto pair_of = [&](std::uint32_t k) {
@@ -335,7 +369,11 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         // one ticket of lookahead: the next cell's record copy and x loads are
         // in flight while this cell computes.  Warp w's first ticket is w.
         std::uint32_t tk = static_cast<std::uint32_t>(warp);
-        if (tk < nc && waited) issue(tk, nit & 1u);  // (the first range's went out in the prologue)
+        if (tk < nt && waited) {  // (the first range's went out in the prologue)
+            int uo;
+            const std::uint32_t c = decode(tk, nc, S, uo);
+            issue(c, uo, nit & 1u);
+        }
         // SHX: panel index i = warp + NC j covers panel (P0 + i) mod Pn; j = 0 is the
         // panel of this warp's first cell.  Each warp builds its panels right
         // after the PDL wait; readers check pflag instead of a CTA barrier.
@@ -372,19 +410,26 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 #endif
         }
         XLane<XLO> xl{};
-        if (!SHX && tk < nc) xl = load_x<XLO>(p, panel_of(tk), lane);
+        if (!SHX && tk < nt) {
+            int uo_;
+            xl = load_x<XLO>(p, panel_of(decode(tk, nc, S, uo_)), lane);
+        }
 #pragma unroll 1
-        while (tk < nc) {
+        while (tk < nt) {
             const std::uint32_t tn = grab();
             XLane<XLO> xn{};
-            if (tn < nc) {
-                issue(tn, (nit + 1u) & 1u);
-                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(tn), lane);
+            if (tn < nt) {
+                int uon;
+                const std::uint32_t cn = decode(tn, nc, S, uon);
+                issue(cn, uon, (nit + 1u) & 1u);
+                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(cn), lane);
             }
             const std::uint32_t slot = nit & 1u;
+            int uo;
+            const std::uint32_t ck = decode(tk, nc, S, uo);  // this ticket's cell (range index)
 
             if constexpr (SHX) {
-                const std::uint32_t P = panel_of(tk);
+                const std::uint32_t P = panel_of(ck);
                 pan = pan_base + P * PANEL;
                 if (pflag[P] == 0u) {
                     while (pflag[P] == 0u) {
@@ -408,219 +453,239 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             const std::uint8_t* cell = ring + slot * p.slot_bytes;
             const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
 
-            // x operands of this panel (shared by both units)
-            float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
+            // the cell's work for NU units: both (whole ticket) or unit uo (half)
+            auto compute = [&]<int NU>(std::integral_constant<int, NU>) {
+                auto unit_of = [&](int ui) { return NU == 2 ? ui : uo; };
+                // x operands of this panel (shared by both units)
+                float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
 #pragma unroll
-            for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(pan + O_SC)[4 * h + t];
+                for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(pan + O_SC)[4 * h + t];
 
-            // lane data of both units
-            std::uint32_t cw[2][G::LANE_WORDS];
-            std::uint32_t ss[2], zz[2];
-            uint4 sc[2][2];
+                // lane data of the units
+                std::uint32_t cw[NU][G::LANE_WORDS];
+                std::uint32_t ss[NU], zz[NU];
+                uint4 sc[NU][2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const std::uint8_t* unit = cell + u * UNIT;
+                for (int ui = 0; ui < NU; ++ui) {
+                    const std::uint8_t* unit = cell + unit_of(ui) * UNIT;
 #pragma unroll
-                for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                    const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                    cw[u][4 * i] = w4.x;
-                    cw[u][4 * i + 1] = w4.y;
-                    cw[u][4 * i + 2] = w4.z;
-                    cw[u][4 * i + 3] = w4.w;
+                    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                        const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                        cw[ui][4 * i] = w4.x;
+                        cw[ui][4 * i + 1] = w4.y;
+                        cw[ui][4 * i + 2] = w4.z;
+                        cw[ui][4 * i + 3] = w4.w;
+                    }
+                    load_stats<BS, BZ>(unit + CODEB, lane, ss[ui], zz[ui]);
+                    sc[ui][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
+                    sc[ui][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
                 }
-                load_stats<BS, BZ>(unit + CODEB, lane, ss[u], zz[u]);
-                sc[u][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
-                sc[u][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
-            }
 
-            // 4 independent MMA chains (super-tile h x unit u), interleaved
-            std::uint32_t bfr[2][4], lfr[2][4];
-            float cc[2][2][4];
+                // 2 NU independent MMA chains (super-tile h x unit), interleaved
+                std::uint32_t bfr[2][4], lfr[2][4];
+                float cc[2][NU][4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+                for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
+                    for (int ui = 0; ui < NU; ++ui)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) cc[h][u][i] = 0.f;
+                        for (int i = 0; i < 4; ++i) cc[h][ui][i] = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
+                        std::uint32_t bq[4], lq[4];
+                        if ((j & 1) == 0) {
+                            const bool act = jact == j;
+                            ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bq);
+                            if constexpr (XLO) ldsm_x4((act ? lane_sa : zl[h]) + (256u * h + (O_LO - O_FRAG)), lq);
+                            bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
+                            if constexpr (XLO) {
+                                lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
+                            }
+                        }
+                        const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
+                        std::uint32_t l0 = 0, l1 = 0;
+                        if constexpr (XLO) {
+                            l0 = lfr[h][2 * (j & 1)];
+                            l1 = lfr[h][2 * (j & 1) + 1];
+                        }
+#pragma unroll
+                        for (int ui = 0; ui < NU; ++ui) {
+                            const std::uint32_t* w = cw[ui] + G::CW * cidx;
+                            std::uint32_t a[4];
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                                const int i = rho * (G::NP / 2) + qq;
+                                const int B = (BW * i) >> 3, pb = (BW * i) & 7;
+                                a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
+                            }
+                            mma16816(cc[h][ui], a, b0, b1);
+                            if constexpr (XLO) mma16816(cc[h][ui], a, l0, l1);
+                        }
+                    }
+                }
+                float2 acc[NU][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
+#pragma unroll
+                for (int ui = 0; ui < NU; ++ui) acc[ui][0] = acc[ui][1] = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                    std::uint32_t bq[4], lq[4];
-                    if ((j & 1) == 0) {
-                        const bool act = jact == j;
-                        ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bq);
-                        if constexpr (XLO) ldsm_x4((act ? lane_sa : zl[h]) + (256u * h + (O_LO - O_FRAG)), lq);
-                        bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
-                        if constexpr (XLO) {
-                            lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
+                    float (&c)[NU][4] = cc[h];
+                    const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
+#pragma unroll
+                    for (int ui = 0; ui < NU; ++ui) {
+                        const uint4 s4 = sc[ui][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
+                        const __half2 s0 = u32_as_h2(s4.x), z0 = u32_as_h2(s4.y), s1 = u32_as_h2(s4.z),
+                                      z1 = u32_as_h2(s4.w);
+                        const float2 Ss = make_float2(__low2float(s0), __low2float(s1));
+                        const float2 Zs = make_float2(__high2float(s0), __high2float(s1));
+                        const float2 Sz = make_float2(__low2float(z0), __low2float(z1));
+                        const float2 Zz = make_float2(-__high2float(z0), -__high2float(z1));
+                        const float2 A1 = fmul2(Ss, SC);                         // s_s * 2^(24-e)
+                        const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));  // -s_s z_s 2^(24-e)
+                        const float2 B0 = fmul2(Sz, Zz);                         // -z_s z_z
+#pragma unroll
+                        for (int rho = 0; rho < 2; ++rho) {
+                            const int e0i = 4 * h + rho, e1i = 4 * h + 2 + rho;  // eps of (bs=0, bs=1)
+                            const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss[ui], e0i * BS, magic),
+                                                                magic_field_rt<SMASK>(ss[ui], e1i * BS, magic)),
+                                                    make_float2(-kMagic, -kMagic));
+                            const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz[ui], e0i * BZ, magic),
+                                                                magic_field_rt<ZMASK>(zz[ui], e1i * BZ, magic)),
+                                                    make_float2(-kMagic, -kMagic));
+                            const float2 shat = ffma2(A1, cs, A0);
+                            const float2 zhat = ffma2(Sz, cz, B0);
+                            const float2 tt = ffma2(zhat, XX, make_float2(c[ui][2 * rho], c[ui][2 * rho + 1]));
+                            acc[ui][rho] = ffma2(shat, tt, acc[ui][rho]);
                         }
                     }
-                    const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
-                    std::uint32_t l0 = 0, l1 = 0;
-                    if constexpr (XLO) {
-                        l0 = lfr[h][2 * (j & 1)];
-                        l1 = lfr[h][2 * (j & 1) + 1];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const std::uint32_t* w = cw[u] + G::CW * cidx;
-                        std::uint32_t a[4];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                            const int i = rho * (G::NP / 2) + qq;
-                            const int B = (BW * i) >> 3, pb = (BW * i) & 7;
-                            a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
-                        }
-                        mma16816(cc[h][u], a, b0, b1);
-                        if constexpr (XLO) mma16816(cc[h][u], a, l0, l1);
-                    }
                 }
-            }
-            float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
-#pragma unroll
-            for (int u = 0; u < 2; ++u) acc[u][0] = acc[u][1] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float (&c)[2][4] = cc[h];
-                const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const uint4 s4 = sc[u][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
-                    const __half2 s0 = u32_as_h2(s4.x), z0 = u32_as_h2(s4.y), s1 = u32_as_h2(s4.z),
-                                  z1 = u32_as_h2(s4.w);
-                    const float2 Ss = make_float2(__low2float(s0), __low2float(s1));
-                    const float2 Zs = make_float2(__high2float(s0), __high2float(s1));
-                    const float2 Sz = make_float2(__low2float(z0), __low2float(z1));
-                    const float2 Zz = make_float2(-__high2float(z0), -__high2float(z1));
-                    const float2 A1 = fmul2(Ss, SC);                         // s_s * 2^(24-e)
-                    const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));  // -s_s z_s 2^(24-e)
-                    const float2 B0 = fmul2(Sz, Zz);                         // -z_s z_z
-#pragma unroll
-                    for (int rho = 0; rho < 2; ++rho) {
-                        const int e0i = 4 * h + rho, e1i = 4 * h + 2 + rho;  // eps of (bs=0, bs=1)
-                        const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss[u], e0i * BS, magic),
-                                                            magic_field_rt<SMASK>(ss[u], e1i * BS, magic)),
-                                                make_float2(-kMagic, -kMagic));
-                        const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz[u], e0i * BZ, magic),
-                                                            magic_field_rt<ZMASK>(zz[u], e1i * BZ, magic)),
-                                                make_float2(-kMagic, -kMagic));
-                        const float2 shat = ffma2(A1, cs, A0);
-                        const float2 zhat = ffma2(Sz, cz, B0);
-                        const float2 tt = ffma2(zhat, XX, make_float2(c[u][2 * rho], c[u][2 * rho + 1]));
-                        acc[u][rho] = ffma2(shat, tt, acc[u][rho]);
-                    }
-                }
-            }
 
-            // outliers: entries (row, col, value) of this cell, sorted by (row,
-            // col), 0xffffffff padding (row 255).  Chunks of 128 entries, 4
-            // consecutive per lane (one 16-byte load): products, a segmented
-            // inclusive scan by row, and the last entry of each row in the
-            // chunk adds the row total to rowsum.  Chunks run in order, so the
-            // sums are deterministic.  Entries beyond the staged part of the
-            // record are read from global memory.
-            const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-            float* rs = rowsum[warp];
-            if (cnt) {
-                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
-                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
-                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
-                auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
-                    uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                    if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
-                    const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
-                    std::uint32_t k[4];
-                    float sv[4];
+                // outliers: entries (row, col, value) of this cell, sorted by (row,
+                // col), 0xffffffff padding (row 255).  Chunks of 128 entries, 4
+                // consecutive per lane (one 16-byte load): products, a segmented
+                // inclusive scan by row, and the last entry of each row in the
+                // chunk adds the row total to rowsum (rows of this ticket's units
+                // only).  Chunks run in order, so the sums are deterministic.
+                // Entries beyond the staged part of the record are read from
+                // global memory.
+                const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+                float* rs = rowsum[warp];
+                if (cnt) {
+                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
+                    const std::uint32_t rlo = NU == 2 ? 0u : 16u * uo, rhi = NU == 2 ? 32u : rlo + 16u;
+                    auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
+                        uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                        if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
+                        const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                        std::uint32_t k[4];
+                        float sv[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        k[j] = e[j] >> 24;
-                        const std::uint32_t c = (e[j] >> 16) & 255u;
-                        float xv;
-                        if constexpr (XLO)
-                            xv = reinterpret_cast<const float*>(pan + O_XP)[c];
-                        else
-                            xv = __half2float(reinterpret_cast<const __half*>(pan + O_XP)[c]);
-                        sv[j] = h2f_bits(e[j] & 0xffffu) * xv;
-                    }
-                    bool same[3];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        same[j] = k[j + 1] == k[j];
-                        if (same[j]) sv[j + 1] += sv[j];
-                    }
-                    const std::uint32_t K = k[3];
-                    const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
-                    const bool head = lane == 0 || pK != K;
-                    const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
-                    const int seg0 = 31 - __clz(heads);
-                    float V = sv[3];
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const float o = __shfl_up_sync(0xffffffffu, V, d);
-                        if (lane - d >= seg0) V += o;
-                    }
-                    float cin = __shfl_up_sync(0xffffffffu, V, 1);
-                    if (lane == 0 || pK != k[0]) cin = 0.f;
-                    const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
-                        if (tail && k[j] < 32u) {
-                            const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
-                            if (first)
-                                rs[k[j]] = tot;
+                        for (int j = 0; j < 4; ++j) {
+                            k[j] = e[j] >> 24;
+                            const std::uint32_t c = (e[j] >> 16) & 255u;
+                            float xv;
+                            if constexpr (XLO)
+                                xv = reinterpret_cast<const float*>(pan + O_XP)[c];
                             else
-                                rs[k[j]] += tot;
+                                xv = __half2float(reinterpret_cast<const __half*>(pan + O_XP)[c]);
+                            sv[j] = h2f_bits(e[j] & 0xffffu) * xv;
                         }
+                        bool same[3];
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) {
+                            same[j] = k[j + 1] == k[j];
+                            if (same[j]) sv[j + 1] += sv[j];
+                        }
+                        const std::uint32_t K = k[3];
+                        const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
+                        const bool head = lane == 0 || pK != K;
+                        const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
+                        const int seg0 = 31 - __clz(heads);
+                        float V = sv[3];
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const float o = __shfl_up_sync(0xffffffffu, V, d);
+                            if (lane - d >= seg0) V += o;
+                        }
+                        float cin = __shfl_up_sync(0xffffffffu, V, 1);
+                        if (lane == 0 || pK != k[0]) cin = 0.f;
+                        const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
+                            if (tail && k[j] >= rlo && k[j] < rhi) {
+                                const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
+                                if (first)
+                                    rs[k[j]] = tot;
+                                else
+                                    rs[k[j]] += tot;
+                            }
+                        }
+                    };
+                    chunk(es, 4u * lane, nfast, true);
+#pragma unroll 1
+                    for (std::uint32_t base = 128; base < nfast; base += 128) {
+                        __syncwarp();
+                        chunk(es, base + 4u * lane, nfast, false);
                     }
-                };
-                chunk(es, 4u * lane, nfast, true);
 #pragma unroll 1
-                for (std::uint32_t base = 128; base < nfast; base += 128) {
-                    __syncwarp();
-                    chunk(es, base + 4u * lane, nfast, false);
+                    for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
+                        __syncwarp();
+                        chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);
+                    }
                 }
-#pragma unroll 1
-                for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
-                    __syncwarp();
-                    chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);
-                }
-            }
 
-            // the cell's 32 row sums.  Lane (g, t) holds partials of rows
-            // 16u + 8rho + g (combo c = 2u + rho) over its blocks; a 4x4
-            // transpose-add across the quad leaves lane t with combo c = t.
-            float* prow = part + tk * 32u;
-            {
-                float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
-                float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
-                const bool o1 = t & 1, o2 = t & 2;
-                const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
-                const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
-                const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 1);
-                const float b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 1);
-                const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
-                prow[16 * (t >> 1) + 8 * (t & 1) + g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-            }
-            __syncwarp();
-            if (cnt) {
-                prow[lane] += rs[lane];
-                rs[lane] = 0.f;
+                // the ticket's row sums.  Lane (g, t) holds partials of rows
+                // 16u + 8rho + g over its blocks; a transpose-add across the quad
+                // (4x4 for a whole cell, 2x4 for a unit) gives each row one lane.
+                float* prow = part + ck * 32u;
+                if constexpr (NU == 2) {
+                    float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
+                    float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
+                    const bool o1 = t & 1, o2 = t & 2;
+                    const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
+                    const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
+                    const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 1);
+                    const float b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 1);
+                    const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
+                    prow[16 * (t >> 1) + 8 * (t & 1) + g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+                } else {
+                    const float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
+                    const bool o1 = t & 1;
+                    float b = (o1 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
+                    b += __shfl_xor_sync(0xffffffffu, b, 2);
+                    if (t < 2) prow[16 * uo + 8 * t + g] = b;
+                }
                 __syncwarp();
-            }
-            // count the cell against its pair; the warp that completes the pair
-            // reduces it (row = lane, cells in order) and writes y
-            const std::uint32_t Gq = pair_of(tk);
+                if (cnt) {
+                    if (NU == 2 || (lane >> 4) == uo) prow[lane] += rs[lane];
+                    rs[lane] = 0.f;
+                    __syncwarp();
+                }
+            };
+            if (uo < 0)
+                compute(std::integral_constant<int, 2>{});
+            else
+                compute(std::integral_constant<int, 1>{});
+
+            // count the ticket against its pair (a split cell counts twice); the
+            // warp that completes the pair reduces it (row = lane, cells in order)
+            // and writes y
+            const std::uint32_t Gq = pair_of(ck);
             const std::uint32_t cs = Gq * p.Pn, ce = cs + p.Pn;
             const std::uint32_t a = max(cs, q0), b = min(ce, q1);
-            __threadfence_block();  // this cell's row sums before the count
+            const std::uint32_t fs = q0 + nc - S;  // first split cell
+            const std::uint32_t want = (b - a) + (b > max(a, fs) ? b - max(a, fs) : 0u);
+            __threadfence_block();  // this ticket's row sums before the count
             std::uint32_t done = 0;
             if (lane == 0) done = atomicAdd(&gdone[Gq - Ga], 1u) + 1u;
             done = __shfl_sync(0xffffffffu, done, 0);
-            if (done == b - a) {
+            if (done == want) {
                 __threadfence_block();
                 float sum = 0.f;
                 const float* src = part + (a - q0) * 32u + lane;

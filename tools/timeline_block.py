@@ -65,6 +65,19 @@ print(f"== {target} (after {groups[upto - 1][0] if upto else groups[-1][0]}): sp
 for k, name in enumerate(["entry", "pdl_wait", "first_cell", "loop_end", "exit"]):
     q = np.percentile(r[:, k], [0, 10, 50, 90, 100])
     print(f"  {name:11s} " + " ".join(f"{v:7.2f}" for v in q))
+Tall = buf.reshape(-1, 8).astype(np.int64)
+per = []
+for b in range(148):
+    rows_b = Tall[16 * b:16 * b + 16]
+    rows_b = rows_b[(rows_b[:, 4] > 0) & (rows_b[:, 7] >= 1000)]
+    if len(rows_b) == 0:
+        continue
+    per.append((((rows_b[:, 3].max() - t0) / 1e3), b, int(rows_b[0, 7] - 1000), (rows_b[:, 0].min() - t0) / 1e3,
+                (rows_b[:, 1].min() - t0) / 1e3, (rows_b[:, 2].min() - t0) / 1e3, (rows_b[:, 3].min() - t0) / 1e3))
+per.sort()
+print("  CTA loop-end percentiles", " ".join(f"{v:6.2f}" for v in np.percentile([x[0] for x in per], [0, 10, 50, 90, 100])))
+for x in per[-6:]:
+    print(f"  slow CTA {x[1]:3d} sm {x[2]:3d}: entry {x[3]:5.2f} pdl {x[4]:5.2f} first {x[5]:5.2f} loop_end {x[6]:5.2f}..{x[0]:5.2f}")
 if T[:, 5].max() > 1e12:  # panels-built stamp (SHX layers)
     q = np.percentile((T[:, 5] - t0) / 1e3, [0, 10, 50, 90, 100])
     print(f"  {'panels':11s} " + " ".join(f"{v:7.2f}" for v in q))
