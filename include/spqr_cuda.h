@@ -116,6 +116,7 @@ typedef struct spqr_layer_opts {
     int32_t keep_stream;   /* 1: keep the raw stream on the device even on the fast path */
     uint32_t row_begin;    /* row band [row_begin, row_end) of the stream; 0,0 = all rows */
     uint32_t row_end;
+    int32_t host_transcode; /* 1: build the HBM layout on the host (comparison); 0: on the GPU */
 } spqr_layer_opts;
 
 /* ---------------------------------------------------------------- host -- */
@@ -221,6 +222,10 @@ int spqr_matvec_host(const spqr_layer* layer, const float* x_host, float* y_host
  * W16 rows x cols row-major fp16, x fp16, y fp32. */
 int spqr_dense_gemv_f16(const void* w_dev, const void* x_dev, float* y_dev, uint32_t rows,
                         uint32_t cols, void* cuda_stream);
+
+/* Test hook: the device-resident cell records (len bytes) and record offsets
+ * (Gn*Pn + 1 entries) of a fast-path layer; cells == NULL queries len. */
+int spqr_debug_layer_cells(const spqr_layer* layer, uint8_t* cells, size_t cap, size_t* len, uint32_t* cell_off);
 
 /* Number of kernel launches the last spqr_matvec* on this thread issued. */
 int spqr_last_launch_count(void);

@@ -76,7 +76,7 @@ class TensorArrays(C.Structure):
 
 class LayerOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("force_generic", C.c_int32), ("keep_stream", C.c_int32),
-                ("row_begin", C.c_uint32), ("row_end", C.c_uint32)]
+                ("row_begin", C.c_uint32), ("row_end", C.c_uint32), ("host_transcode", C.c_int32)]
 
 
 _lib = None
@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
         "spqr_layer_create": (i32, [vp, sz, C.POINTER(LayerOpts), C.POINTER(vp)]),
         "spqr_layer_destroy": (None, [vp]),
         "spqr_layer_create_stacked": (i32, [C.POINTER(vp), C.POINTER(sz), i32, C.POINTER(LayerOpts), C.POINTER(vp)]),
+        "spqr_debug_layer_cells": (i32, [vp, vp, sz, C.POINTER(C.c_size_t), vp]),
         "spqr_layer_get_info": (i32, [vp, C.POINTER(LayerInfo)]),
         "spqr_layer_export_stream": (i32, [vp, vp, sz, C.POINTER(C.c_size_t)]),
         "spqr_dequantize": (i32, [vp, vp, vp]),
@@ -309,10 +310,11 @@ class Layer:
     """A layer resident in HBM (spqr_layer_create: decode + plan + upload)."""
 
     def __init__(self, stream: bytes, device: int = -1, force_generic: bool = False,
-                 rows: tuple[int, int] | None = None):
+                 rows: tuple[int, int] | None = None, host_transcode: bool = False):
         a, p, n = _buf(stream)
         opts = LayerOpts(device=device, force_generic=int(force_generic), keep_stream=1,
-                         row_begin=rows[0] if rows else 0, row_end=rows[1] if rows else 0)
+                         row_begin=rows[0] if rows else 0, row_end=rows[1] if rows else 0,
+                         host_transcode=int(host_transcode))
         h = C.c_void_p()
         _check(lib().spqr_layer_create(p, n, C.byref(opts), C.byref(h)))
         self._h = h
@@ -322,13 +324,14 @@ class Layer:
         self.rows, self.cols = self.info["rows"], self.info["cols"]
 
     @classmethod
-    def stacked(cls, streams: list, device: int = -1) -> "Layer":
+    def stacked(cls, streams: list, device: int = -1, host_transcode: bool = False) -> "Layer":
         """Several layers sharing their input (q/k/v, gate/up) stacked row-wise
         in one handle (spqr_layer_create_stacked): one launch, y = [y_0; y_1; ...]."""
         bufs = [_buf(s) for s in streams]
         ptrs = (C.c_void_p * len(bufs))(*[b[1] for b in bufs])
         sizes = (C.c_size_t * len(bufs))(*[b[2] for b in bufs])
-        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0)
+        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0,
+                         host_transcode=int(host_transcode))
         h = C.c_void_p()
         _check(lib().spqr_layer_create_stacked(ptrs, sizes, len(bufs), C.byref(opts), C.byref(h)))
         self = cls.__new__(cls)
@@ -385,6 +388,16 @@ class Layer:
     def dequantize(self, w, stream=None) -> None:
         """dequantize_full (kernel.hpp:17) into a rows x cols fp32 device buffer."""
         _check(lib().spqr_dequantize(self._h, _ptr(w), _stream_ptr(stream)))
+
+    def debug_cells(self) -> dict:
+        """The device-resident cell records and record offsets (test hook)."""
+        n = C.c_size_t()
+        ncell = ((self.rows + 31) // 32) * ((self.cols + 255) // 256)
+        off = np.zeros(ncell + 1, np.uint32)
+        _check(lib().spqr_debug_layer_cells(self._h, None, 0, C.byref(n), off.ctypes.data_as(C.c_void_p)))
+        cells = np.zeros(n.value, np.uint8)
+        _check(lib().spqr_debug_layer_cells(self._h, cells.ctypes.data_as(C.c_void_p), n.value, C.byref(n), None))
+        return {"cells": cells, "cell_off": off}
 
     def workspace_bytes(self, batch: int = 1) -> int:
         return int(lib().spqr_workspace_bytes(self._h, batch))

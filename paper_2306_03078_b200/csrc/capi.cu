@@ -149,6 +149,19 @@ struct spqr_layer {
 
 namespace {
 
+spqr_dev::RawGeom raw_geom_of(const spqr::detail::StreamView& v, const std::uint8_t* d_stream,
+                              const std::uint32_t* d_order) {
+    spqr_dev::RawGeom g{};
+    g.s = d_stream;
+    g.order = d_order;
+    g.rows = v.rows; g.cols = v.cols; g.b1 = v.b1; g.b2 = v.b2;
+    g.nblocks = v.nblocks; g.ngroups = v.ngroups;
+    g.wb = v.wb; g.sb = v.sb; g.zb = v.zb;
+    g.rec_off = v.rec_off; g.col_block_bytes = v.col_block_bytes;
+    g.csr_off = v.csr_off; g.ent_off = v.ent_off;
+    return g;
+}
+
 spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
     const auto& v = L->geo;
     spqr_dev::RawGeom g{};
@@ -737,14 +750,9 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     ck(cudaMemcpy(c.d_maps + gmap.size(), cmap.data(), 4 * cmap.size(), cudaMemcpyHostToDevice), "H2D tc cmap");
 }
 
-// Device copy of a tiled layer + every launch plan; returns device bytes.
-std::uint64_t upload_tiled(spqr_layer* L, const spqr::detail::TiledHost& t,
-                           const std::vector<spqr::detail::StreamView>& views) {
+// Every launch plan of a tiled layer (geometry + record offsets in t).
+void make_plans(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<spqr::detail::StreamView>& views) {
     L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
-    L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
-    ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
-    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size() + 4);  // + 4: gemv_cta copies 16-B aligned supersets
-    ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice), "H2D cell_off");
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
     plan_partition(L, t, sms, 0);
@@ -752,7 +760,76 @@ std::uint64_t upload_tiled(spqr_layer* L, const spqr::detail::TiledHost& t,
     plan_cta(L, t, sms, 0);
     plan_cta(L, t, sms, 1);
     plan_tc(L, t, views, sms);
+}
+
+// Host-built tiled layer (transcode.cpp) -> HBM + plans; returns device bytes.
+std::uint64_t upload_tiled(spqr_layer* L, const spqr::detail::TiledHost& t,
+                           const std::vector<spqr::detail::StreamView>& views) {
+    L->d_cells = dalloc<std::uint8_t>(t.cells.size() + 16);
+    ck(cudaMemcpy(L->d_cells, t.cells.data(), t.cells.size(), cudaMemcpyHostToDevice), "H2D cells");
+    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size() + 4);  // + 4: gemv_cta copies 16-B aligned supersets
+    ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice), "H2D cell_off");
+    make_plans(L, t, views);
     return t.cells.size() + 4 * t.cell_off.size();
+}
+
+// Device-built tiled layer (transcode_dev.cuh, byte-identical to the host
+// transcode) from streams already resident on the device: per-cell outlier
+// counts on the GPU, record offsets prefixed on the host, then the unit and
+// entry kernels write the cells in place.  Several streams stack row-wise.
+std::uint64_t transcode_on_device(spqr_layer* L, const std::vector<spqr::detail::StreamView>& views,
+                                  const std::vector<const std::uint8_t*>& d_streams) {
+    spqr::detail::TiledHost t;
+    const auto& v0 = views[0];
+    t.Pn = (v0.cols + 255) / 256;
+    t.cell_bytes = spqr_tiled::cell_bytes(v0.wb, v0.sb, v0.zb);
+    t.prefix.assign(v0.base, v0.base + v0.rec_off);
+    std::vector<std::uint32_t> gbase;  // first cell row of each member
+    std::vector<spqr_dev::RawGeom> geos;
+    for (std::size_t i = 0; i < views.size(); ++i) {
+        gbase.push_back(t.Gn);
+        t.Gn += (views[i].rows + 31) / 32;
+        geos.push_back(raw_geom_of(views[i], d_streams[i], nullptr));
+    }
+    const std::size_t ncell = static_cast<std::size_t>(t.Gn) * t.Pn;
+    std::uint32_t* d_cnt = dalloc<std::uint32_t>(ncell);
+    for (std::size_t i = 0; i < views.size(); ++i) {
+        const std::uint32_t gn = (views[i].rows + 31) / 32, cells_i = gn * t.Pn;
+        spqr_dev::tc_entries<true><<<(cells_i * 32 + 255) / 256, 256>>>(
+            geos[i], gn, t.Pn, t.cell_bytes, nullptr, nullptr, d_cnt + static_cast<std::size_t>(gbase[i]) * t.Pn);
+        ck(cudaGetLastError(), "launch tc_entries<count>");
+    }
+    std::vector<std::uint32_t> cnt(ncell);
+    ck(cudaMemcpy(cnt.data(), d_cnt, 4 * ncell, cudaMemcpyDeviceToHost), "D2H outlier counts");
+    cudaFree(d_cnt);
+    t.cell_off.assign(ncell + 1, 0);
+    std::uint64_t total = 0;
+    for (std::size_t q = 0; q < ncell; ++q) {
+        t.cell_off[q] = static_cast<std::uint32_t>(total);
+        total += t.cell_bytes + 16ull * ((cnt[q] + 3) / 4);
+        if (total > 0xfffffff0ull) spqr::fail(spqr::Errc::config_invalid, "layer too large for 32-bit record offsets");
+    }
+    t.cell_off[ncell] = static_cast<std::uint32_t>(total);
+    L->d_cells = dalloc<std::uint8_t>(total + 16);
+    L->d_cell_off = dalloc<std::uint32_t>(t.cell_off.size() + 4);  // + 4: gemv_cta copies 16-B aligned supersets
+    ck(cudaMemcpy(L->d_cell_off, t.cell_off.data(), 4 * t.cell_off.size(), cudaMemcpyHostToDevice), "H2D cell_off");
+    for (std::size_t i = 0; i < views.size(); ++i) {
+        const std::uint32_t gn = (views[i].rows + 31) / 32;
+        const std::uint32_t* off_i = L->d_cell_off + static_cast<std::size_t>(gbase[i]) * t.Pn;
+        const unsigned ub = (2u * gn * t.Pn * 32u + 255u) / 256u;
+        switch (v0.wb) {
+            case 2: spqr_dev::tc_units<2><<<ub, 256>>>(geos[i], gn, t.Pn, off_i, L->d_cells); break;
+            case 3: spqr_dev::tc_units<3><<<ub, 256>>>(geos[i], gn, t.Pn, off_i, L->d_cells); break;
+            default: spqr_dev::tc_units<4><<<ub, 256>>>(geos[i], gn, t.Pn, off_i, L->d_cells); break;
+        }
+        ck(cudaGetLastError(), "launch tc_units");
+        spqr_dev::tc_entries<false><<<(gn * t.Pn * 32 + 255) / 256, 256>>>(geos[i], gn, t.Pn, t.cell_bytes, off_i,
+                                                                          L->d_cells, nullptr);
+        ck(cudaGetLastError(), "launch tc_entries");
+    }
+    ck(cudaDeviceSynchronize(), "device transcode");
+    make_plans(L, t, views);
+    return total + 4 * t.cell_off.size();
 }
 }  // namespace
 
@@ -804,7 +881,9 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
             ck(cudaMemcpy(L->d_stream, s, n, cudaMemcpyHostToDevice), "H2D stream");
             dev_bytes += n;
         }
-        if (L->fast) dev_bytes += upload_tiled(L.get(), spqr::detail::transcode_to_tiled(v, 0), {v});
+        if (L->fast)
+            dev_bytes += o.host_transcode ? upload_tiled(L.get(), spqr::detail::transcode_to_tiled(v, 0), {v})
+                                          : transcode_on_device(L.get(), {v}, {L->d_stream});
         L->info.fast_path = L->fast;
         ensure_own_ws(L.get(), 1);
         dev_bytes += L->ws_bytes;
@@ -860,20 +939,7 @@ int spqr_layer_create_stacked(const uint8_t* const* streams, const size_t* sizes
         L->info.beta1 = v0.b1; L->info.beta2 = v0.b2; L->info.flags = v0.flags;
         L->info.has_permutation = v0.has_permutation; L->info.tau = v0.tau; L->info.lambda_rel = v0.lambda_rel;
         L->info.device = L->device;
-        spqr::detail::TiledHost t;
         for (int i = 0; i < count; ++i) {
-            const spqr::detail::TiledHost ti = spqr::detail::transcode_to_tiled(views[i], 0);
-            const std::uint64_t base = t.cells.size();
-            if (base + ti.cells.size() > 0xfffffff0ull) spqr::fail(spqr::Errc::config_invalid, "stacked: too large");
-            if (i == 0) {
-                t.Pn = ti.Pn;
-                t.cell_bytes = ti.cell_bytes;
-                t.prefix = ti.prefix;
-            }
-            t.Gn += ti.Gn;
-            t.cells.insert(t.cells.end(), ti.cells.begin(), ti.cells.end());
-            if (!t.cell_off.empty()) t.cell_off.pop_back();
-            for (std::uint32_t off : ti.cell_off) t.cell_off.push_back(static_cast<std::uint32_t>(base + off));
             L->info.rows += views[i].rows;
             L->info.outlier_count += views[i].nnz;
             L->info.payload_bytes += sizes[i] - spqr::kSpqrHeaderBytes;
@@ -887,7 +953,39 @@ int spqr_layer_create_stacked(const uint8_t* const* streams, const size_t* sizes
             dev_bytes += 4ull * v0.cols;
         }
         L->fast = true;
-        dev_bytes += upload_tiled(L.get(), t, views);
+        if (o.host_transcode) {
+            spqr::detail::TiledHost t;
+            for (int i = 0; i < count; ++i) {
+                const spqr::detail::TiledHost ti = spqr::detail::transcode_to_tiled(views[i], 0);
+                const std::uint64_t base = t.cells.size();
+                if (base + ti.cells.size() > 0xfffffff0ull) spqr::fail(spqr::Errc::config_invalid, "stacked: too large");
+                if (i == 0) {
+                    t.Pn = ti.Pn;
+                    t.cell_bytes = ti.cell_bytes;
+                    t.prefix = ti.prefix;
+                }
+                t.Gn += ti.Gn;
+                t.cells.insert(t.cells.end(), ti.cells.begin(), ti.cells.end());
+                if (!t.cell_off.empty()) t.cell_off.pop_back();
+                for (std::uint32_t off : ti.cell_off) t.cell_off.push_back(static_cast<std::uint32_t>(base + off));
+            }
+            dev_bytes += upload_tiled(L.get(), t, views);
+        } else {  // members' streams visit the device only for the transcode
+            std::vector<std::uint8_t*> tmp;
+            std::vector<const std::uint8_t*> dv;
+            try {
+                for (int i = 0; i < count; ++i) {
+                    tmp.push_back(dalloc<std::uint8_t>(sizes[i] + 16));
+                    ck(cudaMemcpy(tmp.back(), streams[i], sizes[i], cudaMemcpyHostToDevice), "H2D member stream");
+                    dv.push_back(tmp.back());
+                }
+                dev_bytes += transcode_on_device(L.get(), views, dv);
+            } catch (...) {
+                for (auto* q : tmp) cudaFree(q);
+                throw;
+            }
+            for (auto* q : tmp) cudaFree(q);
+        }
         L->info.fast_path = 1;
         ensure_own_ws(L.get(), 1);
         dev_bytes += L->ws_bytes;
@@ -1030,6 +1128,20 @@ int spqr_dense_gemv_f16(const void* w_dev, const void* x_dev, float* y_dev, uint
 }
 
 int spqr_last_launch_count(void) { return g_launches; }
+
+int spqr_debug_layer_cells(const spqr_layer* L, uint8_t* cells, size_t cap, size_t* len, uint32_t* cell_off) {
+    return guard([&] {
+        if (!L->fast) spqr::fail(spqr::Errc::config_invalid, "not a tiled layer");
+        DevGuard dg(L->device);
+        const std::size_t ncell = static_cast<std::size_t>(L->Gn) * L->Pn;
+        std::vector<std::uint32_t> off(ncell + 1);
+        ck(cudaMemcpy(off.data(), L->d_cell_off, 4 * off.size(), cudaMemcpyDeviceToHost), "D2H cell_off");
+        *len = off.back();
+        if (cell_off) std::memcpy(cell_off, off.data(), 4 * off.size());
+        if (cells && cap >= off.back())
+            ck(cudaMemcpy(cells, L->d_cells, off.back(), cudaMemcpyDeviceToHost), "D2H cells");
+    });
+}
 
 #ifdef SPQR_TIMELINE
 // tools-only: copy the gemv_tiled per-warp timeline (8 x u64 per warp)

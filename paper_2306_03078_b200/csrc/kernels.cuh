@@ -394,4 +394,6 @@ __global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __res
     }
 }
 
+#include "transcode_dev.cuh"
+
 }  // namespace spqr_dev

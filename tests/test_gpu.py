@@ -238,3 +238,21 @@ def test_stacked_layers_match_separate(cuda, oracle_c):
     bad = P.encode_arrays(synth.make_layer(64, 512, seed=1))
     with pytest.raises(P.SpqrError):
         P.Layer.stacked([streams[0], bad])
+
+
+@pytest.mark.parametrize("case", [(96, 544, 3, 0.02, True), (50, 300, 2, 0.05, False), (160, 1000, 4, 0.03, True),
+                                  (256, 4096, 3, 0.01, False)])
+def test_device_transcode_matches_host(cuda, case):
+    """The GPU loader (transcode_dev.cuh) writes byte-identical cell records
+    and offsets to the host transcode (transcode.cpp), single and stacked."""
+    m, n, bw, rate, perm = case
+    a = synth.make_layer(m, n, weight_bits=bw, scale_bits=bw, zero_bits=bw, seed=m, permute=perm, outlier_rate=rate)
+    s = P.encode_arrays(a)
+    host = P.debug_tiled_host(s)
+    dev = P.Layer(s).debug_cells()
+    assert np.array_equal(dev["cell_off"], host["cell_off"])
+    assert np.array_equal(dev["cells"], host["cells"][: dev["cells"].size])
+    if m % 32 == 0:
+        dh = P.Layer.stacked([s, s], host_transcode=True).debug_cells()
+        dd = P.Layer.stacked([s, s]).debug_cells()
+        assert np.array_equal(dh["cell_off"], dd["cell_off"]) and np.array_equal(dh["cells"], dd["cells"])
