@@ -308,8 +308,17 @@ constexpr std::uint32_t kTcMaxN = 64;  // batch columns per launch
 // below this batch, repeated gemv_cta launches beat the dequant-then-MMA
 // kernel (tools/batch_sweep.py, 8192x22016: 3 x 29 us < ~93 us < 4 x 29 us)
 constexpr int kTcMinBatch = 4;
-std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N) {
-    return 3u * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + 16u * 2304u;
+std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N, std::uint32_t na) {
+    return na * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + 16u * 2304u;
+}
+// A stage buffers: a fourth (one more half cell of lookahead between the
+// dequant warps) whenever it fits next to the x tiles of this N
+std::uint32_t tc_na(const spqr_layer* L, std::uint32_t N) {
+    static const bool force3 = [] {
+        const char* e = std::getenv("SPQR_TC_NA");  // "3": measurement override
+        return e && e[0] == '3';
+    }();
+    return !force3 && tc_smem(L, N, 4u) + kTcStaticMax <= kSmemLimit ? 4u : 3u;
 }
 
 template <int BW, int BSZ>
@@ -379,7 +388,8 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
         p.rec_cap = L->tcp.slot_bytes; p.slot_bytes = L->tcp.slot_bytes; p.pn_magic = L->pn_magic;
         p.sigma = L->tcp.sigma;
         p.out_scale = std::ldexp(1.0f, L->tcp.sigma);
-        const std::uint32_t smem = tc_smem(L, N);
+        p.na = tc_na(L, N);
+        const std::uint32_t smem = tc_smem(L, N, p.na);
         switch (L->info.weight_bits * 10 + L->info.scale_bits) {
             case 22: launch_tc_t<2, 2>(p, smem, st); break;
             case 23: launch_tc_t<2, 3>(p, smem, st); break;

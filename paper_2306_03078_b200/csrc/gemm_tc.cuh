@@ -46,6 +46,7 @@ struct TcParams {
     std::uint32_t pn_magic;           // u / Pn == umulhi(u, pn_magic) (Pn > 1)
     float out_scale;                  // 2^sigma
     int sigma;
+    std::uint32_t na;                 // A stage buffers (3 or 4, by shared memory)
 };
 
 namespace tc {
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     constexpr int CTRL = ND;                             // control warp
 
     extern __shared__ __align__(128) std::uint8_t smem[];
-    __shared__ std::uint64_t rec_full[4][2], rec_empty[4][2], a_full[3], a_free[3], b_full[3], b_free[3], d_full[2],
+    __shared__ std::uint64_t rec_full[4][2], rec_empty[4][2], a_full[4], a_free[4], b_full[3], b_free[3], d_full[2],
         d_free[2];
     __shared__ std::uint32_t slot_r[4][2][2];
     __shared__ std::uint32_t tmem_base;
@@ -186,8 +187,9 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
 #define TC_WAIT(i, expr) expr;
 #endif
     const std::uint32_t tcols = N <= 16 ? 32u : (N <= 32 ? 64u : (N <= 64 ? 128u : 256u));
-    std::uint8_t* abuf = smem;                                  // [3][A_STAGE]: stage s in buffer s % 3
-    std::uint8_t* bbuf = smem + 3 * A_STAGE;                    // [3][B_STAGE]: x tiles, 2 stages of lookahead
+    const std::uint32_t NA = p.na;                              // A buffers (3 or 4)
+    std::uint8_t* abuf = smem;                                  // [NA][A_STAGE]: stage s in buffer s % NA
+    std::uint8_t* bbuf = smem + NA * A_STAGE;                   // [3][B_STAGE]: x tiles, 2 stages of lookahead
     std::uint8_t* recs = bbuf + 3 * B_STAGE;                    // [4 cell rows][2][slot_bytes]
     std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [16 warps][16 rows][144 B: 8 blocks x 16 B + pad]
 
@@ -197,9 +199,11 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 mbar_init(&rec_full[i][k], 1);
                 mbar_init(&rec_empty[i][k], 4);  // the four (unit, half) warps of the cell row
             }
-        for (int b = 0; b < 3; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(&a_full[b], 8);  // 4 cell rows x 2 units write a half stage
             mbar_init(&a_free[b], 1);
+        }
+        for (int b = 0; b < 3; ++b) {
             mbar_init(&b_full[b], 1);
             mbar_init(&b_free[b], 1);
         }
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     }
     // zero both A stages once: rows of missing row-group pairs (the layer's last
     // tile) then contribute 0 instead of whatever shared memory held
-    for (std::uint32_t i = threadIdx.x; i < 3u * A_STAGE / 16u; i += blockDim.x)
+    for (std::uint32_t i = threadIdx.x; i < NA * A_STAGE / 16u; i += blockDim.x)
         reinterpret_cast<uint4*>(abuf)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
     if (warp == CTRL) {  // two accumulators of N fp32 columns each
@@ -244,6 +248,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
             };
             for (std::uint32_t s = 0; s < 2 && s < nst; ++s) issue_b(s);
             std::uint32_t tile_i = 0;  // tiles started in this range
+            std::uint32_t b = 0, bn = 0;  // A buffer of stage s = s % NA, its use count s / NA
 #pragma unroll 1
             for (std::uint32_t s = 0; s < nst; ++s) {
                 const std::uint32_t u = u0 + (s >> 1), P = pan(u);
@@ -251,8 +256,8 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 const bool last = (s & 1u) && (u + 1 == u1 || P + 1 == p.Pn);
                 if (first && tile_i >= 2) TC_WAIT(2, mbar_wait(&d_free[tile_i & 1u], ((tile_i >> 1) - 1u) & 1u))
                 if (s + 2 < nst) issue_b(s + 2);
-                const std::uint32_t b = s % 3u, bb = b;
-                TC_WAIT(0, mbar_wait(&a_full[b], (s / 3u) & 1u))
+                const std::uint32_t bb = s % 3u;
+                TC_WAIT(0, mbar_wait(&a_full[b], bn & 1u))
                 TC_WAIT(1, mbar_wait(&b_full[bb], (s / 3u) & 1u))
                 tc::fence_after();
                 const std::uint32_t d = tmem + (tile_i & 1u) * N;
@@ -264,6 +269,10 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                                 (first && kk == 0) ? 0u : 1u);
                 tc::commit(&a_free[b]);   // A buffer b and x buffer bb are free once these MMAs finish
                 tc::commit(&b_free[bb]);
+                if (++b == NA) {
+                    b = 0;
+                    ++bn;
+                }
                 if (last) {
                     tc::commit(&d_full[tile_i & 1u]);
                     ++tile_i;
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
         if (u0 < u1) issue(u0, 0);
         pdl_wait();
         std::uint32_t tile_i = 0;
+        std::uint32_t sb0 = 0, sn0 = 0;  // buffer / use count of stage 2it
         // stmatrix row address of this lane: matrix lane/8 = (row half, k half)
         const std::uint32_t mq = static_cast<std::uint32_t>(lane >> 3);
 #pragma unroll 1
@@ -372,8 +382,15 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 }
                 __syncwarp();
             }
-            const std::uint32_t st_ = 2u * it + static_cast<std::uint32_t>(hh), ab = st_ % 3u;
-            if (st_ >= 3) TC_WAIT(1, mbar_wait(&a_free[ab], ((st_ / 3u) - 1u) & 1u))
+            // this cell's stages 2it (column half 0) and 2it + 1 (half 1)
+            const std::uint32_t ab0 = sb0, ab1 = sb0 + 1u == NA ? 0u : sb0 + 1u;
+            const std::uint32_t ab = hh ? ab1 : ab0, an = (hh && ab1 == 0u) ? sn0 + 1u : sn0;
+            if (an) TC_WAIT(1, mbar_wait(&a_free[ab], (an - 1u) & 1u))
+            sb0 += 2u;
+            if (sb0 >= NA) {
+                sb0 -= NA;
+                ++sn0;
+            }
             std::uint8_t* A = abuf + ab * A_STAGE;
             if (have) {
                 std::uint32_t cw[G::LANE_WORDS];
@@ -412,52 +429,37 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                     do_half(std::integral_constant<int, 0>{});
                 else
                     do_half(std::integral_constant<int, 1>{});
-                __syncwarp();
-                // outliers of this (unit, half): w += v (fp16, scaled by 2^-sigma).
-                // Entries are sorted by (row, col): unit 0's rows come first, so
-                // this warp's unit is one contiguous run [ia, ib) of the list
+            }
+            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  The four
+            // warps of the cell row own both A buffers of the cell (stages 2it,
+            // 2it + 1) between the two row barriers and split the entry list
+            // 128 ways, so no warp searches for its (unit, half) run
+            bar_sync_named(1 + ci, 128);  // the row's stmatrix writes are done
+            if (have) {
                 const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-                if (cnt) {
-                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
-                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
-                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
-                    auto entry = [&](std::uint32_t i) { return i < nfast ? es[i] : __ldg(eg + i); };
-                    // n0 = entries of rows 0..15 = first index whose row is >= 16
-                    // (padding sorts last: row 255): two rounds of 32 probes
-                    std::uint32_t lo = 0, span = cnt;  // the boundary lies in [lo, lo + span]
+                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL);
+                const std::uint32_t rowb = (4u * ci) * 128u;
+                const std::uint32_t a_h0 = smem_u32(abuf) + ab0 * A_STAGE + rowb;
+                const std::uint32_t a_h1 = smem_u32(abuf) + ab1 * A_STAGE + rowb;
 #pragma unroll 1
-                    while (span > 32) {
-                        const std::uint32_t step = (span + 31) / 32;
-                        const std::uint32_t i = lo + lane * step;  // probe: is entry i still unit 0?
-                        const bool below = i < cnt && (entry(i) >> 24) < 16u;
-                        const std::uint32_t nb = __popc(__ballot_sync(0xffffffffu, below));  // probes below
-                        if (nb == 0) break;  // boundary at lo
-                        lo += (nb - 1) * step + 1;
-                        span = step - 1;
-                    }
-                    const bool below = lane < span && lo + lane < cnt && (entry(lo + lane) >> 24) < 16u;
-                    const std::uint32_t n0 = lo + __popc(__ballot_sync(0xffffffffu, below));
-                    const std::uint32_t ia = uu ? n0 : 0u, ib = uu ? cnt : n0;
-                    const std::uint32_t a_row0 = smem_u32(A) + (4u * ci) * 128u;
-#pragma unroll 1
-                    for (std::uint32_t i = ia + lane; i < ib; i += 32) {
-                        const std::uint32_t e = entry(i);
-                        const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
-                        if (row < 32u && (col >> 7) == static_cast<std::uint32_t>(hh)) {
-                            const std::uint32_t kq = col & 127u;
-                            const std::uint32_t sa = a_row0 + (kq >> 3) * KC_A + (row >> 3) * 128u + (row & 7u) * 16u +
-                                                     (kq & 7u) * 2u;
-                            unsigned short hb;
-                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hb) : "r"(sa));
-                            const float wv = __half2float(__ushort_as_half(hb)) + h2f_bits(e & 0xffffu) * sig_scale;
-                            hb = __half_as_ushort(__float2half_rn(wv));
-                            asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa), "h"(hb));
-                        }
+                for (std::uint32_t i = 32u * static_cast<std::uint32_t>(warp >> 2) + lane; i < cnt; i += 128) {
+                    const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
+                    const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
+                    if (row < 32u) {
+                        const std::uint32_t sa = ((col & 128u) ? a_h1 : a_h0) + ((col & 127u) >> 3) * KC_A +
+                                                 (row >> 3) * 128u + (row & 7u) * 16u + (col & 7u) * 2u;
+                        unsigned short hb;
+                        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hb) : "r"(sa));
+                        const float wv = __half2float(__ushort_as_half(hb)) + h2f_bits(e & 0xffffu) * sig_scale;
+                        hb = __half_as_ushort(__float2half_rn(wv));
+                        asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa), "h"(hb));
                     }
                 }
             }
-            fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
-            __syncwarp();
+            fence_proxy_async();          // generic-proxy smem writes -> tensor core reads
+            bar_sync_named(1 + ci, 128);  // ... of every warp of the row
             if (lane == 0) mbar_arrive(&a_full[ab]);
             if (have) {
                 if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);  // this warp is done with the record
