@@ -72,9 +72,10 @@ def make_streams():
             s = open(path, "rb").read()
         else:
             s = synth.random_stream(m, n, BITS, 3, 3, RATE, seed=100 + i)
-            with open(path + ".tmp", "wb") as f:
+            tmp = f"{path}.{os.getpid()}.tmp"  # ranks of one node may generate concurrently
+            with open(tmp, "wb") as f:
                 f.write(s)
-            os.replace(path + ".tmp", path)
+            os.replace(tmp, path)
         out.append(s)
     return out
 
@@ -396,6 +397,32 @@ def run_ours(args) -> None:
             "GB/s": round(alg_bytes(pb, gp["L"].rows, gp["n"]) / (us * 1e-6) / 1e9, 1),
             "l2_resident_risk": pb < 126e6}
 
+    # ---- multi-GPU split: kernels alone, all-gathers alone, the
+    # step, each the max over ranks ----
+    multi = None
+    if world > 1:
+        def gathers():
+            for gp in groups:
+                gather(gp)
+        if share:  # gloo: eager, host-timed
+            gathers()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(10):
+                gathers()
+            torch.cuda.synchronize()
+            gms = 1e3 * (time.perf_counter() - t0) / 10
+        else:
+            gms = graph_time(gathers, max(20, args.steps // 5))
+        t = torch.tensor([kms, gms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        multi = {"kernel_us_per_step": round(1e3 * float(t[0]), 3),
+                 "allgather_us_per_step": round(1e3 * float(t[1]), 3),
+                 "end_to_end_us_per_step": round(1e3 * ms_per_step, 3),
+                 "allgathers_per_step": len(groups), "allgather_bytes_per_rank": [4 * gp["yfull"].numel() // world
+                                                                                  for gp in groups],
+                 "backend": dist.get_backend()}
+
     # ---- dense fp16 GEMV comparator (ours and cuBLAS), same stacked shapes ----
     dense = {}
     if world == 1:
@@ -470,7 +497,7 @@ def run_ours(args) -> None:
             "config": workload_config(world),
             "bytes_per_step": bytes_step, "payload_bytes_per_step": payload_step,
             "roofline": roofline, "per_layer": per_layer, "dense_fp16": dense or None,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "multi_gpu": multi,
             "gpu_launches": args.steps * launches_per_step,
         }
         print(json.dumps(line), flush=True)

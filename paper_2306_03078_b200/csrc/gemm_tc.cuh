@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int 
     *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// 17 warps: 96 registers (five warps share one SM sub-partition's 16K registers)
 template <int BW, int BS, int BZ>
 __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
@@ -393,25 +394,32 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
             }
             std::uint8_t* A = abuf + ab * A_STAGE;
             if (have) {
-                std::uint32_t cw[G::LANE_WORDS];
-#pragma unroll
-                for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                    const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                    cw[4 * i] = w4.x;
-                    cw[4 * i + 1] = w4.y;
-                    cw[4 * i + 2] = w4.z;
-                    cw[4 * i + 3] = w4.w;
-                }
                 const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
                                              (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
                 auto do_half = [&](auto HH) {
                     constexpr int h_ = decltype(HH)::value;
+                    // only this half's code containers (blocks 8h .. 8h+7), as 8 B loads
+                    constexpr int W0 = G::CW * (8 * h_ / G::MPC), W1 = G::CW * ((8 * h_ + 7) / G::MPC + 1);
+                    static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a half: 8 B aligned");
+                    std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+                    for (int i = W0; i < W1; i += 2) {
+                        const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
+                        cw[i] = w2.x;
+                        cw[i + 1] = w2.y;
+                    }
+                    // table entries one block ahead of their use (LDS latency)
+                    uint4 n0 = *reinterpret_cast<const uint4*>(tab + g * 144);
+                    uint4 n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144);
 #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
                         const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
                         const std::uint32_t* w = cw + G::CW * cidx;
-                        const uint4 e0 = *reinterpret_cast<const uint4*>(tab + g * 144 + jj * 16);
-                        const uint4 e1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144 + jj * 16);
+                        const uint4 e0 = n0, e1 = n1;
+                        if (jj < 7) {
+                            n0 = *reinterpret_cast<const uint4*>(tab + g * 144 + (jj + 1) * 16);
+                            n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144 + (jj + 1) * 16);
+                        }
                         std::uint32_t a[4];
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
