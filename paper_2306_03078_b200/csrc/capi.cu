@@ -118,6 +118,8 @@ struct spqr_layer {
         std::uint32_t pan_off = 0, part_off = 0, off_off = 0, gd_off = 0, part_cap = 0, smem = 0;
         bool shared_x = false;  // x panels prepared once per CTA (they fit in shared memory)
         std::uint32_t* d_start = nullptr;  // [nvcta+1]
+        std::uint32_t* d_first = nullptr;  // [grid][kNC][2] record byte range of warp w's first cell
+        std::vector<std::uint32_t> h_start;  // cta_start on the host (the first grid + 1 go by value)
     } cta[2];
     std::uint32_t pn_magic = 0;
     // gemm_tc plan (batch >= 2): ranges of (128-row tile, panel) units
@@ -141,6 +143,7 @@ struct spqr_layer {
                         static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
                         static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
+                        static_cast<void*>(cta[0].d_first), static_cast<void*>(cta[1].d_first),
                         static_cast<void*>(tcp.d_start), static_cast<void*>(tcp.d_maps),
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
@@ -495,6 +498,9 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
             p.rec_cap = c.rec_cap; p.slot_bytes = c.slot_bytes;
             p.pan_off = c.pan_off; p.part_off = c.part_off; p.off_off = c.off_off; p.gd_off = c.gd_off;
             p.part_cap = c.part_cap;
+            p.first_rec = reinterpret_cast<const uint2*>(c.d_first);
+            if (c.grid < static_cast<std::uint32_t>(spqr_dev::kQFirst))
+                std::copy(c.h_start.begin(), c.h_start.begin() + c.grid + 1, p.q_first);
             p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0) ? 1u : 0u;
             dispatch_cta(p, L, !f16, st);
         }
@@ -679,6 +685,19 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     c.smem = c.gd_off + gd_bytes;
     c.d_start = dalloc<std::uint32_t>(st.size());
     ck(cudaMemcpy(c.d_start, st.data(), 4 * st.size(), cudaMemcpyHostToDevice), "H2D cta_start");
+    c.h_start = st;
+    // CTA v's first range is range v; its warp w takes cell w first
+    std::vector<std::uint32_t> first(2ull * c.grid * kNC, 0u);
+    for (std::uint32_t v = 0; v < c.grid; ++v)
+        for (std::uint32_t w = 0; w < static_cast<std::uint32_t>(kNC); ++w) {
+            const std::uint32_t q = st[v] + w;
+            if (q < st[v + 1]) {
+                first[2 * (v * kNC + w)] = t.cell_off[q];
+                first[2 * (v * kNC + w) + 1] = t.cell_off[q + 1];
+            }
+        }
+    c.d_first = dalloc<std::uint32_t>(first.size());
+    ck(cudaMemcpy(c.d_first, first.data(), 4 * first.size(), cudaMemcpyHostToDevice), "H2D first records");
     if (xi == 0) {  // q / Pn as a multiply-high (Pn == 1: the kernel uses q itself)
         const std::uint64_t mg = t.Pn > 1 ? ((1ull << 32) + t.Pn - 1) / t.Pn : 0;
         L->pn_magic = static_cast<std::uint32_t>(mg);

@@ -300,12 +300,22 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
         };
         // record k of this cell row goes to slot k & 1; warp (ci, 0, 0) issues it
         // once all four warps of the row released the slot's previous record
+        // The record offsets of unit u + 1 are loaded one step ahead into
+        // (nr0, nr1), so the issuing lane never waits on a global load.
+        std::uint32_t nr0 = 0, nr1 = 0;
+        auto load_off = [&](std::uint32_t u) {
+            std::uint32_t q;
+            if (warp == ci && lane == 0 && u < u1 && cell_of(u, q)) {
+                nr0 = __ldg(p.cell_off + q);
+                nr1 = __ldg(p.cell_off + q + 1);
+            }
+        };
         auto issue = [&](std::uint32_t u, std::uint32_t k) {
             std::uint32_t q;
             if (warp == ci && lane == 0 && cell_of(u, q)) {
                 const std::uint32_t sl = k & 1u;
                 if (k >= 2) mbar_wait(&rec_empty[ci][sl], ((k >> 1) - 1u) & 1u);
-                const std::uint32_t r0 = __ldg(p.cell_off + q), r1 = __ldg(p.cell_off + q + 1);
+                const std::uint32_t r0 = nr0, r1 = nr1;
                 slot_r[ci][sl][0] = r0;
                 slot_r[ci][sl][1] = r1;
                 const std::uint32_t nb = min(r1 - r0, p.rec_cap);
@@ -326,7 +336,9 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
             g1 = make_float2(pw(T::prescale_p(BW, 2 * mm0 + 1) - 24), pw(T::prescale_p(BW, 2 * mm1 + 1) - 24));
         }
         std::uint32_t k = 0;  // records of this cell row consumed so far
+        load_off(u0);
         if (u0 < u1) issue(u0, 0);
+        load_off(u0 + 1);
         pdl_wait();
         std::uint32_t tile_i = 0;
         std::uint32_t sb0 = 0, sn0 = 0;  // buffer / use count of stage 2it
@@ -337,7 +349,10 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
             const std::uint32_t it = u - u0;
             std::uint32_t q;
             const bool have = cell_of(u, q);
-            if (have && u + 1 < u1) issue(u + 1, k + 1);
+            if (have && u + 1 < u1) {
+                issue(u + 1, k + 1);
+                load_off(u + 2);
+            }
             const std::uint32_t sl = k & 1u;
             const std::uint8_t* cell = ring + sl * p.slot_bytes;
             const std::uint8_t* unit = cell + uu * UNIT;

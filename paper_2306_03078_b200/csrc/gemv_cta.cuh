@@ -40,8 +40,10 @@
 // off by default; -DSPQR_SPLIT_CELLS_FN='min(NC / 2u, nc / 2u)' turns it on.
 #ifndef SPQR_SPLIT_CELLS_FN
 #define SPQR_SPLIT_CELLS_FN 0u
+#define SPQR_SPLIT_OFF 1
 #endif
 
+constexpr int kQFirst = 161;
 struct CtaParams {
     const std::uint8_t* cells;        // cell records
     const std::uint32_t* cell_off;    // [ncell+1]
@@ -55,6 +57,11 @@ struct CtaParams {
     std::uint32_t rec_cap, slot_bytes;
     std::uint32_t pan_off, part_off, off_off, gd_off, part_cap;
     std::uint32_t x_vec;              // x is 16-B aligned and not permuted: vector loads
+    const uint2* first_rec;           // [grid][NC] {r0, r1}: record of warp w's first cell (r0 == r1: none)
+    // cta_start[0 .. grid] by value (grid < kQFirst): the first range's bounds
+    // come from the parameter bank, not from HBM while the preceding kernel
+    // saturates it (a ~1.4 us load ahead of the PDL wait)
+    std::uint32_t q_first[kQFirst];
 };
 
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
@@ -266,26 +273,42 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             if (ol) bulk_g2s(dst + CELL, p.cells + r0 + CELL, ol, bar);
         }
     };
-    // the first record of this warp's first ticket goes out before anything
-    // else, from the global offsets (the range's offset table loads meanwhile)
+    std::uint32_t* const coff_base = reinterpret_cast<std::uint32_t*>(smem + p.off_off);
+    std::uint32_t* coff = coff_base;
+    std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
+    for (std::uint32_t i = threadIdx.x; i <= p.part_cap; i += NT) gdone[i] = 0;  // whole capacity
+    // Shared state is ready at this barrier, and no global load precedes it: a
+    // CTA that becomes resident late (its SM's previous CTA was the slowest of
+    // the preceding kernel) reaches the PDL wait without a round trip.
+    __syncthreads();
+    // the first record of this warp's first ticket goes out first, its offsets
+    // from the plan's per-CTA table (one load, no cta_start -> cell_off chain)
     if (blockIdx.x < p.nvcta && lane == 0) {
+        std::uint32_t r0, r1;
+        int uo = -1;
+        bool have = false;
+#ifdef SPQR_SPLIT_OFF
+        const uint2 r = __ldg(p.first_rec + blockIdx.x * NC + warp);
+        r0 = r.x;
+        r1 = r.y;
+        have = r1 > r0;
+#else
         const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
         const std::uint32_t S0 = split_of(q1 - q0);
-        if (static_cast<std::uint32_t>(warp) < q1 - q0 + S0) {
-            int uo;
-            const std::uint32_t c = decode(warp, q1 - q0, S0, uo);
-            const std::uint32_t r0 = __ldg(p.cell_off + q0 + c), r1 = __ldg(p.cell_off + q0 + c + 1);
+        have = static_cast<std::uint32_t>(warp) < q1 - q0 + S0;
+        const std::uint32_t c = have ? decode(warp, q1 - q0, S0, uo) : 0u;
+        r0 = have ? __ldg(p.cell_off + q0 + c) : 0u;
+        r1 = have ? __ldg(p.cell_off + q0 + c + 1) : 0u;
+#endif
+        if (have) {
             slot_r[warp][0][0] = r0;
             slot_r[warp][0][1] = r1;
             copy_rec(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, r0, r1, uo, &full[warp][0]);
         }
     }
     // record offsets of the range: the first range's arrive by one bulk copy
-    // (16-B aligned superset; cell_off is padded), so nothing before the PDL
-    // wait waits on a global load; later ranges load them after a barrier
-    std::uint32_t* const coff_base = reinterpret_cast<std::uint32_t*>(smem + p.off_off);
-    std::uint32_t* coff = coff_base;
-    std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
+    // (16-B aligned superset; cell_off is padded), waited on only where used;
+    // later ranges load them after a barrier
     auto range_setup = [&](std::uint32_t v) {
         const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
         coff = coff_base;
@@ -294,17 +317,25 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             gdone[i] = 0;
         }
     };
+    auto range_bounds = [&](std::uint32_t v, std::uint32_t& q0, std::uint32_t& q1) {
+        if (v == blockIdx.x && gridDim.x < static_cast<unsigned>(kQFirst)) {
+            q0 = p.q_first[v];
+            q1 = p.q_first[v + 1];
+        } else {
+            q0 = __ldg(p.cta_start + v);
+            q1 = __ldg(p.cta_start + v + 1);
+        }
+    };
     if (blockIdx.x < p.nvcta) {
-        const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
+        std::uint32_t q0, q1;
+        range_bounds(blockIdx.x, q0, q1);
         const std::uint32_t qa = q0 & ~3u, qb = (q1 + 4u) & ~3u;
         coff = coff_base + (q0 - qa);
-        for (std::uint32_t i = threadIdx.x; i <= q1 - q0; i += NT) gdone[i] = 0;
         if (threadIdx.x == 0) {  // the thread that initialised coff_bar
             mbar_expect_tx(&coff_bar, 4u * (qb - qa));
             bulk_g2s(coff_base, p.cell_off + qa, 4u * (qb - qa), &coff_bar);
         }
     }
-    __syncthreads();
     // the next kernel in the stream may be scheduled now; it reads what we
     // write only after this grid has completed (its griddepcontrol.wait)
     pdl_launch();
@@ -348,7 +379,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     bool waited = false;
 #pragma unroll 1
     for (std::uint32_t v = blockIdx.x; v < p.nvcta; v += gridDim.x, ++it) {
-        const std::uint32_t q0 = __ldg(p.cta_start + v), q1 = __ldg(p.cta_start + v + 1);
+        std::uint32_t q0, q1;
+        range_bounds(v, q0, q1);
         const std::uint32_t nc = q1 - q0;
         const std::uint32_t S = split_of(nc), nt = nc + S;  // tickets
         float* part = part_base;
