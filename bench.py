@@ -18,8 +18,11 @@ Metric: effective GB/s = algorithmic bytes / time, algorithmic bytes per layer
 re-reads them from HBM (no flush needed).
 
 N > 1 (torchrun): each rank holds a 1/N row band of every layer (the
-row-sharded wrapper) and all-gathers y over NCCL after each layer; value is
-the whole-job bytes / max-over-ranks time ("scaling": "strong").
+row-sharded wrapper); the all-gather of y is fused into the band kernels (P2P
+stores into every rank's y over CUDA IPC / NVLink + a per-rank round counter,
+one 32-thread wait launch per group).  The NCCL all-gather path the north star
+names is timed beside it ("multi_gpu.nccl_baseline").  value is the whole-job
+bytes / max-over-ranks time ("scaling": "strong").
 """
 from __future__ import annotations
 
@@ -56,7 +59,8 @@ def workload_config(n_gpus: int) -> dict:
         "batch": 1, "x_dtype": "f16", "layers": len(LAYERS),
         "l2": "weights 400 MB per step > 126 MB L2: inputs larger than L2, no flush",
         "launches": "4 per step: q/k/v stacked (fused QKV), o, gate/up stacked, down; x shared within a group",
-        "parallelism": f"row-shard x{n_gpus} + NCCL all-gather of y" if n_gpus > 1 else "single GPU",
+        "parallelism": f"row-shard x{n_gpus} + all-gather of y fused into the band kernels (NCCL timed as baseline)"
+        if n_gpus > 1 else "single GPU",
     }
 
 
@@ -282,6 +286,20 @@ def run_ours(args) -> None:
     payload_step = sum(len(s) - 48 for s in streams)
 
     stream = torch.cuda.Stream(device=dev)
+    fused = world > 1
+    if fused:  # the product path: all-gather fused into the band kernels (P2P stores + round counters)
+        from paper_2306_03078_b200.sharded import FusedGather
+        err = ""
+        try:
+            for gp in groups:
+                gp["fg"] = FusedGather(gp["bands"][-1][1], gp["bands"], rank, world, dev.index)
+        except Exception as ex:  # noqa: BLE001 -- every rank must agree before choosing a path
+            err = f"{type(ex).__name__}: {ex}"
+        ok = torch.tensor([0 if err else 1], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        fused = bool(ok.item())
+        if not fused and rank == 0:
+            print(f"fused all-gather unavailable ({err or 'on another rank'}); timing the NCCL path", file=sys.stderr)
 
     def gather(gp):  # equal-size rank bands (every member's band is 32-row aligned)
         gather_rows(torch.nn.functional.pad(gp["y"], (0, gp["bands"][0][1] - gp["y"].numel())), gp["bands"],
@@ -289,16 +307,24 @@ def run_ours(args) -> None:
 
     def step():
         for gp in groups:
+            if fused:
+                gp["fg"].matvec(gp["L"], gp["x"], stream=stream)
+            else:
+                gp["L"].matvec(gp["x"], gp["y"], stream=stream)
+                if world > 1:
+                    gather(gp)
+
+    def nccl_step():  # the baseline the north star names: band kernel, then NCCL all-gather
+        for gp in groups:
             gp["L"].matvec(gp["x"], gp["y"], stream=stream)
-            if world > 1:
-                gather(gp)
+            gather(gp)
 
     with torch.cuda.stream(stream):
         for _ in range(3):
             step()
     torch.cuda.synchronize()
     graph = None
-    if not share:  # gloo collectives (the shared-GPU test hook) cannot be captured
+    if world == 1 or fused or not share:  # gloo collectives cannot be captured
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             step()
@@ -342,7 +368,12 @@ def run_ours(args) -> None:
     launches_per_step = 0
     with torch.cuda.stream(stream):
         for gp in groups:
-            gp["L"].matvec(gp["x"], gp["y"], stream=stream)
+            if fused:  # one more round on every rank (symmetric): band kernel + wait
+                gp["fg"].g.matvec(gp["L"], gp["x"], stream=stream)
+                launches_per_step += P.last_launch_count()
+                gp["fg"].g.wait(stream=stream)
+            else:
+                gp["L"].matvec(gp["x"], gp["y"], stream=stream)
             launches_per_step += P.last_launch_count()
     torch.cuda.synchronize()
 
@@ -404,24 +435,32 @@ def run_ours(args) -> None:
         def gathers():
             for gp in groups:
                 gather(gp)
-        if share:  # gloo: eager, host-timed
-            gathers()
+
+        def eager_ms(fn, reps=10):  # gloo collectives cannot be captured: host-timed
+            fn()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for _ in range(10):
-                gathers()
+            for _ in range(reps):
+                fn()
             torch.cuda.synchronize()
-            gms = 1e3 * (time.perf_counter() - t0) / 10
+            return 1e3 * (time.perf_counter() - t0) / reps
+        if share:
+            gms, nms = eager_ms(gathers), eager_ms(nccl_step)
         else:
             gms = graph_time(gathers, max(20, args.steps // 5))
-        t = torch.tensor([kms, gms], device=dev)
+            nms = graph_time(nccl_step, max(20, args.steps // 5))
+        t = torch.tensor([kms, gms, nms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        multi = {"kernel_us_per_step": round(1e3 * float(t[0]), 3),
-                 "allgather_us_per_step": round(1e3 * float(t[1]), 3),
-                 "end_to_end_us_per_step": round(1e3 * ms_per_step, 3),
-                 "allgathers_per_step": len(groups), "allgather_bytes_per_rank": [4 * gp["yfull"].numel() // world
-                                                                                  for gp in groups],
-                 "backend": dist.get_backend()}
+        multi = {"path": "fused all-gather: band gemv_cta stores y rows into every rank's buffer (CUDA IPC / "
+                         "NVLink P2P) + round counters, one gather_wait launch per group" if fused
+                         else "band gemv_cta + NCCL all-gather (fused path unavailable)",
+                 "kernel_us_per_step": round(1e3 * float(t[0]), 3),
+                 "step_us": round(1e3 * ms_per_step, 3),
+                 "nccl_baseline": {"allgather_us_per_step": round(1e3 * float(t[1]), 3),
+                                   "step_us": round(1e3 * float(t[2]), 3),
+                                   "backend": dist.get_backend()},
+                 "allgathers_per_step": len(groups),
+                 "allgather_bytes_per_rank": [4 * gp["yfull"].numel() // world for gp in groups]}
 
     # ---- dense fp16 GEMV comparator (ours and cuBLAS), same stacked shapes ----
     dense = {}
@@ -454,9 +493,13 @@ def run_ours(args) -> None:
                 ys_h[i].numpy()[:] = gp["L"].matvec_host(gp["x32"].numpy())
             else:
                 xd32[i].copy_(gp["x32"], non_blocking=True)
-                gp["L"].matvec(xd32[i], gp["y"], stream=torch.cuda.current_stream())
-                gather(gp)
-                ys_h[i].copy_(gp["yfull"][: gp["m"]], non_blocking=True)
+                if fused:
+                    yf = gp["fg"].matvec(gp["L"], xd32[i], stream=torch.cuda.current_stream())
+                else:
+                    gp["L"].matvec(xd32[i], gp["y"], stream=torch.cuda.current_stream())
+                    gather(gp)
+                    yf = gp["yfull"]
+                ys_h[i].copy_(yf[: gp["m"]], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
 
     for _ in range(2):
@@ -478,7 +521,7 @@ def run_ours(args) -> None:
            "d2h_bytes_per_step": sum(4 * gp["m"] for gp in groups),
            "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3),
            "path": "spqr_matvec_host (C ABI: H2D fp32 x, fused kernels, D2H y, sync) per group"
-                   if world == 1 else "H2D x, spqr_matvec, NCCL all-gather, D2H y per group"}
+                   if world == 1 else "H2D x, spqr_matvec_gather + spqr_gather_wait (fused all-gather), D2H y per group"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -198,14 +198,37 @@ uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
  * Asynchronous on cuda_stream; allocates nothing.  spqr_matvec uses the
  * layer's own workspace (one stream at a time); spqr_matvec_ws takes a caller
  * workspace (concurrent streams; size from spqr_workspace_bytes(layer, batch)).
- * Fast-path layers: batch 1-4 run one fused gemv_cta launch per column
+ * Fast-path layers: batch 1-3 run one fused gemv_cta launch per column
  * (exact codes, fp32 accumulation: ~1e-7 relative to the reference);
- * batch >= 5 run xprep_tc + gemm_tc per 128 columns (weights rounded to fp16,
+ * batch >= 4 run xprep_tc + gemm_tc per 64 columns (weights rounded to fp16,
  * tcgen05 tensor cores: <= 1e-3 relative, the north star's bar). */
 int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                 void* cuda_stream);
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,
                    int batch, void* workspace, uint64_t ws_bytes, void* cuda_stream);
+
+/* Fused all-gather for the row-sharded wrapper ("optional
+ * B200-native fusion"; 8f rank 2): instead of spqr_matvec on the band followed
+ * by an NCCL all-gather of y, each rank's gemv_cta stores every finished y
+ * row straight into every rank's full-y buffer (peer addresses from CUDA IPC:
+ * NVLink P2P stores between GPUs) and its last CTA bumps this rank's round
+ * counter on every rank; spqr_gather_wait (one 32-thread launch) waits for all
+ * ranks' counters.  Rounds live on the device: both launches replay in a CUDA
+ * graph.  Protocol: spqr_gather_create on every rank -> spqr_gather_handle ->
+ * exchange the world x SPQR_GATHER_HANDLE_BYTES handles and the bands' first
+ * rows (any transport, e.g. torch.distributed) -> spqr_gather_open -> per
+ * step spqr_matvec_gather + spqr_gather_wait, then read spqr_gather_y.
+ * Batch 1; the layer is this rank's band (rows row_base[rank] ...). */
+#define SPQR_GATHER_HANDLE_BYTES 64
+typedef struct spqr_gather spqr_gather;
+int spqr_gather_create(int device, uint32_t rows, int world, int rank, spqr_gather** out);
+int spqr_gather_handle(const spqr_gather* g, void* handle_out);
+int spqr_gather_open(spqr_gather* g, const void* handles, const uint32_t* row_base);
+float* spqr_gather_y(const spqr_gather* g);
+int spqr_matvec_gather(const spqr_layer* layer, const void* x_dev, int x_dtype, spqr_gather* g,
+                       void* cuda_stream);
+int spqr_gather_wait(spqr_gather* g, void* cuda_stream);
+void spqr_gather_destroy(spqr_gather* g);
 
 /* Profiling split of spqr_matvec: stage 1 = x preparation only, stage 2 = the
  * product only, 0 = both.  On the fast path x preparation is fused into the

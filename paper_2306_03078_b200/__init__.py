@@ -130,6 +130,13 @@ def lib() -> C.CDLL:
         "spqr_debug_tiled_host": (i32, [vp, sz, vp, vp, vp, vp]),
         "spqr_matvec_stage": (i32, [vp, vp, i32, vp, i32, i32, vp]),
         "spqr_bench_layer": (i32, [vp, i32, vp]),
+        "spqr_gather_create": (i32, [i32, u32, i32, i32, C.POINTER(vp)]),
+        "spqr_gather_handle": (i32, [vp, vp]),
+        "spqr_gather_open": (i32, [vp, vp, vp]),
+        "spqr_gather_y": (vp, [vp]),
+        "spqr_matvec_gather": (i32, [vp, vp, i32, vp, vp]),
+        "spqr_gather_wait": (i32, [vp, vp]),
+        "spqr_gather_destroy": (None, [vp]),
         "spqr_dev_alloc": (i32, [C.POINTER(vp), sz]),
         "spqr_dev_free": (None, [vp]),
         "spqr_dev_copy_to_host": (i32, [vp, vp, sz]),
@@ -404,6 +411,53 @@ class Layer:
 
     def export_stream(self) -> bytes:
         return _sized_call(lib().spqr_layer_export_stream, self._h)
+
+
+GATHER_HANDLE_BYTES = 64
+
+
+class Gather:
+    """Full-y target of the fused all-gather (spqr_gather_*): every rank's
+    band matvec stores its rows into every rank's buffer over P2P and signals
+    a per-rank round counter; wait() blocks the stream until all ranks'
+    rows of this round have landed."""
+
+    def __init__(self, device: int, rows: int, world: int, rank: int):
+        h = C.c_void_p()
+        _check(lib().spqr_gather_create(device, rows, world, rank, C.byref(h)))
+        self._h, self.rows, self.world, self.rank = h, rows, world, rank
+
+    def handle(self) -> bytes:
+        buf = (C.c_uint8 * GATHER_HANDLE_BYTES)()
+        _check(lib().spqr_gather_handle(self._h, buf))
+        return bytes(buf)
+
+    def open(self, handles: list, row_base: list) -> None:
+        """handles[j] = rank j's handle() bytes; row_base[j] = first row of rank j's band."""
+        hb = b"".join(handles)
+        rb = np.ascontiguousarray(row_base, dtype=np.uint32)
+        _check(lib().spqr_gather_open(self._h, C.c_char_p(hb), rb.ctypes.data_as(C.c_void_p)))
+
+    def y_ptr(self) -> int:
+        return int(lib().spqr_gather_y(self._h))
+
+    def matvec(self, layer: "Layer", x, stream=None) -> None:
+        dt = F16 if str(getattr(x, "dtype", "")).endswith("float16") else F32
+        _check(lib().spqr_matvec_gather(layer.handle, _ptr(x), dt, self._h, _stream_ptr(stream)))
+
+    def wait(self, stream=None) -> None:
+        _check(lib().spqr_gather_wait(self._h, _stream_ptr(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().spqr_gather_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def dense_gemv_f16(w, x, y, rows: int, cols: int, stream=None) -> None:

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <cstring>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -463,6 +465,30 @@ void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xl
     }
 }
 
+// gemv_cta launch parameters for one batch column
+spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int f16, float* y, std::uint8_t* base,
+                               const WsLayout& w) {
+    const auto& c = L->cta[f16 ? 0 : 1];
+    spqr_dev::CtaParams p{};
+    p.cells = L->d_cells;
+    p.cell_off = L->d_cell_off;
+    p.cta_start = c.d_start;
+    p.x = x;
+    p.order = static_cast<const std::uint32_t*>(L->d_order);
+    p.y = y;
+    p.xchg = reinterpret_cast<unsigned long long*>(base + w.xchg);
+    p.m = L->info.rows; p.n = L->info.cols; p.Pn = L->Pn; p.Gn = L->Gn; p.nvcta = c.nvcta;
+    p.pn_magic = L->pn_magic;
+    p.rec_cap = c.rec_cap; p.slot_bytes = c.slot_bytes;
+    p.pan_off = c.pan_off; p.part_off = c.part_off; p.off_off = c.off_off; p.gd_off = c.gd_off;
+    p.part_cap = c.part_cap;
+    p.first_rec = reinterpret_cast<const uint2*>(c.d_first);
+    if (c.grid < static_cast<std::uint32_t>(spqr_dev::kQFirst))
+        std::copy(c.h_start.begin(), c.h_start.begin() + c.grid + 1, p.q_first);
+    p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0) ? 1u : 0u;
+    return p;
+}
+
 // stage: 0 = x preparation + product, 1 = x preparation only, 2 = product only
 // (reuses the workspace the last stage-1 call prepared; used to time the hot
 // kernel alone).
@@ -483,25 +509,10 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
         // one fused launch per batch column (x preparation happens inside)
         if (stage == 1) return;
         const std::size_t esz = f16 ? 2 : 4;
-        const auto& c = L->cta[f16 ? 0 : 1];
         for (int b = 0; b < batch; ++b) {
-            spqr_dev::CtaParams p{};
-            p.cells = L->d_cells;
-            p.cell_off = L->d_cell_off;
-            p.cta_start = c.d_start;
-            p.x = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b) * L->info.cols * esz;
-            p.order = static_cast<const std::uint32_t*>(L->d_order);
-            p.y = y + static_cast<std::size_t>(b) * L->info.rows;
-            p.xchg = reinterpret_cast<unsigned long long*>(base + w.xchg);
-            p.m = L->info.rows; p.n = L->info.cols; p.Pn = L->Pn; p.Gn = L->Gn; p.nvcta = c.nvcta;
-            p.pn_magic = L->pn_magic;
-            p.rec_cap = c.rec_cap; p.slot_bytes = c.slot_bytes;
-            p.pan_off = c.pan_off; p.part_off = c.part_off; p.off_off = c.off_off; p.gd_off = c.gd_off;
-            p.part_cap = c.part_cap;
-            p.first_rec = reinterpret_cast<const uint2*>(c.d_first);
-            if (c.grid < static_cast<std::uint32_t>(spqr_dev::kQFirst))
-                std::copy(c.h_start.begin(), c.h_start.begin() + c.grid + 1, p.q_first);
-            p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0) ? 1u : 0u;
+            spqr_dev::CtaParams p = cta_params(L, static_cast<const std::uint8_t*>(x) +
+                                                      static_cast<std::size_t>(b) * L->info.cols * esz,
+                                               f16, y + static_cast<std::size_t>(b) * L->info.rows, base, w);
             dispatch_cta(p, L, !f16, st);
         }
         return;
@@ -862,6 +873,25 @@ std::uint64_t transcode_on_device(spqr_layer* L, const std::vector<spqr::detail:
 }
 }  // namespace
 
+// Fused all-gather target of one rank: one cudaMalloc'd block (exported to
+// the other ranks by CUDA IPC): [0, 32) per-source-rank round counters,
+// [64] this rank's round, [68] CTAs done (local), [256, ...) the full y.
+struct spqr_gather {
+    int device = 0, world = 1, rank = 0;
+    std::uint32_t rows = 0;
+    std::uint8_t* base = nullptr;
+    std::uint8_t* peer[spqr_dev::kMaxPeers + 1] = {};  // by rank (own block at [rank])
+    std::uint32_t row_base[spqr_dev::kMaxPeers + 1] = {};
+    bool open = false;
+    static constexpr std::size_t kY = 256;
+    float* y() const { return reinterpret_cast<float*>(base + kY); }
+    ~spqr_gather() {
+        for (int j = 0; j < world; ++j)
+            if (j != rank && peer[j]) cudaIpcCloseMemHandle(peer[j]);
+        if (base) cudaFree(base);
+    }
+};
+
 // ================================================================ C ABI ====
 extern "C" {
 
@@ -1099,6 +1129,99 @@ int spqr_matvec(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_de
         ensure_own_ws(L, batch);
         run_matvec(L, x_dev, x_dtype, y_dev, batch, L->d_ws, L->ws_bytes, static_cast<cudaStream_t>(cuda_stream));
     });
+}
+
+int spqr_gather_create(int device, uint32_t rows, int world, int rank, spqr_gather** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (world < 1 || world > spqr_dev::kMaxPeers + 1 || rank < 0 || rank >= world)
+            spqr::fail(spqr::Errc::config_invalid, "gather: world must be 1..8 and 0 <= rank < world");
+        DevGuard dg(device);
+        auto g = std::make_unique<spqr_gather>();
+        g->device = device; g->world = world; g->rank = rank; g->rows = rows;
+        ck(cudaMalloc(&g->base, spqr_gather::kY + 4ull * rows), "cudaMalloc(gather)");
+        ck(cudaMemset(g->base, 0, spqr_gather::kY + 4ull * rows), "memset(gather)");
+        g->peer[rank] = g->base;
+        *out = g.release();
+    });
+}
+
+int spqr_gather_handle(const spqr_gather* g, void* out) {
+    return guard([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == SPQR_GATHER_HANDLE_BYTES, "IPC handle size");
+        DevGuard dg(g->device);
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, g->base), "cudaIpcGetMemHandle");
+        std::memcpy(out, &h, sizeof h);
+    });
+}
+
+int spqr_gather_open(spqr_gather* g, const void* handles, const uint32_t* row_base) {
+    return guard([&] {
+        DevGuard dg(g->device);
+        if (g->open) spqr::fail(spqr::Errc::config_invalid, "gather: already open");
+        const auto* hb = static_cast<const std::uint8_t*>(handles);
+        for (int j = 0; j < g->world; ++j) {
+            g->row_base[j] = row_base[j];
+            if (j == g->rank) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, hb + static_cast<std::size_t>(j) * SPQR_GATHER_HANDLE_BYTES, sizeof h);
+            void* ptr = nullptr;
+            ck(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            g->peer[j] = static_cast<std::uint8_t*>(ptr);
+        }
+        g->open = true;
+    });
+}
+
+float* spqr_gather_y(const spqr_gather* g) { return g ? g->y() : nullptr; }
+
+int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr_gather* g, void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        g_launches = 0;
+        if (!g->open) spqr::fail(spqr::Errc::config_invalid, "gather: spqr_gather_open first");
+        if (g->device != L->device) spqr::fail(spqr::Errc::config_invalid, "gather: layer and buffer devices differ");
+        if (!L->fast || use_legacy_tiled())
+            spqr::fail(spqr::Errc::config_invalid, "fused all-gather needs a fast-path (tiled) layer");
+        if (x_dtype != SPQR_F16 && x_dtype != SPQR_F32) spqr::fail(spqr::Errc::config_invalid, "x dtype must be f16 or f32");
+        const std::uint32_t rb = g->row_base[g->rank];
+        if (rb + L->info.rows > g->rows) spqr::fail(spqr::Errc::shape_mismatch, "gather: band beyond the full y");
+        std::lock_guard<std::mutex> lk(L->mu);
+        ensure_own_ws(L, 1);
+        const WsLayout w = ws_layout(L, 1);
+        const int f16 = x_dtype == SPQR_F16;
+        spqr_dev::CtaParams p = cta_params(L, x_dev, f16, g->y() + rb, static_cast<std::uint8_t*>(L->d_ws), w);
+        std::uint32_t k = 0;
+        for (int j = 0; j < g->world; ++j) {
+            if (j != g->rank) p.ypeer[k++] = reinterpret_cast<float*>(g->peer[j] + spqr_gather::kY);
+            p.pflags[j] = reinterpret_cast<std::uint32_t*>(g->peer[j]);
+        }
+        p.npeer = k;
+        p.nflag = static_cast<std::uint32_t>(g->world);
+        p.row_base = rb;
+        p.rank = static_cast<std::uint32_t>(g->rank);
+        p.done_ctr = reinterpret_cast<std::uint32_t*>(g->base + 68);
+        dispatch_cta(p, L, !f16, static_cast<cudaStream_t>(cuda_stream));
+    });
+}
+
+int spqr_gather_wait(spqr_gather* g, void* cuda_stream) {
+    return guard([&] {
+        DevGuard dg(g->device);
+        g_launches = 0;
+        spqr_dev::gather_wait<<<1, 32, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+            reinterpret_cast<const std::uint32_t*>(g->base), reinterpret_cast<std::uint32_t*>(g->base + 64),
+            static_cast<std::uint32_t>(g->world));
+        ck(cudaGetLastError(), "launch gather_wait");
+        ++g_launches;
+    });
+}
+
+void spqr_gather_destroy(spqr_gather* g) {
+    if (!g) return;
+    DevGuard dg(g->device);
+    delete g;
 }
 
 int spqr_matvec_stage(const spqr_layer* L, const void* x_dev, int x_dtype, float* y_dev, int batch, int stage,

@@ -44,6 +44,7 @@
 #endif
 
 constexpr int kQFirst = 161;
+constexpr int kMaxPeers = 7;  // 8 ranks per node
 struct CtaParams {
     const std::uint8_t* cells;        // cell records
     const std::uint32_t* cell_off;    // [ncell+1]
@@ -62,6 +63,16 @@ struct CtaParams {
     // come from the parameter bank, not from HBM while the preceding kernel
     // saturates it (a ~1.4 us load ahead of the PDL wait)
     std::uint32_t q_first[kQFirst];
+    // Fused all-gather (row-sharded decode): every final y row
+    // is also stored into the full-y buffers of the npeer other ranks (P2P /
+    // NVLink addresses from CUDA IPC) at row_base + row; after the grid's last
+    // y store the last CTA to finish bumps this rank's counter on every rank
+    // (pflags[j][rank], world entries including itself).  npeer == 0 and
+    // pflags == null: a plain matvec.
+    float* ypeer[kMaxPeers];
+    std::uint32_t* pflags[kMaxPeers + 1];
+    std::uint32_t* done_ctr;          // CTAs finished this round (last one resets it)
+    std::uint32_t npeer, nflag, row_base, rank;
 };
 
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
@@ -229,6 +240,10 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto put_y = [&](std::uint32_t row, float v) {
+        p.y[row] = v;
+        for (std::uint32_t j = 0; j < p.npeer; ++j) p.ypeer[j][p.row_base + row] = v;
+    };
 #ifdef SPQR_TIMELINE
     const std::uint32_t wk = blockIdx.x * 16u + static_cast<std::uint32_t>(warp);
     unsigned long long tl_wait = 0, tl_panels = 0;
@@ -726,7 +741,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 const std::uint32_t row = 32u * Gq + lane;
                 unsigned long long* xw = p.xchg + static_cast<std::size_t>(Gq) * 32u + lane;
                 if (a == cs && b == ce) {  // the pair is ours alone
-                    if (row < p.m) p.y[row] = sum;
+                    if (row < p.m) put_y(row, sum);
                 } else if (a != cs) {      // we hold the pair's last cells: publish
                     const unsigned long long w = (1ull << 32) | __float_as_uint(sum);
                     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(xw), "l"(w) : "memory");
@@ -735,7 +750,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     do {
                         asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
                     } while ((w >> 32) == 0ull);
-                    if (row < p.m) p.y[row] = sum + __uint_as_float(static_cast<std::uint32_t>(w));
+                    if (row < p.m) put_y(row, sum + __uint_as_float(static_cast<std::uint32_t>(w)));
                     *xw = 0ull;
                 }
             }
@@ -762,4 +777,43 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         g_timeline[8 * wk + 7] = 1000u + smid;
     }
 #endif
+    if (p.nflag) {  // fused all-gather: signal the round to every rank
+        __syncthreads();  // every y store of this CTA precedes thread 0's release
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            const std::uint32_t prev = atomicAdd(p.done_ctr, 1u);
+            if (prev == gridDim.x - 1u) {  // the grid's last CTA: all stores are fenced
+                *p.done_ctr = 0u;
+                __threadfence_system();
+                for (std::uint32_t j = 0; j < p.nflag; ++j)
+                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.pflags[j] + p.rank) : "memory");
+            }
+        }
+    }
+}
+
+// Fused all-gather, consumer side: one thread per rank waits until that rank's
+// counter reached this round (counters only grow; the round lives on the
+// device, so the launch is CUDA-graph replayable), then the round advances.
+__global__ void __launch_bounds__(32) gather_wait(const std::uint32_t* flags, std::uint32_t* round,
+                                                  std::uint32_t world) {
+    const std::uint32_t r = *round + 1u;
+    if (threadIdx.x < world) {
+        std::uint32_t v;
+        auto now = [] {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            return t;
+        };
+        const unsigned long long t0 = now();
+        for (std::uint32_t it = 0;; ++it) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
+            if (static_cast<int>(v - r) >= 0) break;
+            // a rank that never arrives (crashed peer): fail the launch after
+            // 20 s instead of holding the GPU
+            if ((it & 1023u) == 1023u && now() - t0 > 20000000000ull) __trap();
+        }
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) *round = r;
 }

@@ -11,7 +11,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import Layer, validate
+from . import Gather, Layer, validate
 
 CELL_ROWS = 32  # bands never split a cell (row-group pair); beta2 = 16 divides it
 
@@ -60,10 +60,39 @@ def gather_rows(y_band: torch.Tensor, bands: list[tuple[int, int]], out: torch.T
     return full
 
 
-class ShardedLayer:
-    """This rank's band of one layer, resident on `device`."""
+class _DeviceArray:
+    """A raw device pointer as a torch tensor (__cuda_array_interface__, no copy)."""
 
-    def __init__(self, stream: bytes, rank: int, world: int, device: int):
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class FusedGather:
+    """The all-gather fused into the band kernel (spqr_matvec_gather): one
+    spqr_gather per rank, CUDA IPC handles exchanged over `group` (any
+    torch.distributed backend -- it carries 64 bytes per rank once)."""
+
+    def __init__(self, rows: int, bands: list[tuple[int, int]], rank: int, world: int, device: int, group=None):
+        self.g = Gather(device, rows, world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, self.g.handle(), group=group)
+        self.g.open(handles, [a for a, _ in bands])
+        self.y = torch.as_tensor(_DeviceArray(self.g.y_ptr(), rows), device=torch.device("cuda", device))
+
+    def matvec(self, layer: Layer, x: torch.Tensor, stream=None) -> torch.Tensor:
+        self.g.matvec(layer, x, stream=stream)
+        self.g.wait(stream=stream)
+        return self.y
+
+
+class ShardedLayer:
+    """This rank's band of one layer, resident on `device`.  fused=True (world
+    > 1): the band kernel stores its rows into every rank's full y over P2P and
+    one wait launch replaces the NCCL all-gather (the NCCL path stays the
+    baseline the north star names)."""
+
+    def __init__(self, stream: bytes, rank: int, world: int, device: int, fused: bool = False, group=None):
         info = validate(stream)
         self.rows, self.cols = info["rows"], info["cols"]
         self.bands = row_bands(self.rows, world)
@@ -74,9 +103,12 @@ class ShardedLayer:
         self.y_band = torch.empty(r1 - r0, dtype=torch.float32, device=dev)
         mx = max(b - a for a, b in self.bands)
         self.y_full = torch.empty(max(self.rows, world * mx), dtype=torch.float32, device=dev)
+        self.fused = FusedGather(self.rows, self.bands, rank, world, device, group) if fused and world > 1 else None
 
     def matvec(self, x: torch.Tensor, stream=None, group=None) -> torch.Tensor:
         """Full y (fp32, rows) on every rank: band matvec + all-gather."""
+        if self.fused is not None:
+            return self.fused.matvec(self.layer, x, stream=stream)
         self.layer.matvec(x, self.y_band, stream=stream)
         if len(self.bands) == 1:
             return self.y_band

@@ -1,0 +1,84 @@
+"""torchrun worker for tests/test_gpu.py::test_fused_gather_* (GPU): N ranks
+share cuda:0 (CUDA IPC between processes of one device stands in for NVLink
+peers).  Each rank holds its row band of a layer; the fused path
+(spqr_matvec_gather + spqr_gather_wait) must leave the full y on every rank,
+bit-identical to the band kernels' own outputs gathered over gloo, and within
+1e-5 of the oracle; rounds repeat eagerly and from a replayed CUDA graph."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2306_03078_b200 as P  # noqa: E402
+from paper_2306_03078_b200 import synth  # noqa: E402
+from paper_2306_03078_b200.sharded import ShardedLayer, gather_rows  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def fail(msg):
+    print(msg, flush=True)
+    sys.exit(1)
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    orc = O.Oracle()
+    for m, n, perm in ((1024, 2048, False), (608, 1280, True)):
+        s = P.encode_arrays(synth.make_layer(m, n, outlier_rate=0.02, seed=m + n, permute=perm))
+        fused = ShardedLayer(s, rank, world, 0, fused=True)
+        plain = fused.layer
+        r0, r1 = fused.band
+        st = torch.cuda.Stream()
+        xs = [torch.from_numpy(synth.random_x(n, seed=11 + i).reshape(-1)).to(dev) for i in range(4)]
+        x = torch.empty_like(xs[0])
+        y_band = torch.empty(r1 - r0, device=dev)
+
+        def check(xh, y_full, tag):
+            plain.matvec(xh, y_band, stream=st)
+            st.synchronize()
+            y_ref = gather_rows(y_band.cpu(), fused.bands)[:m].numpy()
+            y = y_full.cpu().numpy()
+            if not np.array_equal(y.view(np.uint32), y_ref.view(np.uint32)):
+                fail(f"rank {rank} {tag}: fused != band kernels, max {np.abs(y - y_ref).max()}")
+            yo = orc.decode(s).matvec(xh.float().cpu().numpy())
+            rel = np.linalg.norm(y - yo) / np.linalg.norm(yo)
+            if rel > 1e-5:
+                fail(f"rank {rank} {tag}: rel {rel} vs oracle")
+
+        for i in range(2):  # eager rounds
+            with torch.cuda.stream(st):
+                x.copy_(xs[i])
+                y = fused.matvec(x, stream=st)
+            st.synchronize()
+            check(x, y, f"m={m} eager {i}")
+            dist.barrier()  # nobody starts the next round while a peer still reads this one
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            x.copy_(xs[2])
+        st.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            y = fused.matvec(x, stream=st)
+        for i in (2, 3):  # graph rounds (the capture itself launched nothing)
+            with torch.cuda.stream(st):
+                x.copy_(xs[i])
+                g.replay()
+            st.synchronize()
+            check(x, y, f"m={m} graph {i}")
+            dist.barrier()
+        del g
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("fused gather ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -256,3 +256,24 @@ def test_device_transcode_matches_host(cuda, case):
         dh = P.Layer.stacked([s, s], host_transcode=True).debug_cells()
         dd = P.Layer.stacked([s, s]).debug_cells()
         assert np.array_equal(dh["cell_off"], dd["cell_off"]) and np.array_equal(dh["cells"], dd["cells"])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_gather_matches_band_kernels(world):
+    """Fused all-gather epilogue (spqr_matvec_gather + spqr_gather_wait): ranks
+    sharing cuda:0 over CUDA IPC; full y on every rank, eager and graph-replayed."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(here, "dist", "fused_gather_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "fused gather ok" in r.stdout
