@@ -314,7 +314,7 @@ constexpr std::uint32_t kTcMaxN = 64;  // batch columns per launch
 // kernel (tools/batch_sweep.py, 8192x22016: 3 x 29 us < ~93 us < 4 x 29 us)
 constexpr int kTcMinBatch = 4;
 std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N, std::uint32_t na) {
-    return na * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + 16u * 2304u;
+    return na * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + spqr_dev::kTcTabBytes;
 }
 // A stage buffers: a fourth (one more half cell of lookahead between the
 // dequant warps) whenever it fits next to the x tiles of this N
@@ -343,7 +343,7 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nv);
-    cfg.blockDim = dim3(544);
+    cfg.blockDim = dim3(spqr_dev::kTcThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -765,7 +765,7 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     }
     c.pslots = slots;
     c.slot_bytes = (t.cell_bytes + 512u + 127u) & ~127u;  // outliers beyond a slot are read from HBM
-    const std::uint32_t need = 3u * 128u * 128u * 2u + 3u * 256u * kTcMaxN + 8u * c.slot_bytes + 16u * 2304u;
+    const std::uint32_t need = 3u * 128u * 128u * 2u + 3u * 256u * kTcMaxN + 8u * c.slot_bytes + spqr_dev::kTcTabBytes;
     if (need + kTcStaticMax > kSmemLimit)
         c.slot_bytes = ((kSmemLimit - kTcStaticMax - (need - 8u * c.slot_bytes)) / 8u) & ~127u;
     if (c.slot_bytes < t.cell_bytes + 16u) spqr::fail(spqr::Errc::config_invalid, "gemm_tc: shared memory plan");

@@ -150,9 +150,23 @@ __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int 
     *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// 17 warps: 96 registers (five warps share one SM sub-partition's 16K registers)
+// Dequant warps: each owns HPW column halves of one 16-row unit of one cell
+// row, so 16 / HPW dequant warps + 1 control warp.  HPW = 1 (default): 17
+// warps at 96 registers (five share an SM sub-partition's 16K registers).
+// HPW = 2: 9 warps, both halves interleaved in one warp -- 30 % fewer
+// instructions (per-step bookkeeping and waits halve) but issue efficiency
+// drops from 51 % to 38 % with two warps per sub-partition: measured equal at
+// batch <= 32 (-1..2 %) and 12 % slower at 64 (tools/batch_sweep.py).
+#ifndef SPQR_TC_HPW
+#define SPQR_TC_HPW 1
+#endif
+constexpr int kTcHpw = SPQR_TC_HPW;
+constexpr int kTcDequantWarps = 16 / kTcHpw;
+constexpr int kTcThreads = 32 * (kTcDequantWarps + 1);
+constexpr std::uint32_t kTcTabStride = 16u * 8u * kTcHpw + 16u;          // one row: 8 HPW blocks x 16 B + pad
+constexpr std::uint32_t kTcTabBytes = kTcDequantWarps * 16u * kTcTabStride;  // all warps' tables
 template <int BW, int BS, int BZ>
-__global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
+__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
@@ -163,7 +177,9 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     constexpr float kMagic = 8388608.0f;
     constexpr std::uint32_t A_STAGE = 128u * 128u * 2u;  // 32 KB
     constexpr std::uint32_t KC_A = 2048u;                // A: bytes between k core matrices (16 row groups)
-    constexpr int ND = 16;                               // dequant warps
+    constexpr int HPW = kTcHpw, ND = kTcDequantWarps;   // halves per dequant warp, dequant warps
+    constexpr int RW = ND / 4;                           // dequant warps per cell row
+    constexpr std::uint32_t TS = kTcTabStride;
     constexpr int CTRL = ND;                             // control warp
 
     extern __shared__ __align__(128) std::uint8_t smem[];
@@ -192,13 +208,13 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
     std::uint8_t* abuf = smem;                                  // [NA][A_STAGE]: stage s in buffer s % NA
     std::uint8_t* bbuf = smem + NA * A_STAGE;                   // [3][B_STAGE]: x tiles, 2 stages of lookahead
     std::uint8_t* recs = bbuf + 3 * B_STAGE;                    // [4 cell rows][2][slot_bytes]
-    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [16 warps][16 rows][144 B: 8 blocks x 16 B + pad]
+    std::uint8_t* stab = recs + 8u * p.slot_bytes;              // [ND warps][16 rows][TS B: 8 HPW blocks x 16 B + pad]
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i)
             for (int k = 0; k < 2; ++k) {
                 mbar_init(&rec_full[i][k], 1);
-                mbar_init(&rec_empty[i][k], 4);  // the four (unit, half) warps of the cell row
+                mbar_init(&rec_empty[i][k], RW);  // the dequant warps of the cell row
             }
         for (int b = 0; b < 4; ++b) {
             mbar_init(&a_full[b], 8);  // 4 cell rows x 2 units write a half stage
@@ -283,13 +299,16 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
         __syncwarp();
     } else {
         // ------------------------------------------------------- dequant --
-        // warp = 8 uu + 4 hh + ci: cell row ci (row-group pair 4T + ci), column
-        // half hh (blocks 8hh .. 8hh+7) and unit uu (rows 16uu .. 16uu+15) of
-        // every cell; warp % 4 == ci, the TMEM lane quarter the epilogue reads
-        const int ci = warp & 3, hh = (warp >> 2) & 1, uu = warp >> 3;
+        // warp = 4 (HPW uu + hh) + ci (HPW = 1) or 4 uu + ci (HPW = 2): cell row
+        // ci (row-group pair 4T + ci), unit uu (rows 16uu .. 16uu+15), column
+        // half hh (blocks 8hh .. 8hh+7) or both; warp % 4 == ci, the TMEM lane
+        // quarter the epilogue reads
+        const int ci = warp & 3;
+        const int uu = HPW == 2 ? warp >> 2 : warp >> 3;
+        const int h0 = HPW == 2 ? 0 : (warp >> 2) & 1;  // first column half of this warp
         const int g = lane >> 2, t = lane & 3;
         std::uint8_t* ring = recs + static_cast<std::uint32_t>(ci) * 2u * p.slot_bytes;
-        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 2304u;  // 16 rows x 144 B (padded: no bank conflicts)
+        std::uint8_t* tab = stab + static_cast<std::uint32_t>(warp) * 16u * TS;  // 16 rows x TS B (padded: no bank conflicts)
         const std::uint32_t magic = 0x4B000000u;
         auto tile_of = [&](std::uint32_t u) { return p.Pn == 1u ? u : __umulhi(u, p.pn_magic); };
         auto cell_of = [&](std::uint32_t u, std::uint32_t& q) {
@@ -298,10 +317,10 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
             q = Gq * p.Pn + P;
             return Gq < p.Gn;
         };
-        // record k of this cell row goes to slot k & 1; warp (ci, 0, 0) issues it
-        // once all four warps of the row released the slot's previous record
-        // The record offsets of unit u + 1 are loaded one step ahead into
-        // (nr0, nr1), so the issuing lane never waits on a global load.
+        // record k of this cell row goes to slot k & 1; warp ci (unit 0, half 0)
+        // issues it once all warps of the row released the slot's previous
+        // record.  The record offsets of unit u + 1 are loaded one step ahead
+        // into (nr0, nr1), so the issuing lane never waits on a global load.
         std::uint32_t nr0 = 0, nr1 = 0;
         auto load_off = [&](std::uint32_t u) {
             std::uint32_t q;
@@ -346,7 +365,6 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
         const std::uint32_t mq = static_cast<std::uint32_t>(lane >> 3);
 #pragma unroll 1
         for (std::uint32_t u = u0; u < u1; ++u) {
-            const std::uint32_t it = u - u0;
             std::uint32_t q;
             const bool have = cell_of(u, q);
             if (have && u + 1 < u1) {
@@ -361,79 +379,130 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 TC_WAIT(0, mbar_wait(&rec_full[ci][sl], (k >> 1) & 1u))
                 r0 = slot_r[ci][sl][0];
                 r1 = slot_r[ci][sl][1];
-                // statistics: lane owns (row g + 8rho, block 8hh + 2t + bs) of unit uu;
-                // the two blocks bs = 0, 1 ride in the halves of packed f32x2 math
+                // statistics: lane owns (row g + 8rho, block 8hh + 2t + bs) of unit uu
+                // for this warp's halves hh; the two blocks bs = 0, 1 ride in the
+                // halves of packed f32x2 math
                 std::uint32_t ss, zz;
                 load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
-                const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * hh + 2 * t) * 8);
-                const __half2 sh0 = u32_as_h2(s4.x), zh0 = u32_as_h2(s4.y), sh1 = u32_as_h2(s4.z), zh1 = u32_as_h2(s4.w);
-                const float2 Ss = make_float2(__low2float(sh0), __low2float(sh1));
-                const float2 Zs = make_float2(-__high2float(sh0), -__high2float(sh1));
-                const float2 Sz = make_float2(__low2float(zh0), __low2float(zh1));
-                const float2 Zz = make_float2(-__high2float(zh0), -__high2float(zh1));
 #pragma unroll
-                for (int rho = 0; rho < 2; ++rho) {
-                    const int e0 = 4 * hh + rho, e1 = 4 * hh + 2 + rho;  // eps of bs = 0, 1
-                    const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss, e0 * BS, magic),
-                                                        magic_field_rt<SMASK>(ss, e1 * BS, magic)),
-                                            make_float2(-kMagic, -kMagic));
-                    const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz, e0 * BZ, magic),
-                                                        magic_field_rt<ZMASK>(zz, e1 * BZ, magic)),
-                                            make_float2(-kMagic, -kMagic));
-                    const float2 shat = fmul2(Ss, fadd2(cs, Zs));
-                    const float2 zhat = fmul2(Sz, fadd2(cz, Zz));
-                    // integer part of the zero goes into the codes exactly; the
-                    // fraction (|.| <= 1/2) is the fp16 addend
-                    const float2 zi = make_float2(fminf(fmaxf(rintf(zhat.x), -1000.f), 1000.f),
-                                                  fminf(fmaxf(rintf(zhat.y), -1000.f), 1000.f));
-                    const float2 S0 = fmul2(shat, f0), S1 = fmul2(shat, f1);
-                    const float2 Z0 = fmul2(zi, g0), Z1 = fmul2(zi, g1);
-                    const float2 C = fmul2(fmul2(shat, fadd2(zi, make_float2(-zhat.x, -zhat.y))),
-                                           make_float2(sig_scale, sig_scale));
-                    const int row = g + 8 * rho;
-                    *reinterpret_cast<uint4*>(tab + row * 144 + (2 * t) * 16) =
-                        make_uint4(pack_h2_rn(S0.x, S1.x), pack_h2_rn(Z0.x, Z1.x), pack_h2_rn(C.x, 0.f), 0u);
-                    *reinterpret_cast<uint4*>(tab + row * 144 + (2 * t + 1) * 16) =
-                        make_uint4(pack_h2_rn(S0.y, S1.y), pack_h2_rn(Z0.y, Z1.y), pack_h2_rn(C.y, 0.f), 0u);
+                for (int hi = 0; hi < HPW; ++hi) {
+                    const int hh = h0 + hi;
+                    const uint4 s4 = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 * hh + 2 * t) * 8);
+                    const __half2 sh0 = u32_as_h2(s4.x), zh0 = u32_as_h2(s4.y), sh1 = u32_as_h2(s4.z),
+                                  zh1 = u32_as_h2(s4.w);
+                    const float2 Ss = make_float2(__low2float(sh0), __low2float(sh1));
+                    const float2 Zs = make_float2(-__high2float(sh0), -__high2float(sh1));
+                    const float2 Sz = make_float2(__low2float(zh0), __low2float(zh1));
+                    const float2 Zz = make_float2(-__high2float(zh0), -__high2float(zh1));
+#pragma unroll
+                    for (int rho = 0; rho < 2; ++rho) {
+                        const int e0 = 4 * hh + rho, e1 = 4 * hh + 2 + rho;  // eps of bs = 0, 1
+                        const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss, e0 * BS, magic),
+                                                            magic_field_rt<SMASK>(ss, e1 * BS, magic)),
+                                                make_float2(-kMagic, -kMagic));
+                        const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz, e0 * BZ, magic),
+                                                            magic_field_rt<ZMASK>(zz, e1 * BZ, magic)),
+                                                make_float2(-kMagic, -kMagic));
+                        const float2 shat = fmul2(Ss, fadd2(cs, Zs));
+                        const float2 zhat = fmul2(Sz, fadd2(cz, Zz));
+                        // integer part of the zero goes into the codes exactly; the
+                        // fraction (|.| <= 1/2) is the fp16 addend
+                        const float2 zi = make_float2(fminf(fmaxf(rintf(zhat.x), -1000.f), 1000.f),
+                                                      fminf(fmaxf(rintf(zhat.y), -1000.f), 1000.f));
+                        const float2 S0 = fmul2(shat, f0), S1 = fmul2(shat, f1);
+                        const float2 Z0 = fmul2(zi, g0), Z1 = fmul2(zi, g1);
+                        const float2 C = fmul2(fmul2(shat, fadd2(zi, make_float2(-zhat.x, -zhat.y))),
+                                               make_float2(sig_scale, sig_scale));
+                        const int row = g + 8 * rho;
+                        std::uint8_t* te = tab + row * TS + (8 * hi + 2 * t) * 16;
+                        *reinterpret_cast<uint4*>(te) =
+                            make_uint4(pack_h2_rn(S0.x, S1.x), pack_h2_rn(Z0.x, Z1.x), pack_h2_rn(C.x, 0.f), 0u);
+                        *reinterpret_cast<uint4*>(te + 16) =
+                            make_uint4(pack_h2_rn(S0.y, S1.y), pack_h2_rn(Z0.y, Z1.y), pack_h2_rn(C.y, 0.f), 0u);
+                    }
                 }
                 __syncwarp();
             }
             // this cell's stages 2it (column half 0) and 2it + 1 (half 1)
-            const std::uint32_t ab0 = sb0, ab1 = sb0 + 1u == NA ? 0u : sb0 + 1u;
-            const std::uint32_t ab = hh ? ab1 : ab0, an = (hh && ab1 == 0u) ? sn0 + 1u : sn0;
-            if (an) TC_WAIT(1, mbar_wait(&a_free[ab], (an - 1u) & 1u))
+            const std::uint32_t ab0 = sb0, an0 = sn0;  // buffer, use count
+            const std::uint32_t ab1 = sb0 + 1u == NA ? 0u : sb0 + 1u, an1 = ab1 == 0u ? sn0 + 1u : sn0;
             sb0 += 2u;
             if (sb0 >= NA) {
                 sb0 -= NA;
                 ++sn0;
             }
-            std::uint8_t* A = abuf + ab * A_STAGE;
-            if (have) {
+            auto do_half = [&](auto HH) {
+                constexpr int h_ = decltype(HH)::value;
+                const std::uint32_t ab = h_ ? ab1 : ab0;
+                std::uint8_t* A = abuf + ab * A_STAGE;
+                // only this half's code containers (blocks 8h .. 8h+7), as 8 B loads
+                constexpr int W0 = G::CW * (8 * h_ / G::MPC), W1 = G::CW * ((8 * h_ + 7) / G::MPC + 1);
+                static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a half: 8 B aligned");
+                std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+                for (int i = W0; i < W1; i += 2) {
+                    const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
+                    cw[i] = w2.x;
+                    cw[i + 1] = w2.y;
+                }
+                const int tb = HPW == 2 ? 8 * h_ : 0;  // this half's first table block
                 const std::uint32_t row_sa = smem_u32(A) + (mq >> 1) * KC_A +
                                              (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
-                auto do_half = [&](auto HH) {
-                    constexpr int h_ = decltype(HH)::value;
-                    // only this half's code containers (blocks 8h .. 8h+7), as 8 B loads
-                    constexpr int W0 = G::CW * (8 * h_ / G::MPC), W1 = G::CW * ((8 * h_ + 7) / G::MPC + 1);
-                    static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a half: 8 B aligned");
-                    std::uint32_t cw[G::LANE_WORDS];
+                // table entries one block ahead of their use (LDS latency)
+                uint4 n0 = *reinterpret_cast<const uint4*>(tab + g * TS + tb * 16);
+                uint4 n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * TS + tb * 16);
 #pragma unroll
-                    for (int i = W0; i < W1; i += 2) {
-                        const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
-                        cw[i] = w2.x;
-                        cw[i + 1] = w2.y;
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
+                    const std::uint32_t* w = cw + G::CW * cidx;
+                    const uint4 e0 = n0, e1 = n1;
+                    if (jj < 7) {
+                        n0 = *reinterpret_cast<const uint4*>(tab + g * TS + (tb + jj + 1) * 16);
+                        n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * TS + (tb + jj + 1) * 16);
                     }
-                    // table entries one block ahead of their use (LDS latency)
-                    uint4 n0 = *reinterpret_cast<const uint4*>(tab + g * 144);
-                    uint4 n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144);
+                    std::uint32_t a[4];
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const int mu = 8 * h_ + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
+                    for (int r = 0; r < 4; ++r) {
+                        const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                        const int i = rho * (G::NP / 2) + qq;
+                        const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
+                        const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                        const uint4 e = rho ? e1 : e0;
+                        a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
+                    }
+                    tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
+                }
+            };
+            // HPW = 2: both halves in one pass, block jj of half 0 next to block jj
+            // of half 1 (two independent chains per step for latency hiding)
+            auto do_both = [&]() {
+                std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+                for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                    const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                    cw[4 * i] = w4.x;
+                    cw[4 * i + 1] = w4.y;
+                    cw[4 * i + 2] = w4.z;
+                    cw[4 * i + 3] = w4.w;
+                }
+                const std::uint32_t rs = (mq >> 1) * KC_A + (4u * ci + 2u * uu + (mq & 1u)) * 128u + (lane & 7) * 16u;
+                const std::uint32_t sa[2] = {smem_u32(abuf + ab0 * A_STAGE) + rs, smem_u32(abuf + ab1 * A_STAGE) + rs};
+                uint4 n[2][2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    n[h][0] = *reinterpret_cast<const uint4*>(tab + g * TS + (8 * h) * 16);
+                    n[h][1] = *reinterpret_cast<const uint4*>(tab + (g + 8) * TS + (8 * h) * 16);
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int mu = 8 * h + jj, cidx = mu / G::MPC, mm = mu % G::MPC;
                         const std::uint32_t* w = cw + G::CW * cidx;
-                        const uint4 e0 = n0, e1 = n1;
+                        const uint4 e0 = n[h][0], e1 = n[h][1];
                         if (jj < 7) {
-                            n0 = *reinterpret_cast<const uint4*>(tab + g * 144 + (jj + 1) * 16);
-                            n1 = *reinterpret_cast<const uint4*>(tab + (g + 8) * 144 + (jj + 1) * 16);
+                            n[h][0] = *reinterpret_cast<const uint4*>(tab + g * TS + (8 * h + jj + 1) * 16);
+                            n[h][1] = *reinterpret_cast<const uint4*>(tab + (g + 8) * TS + (8 * h + jj + 1) * 16);
                         }
                         std::uint32_t a[4];
 #pragma unroll
@@ -445,19 +514,29 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                             const uint4 e = rho ? e1 : e0;
                             a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
                         }
-                        tc::stsm_x4(row_sa + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
+                        tc::stsm_x4(sa[h] + 2u * jj * KC_A, a[0], a[1], a[2], a[3]);
                     }
-                };
-                if (hh == 0)
+                }
+            };
+            // this warp's A buffers are free once the MMAs of their previous stages completed
+            if (HPW == 2 || h0 == 0)
+                if (an0) TC_WAIT(1, mbar_wait(&a_free[ab0], (an0 - 1u) & 1u))
+            if (HPW == 2 || h0 == 1)
+                if (an1) TC_WAIT(1, mbar_wait(&a_free[ab1], (an1 - 1u) & 1u))
+            if (have) {
+                if (HPW == 2) {
+                    do_both();
+                } else if (h0 == 0) {
                     do_half(std::integral_constant<int, 0>{});
-                else
+                } else {
                     do_half(std::integral_constant<int, 1>{});
+                }
             }
-            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  The four
+            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  The
             // warps of the cell row own both A buffers of the cell (stages 2it,
             // 2it + 1) between the two row barriers and split the entry list
-            // 128 ways, so no warp searches for its (unit, half) run
-            bar_sync_named(1 + ci, 128);  // the row's stmatrix writes are done
+            // 32 RW ways, so no warp searches for its (unit, half) run
+            bar_sync_named(1 + ci, 32 * RW);  // the row's stmatrix writes are done
             if (have) {
                 const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
                 const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
@@ -467,7 +546,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 const std::uint32_t a_h0 = smem_u32(abuf) + ab0 * A_STAGE + rowb;
                 const std::uint32_t a_h1 = smem_u32(abuf) + ab1 * A_STAGE + rowb;
 #pragma unroll 1
-                for (std::uint32_t i = 32u * static_cast<std::uint32_t>(warp >> 2) + lane; i < cnt; i += 128) {
+                for (std::uint32_t i = 32u * static_cast<std::uint32_t>(warp >> 2) + lane; i < cnt; i += 32u * RW) {
                     const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
                     const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
                     if (row < 32u) {
@@ -481,19 +560,22 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                     }
                 }
             }
-            fence_proxy_async();          // generic-proxy smem writes -> tensor core reads
-            bar_sync_named(1 + ci, 128);  // ... of every warp of the row
-            if (lane == 0) mbar_arrive(&a_full[ab]);
+            fence_proxy_async();               // generic-proxy smem writes -> tensor core reads
+            bar_sync_named(1 + ci, 32 * RW);  // ... of every warp of the row
+            if (lane == 0) {
+                if (HPW == 2 || h0 == 0) mbar_arrive(&a_full[ab0]);
+                if (HPW == 2 || h0 == 1) mbar_arrive(&a_full[ab1]);
+            }
             if (have) {
                 if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);  // this warp is done with the record
                 ++k;
             }
-            // epilogue after the tile's last unit in this range: the four warps
-            // of a cell row split the accumulator's 16-column chunks
+            // epilogue after the tile's last unit in this range: the warps of a
+            // cell row split the accumulator's 16-column chunks
             const std::uint32_t T_ = tile_of(u), P = u - T_ * p.Pn;
             if (u + 1 == u1 || P + 1 == p.Pn) {
                 const std::uint32_t db = tile_i & 1u;
-                const std::uint32_t part4 = static_cast<std::uint32_t>(warp >> 2);  // 0..3
+                const std::uint32_t part = static_cast<std::uint32_t>(warp >> 2);  // 0 .. RW-1
                 TC_WAIT(2, mbar_wait(&d_full[db], (tile_i >> 1) & 1u))
                 tc::fence_after();
                 const std::uint32_t row = 128u * T_ + 32u * ci + lane;
@@ -503,7 +585,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                 const uint2 gm = whole ? make_uint2(0, 0) : __ldg(reinterpret_cast<const uint2*>(p.gmap) + T_);
                 const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == tile_of(u0) ? 0u : 1u));
 #pragma unroll 1
-                for (std::uint32_t c0 = 16u * part4; c0 < N; c0 += 64) {
+                for (std::uint32_t c0 = 16u * part; c0 < N; c0 += 16u * RW) {
                     float vv[16];
                     tc::ld16(ta + c0, vv);
 #pragma unroll
@@ -531,7 +613,7 @@ __global__ void __launch_bounds__(544, 1) gemm_tc(const TcParams p) {
                     __syncwarp();
                     if (prev == gm.y - 1u) {
 #pragma unroll 1
-                        for (std::uint32_t c0 = 16u * part4; c0 < N; c0 += 64)
+                        for (std::uint32_t c0 = 16u * part; c0 < N; c0 += 16u * RW)
                             for (std::uint32_t bcol = c0; bcol < c0 + 16u && bcol < p.B; ++bcol) {
                                 float sum = 0.f;
                                 for (std::uint32_t j = 0; j < gm.y; ++j)
