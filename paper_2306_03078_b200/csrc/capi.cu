@@ -1202,7 +1202,12 @@ int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr
         p.row_base = rb;
         p.rank = static_cast<std::uint32_t>(g->rank);
         p.done_ctr = reinterpret_cast<std::uint32_t*>(g->base + 68);
-        dispatch_cta(p, L, !f16, static_cast<cudaStream_t>(cuda_stream));
+        const auto& c = L->cta[f16 ? 0 : 1];
+        ck(spqr_dev::launch_cta_gather(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits), !f16,
+                                       c.shared_x, p, c.grid, c.smem, kNC, kSmemLimit,
+                                       static_cast<cudaStream_t>(cuda_stream)),
+           "launch gemv_cta (fused all-gather)");
+        ++g_launches;
     });
 }
 

@@ -119,7 +119,7 @@ __device__ __forceinline__ std::uint32_t deq2(std::uint32_t a, std::uint32_t z, 
 // x tiles for the tensor cores: stage (P, h) holds columns 256P + 128h + k,
 // k < 128, of every batch column n < N (zero for n >= B or beyond the layer)
 // as fp16, K-major core matrices: byte (k/8)*16N + (n/8)*128 + (n%8)*16 + (k%8)*2.
-__global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int x_f16, std::uint32_t n,
+static __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int x_f16, std::uint32_t n,
                                                 std::uint32_t B, std::uint32_t N, std::uint32_t Pn,
                                                 const std::uint32_t* __restrict__ order, std::uint8_t* __restrict__ out) {
     pdl_launch();

@@ -215,7 +215,7 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
 
 // SHX: the CTA prepares all Pn x panels once (shared memory) instead of each
 // warp preparing its cell's panel -- for layers whose panels fit.
-template <int BW, int BS, int BZ, bool XLO, int NC, bool SHX>
+template <int BW, int BS, int BZ, bool XLO, int NC, bool SHX, bool GATHER = false>
 __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     auto put_y = [&](std::uint32_t row, float v) {
         p.y[row] = v;
-        for (std::uint32_t j = 0; j < p.npeer; ++j) p.ypeer[j][p.row_base + row] = v;
+        if constexpr (GATHER)
+            for (std::uint32_t j = 0; j < p.npeer; ++j) p.ypeer[j][p.row_base + row] = v;
     };
 #ifdef SPQR_TIMELINE
     const std::uint32_t wk = blockIdx.x * 16u + static_cast<std::uint32_t>(warp);
@@ -777,12 +778,12 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         g_timeline[8 * wk + 7] = 1000u + smid;
     }
 #endif
-    if (p.nflag) {  // fused all-gather: signal the round to every rank
-        __syncthreads();  // every y store of this CTA precedes thread 0's release
+    if constexpr (GATHER) {  // fused all-gather: signal the round to every rank
+        __syncthreads();        // every y store of this CTA precedes thread 0's release
         if (threadIdx.x == 0) {
             __threadfence_system();
             const std::uint32_t prev = atomicAdd(p.done_ctr, 1u);
-            if (prev == gridDim.x - 1u) {  // the grid's last CTA: all stores are fenced
+            if (prev == gridDim.x - 1u) {  // the grid's last CTA: every CTA's stores are fenced
                 *p.done_ctr = 0u;
                 __threadfence_system();
                 for (std::uint32_t j = 0; j < p.nflag; ++j)
@@ -792,10 +793,15 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     }
 }
 
+// The GATHER = true instantiations live in gather.cu (compiled in parallel
+// with capi.cu); the single-GPU kernels carry none of the gather code.
+cudaError_t launch_cta_gather(int bw, int bsz, bool xlo, bool shx, const CtaParams& p, std::uint32_t grid,
+                              std::uint32_t smem, int nc, std::uint32_t smem_limit, cudaStream_t st);
+
 // Fused all-gather, consumer side: one thread per rank waits until that rank's
 // counter reached this round (counters only grow; the round lives on the
 // device, so the launch is CUDA-graph replayable), then the round advances.
-__global__ void __launch_bounds__(32) gather_wait(const std::uint32_t* flags, std::uint32_t* round,
+static __global__ void __launch_bounds__(32) gather_wait(const std::uint32_t* flags, std::uint32_t* round,
                                                   std::uint32_t world) {
     const std::uint32_t r = *round + 1u;
     if (threadIdx.x < world) {

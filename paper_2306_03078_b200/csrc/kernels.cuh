@@ -290,7 +290,7 @@ struct RawGeom {
 };
 
 // W[r, order[c]] = s * (q - z), binary32 (dequant_value, quantizer.hpp:60-62)
-__global__ void dequant_raw(const RawGeom geo, float* __restrict__ w) {
+static __global__ void dequant_raw(const RawGeom geo, float* __restrict__ w) {
     const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
     for (std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -311,7 +311,7 @@ __global__ void dequant_raw(const RawGeom geo, float* __restrict__ w) {
 }
 
 // outlier corrections: a separate binary32 add (solver.hpp:360)
-__global__ void outliers_raw(const RawGeom geo, float* __restrict__ w) {
+static __global__ void outliers_raw(const RawGeom geo, float* __restrict__ w) {
     const std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= geo.rows) return;
     const std::uint32_t i0 = geo.u32(geo.csr_off + 4ull * r), i1 = geo.u32(geo.csr_off + 4ull * r + 4);
@@ -325,7 +325,7 @@ __global__ void outliers_raw(const RawGeom geo, float* __restrict__ w) {
 }
 
 // xp[b][k] = x[b][order[k]] in fp32 (kernel.hpp:93-98)
-__global__ void xprep_raw(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t batch,
+static __global__ void xprep_raw(const void* __restrict__ x, int x_f16, std::uint32_t n, std::uint32_t batch,
                           const std::uint32_t* __restrict__ order, float* __restrict__ xp) {
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<std::uint64_t>(n) * batch) return;
@@ -336,7 +336,7 @@ __global__ void xprep_raw(const void* __restrict__ x, int x_f16, std::uint32_t n
 }
 
 // generic matvec: one warp per row, lanes over column blocks, fp32 accumulate
-__global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp, float* __restrict__ y) {
+static __global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp, float* __restrict__ y) {
     const std::uint32_t warps = blockDim.x >> 5;
     const std::uint32_t r = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -364,7 +364,7 @@ __global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp, float*
 
 // ========================================================= dense baseline ==
 // y = W16 * x16, fp32 accumulate; one warp per row, 128-bit loads.
-__global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __restrict__ x, float* __restrict__ y,
+static __global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __restrict__ x, float* __restrict__ y,
                                std::uint32_t rows, std::uint32_t cols) {
     const std::uint32_t warps = blockDim.x >> 5;
     const int lane = threadIdx.x & 31;
