@@ -489,8 +489,8 @@ def run_ours(args) -> None:
 
     def e2e_step():
         for i, gp in enumerate(groups):
-            if world == 1:
-                ys_h[i].numpy()[:] = gp["L"].matvec_host(gp["x32"].numpy())
+            if world == 1:  # x and y pinned: the call's copies are plain DMA
+                gp["L"].matvec_host(gp["x32"].numpy(), out=ys_h[i].numpy())
             else:
                 xd32[i].copy_(gp["x32"], non_blocking=True)
                 if fused:

@@ -384,11 +384,15 @@ class Layer:
         _check(lib().spqr_bench_layer(self._h, repeats, out.ctypes.data_as(C.c_void_p)))
         return out
 
-    def matvec_host(self, x: np.ndarray) -> np.ndarray:
-        """Drop-in matvec(t, x) with host buffers (kernel.hpp:126)."""
+    def matvec_host(self, x: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Drop-in matvec(t, x) with host buffers (kernel.hpp:126).  Page-locked
+        x / out (e.g. numpy views of pinned torch tensors) are copied directly;
+        pageable ones go through the layer's pinned staging."""
         x = np.ascontiguousarray(x, dtype=np.float32)
         batch = x.size // self.cols
-        y = np.empty(batch * self.rows, np.float32)
+        y = np.empty(batch * self.rows, np.float32) if out is None else out
+        if y.dtype != np.float32 or not y.flags.c_contiguous or y.size != batch * self.rows:
+            raise ValueError("out must be a contiguous float32 array of batch * rows elements")
         _check(lib().spqr_matvec_host(self._h, x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), batch))
         return y.reshape(batch, self.rows) if batch > 1 else y
 

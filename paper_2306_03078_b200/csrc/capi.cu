@@ -138,8 +138,22 @@ struct spqr_layer {
     mutable float* d_xh = nullptr;  // host-API staging
     mutable float* d_yh = nullptr;
     mutable std::size_t xh_cap = 0, yh_cap = 0;
+    // spqr_matvec_host: own non-blocking stream, pinned staging (used when the
+    // caller's buffers are pageable), and the [H2D x, kernels, D2H y] sequence
+    // as one CUDA graph keyed by (batch, host source, host destination)
+    mutable cudaStream_t hst = nullptr;
+    mutable float* h_x = nullptr;
+    mutable float* h_y = nullptr;
+    mutable cudaGraphExec_t hgraph = nullptr;
+    mutable int hg_batch = 0, hg_launches = 0;
+    mutable const void* hg_src = nullptr;
+    mutable void* hg_dst = nullptr;
 
     ~spqr_layer() {
+        if (hgraph) cudaGraphExecDestroy(hgraph);
+        if (hst) cudaStreamDestroy(hst);
+        if (h_x) cudaFreeHost(h_x);
+        if (h_y) cudaFreeHost(h_y);
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
                         static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start[0]),
                         static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
@@ -1251,21 +1265,73 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
         ensure_own_ws(L, batch);
         const std::size_t nx = static_cast<std::size_t>(L->info.cols) * batch;
         const std::size_t ny = static_cast<std::size_t>(L->info.rows) * batch;
-        if (L->xh_cap < nx) {
-            if (L->d_xh) cudaFree(L->d_xh);
-            L->d_xh = dalloc<float>(nx);
-            L->xh_cap = nx;
+        if (L->xh_cap < nx || L->yh_cap < ny) {  // device and pinned staging, grown together
+            if (L->hgraph) cudaGraphExecDestroy(L->hgraph);
+            L->hgraph = nullptr;
+            for (float** d : {&L->d_xh, &L->d_yh})
+                if (*d) cudaFree(*d);
+            for (float** h : {&L->h_x, &L->h_y})
+                if (*h) cudaFreeHost(*h);
+            L->d_xh = L->d_yh = L->h_x = L->h_y = nullptr;
+            L->xh_cap = std::max(L->xh_cap, nx);
+            L->yh_cap = std::max(L->yh_cap, ny);
+            L->d_xh = dalloc<float>(L->xh_cap);
+            L->d_yh = dalloc<float>(L->yh_cap);
+            ck(cudaHostAlloc(&L->h_x, 4 * L->xh_cap, cudaHostAllocDefault), "cudaHostAlloc(x staging)");
+            ck(cudaHostAlloc(&L->h_y, 4 * L->yh_cap, cudaHostAllocDefault), "cudaHostAlloc(y staging)");
         }
-        if (L->yh_cap < ny) {
-            if (L->d_yh) cudaFree(L->d_yh);
-            L->d_yh = dalloc<float>(ny);
-            L->yh_cap = ny;
+        if (!L->hst) ck(cudaStreamCreateWithFlags(&L->hst, cudaStreamNonBlocking), "stream (host API)");
+        // caller buffers that are page-locked are copied directly (true async
+        // DMA); pageable ones go through the pinned staging
+        auto pinned = [](const void* p) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return a.type == cudaMemoryTypeHost;
+        };
+        const bool px = pinned(x_host), py = pinned(y_host);
+        const void* src = px ? static_cast<const void*>(x_host) : L->h_x;
+        void* dst = py ? static_cast<void*>(y_host) : L->h_y;
+        if (!px) std::memcpy(L->h_x, x_host, 4 * nx);
+        if (!L->hgraph || L->hg_batch != batch || L->hg_src != src || L->hg_dst != dst) {
+            if (L->hgraph) cudaGraphExecDestroy(L->hgraph);
+            L->hgraph = nullptr;
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(L->hst, cudaStreamCaptureModeThreadLocal), "capture (host API)");
+            try {
+                // x: a copy kernel reads the page-locked host vector over the
+                // bus (UVA); y: the kernels store straight into page-locked
+                // host memory (posted writes, flushed by kernel completion)
+                if ((nx & 3u) == 0 && (reinterpret_cast<std::uintptr_t>(src) & 15u) == 0) {
+                    const std::uint32_t n16 = static_cast<std::uint32_t>(nx / 4);
+                    spqr_dev::copy_in<<<std::min<std::uint32_t>((n16 + 255) / 256, 64), 256, 0, L->hst>>>(
+                        static_cast<const uint4*>(src), reinterpret_cast<uint4*>(L->d_xh), n16);
+                    ck(cudaGetLastError(), "launch copy_in");
+                    ++g_launches;
+                } else {
+                    ck(cudaMemcpyAsync(L->d_xh, src, 4 * nx, cudaMemcpyHostToDevice, L->hst), "H2D x");
+                }
+                run_matvec(L, L->d_xh, SPQR_F32, static_cast<float*>(dst), batch, L->d_ws, L->ws_bytes, L->hst);
+            } catch (...) {
+                cudaStreamEndCapture(L->hst, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ck(cudaStreamEndCapture(L->hst, &g), "end capture (host API)");
+            const cudaError_t e = cudaGraphInstantiate(&L->hgraph, g, 0);
+            cudaGraphDestroy(g);
+            ck(e, "instantiate (host API)");
+            L->hg_batch = batch;
+            L->hg_src = src;
+            L->hg_dst = dst;
+            L->hg_launches = g_launches;
         }
-        cudaStream_t st = nullptr;
-        ck(cudaMemcpyAsync(L->d_xh, x_host, 4 * nx, cudaMemcpyHostToDevice, st), "H2D x");
-        run_matvec(L, L->d_xh, SPQR_F32, L->d_yh, batch, L->d_ws, L->ws_bytes, st);
-        ck(cudaMemcpyAsync(y_host, L->d_yh, 4 * ny, cudaMemcpyDeviceToHost, st), "D2H y");
-        ck(cudaStreamSynchronize(st), "sync");
+        ck(cudaGraphLaunch(L->hgraph, L->hst), "graph launch (host API)");
+        ck(cudaStreamSynchronize(L->hst), "sync");
+        g_launches = L->hg_launches;
+        if (!py) std::memcpy(y_host, L->h_y, 4 * ny);
     });
 }
 

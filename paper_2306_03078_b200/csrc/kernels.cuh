@@ -363,6 +363,15 @@ static __global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp,
 }
 
 // ========================================================= dense baseline ==
+// spqr_matvec_host: x from page-locked host memory (UVA-mapped) into the
+// device, 16 B per thread -- a kernel node is cheaper than a copy-engine node
+// for the 16-88 KB vectors of a decode step
+static __global__ void __launch_bounds__(256) copy_in(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                      std::uint32_t n16) {
+    for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // y = W16 * x16, fp32 accumulate; one warp per row, 128-bit loads.
 static __global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __restrict__ x, float* __restrict__ y,
                                std::uint32_t rows, std::uint32_t cols) {

@@ -140,6 +140,33 @@ def test_batch_and_host_api(cuda, oracle_c):
             assert relative_l2(Yh[b], ref) < tol
 
 
+def test_host_api_graph_reuse(cuda, oracle_c):
+    """spqr_matvec_host replays one captured [H2D, kernels, D2H] graph: new x
+    every call, pageable and page-locked buffers, batch changes re-capture."""
+    s = synth.random_stream(512, 1024, seed=7)
+    t = oracle_c.decode(s)
+    L = P.Layer(s)
+    rng = np.random.default_rng(4)
+    xp = cuda.empty(1024, dtype=cuda.float32).pin_memory()
+    yp = cuda.empty(512, dtype=cuda.float32).pin_memory()
+    for i in range(6):
+        x = rng.standard_normal(1024).astype(np.float32)
+        ref = t.matvec(x)
+        if i % 2:
+            xp.numpy()[:] = x
+            y = L.matvec_host(xp.numpy(), out=yp.numpy()).copy()
+        else:
+            y = L.matvec_host(x)
+        assert relative_l2(y, ref) < 1e-5, i
+        assert P.last_launch_count() >= 1
+    X = rng.standard_normal((2, 1024)).astype(np.float32)  # batch 2: a new graph
+    Y = L.matvec_host(X)
+    for b in range(2):
+        assert relative_l2(Y[b], t.matvec(X[b])) < 1e-5
+    x = rng.standard_normal(1024).astype(np.float32)  # back to batch 1
+    assert relative_l2(L.matvec_host(x), t.matvec(x)) < 1e-5
+
+
 def test_deterministic_and_workspace(cuda):
     s = synth.random_stream(1024, 4096, seed=3)
     L = P.Layer(s)
