@@ -520,7 +520,7 @@ def run_ours(args) -> None:
            "h2d_bytes_per_step": sum(4 * gp["n"] for gp in groups),
            "d2h_bytes_per_step": sum(4 * gp["m"] for gp in groups),
            "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3),
-           "path": "spqr_matvec_host (C ABI: H2D fp32 x, fused kernels, D2H y, sync) per group"
+           "path": "spqr_matvec_host (C ABI, page-locked host x/y: copy kernel reads x, fused kernel stores y to host, sync) per group"
                    if world == 1 else "H2D x, spqr_matvec_gather + spqr_gather_wait (fused all-gather), D2H y per group"}
 
     cpu = None
