@@ -75,6 +75,23 @@ struct CtaParams {
     std::uint32_t npeer, nflag, row_base, rank;
 };
 
+// The neighbouring range's published partial row sum: the CTAs of a launch
+// are co-resident (grid <= SMs, one CTA per SM), so it arrives; if it does not
+// within 10 s (e.g. SMs withheld by an MPS partition), fail the launch rather
+// than hold the GPU.
+static __device__ __noinline__ unsigned long long spin_published(const unsigned long long* xw) {
+    unsigned long long w, t0, t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    for (std::uint32_t it = 1;; ++it) {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
+        if ((w >> 32) != 0ull) return w;
+        if ((it & 4095u) == 0u) {
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000ull) __trap();
+        }
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -748,9 +765,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(xw), "l"(w) : "memory");
                 } else {                   // we hold its first cells: add the published rest
                     unsigned long long w;
-                    do {
-                        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
-                    } while ((w >> 32) == 0ull);
+                    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
+                    if ((w >> 32) == 0ull) w = spin_published(xw);
                     if (row < p.m) put_y(row, sum + __uint_as_float(static_cast<std::uint32_t>(w)));
                     *xw = 0ull;
                 }
