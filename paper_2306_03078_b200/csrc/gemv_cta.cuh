@@ -733,10 +733,14 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     __syncwarp();
                 }
             };
+#ifdef SPQR_SPLIT_OFF
+            compute(std::integral_constant<int, 2>{});  // whole cells only: no half-ticket code in the kernel
+#else
             if (uo < 0)
                 compute(std::integral_constant<int, 2>{});
             else
                 compute(std::integral_constant<int, 1>{});
+#endif
 
             // count the ticket against its pair (a split cell counts twice); the
             // warp that completes the pair reduces it (row = lane, cells in order)
