@@ -139,6 +139,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(busy)}
 
 
+def host_cpu() -> dict:
+    """The box's host CPU (state the cores the CPU numbers ran on)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+
+
 def load_peaks() -> tuple[float, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -167,7 +181,7 @@ def cpu_reference_sample(streams) -> dict:
         del t
     return {"value": total_bytes / total_t / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
             "sample": "one pass over the 7 layers of the block, reference matvec(t, x, plan), 1 thread",
-            "seconds": round(total_t, 3)}
+            "seconds": round(total_t, 3), "host": host_cpu()}
 
 
 # ------------------------------------------------------------ reference arm --
@@ -220,7 +234,7 @@ def run_reference(args) -> None:
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
                          "sample": f"{sample}; reference matvec(t, x, plan) on {threads} row bands, "
-                                   f"{threads} threads (oracle/_ref, unmodified headers)"},
+                                   f"{threads} threads (oracle/_ref, unmodified headers)", "host": host_cpu()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -456,6 +470,7 @@ def run_ours(args) -> None:
                          else "band gemv_cta + NCCL all-gather (fused path unavailable)",
                  "kernel_us_per_step": round(1e3 * float(t[0]), 3),
                  "step_us": round(1e3 * ms_per_step, 3),
+                 "gather_us_per_step": round(1e3 * ms_per_step - 1e3 * float(t[0]), 3),
                  "nccl_baseline": {"allgather_us_per_step": round(1e3 * float(t[1]), 3),
                                    "step_us": round(1e3 * float(t[2]), 3),
                                    "backend": dist.get_backend()},
