@@ -1,4 +1,4 @@
-# round-1 closing measurement pass: smoke, GPU tests, bench line, launch list,
+# closing measurement pass of a round (run under gpurun from the repo root): smoke, GPU tests,
 # DRAM traffic per launch, full ncu captures of the batch-1 and batched kernels,
 # batch and config sweeps
 set -x
