@@ -1,6 +1,6 @@
 # closing measurement pass of a round (run under gpurun from the repo root): smoke, GPU tests,
-# DRAM traffic per launch, full ncu captures of the batch-1 and batched kernels,
-# batch and config sweeps
+# bench both arms, launch list, DRAM traffic per launch, full ncu captures of the batch-1 and
+# batched kernels, batch and config sweeps
 set -x
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 python -m pytest tests -q -m gpu --tb=short 2>&1 | tail -4
