@@ -59,6 +59,7 @@ def workload_config(n_gpus: int) -> dict:
         "batch": 1, "x_dtype": "f16", "layers": len(LAYERS),
         "l2": "weights 400 MB per step > 126 MB L2: inputs larger than L2, no flush",
         "launches": "4 per step: q/k/v stacked (fused QKV), o, gate/up stacked, down; x shared within a group",
+        "graph": "10 steps per CUDA graph (PDL between all launches inside), replayed; remainder by a 1-step graph",
         "parallelism": f"row-shard x{n_gpus} + all-gather of y fused into the band kernels (NCCL timed as baseline)"
         if n_gpus > 1 else "single GPU",
     }
@@ -337,20 +338,31 @@ def run_ours(args) -> None:
         for _ in range(3):
             step()
     torch.cuda.synchronize()
-    graph = None
+    # CUDA graphs of SPG steps (a serving stack captures a whole decode pass --
+    # every block's launches back to back -- in one graph, so block boundaries
+    # inside it overlap through PDL like the launches within a block) and of
+    # one step for the remainder; K steps = K // SPG long replays + K % SPG short
+    SPG = 10
+    graph = graph1 = None
     if world == 1 or fused or not share:  # gloo collectives cannot be captured
-        graph = torch.cuda.CUDAGraph()
+        graph, graph1 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
+            for _ in range(SPG):
+                step()
+        with torch.cuda.graph(graph1, stream=stream):
             step()
         torch.cuda.synchronize()
 
     def replay(n):
         with torch.cuda.stream(stream):
-            for _ in range(n):
-                if graph is None:
+            if graph is None:
+                for _ in range(n):
                     step()
-                else:
-                    graph.replay()
+                return
+            for _ in range(n // SPG):
+                graph.replay()
+            for _ in range(n % SPG):
+                graph1.replay()
 
     # clocks: sample through a ~1.5 s soak plus the timed region
     with ClockSampler(dev.index) as clk:
@@ -392,25 +404,29 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
 
     # ---- dominant kernel alone (no all-gather), per group and over the block ----
-    def graph_time(fn, reps):
+    def graph_time(fn, reps, inner=SPG):
+        """ms per fn(): `inner` calls captured back to back in one graph (as
+        the step), the graph replayed ceil(reps / inner) times."""
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
             fn()
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=stream):
-            fn()
+            for _ in range(inner):
+                fn()
         with torch.cuda.stream(stream):
-            for _ in range(3):
+            for _ in range(2):
                 g.replay()
         torch.cuda.synchronize()
+        nrep = max(1, -(-reps // inner))
         a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a_.record(stream)
         with torch.cuda.stream(stream):
-            for _ in range(reps):
+            for _ in range(nrep):
                 g.replay()
         b_.record(stream)
         torch.cuda.synchronize()
-        return a_.elapsed_time(b_) / reps
+        return a_.elapsed_time(b_) / (nrep * inner)
 
     kms = graph_time(lambda: [gp["L"].matvec(gp["x"], gp["y"], stream=stream) for gp in groups],
                      max(20, args.steps // 5))
