@@ -223,6 +223,33 @@ def test_llama7b_shapes_vs_oracle(cuda, oracle_c, shape):
     assert np.array_equal(w.cpu().numpy().view(np.uint32), t.dequantize_full().view(np.uint32))
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("shape", [(8192, 8192), (22016, 8192), (8192, 22016)])
+def test_llama65b_shapes_vs_oracle(cuda, oracle_c, shape):
+    """BASELINE configs[2]/[3] at full size: the fast kernel (f16 and f32 x)
+    against the oracle, plus the size-independent properties -- linearity in x
+    and run-to-run bit equality."""
+    s = synth.random_stream(*shape, seed=3)
+    L = P.Layer(s)
+    t = oracle_c.decode(s)
+    rng = np.random.default_rng(5)
+    x1 = rng.standard_normal(shape[1]).astype(np.float32)
+    x2 = rng.standard_normal(shape[1]).astype(np.float32)
+    y = cuda.empty(shape[0], device="cuda")
+    L.matvec(_dev(cuda, x1), y)
+    y1 = y.cpu().numpy()
+    assert relative_l2(y1, t.matvec(x1)) < 1e-5  # fp32 x: hi/lo split, fp32 accumulation
+    xh = x1.astype(np.float16)
+    L.matvec(_dev(cuda, xh), y)
+    assert relative_l2(y.cpu().numpy(), t.matvec(xh.astype(np.float32))) < TOL
+    L.matvec(_dev(cuda, x2), y)
+    y2 = y.cpu().numpy()
+    L.matvec(_dev(cuda, x1 + x2), y)
+    assert relative_l2(y.cpu().numpy(), y1 + y2) < 1e-5  # linearity
+    L.matvec(_dev(cuda, x1), y)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), y1.view(np.uint32))  # deterministic
+
+
 def test_dense_gemv_f16(cuda):
     W = cuda.randn(300, 1024, device="cuda", dtype=cuda.float16)
     x = cuda.randn(1024, device="cuda", dtype=cuda.float16)
