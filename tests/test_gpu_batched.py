@@ -71,3 +71,31 @@ def test_batched_deterministic(cuda):
     L.matvec(X, Y2, batch=20)
     assert cuda.equal(Y1, Y2)
     assert P.last_launch_count() == 2  # xprep_tc + gemm_tc
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("batch", [16, 64])
+def test_batched_full_size_down_proj(cuda, oracle_c, batch):
+    """BASELINE configs[3] shape (8192x22016, random-stream statistics) at full
+    size: every 8th batch column against the oracle, the rest through
+    linearity (column b of X1 + X2 equals column b of Y1 + Y2)."""
+    m, n = 8192, 22016
+    s = synth.random_stream(m, n, seed=11)
+    L = P.Layer(s)
+    t = oracle_c.decode(s)
+    rng = np.random.default_rng(batch)
+    # multiples of 1/64 below 8 in magnitude: X1, X2 and X1 + X2 are exact in
+    # binary16 (the path's x precision), so linearity holds to fp32 rounding
+    X1 = np.clip(np.round(rng.standard_normal((batch, n)) * 64) / 64, -7.9, 7.9).astype(np.float16)
+    X2 = np.clip(np.round(rng.standard_normal((batch, n)) * 64) / 64, -7.9, 7.9).astype(np.float16)
+    Y = cuda.empty((batch, m), device="cuda")
+    L.matvec(_dev(cuda, X1), Y, batch=batch)
+    y1 = Y.cpu().numpy()
+    for b in range(0, batch, 8):
+        assert relative_l2(y1[b], t.matvec(X1[b].astype(np.float32))) <= TOL, b
+    L.matvec(_dev(cuda, X2), Y, batch=batch)
+    y2 = Y.cpu().numpy()
+    X12 = (X1.astype(np.float32) + X2.astype(np.float32)).astype(np.float16)
+    assert np.array_equal(X12.astype(np.float32), X1.astype(np.float32) + X2.astype(np.float32))
+    L.matvec(_dev(cuda, X12), Y, batch=batch)
+    assert relative_l2(Y.cpu().numpy().ravel(), (y1 + y2).ravel()) <= 1e-5
