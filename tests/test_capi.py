@@ -82,3 +82,15 @@ def test_cpp_dropin_kernel_api(tmp_path, golden, cuda):
         y = np.fromfile(tmp_path / "y.bin", np.float32)
         ref = golden[f"{name}/y"][0]
         assert float(np.linalg.norm(y - ref) / np.linalg.norm(ref)) < 1e-5
+
+
+def test_gather_api_validates_without_gpu():
+    """spqr_gather_create rejects bad world/rank before touching the device
+    (the fused all-gather's host-side contract)."""
+    import pytest as _pytest
+
+    for world, rank in ((0, 0), (9, 0), (2, 2), (2, -1)):
+        with _pytest.raises(P.SpqrError) as e:
+            P.Gather(0, 1024, world, rank)
+        assert e.value.errc == "config_invalid"
+        assert "gather" in str(e.value)
