@@ -13,23 +13,28 @@
 //
 // Tiles: 128 rows (four 32-row cell rows) x 128 columns (half a 256-column
 // panel) per MMA stage, N = batch padded to 16 (<= 64 per launch).
-//   * warps 0-3 ("dequant warps"): warp i streams the cells of row-group pair
-//     4T+i (cp.async.bulk, two record slots, one cell of lookahead), decodes
-//     the bilevel statistics into a per-(row, block) fp16 table
-//     {s 2^(24-p-sigma) for both column halves, -s z 2^-sigma}, turns every
-//     A-fragment register of codes (the batch-1 layout: codes as binary16
-//     subnormals code*2^(p-24), ONE LOP3) into weights with ONE HFMA2, writes
-//     them with stmatrix into the UMMA K-major core-matrix layout, adds the
-//     cell's outliers in place, and after the tile's last stage reads the
-//     accumulator back (tcgen05.ld) and writes y;
-//   * warp 4 ("control"): allocates TMEM (two accumulators of N columns),
-//     copies each stage's x tile (prepared by xprep_tc in the same layout),
-//     issues the 8 tcgen05.mma of a stage and commits them to mbarriers.
-// A and x tiles are double-buffered; accumulators are double-buffered across
-// 128-row tiles so the epilogue of one tile overlaps the next tile's MMAs.
-// Split-K across CTAs: each CTA owns a contiguous, byte-balanced range of
-// (tile, panel) units; partial tiles go through partial slots and a per-warp
-// acq_rel counter, the last contributor adding them in range order.
+//   * 16 dequant warps (warp = 8 unit + 4 half + cell row; HPW = 2 folds the
+//     two column halves into one warp): the first warp of each cell row streams
+//     that row's cells (cp.async.bulk, two record slots, one cell of
+//     lookahead, record offsets loaded a step ahead); each warp decodes the
+//     bilevel statistics of its (unit, half) into a per-(row, block) fp16 table
+//     {s 2^(24-p-sigma) for both k halves, round(z) 2^(p-24), -s (z - round z)
+//     2^-sigma}, turns every A-fragment register of codes (the batch-1 layout:
+//     codes as binary16 subnormals code*2^(p-24), ONE LOP3) into weights with
+//     one exact HSUB2 and ONE HFMA2, and writes them with stmatrix into the
+//     UMMA K-major core-matrix layout; the four warps of a cell row then add the
+//     cell's outliers in place between two named barriers; after a tile's last
+//     stage the warps whose TMEM lane quarter holds the rows read the
+//     accumulator back (tcgen05.ld) and write y;
+//   * the control warp: allocates TMEM (two accumulators of N columns), copies
+//     each stage's x tile (prepared by xprep_tc in the same layout), issues the
+//     8 tcgen05.mma of a stage and commits them to mbarriers.
+// A stages are 3- or 4-buffered (by shared memory), x tiles 3-buffered;
+// accumulators are double-buffered across 128-row tiles so the epilogue of one
+// tile overlaps the next tile's MMAs.  Split-K across CTAs: each CTA owns a
+// contiguous, byte-balanced range of (tile, panel) units; partial tiles go
+// through partial slots and a per-warp acq_rel counter, the last contributor
+// adding them in range order.
 
 struct TcParams {
     const std::uint8_t* cells;        // cell records (batch-1 layout)
