@@ -19,10 +19,14 @@
 //    computes the current one.  Issue is spread over all warps on purpose: a
 //    single producer thread caps at ~240 cycles per bulk copy (~4.8 TB/s for
 //    4 KB records, tools/tma_bench.cu).  The first records are issued before
-//    the preceding kernel has finished (PDL: weights do not depend on it);
-//  * each consumer prepares its cell's x panel itself (x gather through the
-//    permutation, per-block power-of-two scale, 2^-p column pre-scale, block
-//    sums) -- no separate x-preparation kernel, no x traffic through the ring;
+//    the preceding kernel has finished (PDL: weights do not depend on it), from
+//    offsets the plan precomputed per CTA; the first range's bounds arrive by
+//    value in the launch parameters, so no global load precedes the PDL wait;
+//  * x panels (x gather through the permutation, per-block power-of-two
+//    scale, 2^-p column pre-scale, block sums) are built after the PDL wait:
+//    once per CTA into shared memory when all Pn panels fit (SHX, per-panel
+//    ready flags, no CTA barrier), else by each warp for its cell -- no
+//    separate x-preparation kernel, no x traffic through the ring;
 //  * per cell the warp writes 32 row sums (MMA part + outliers) to a per-CTA
 //    array and counts the cell against its row-group pair; the warp that
 //    completes a pair adds its cells' row sums in cell order and writes y --
@@ -31,7 +35,11 @@
 //    through one 64-bit {value, flag} word per row: the range that starts
 //    inside the pair finishes it first and publishes; the range that ends
 //    inside it adds the published value after its own and resets the word.
-//    No atomics on global memory, no fences, no end-of-kernel barrier.
+//    No atomics on global memory, no fences, no end-of-kernel barrier (the
+//    wait is bounded: a launch whose CTAs are not co-resident traps).
+//  * GATHER = true (row-sharded decode, gather.cu): every y row is also stored
+//    into the other ranks' full-y buffers and the grid's last CTA bumps this
+//    rank's round counter on every rank; gather_wait consumes it.
 // Every reduction order is fixed by the partition, not by the schedule, so y
 // is bitwise reproducible run to run.
 
