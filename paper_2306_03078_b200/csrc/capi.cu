@@ -651,8 +651,6 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     const std::uint32_t cellb = t.cell_bytes;
     const std::uint32_t panel = spqr_tiled::panel_bytes(xi == 1);
     const std::uint32_t budget = kSmemLimit - kCtaStaticMax;
-    c.shared_x = t.Pn * panel <= 40u * 1024u;
-    const std::uint32_t pan_bytes = c.shared_x ? t.Pn * panel : kNC * panel;
     constexpr std::uint32_t kPartMax = 48u * 1024u;  // row-sum array cap
     const std::uint32_t S = static_cast<std::uint32_t>(sms);
     std::vector<double> pre(Q + 1, 0.0);
@@ -697,6 +695,16 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     const std::uint32_t part_bytes = (c.part_cap * 128u + 127u) & ~127u;
     const std::uint32_t off_bytes = ((c.part_cap + 9u) * 4u + 127u) & ~127u;  // 16-B aligned superset
     const std::uint32_t gd_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
+    // x panels once per CTA (all Pn in shared memory) whenever the two record
+    // slots per warp still hold a cell plus ~256 outliers next to them; else
+    // each warp builds its cell's panel (fp32 x panels are twice as large:
+    // 8192-column layers were per-warp under the old fixed 40 KB rule)
+    const std::uint32_t fixed = part_bytes + off_bytes + gd_bytes;
+    const std::uint32_t shx_bytes = t.Pn * panel;
+    c.shared_x = t.Pn <= 64u && shx_bytes + fixed < budget &&  // 64: the kernel's panel-ready flags
+                 (shx_bytes <= 40u * 1024u ||
+                  ((budget - shx_bytes - fixed) / (2u * kNC) & ~127u) >= cellb + 1024u);
+    const std::uint32_t pan_bytes = c.shared_x ? shx_bytes : kNC * panel;
     const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
     // two record slots per warp; outliers beyond a slot are read from HBM
     const std::uint32_t slot = std::min((ring_avail / (2u * kNC)) & ~127u, (cellb + 4096u + 127u) & ~127u);
