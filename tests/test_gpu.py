@@ -163,6 +163,10 @@ def test_host_api_graph_reuse(cuda, oracle_c):
     Y = L.matvec_host(X)
     for b in range(2):
         assert relative_l2(Y[b], t.matvec(X[b])) < 1e-5
+    X = rng.standard_normal((6, 1024)).astype(np.float32)  # batch 6: gemm_tc stores y to host memory
+    Y = L.matvec_host(X)
+    for b in range(6):
+        assert relative_l2(Y[b], t.matvec(X[b])) < TOL
     x = rng.standard_normal(1024).astype(np.float32)  # back to batch 1
     assert relative_l2(L.matvec_host(x), t.matvec(x)) < 1e-5
 
