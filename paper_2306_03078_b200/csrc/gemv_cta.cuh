@@ -398,7 +398,11 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     const std::uint32_t lane_off = O_FRAG + 32u * lr + 16u * (lm & 1);
     const std::uint32_t zero_sa = smem_u32(&zrow[warp][0]);
     const std::uint32_t zb[2] = {zero_sa, zero_sa - 256u};
-    const std::uint32_t zl[2] = {zero_sa - (O_LO - O_FRAG), zero_sa - 256u - (O_LO - O_FRAG)};
+    // fp32 x: this lane's B row in a quarter super-tile -- rows 0-3 the hi
+    // fragments of blocks 0-3, rows 4-7 their lo fragments; active in the call
+    // of MMA jj == lr % 4
+    const int jact4 = (lr & 3) - (lm >> 1);
+    const std::uint32_t hl_off = (lr < 4 ? O_FRAG + 32u * lr : O_LO + 32u * (lr - 4)) + 16u * (lm & 1);
     const std::uint32_t magic = 0x4B000000u;
     // this lane's x-preparation columns: block lane/2 of the panel, k half lane%2
     const int pp = T::column_prescale(BW, static_cast<std::uint32_t>(lane >> 1), 8u * (lane & 1));
@@ -514,6 +518,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 __syncwarp();
             }
             const std::uint32_t lane_sa = smem_u32(pan) + lane_off;
+            const std::uint32_t hl_sa = smem_u32(pan) + hl_off;  // fp32 x
 #ifdef SPQR_TIMELINE
             const unsigned long long tw0 = gtime();
 #endif
@@ -534,78 +539,34 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(pan + O_SC)[4 * h + t];
 
-                // lane data of the units
+                // lane data of the units (fp32 x loads its code words per super-tile)
                 std::uint32_t cw[NU][G::LANE_WORDS];
                 std::uint32_t ss[NU], zz[NU];
                 uint4 sc[NU][2];
 #pragma unroll
                 for (int ui = 0; ui < NU; ++ui) {
                     const std::uint8_t* unit = cell + unit_of(ui) * UNIT;
+                    if constexpr (!XLO) {
 #pragma unroll
-                    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                        const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                        cw[ui][4 * i] = w4.x;
-                        cw[ui][4 * i + 1] = w4.y;
-                        cw[ui][4 * i + 2] = w4.z;
-                        cw[ui][4 * i + 3] = w4.w;
+                        for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                            const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                            cw[ui][4 * i] = w4.x;
+                            cw[ui][4 * i + 1] = w4.y;
+                            cw[ui][4 * i + 2] = w4.z;
+                            cw[ui][4 * i + 3] = w4.w;
+                        }
                     }
                     load_stats<BS, BZ>(unit + CODEB, lane, ss[ui], zz[ui]);
                     sc[ui][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
                     sc[ui][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
                 }
 
-                // 2 NU independent MMA chains (super-tile h x unit), interleaved
-                std::uint32_t bfr[2][4], lfr[2][4];
-                float cc[2][NU][4];
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int ui = 0; ui < NU; ++ui)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) cc[h][ui][i] = 0.f;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                        std::uint32_t bq[4], lq[4];
-                        if ((j & 1) == 0) {
-                            const bool act = jact == j;
-                            ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bq);
-                            if constexpr (XLO) ldsm_x4((act ? lane_sa : zl[h]) + (256u * h + (O_LO - O_FRAG)), lq);
-                            bfr[h][0] = bq[0]; bfr[h][1] = bq[1]; bfr[h][2] = bq[2]; bfr[h][3] = bq[3];
-                            if constexpr (XLO) {
-                                lfr[h][0] = lq[0]; lfr[h][1] = lq[1]; lfr[h][2] = lq[2]; lfr[h][3] = lq[3];
-                            }
-                        }
-                        const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
-                        std::uint32_t l0 = 0, l1 = 0;
-                        if constexpr (XLO) {
-                            l0 = lfr[h][2 * (j & 1)];
-                            l1 = lfr[h][2 * (j & 1) + 1];
-                        }
-#pragma unroll
-                        for (int ui = 0; ui < NU; ++ui) {
-                            const std::uint32_t* w = cw[ui] + G::CW * cidx;
-                            std::uint32_t a[4];
-#pragma unroll
-                            for (int r = 0; r < 4; ++r) {
-                                const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                                const int i = rho * (G::NP / 2) + qq;
-                                const int B = (BW * i) >> 3, pb = (BW * i) & 7;
-                                a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
-                            }
-                            mma16816(cc[h][ui], a, b0, b1);
-                            if constexpr (XLO) mma16816(cc[h][ui], a, l0, l1);
-                        }
-                    }
-                }
+                // epilogue of super-tile h: y partials += s 2^(24-e) (C + z XX)
                 float2 acc[NU][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
 #pragma unroll
                 for (int ui = 0; ui < NU; ++ui) acc[ui][0] = acc[ui][1] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    float (&c)[NU][4] = cc[h];
+                auto epilogue = [&](auto HC, const float (&c)[NU][4]) {
+                    constexpr int h = decltype(HC)::value;
                     const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
 #pragma unroll
                     for (int ui = 0; ui < NU; ++ui) {
@@ -634,6 +595,114 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                             acc[ui][rho] = ffma2(shat, tt, acc[ui][rho]);
                         }
                     }
+                };
+                // A fragments of MMA (super-tile h, block j) of unit ui from code words w
+                auto afrag = [&](const std::uint32_t* cwu, int h, int j, std::uint32_t (&a)[4]) {
+                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
+                    const std::uint32_t* w = cwu + G::CW * cidx;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                        const int i = rho * (G::NP / 2) + qq;
+                        const int B = (BW * i) >> 3, pb = (BW * i) & 7;
+                        a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
+                    }
+                };
+                if constexpr (!XLO) {
+                    // 2 NU independent MMA chains (super-tile h x unit), interleaved
+                    std::uint32_t bfr[2][4];
+                    float cc[2][NU][4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int ui = 0; ui < NU; ++ui)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) cc[h][ui][i] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if ((j & 1) == 0) {
+                                const bool act = jact == j;
+                                ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bfr[h]);
+                            }
+                            const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
+#pragma unroll
+                            for (int ui = 0; ui < NU; ++ui) {
+                                std::uint32_t a[4];
+                                afrag(cw[ui], h, j, a);
+                                mma16816(cc[h][ui], a, b0, b1);
+                            }
+                        }
+                    }
+                    epilogue(std::integral_constant<int, 0>{}, cc[0]);
+                    epilogue(std::integral_constant<int, 1>{}, cc[1]);
+                } else {
+                    // fp32 x = hi + lo, both f16: quarter super-tiles of 4 blocks,
+                    // MMA jj routes block jj's hi part to output column jj and its
+                    // lo part to column jj + 4, so hi and lo share one MMA (32 per
+                    // cell, as for f16 x, instead of 64).  hi + lo meet across
+                    // lanes t and t^2; lanes t < 2 keep quarter 2h, lanes t >= 2
+                    // quarter 2h + 1 -- exactly the (row, block) pairs whose
+                    // statistics the lane holds (blocks 8h + 2t + bs), so the
+                    // epilogue is the f16 one.
+                    auto half = [&](auto HC) {
+                        constexpr int h = decltype(HC)::value;
+                        constexpr int W0 = G::CW * (8 * h / G::MPC), W1 = G::CW * ((8 * h + 7) / G::MPC + 1);
+                        static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a super-tile: 8 B aligned");
+                        std::uint32_t cwh[NU][G::LANE_WORDS];
+#pragma unroll
+                        for (int ui = 0; ui < NU; ++ui) {
+                            const std::uint8_t* unit = cell + unit_of(ui) * UNIT;
+#pragma unroll
+                            for (int i = W0; i < W1; i += 2) {
+                                const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
+                                cwh[ui][i] = w2.x;
+                                cwh[ui][i + 1] = w2.y;
+                            }
+                        }
+                        float d[2][NU][4];  // [quarter 2h + qq][unit]
+#pragma unroll
+                        for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+                            for (int ui = 0; ui < NU; ++ui)
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) d[qq][ui][i] = 0.f;
+#pragma unroll
+                        for (int qq = 0; qq < 2; ++qq) {
+                            const int q = 2 * h + qq;
+#pragma unroll
+                            for (int c2 = 0; c2 < 2; ++c2) {  // MMAs jj = 2 c2, 2 c2 + 1
+                                std::uint32_t bq[4];
+                                ldsm_x4(jact4 == 2 * c2 ? hl_sa + 128u * q : zero_sa, bq);
+#pragma unroll
+                                for (int m2 = 0; m2 < 2; ++m2) {
+                                    const int jj = 2 * c2 + m2, j = 4 * (q & 1) + jj;  // block 8h + j
+#pragma unroll
+                                    for (int ui = 0; ui < NU; ++ui) {
+                                        std::uint32_t a[4];
+                                        afrag(cwh[ui], h, j, a);
+                                        mma16816(d[qq][ui], a, bq[2 * m2], bq[2 * m2 + 1]);
+                                    }
+                                }
+                            }
+                        }
+                        // each lane sends its partner (t ^ 2, the other class) the
+                        // quarter the partner keeps: one shuffle per value
+                        float ch[NU][4];
+                        const bool lowt = t < 2;
+#pragma unroll
+                        for (int ui = 0; ui < NU; ++ui)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float keep = lowt ? d[0][ui][i] : d[1][ui][i];
+                                const float send = lowt ? d[1][ui][i] : d[0][ui][i];
+                                ch[ui][i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+                            }
+                        epilogue(HC, ch);
+                    };
+                    half(std::integral_constant<int, 0>{});
+                    half(std::integral_constant<int, 1>{});
                 }
 
                 // outliers: entries (row, col, value) of this cell, sorted by (row,
