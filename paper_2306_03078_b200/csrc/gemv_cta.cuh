@@ -196,8 +196,15 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
     // exact multiply; fp32 x can reach the edges of the exponent range
     float s[8];
     if constexpr (XLO) {
+        const int k = e - pp;
+        if (k >= -126 && k <= 127) {  // 2^k is a normal float: one exact-as-ldexpf multiply
+            const float sc = __uint_as_float(static_cast<std::uint32_t>(127 + k) << 23);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = ldexpf(f[i], e - pp);
+            for (int i = 0; i < 8; ++i) s[i] = f[i] * sc;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i] = ldexpf(f[i], k);
+        }
     } else {
         const float sc = __uint_as_float(static_cast<std::uint32_t>(127 + e - pp) << 23);
 #pragma unroll
@@ -233,7 +240,9 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
     if ((lane & 1) == 0) {
         const int kk = lane >> 1;  // block 8h + 2t + bs
         float* scp = reinterpret_cast<float*>(pan + O_SC) + 4 * (kk >> 1) + (kk & 1);
-        scp[0] = XLO ? ldexpf(1.0f, 24 - e) : __uint_as_float(static_cast<std::uint32_t>(127 + 24 - e) << 23);
+        scp[0] = (XLO && (24 - e < -126 || 24 - e > 127))
+                     ? ldexpf(1.0f, 24 - e)
+                     : __uint_as_float(static_cast<std::uint32_t>(127 + 24 - e) << 23);
         scp[2] = -X * 5.9604644775390625e-08f;
     }
 }
