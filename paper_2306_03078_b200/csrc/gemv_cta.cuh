@@ -188,9 +188,12 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     int e = 0;
     if (mx > 0.f && mx < INFINITY) {
-        int E;
-        frexpf(mx, &E);  // mx = m * 2^E, m in [0.5, 1)
-        e = 15 - E;      // mx * 2^e in [2^14, 2^15)
+        // mx = m * 2^E, m in [0.5, 1): E from the exponent field (frexpf for
+        // fp32 subnormals; fp16 x is always normal as fp32)
+        const std::uint32_t eb = __float_as_uint(mx) >> 23;
+        int E = static_cast<int>(eb) - 126;
+        if (XLO && eb == 0u) frexpf(mx, &E);
+        e = 15 - E;  // mx * 2^e in [2^14, 2^15)
     }
     // 2^(e - pp): for fp16 x, e - pp is in [-8, 38] and the scaling is a plain
     // exact multiply; fp32 x can reach the edges of the exponent range
