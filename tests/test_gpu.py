@@ -93,6 +93,22 @@ def test_matvec_fast_vs_oracle(cuda, oracle_c, bw, shape):
         assert relative_l2(y.cpu().numpy(), ref) < 1e-5
 
 
+def test_f32_x_exponent_extremes(cuda, oracle_c):
+    """fp32 x far from 1 (block exponents where 2^k is not a normal float, and
+    fp32 subnormals): the panel scaling falls back to ldexpf/frexpf."""
+    a = synth.make_layer(96, 1024, seed=11, outlier_rate=0.02)
+    s = P.encode_arrays(a)
+    L = P.Layer(s)
+    t = oracle_c.decode(s)
+    rng = np.random.default_rng(9)
+    for scale in (1e-38, 1e-30, 1e25):
+        x = (rng.standard_normal(1024) * scale).astype(np.float32)
+        y = cuda.empty(96, device="cuda")
+        L.matvec(_dev(cuda, x), y)
+        ref = t.matvec(x)
+        assert relative_l2(y.cpu().numpy(), ref) < 1e-5, scale
+
+
 def test_outlier_density_sweep(cuda, oracle_c):
     for rate in (0.0, 0.005, 0.01, 0.02, 0.05):
         a = synth.make_layer(256, 2048, seed=3, outlier_rate=rate)
