@@ -410,11 +410,11 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     const std::uint32_t lane_off = O_FRAG + 32u * lr + 16u * (lm & 1);
     const std::uint32_t zero_sa = smem_u32(&zrow[warp][0]);
     const std::uint32_t zb[2] = {zero_sa, zero_sa - 256u};
-    // fp32 x: this lane's B row in a quarter super-tile -- rows 0-3 the hi
-    // fragments of blocks 0-3, rows 4-7 their lo fragments; active in the call
-    // of MMA jj == lr % 4
-    const int jact4 = (lr & 3) - (lm >> 1);
-    const std::uint32_t hl_off = (lr < 4 ? O_FRAG + 32u * lr : O_LO + 32u * (lr - 4)) + 16u * (lm & 1);
+    // fp32 x: in the MMA of slot s of a half super-tile (blocks 8h + 2s + par),
+    // B row 2s is the block's hi fragment and row 2s + 1 its lo fragment; this
+    // lane addresses row lr, active in the call of slot lr / 2
+    const int jact2 = (lr >> 1) - (lm >> 1);
+    const std::uint32_t hl_off = ((lr & 1) ? O_LO : O_FRAG) + 64u * static_cast<std::uint32_t>(lr >> 1) + 16u * (lm & 1);
     const std::uint32_t magic = 0x4B000000u;
     // this lane's x-preparation columns: block lane/2 of the panel, k half lane%2
     const int pp = T::column_prescale(BW, static_cast<std::uint32_t>(lane >> 1), 8u * (lane & 1));
@@ -650,14 +650,13 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     epilogue(std::integral_constant<int, 0>{}, cc[0]);
                     epilogue(std::integral_constant<int, 1>{}, cc[1]);
                 } else {
-                    // fp32 x = hi + lo, both f16: quarter super-tiles of 4 blocks,
-                    // MMA jj routes block jj's hi part to output column jj and its
-                    // lo part to column jj + 4, so hi and lo share one MMA (32 per
-                    // cell, as for f16 x, instead of 64).  hi + lo meet across
-                    // lanes t and t^2; lanes t < 2 keep quarter 2h, lanes t >= 2
-                    // quarter 2h + 1 -- exactly the (row, block) pairs whose
-                    // statistics the lane holds (blocks 8h + 2t + bs), so the
-                    // epilogue is the f16 one.
+                    // fp32 x = hi + lo, both f16, sharing one MMA: super-tile h
+                    // runs as its even blocks then its odd blocks (parity par);
+                    // the MMA of block 8h + 2s + par routes the hi part to
+                    // output column 2s and the lo part to 2s + 1, so lane (g, t)
+                    // gets hi and lo of block 8h + 2t + par side by side -- the
+                    // (row, block) pairs whose statistics it holds -- and adds
+                    // them in-lane: 32 MMAs per cell as for f16 x, no shuffles.
                     auto half = [&](auto HC) {
                         constexpr int h = decltype(HC)::value;
                         constexpr int W0 = G::CW * (8 * h / G::MPC), W1 = G::CW * ((8 * h + 7) / G::MPC + 1);
@@ -673,44 +672,39 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                                 cwh[ui][i + 1] = w2.y;
                             }
                         }
-                        float d[2][NU][4];  // [quarter 2h + qq][unit]
+                        float d[2][NU][4];  // [parity][unit]: {hi, lo} of block 8h + 2t + par, rows g / g + 8
 #pragma unroll
-                        for (int qq = 0; qq < 2; ++qq)
+                        for (int par = 0; par < 2; ++par)
 #pragma unroll
                             for (int ui = 0; ui < NU; ++ui)
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) d[qq][ui][i] = 0.f;
+                                for (int i = 0; i < 4; ++i) d[par][ui][i] = 0.f;
 #pragma unroll
-                        for (int qq = 0; qq < 2; ++qq) {
-                            const int q = 2 * h + qq;
+                        for (int par = 0; par < 2; ++par) {
 #pragma unroll
-                            for (int c2 = 0; c2 < 2; ++c2) {  // MMAs jj = 2 c2, 2 c2 + 1
+                            for (int c2 = 0; c2 < 2; ++c2) {  // slots s = 2 c2, 2 c2 + 1
                                 std::uint32_t bq[4];
-                                ldsm_x4(jact4 == 2 * c2 ? hl_sa + 128u * q : zero_sa, bq);
+                                ldsm_x4(jact2 == 2 * c2 ? hl_sa + 256u * h + 32u * par : zero_sa, bq);
 #pragma unroll
                                 for (int m2 = 0; m2 < 2; ++m2) {
-                                    const int jj = 2 * c2 + m2, j = 4 * (q & 1) + jj;  // block 8h + j
+                                    const int j = 2 * (2 * c2 + m2) + par;  // block 8h + j
 #pragma unroll
                                     for (int ui = 0; ui < NU; ++ui) {
                                         std::uint32_t a[4];
                                         afrag(cwh[ui], h, j, a);
-                                        mma16816(d[qq][ui], a, bq[2 * m2], bq[2 * m2 + 1]);
+                                        mma16816(d[par][ui], a, bq[2 * m2], bq[2 * m2 + 1]);
                                     }
                                 }
                             }
                         }
-                        // each lane sends its partner (t ^ 2, the other class) the
-                        // quarter the partner keeps: one shuffle per value
-                        float ch[NU][4];
-                        const bool lowt = t < 2;
+                        float ch[NU][4];  // the f16 layout: (g, 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
 #pragma unroll
-                        for (int ui = 0; ui < NU; ++ui)
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float keep = lowt ? d[0][ui][i] : d[1][ui][i];
-                                const float send = lowt ? d[1][ui][i] : d[0][ui][i];
-                                ch[ui][i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-                            }
+                        for (int ui = 0; ui < NU; ++ui) {
+                            ch[ui][0] = d[0][ui][0] + d[0][ui][1];
+                            ch[ui][1] = d[1][ui][0] + d[1][ui][1];
+                            ch[ui][2] = d[0][ui][2] + d[0][ui][3];
+                            ch[ui][3] = d[1][ui][2] + d[1][ui][3];
+                        }
                         epilogue(HC, ch);
                     };
                     half(std::integral_constant<int, 0>{});
