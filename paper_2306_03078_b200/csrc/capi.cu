@@ -372,9 +372,13 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
 void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
             cudaStream_t st) {
     const std::size_t esz = f16 ? 2 : 4;
-    for (int b0 = 0; b0 < batch; b0 += static_cast<int>(kTcMaxN)) {
-        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, static_cast<int>(kTcMaxN)));
-        const std::uint32_t N = (B + 15u) & ~15u;
+    // fp32 x: hi and lo fp16 parts as two column sets of the MMA (<= 32 batch
+    // columns per launch); fp16 x: <= 64
+    const int per = f16 ? static_cast<int>(kTcMaxN) : static_cast<int>(kTcMaxN / 2);
+    for (int b0 = 0; b0 < batch; b0 += per) {
+        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, per));
+        const std::uint32_t Nh = f16 ? 0u : (B + 15u) & ~15u;
+        const std::uint32_t N = f16 ? (B + 15u) & ~15u : 2u * Nh;
         const void* xb = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b0) * L->info.cols * esz;
         std::uint8_t* xpan = base + w.tc_x;
         {
@@ -389,7 +393,7 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_tc, xb, f16, L->info.cols, B, N, L->Pn,
-                                  static_cast<const std::uint32_t*>(L->d_order), xpan),
+                                  static_cast<const std::uint32_t*>(L->d_order), xpan, Nh),
                "launch xprep_tc");
             ++g_launches;
         }
@@ -404,6 +408,7 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
         p.partial = reinterpret_cast<float*>(base + w.tc_part);
         p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
         p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
+        p.Nh = Nh;
         p.rec_cap = L->tcp.slot_bytes; p.slot_bytes = L->tcp.slot_bytes; p.pn_magic = L->pn_magic;
         p.sigma = L->tcp.sigma;
         p.out_scale = std::ldexp(1.0f, L->tcp.sigma);
@@ -804,7 +809,9 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
             }
     }
     c.sigma = 0;
-    if (smax > 0 && std::isfinite(smax)) c.sigma = std::clamp(static_cast<int>(std::ceil(std::log2(smax))) + 9, -90, 90);
+    // weights w 2^-sigma up to ~2^12 (s (q - z) <= ~8 smax): binary16 normals
+    // for the whole useful range, no subnormal underflow of small weights
+    if (smax > 0 && std::isfinite(smax)) c.sigma = std::clamp(static_cast<int>(std::ceil(std::log2(smax))) - 9, -100, 100);
     c.d_start = dalloc<std::uint32_t>(st.size());
     c.d_maps = dalloc<std::uint32_t>(gmap.size() + cmap.size());
     ck(cudaMemcpy(c.d_start, st.data(), 4 * st.size(), cudaMemcpyHostToDevice), "H2D tc start");

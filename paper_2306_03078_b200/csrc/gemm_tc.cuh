@@ -18,10 +18,12 @@
 //     that row's cells (cp.async.bulk, two record slots, one cell of
 //     lookahead, record offsets loaded a step ahead); each warp decodes the
 //     bilevel statistics of its (unit, half) into a per-(row, block) fp16 table
-//     {s 2^(24-p-sigma) for both k halves, round(z) 2^(p-24), -s (z - round z)
-//     2^-sigma}, turns every A-fragment register of codes (the batch-1 layout:
-//     codes as binary16 subnormals code*2^(p-24), ONE LOP3) into weights with
-//     one exact HSUB2 and ONE HFMA2, and writes them with stmatrix into the
+//     {s 2^(-p-sigma) for both k halves, 1024 + round(z) 2^p, -s (z - round z)
+//     2^-sigma}, turns every A-fragment register of codes (the batch-1 layout;
+//     ONE LOP3 makes each half the binary16 normal 1024 + code*2^p, p <= 7)
+//     into weights with one exact HSUB2 and ONE HFMA2 (sigma puts the largest
+//     weights near 2^12, so small weights stay binary16 normals), and writes
+//     them with stmatrix into the
 //     UMMA K-major core-matrix layout; the four warps of a cell row then add the
 //     cell's outliers in place between two named barriers; after a tile's last
 //     stage the warps whose TMEM lane quarter holds the rows read the
@@ -52,6 +54,7 @@ struct TcParams {
     float out_scale;                  // 2^sigma
     int sigma;
     std::uint32_t na;                 // A stage buffers (3 or 4, by shared memory)
+    std::uint32_t Nh;                 // fp32 x: lo parts in accumulator columns Nh .. 2Nh-1 (0: fp16 x)
 };
 
 namespace tc {
@@ -96,8 +99,8 @@ __device__ __forceinline__ void stsm_x4(std::uint32_t addr, std::uint32_t a0, st
                  "r"(a2), "r"(a3));
 }
 // (a - (z, z)) * (s, s) + (c, c) per f16 lane; z, s, c are the low (HI=false)
-// or high (HI=true) halves of their registers.  a - z is exact (both are
-// integers times the same power of two), so the weight is rounded once.
+// or high (HI=true) halves of their registers.  a - z is exact (1024 + q 2^p
+// minus 1024 + round(z) 2^p, |round(z)| <= 15), so the weight is rounded once.
 template <bool HI>
 __device__ __forceinline__ std::uint32_t deq2(std::uint32_t a, std::uint32_t z, std::uint32_t s, std::uint32_t c) {
     std::uint32_t d;
@@ -124,9 +127,13 @@ __device__ __forceinline__ std::uint32_t deq2(std::uint32_t a, std::uint32_t z, 
 // x tiles for the tensor cores: stage (P, h) holds columns 256P + 128h + k,
 // k < 128, of every batch column n < N (zero for n >= B or beyond the layer)
 // as fp16, K-major core matrices: byte (k/8)*16N + (n/8)*128 + (n%8)*16 + (k%8)*2.
+// fp32 x (Nh > 0): columns nn < Nh carry fp16(x) of batch column nn, columns
+// Nh + nn the residual fp16(x - fp16(x)); the epilogue adds the two
+// accumulator columns, so x keeps ~22 significant bits on the tensor cores.
 static __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ x, int x_f16, std::uint32_t n,
                                                 std::uint32_t B, std::uint32_t N, std::uint32_t Pn,
-                                                const std::uint32_t* __restrict__ order, std::uint8_t* __restrict__ out) {
+                                                const std::uint32_t* __restrict__ order, std::uint8_t* __restrict__ out,
+                                                std::uint32_t Nh) {
     pdl_launch();
     const std::uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;  // (stage, n, k core)
     const std::uint32_t total = 2u * Pn * N * 16u;
@@ -142,10 +149,13 @@ static __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ 
         for (int q = 0; q < 2; ++q) {
             const std::uint32_t c = c0 + 2 * e + q;
             float v = 0.f;
-            if (nn < B && c < n) {
+            const bool lo = Nh && nn >= Nh;
+            const std::uint32_t bc = lo ? nn - Nh : nn;  // batch column
+            if (bc < B && c < n) {
                 const std::uint32_t src = order ? __ldg(order + c) : c;
-                const std::size_t off = static_cast<std::size_t>(nn) * n + src;
+                const std::size_t off = static_cast<std::size_t>(bc) * n + src;
                 v = x_f16 ? __half2float(static_cast<const __half*>(x)[off]) : static_cast<const float*>(x)[off];
+                if (lo) v -= __half2float(__float2half_rn(v));
             }
             v2[q] = v;
         }
@@ -353,11 +363,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
         {
             const int mm0 = (2 * t) % G::MPC, mm1 = (2 * t + 1) % G::MPC;
             auto pw = [](int e) { return __uint_as_float(static_cast<std::uint32_t>(127 + e) << 23); };
-            f0 = make_float2(pw(24 - T::prescale_p(BW, 2 * mm0) - p.sigma), pw(24 - T::prescale_p(BW, 2 * mm1) - p.sigma));
-            f1 = make_float2(pw(24 - T::prescale_p(BW, 2 * mm0 + 1) - p.sigma),
-                             pw(24 - T::prescale_p(BW, 2 * mm1 + 1) - p.sigma));
-            g0 = make_float2(pw(T::prescale_p(BW, 2 * mm0) - 24), pw(T::prescale_p(BW, 2 * mm1) - 24));
-            g1 = make_float2(pw(T::prescale_p(BW, 2 * mm0 + 1) - 24), pw(T::prescale_p(BW, 2 * mm1 + 1) - 24));
+            f0 = make_float2(pw(-T::prescale_p(BW, 2 * mm0) - p.sigma), pw(-T::prescale_p(BW, 2 * mm1) - p.sigma));
+            f1 = make_float2(pw(-T::prescale_p(BW, 2 * mm0 + 1) - p.sigma), pw(-T::prescale_p(BW, 2 * mm1 + 1) - p.sigma));
+            g0 = make_float2(pw(T::prescale_p(BW, 2 * mm0)), pw(T::prescale_p(BW, 2 * mm1)));
+            g1 = make_float2(pw(T::prescale_p(BW, 2 * mm0 + 1)), pw(T::prescale_p(BW, 2 * mm1 + 1)));
         }
         std::uint32_t k = 0;  // records of this cell row consumed so far
         load_off(u0);
@@ -412,10 +421,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                         const float2 zhat = fmul2(Sz, fadd2(cz, Zz));
                         // integer part of the zero goes into the codes exactly; the
                         // fraction (|.| <= 1/2) is the fp16 addend
-                        const float2 zi = make_float2(fminf(fmaxf(rintf(zhat.x), -1000.f), 1000.f),
-                                                      fminf(fmaxf(rintf(zhat.y), -1000.f), 1000.f));
+                        const float2 zi = make_float2(fminf(fmaxf(rintf(zhat.x), -15.f), 15.f),
+                                                      fminf(fmaxf(rintf(zhat.y), -15.f), 15.f));
                         const float2 S0 = fmul2(shat, f0), S1 = fmul2(shat, f1);
-                        const float2 Z0 = fmul2(zi, g0), Z1 = fmul2(zi, g1);
+                        // 1024 + zi 2^p: exact in binary16 for |zi| <= 15, p <= 7
+                        const float2 Z0 = ffma2(zi, g0, make_float2(1024.f, 1024.f));
+                        const float2 Z1 = ffma2(zi, g1, make_float2(1024.f, 1024.f));
                         const float2 C = fmul2(fmul2(shat, fadd2(zi, make_float2(-zhat.x, -zhat.y))),
                                                make_float2(sig_scale, sig_scale));
                         const int row = g + 8 * rho;
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                         const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
                         const int i = rho * (G::NP / 2) + qq;
                         const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                        const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                        const std::uint32_t code = (window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u)) | 0x64006400u;
                         const uint4 e = rho ? e1 : e0;
                         a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
                     }
@@ -515,7 +526,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                             const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
                             const int i = rho * (G::NP / 2) + qq;
                             const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                            const std::uint32_t code = window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u);
+                            const std::uint32_t code = (window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u)) | 0x64006400u;
                             const uint4 e = rho ? e1 : e0;
                             a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
                         }
@@ -589,10 +600,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const bool whole = ua == T_ * p.Pn && u + 1 == (T_ + 1) * p.Pn;
                 const uint2 gm = whole ? make_uint2(0, 0) : __ldg(reinterpret_cast<const uint2*>(p.gmap) + T_);
                 const std::uint32_t ord = whole ? 0u : __ldg(p.cmap + 2u * v + (T_ == tile_of(u0) ? 0u : 1u));
+                const std::uint32_t Nout = p.Nh ? p.Nh : N;  // output columns of this launch
 #pragma unroll 1
-                for (std::uint32_t c0 = 16u * part; c0 < N; c0 += 16u * RW) {
+                for (std::uint32_t c0 = 16u * part; c0 < Nout; c0 += 16u * RW) {
                     float vv[16];
                     tc::ld16(ta + c0, vv);
+                    if (p.Nh) {  // + the lo parts of x
+                        float vl[16];
+                        tc::ld16(ta + c0 + p.Nh, vl);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) vv[j] += vl[j];
+                    }
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const std::uint32_t bcol = c0 + j;
@@ -618,7 +636,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     __syncwarp();
                     if (prev == gm.y - 1u) {
 #pragma unroll 1
-                        for (std::uint32_t c0 = 16u * part; c0 < N; c0 += 16u * RW)
+                        for (std::uint32_t c0 = 16u * part; c0 < Nout; c0 += 16u * RW)
                             for (std::uint32_t bcol = c0; bcol < c0 + 16u && bcol < p.B; ++bcol) {
                                 float sum = 0.f;
                                 for (std::uint32_t j = 0; j < gm.y; ++j)

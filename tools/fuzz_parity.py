@@ -1,0 +1,60 @@
+"""Randomised parity sweep against the oracle: random shapes (ragged), weight /
+statistic widths, outlier rates, permutation, x dtype and batch.
+    python tools/fuzz_parity.py [N_CASES]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2306_03078_b200 as P  # noqa: E402
+from paper_2306_03078_b200 import synth  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+rng = np.random.default_rng(1234)
+orc = O.Oracle()
+worst = {}
+for case in range(n_cases):
+    m = int(rng.integers(1, 40)) * int(rng.choice([1, 8, 32]))
+    n = int(rng.integers(1, 40)) * int(rng.choice([1, 16, 64]))
+    bw = int(rng.choice([2, 3, 4]))
+    rate = float(rng.choice([0.0, 0.01, 0.05]))
+    perm = bool(rng.integers(0, 2))
+    a = synth.make_layer(m, n, weight_bits=bw, scale_bits=bw, zero_bits=bw, seed=case, permute=perm,
+                         outlier_rate=rate)
+    s = P.encode_arrays(a)
+    t = orc.decode(s)
+    L = P.Layer(s)
+    batch = int(rng.choice([1, 2, 5, 17]))
+    dt = [np.float16, np.float32][int(rng.integers(0, 2))]
+    X = rng.standard_normal((batch, n)).astype(dt)
+    Y = torch.empty(batch, m, device="cuda")
+    L.matvec(torch.from_numpy(X).cuda(), Y, batch=batch)
+    got = Y.cpu().numpy()
+    tc = batch >= 4 and L.info["fast_path"]
+    tol = 1e-3 if tc else 1e-5
+    Wabs = np.abs(t.dequantize_full().astype(np.float64))
+    for b in range(batch):
+        ref = t.matvec(X[b].astype(np.float32))
+        err = O.relative_l2(got[b], ref)
+        key = (L.info["fast_path"], batch >= 4, dt.__name__)
+        worst[key] = max(worst.get(key, 0.0), err)
+        ok = err <= tol
+        if tc and not ok:
+            # fp16 weights: a forward-error bound for outputs with heavy cancellation
+            # (|y| << |W||x|), where no fp16-weight contraction meets 1e-3 relative
+            bound = 1e-3 * np.linalg.norm(ref) + 2.0 ** -10 * np.linalg.norm(Wabs @ np.abs(X[b].astype(np.float64)))
+            ok = np.linalg.norm(got[b].astype(np.float64) - ref) <= bound
+        if not ok:
+            print(f"FAIL case {case}: m={m} n={n} bw={bw} rate={rate} perm={perm} batch={batch} {dt.__name__}"
+                  f" fast={L.info['fast_path']} col {b}: rel {err:.3e} > {tol}", flush=True)
+            sys.exit(1)
+    W = torch.empty(m, n, device="cuda")
+    L.dequantize(W)
+    if not np.array_equal(W.cpu().numpy().view(np.uint32), t.dequantize_full().view(np.uint32)):
+        print(f"FAIL case {case}: dequantize not bit-exact (m={m} n={n} bw={bw})", flush=True)
+        sys.exit(1)
+print("fuzz ok:", n_cases, "cases; worst rel by (fast, tensor-core, x dtype):",
+      {k: f"{v:.2e}" for k, v in sorted(worst.items())}, flush=True)
