@@ -22,8 +22,16 @@ for case in range(n_cases):
     bw = int(rng.choice([2, 3, 4]))
     rate = float(rng.choice([0.0, 0.01, 0.05]))
     perm = bool(rng.integers(0, 2))
-    a = synth.make_layer(m, n, weight_bits=bw, scale_bits=bw, zero_bits=bw, seed=case, permute=perm,
-                         outlier_rate=rate)
+    generic = case % 4 == 3  # every 4th case off the fast geometry: other group sizes / widths
+    if generic:
+        bw = int(rng.choice([1, 2, 3, 4, 5, 8]))
+        sb = int(rng.choice([2, 3, 4, 16]))
+        b1, b2 = int(rng.choice([8, 16, 32])), int(rng.choice([8, 16, 32]))
+        a = synth.make_layer(m, n, weight_bits=bw, scale_bits=sb, zero_bits=sb, beta1=b1, beta2=b2, seed=case,
+                             permute=perm, outlier_rate=rate)
+    else:
+        a = synth.make_layer(m, n, weight_bits=bw, scale_bits=bw, zero_bits=bw, seed=case, permute=perm,
+                             outlier_rate=rate)
     s = P.encode_arrays(a)
     t = orc.decode(s)
     L = P.Layer(s)
