@@ -98,6 +98,29 @@ __device__ __forceinline__ void stsm_x4(std::uint32_t addr, std::uint32_t a0, st
     asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a0), "r"(a1),
                  "r"(a2), "r"(a3));
 }
+// (w & M) | bias in ONE LOP3 (the mask an immediate, the bias in a register;
+// written as a plain C++ expression the compiler emits two)
+template <std::uint32_t M>
+__device__ __forceinline__ std::uint32_t and_or(std::uint32_t a, std::uint32_t c) {
+    std::uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(M), "r"(c));
+    return d;
+}
+// the code pair at bit offset pb of a window as binary16 normals 1024 + q 2^pb
+// (pb is a constant after unrolling, so the switch folds away)
+template <std::uint32_t MASK>
+__device__ __forceinline__ std::uint32_t code_bias(std::uint32_t win, int pb, std::uint32_t bias) {
+    switch (pb) {
+        case 0: return and_or<(MASK << 0) * 0x00010001u>(win, bias);
+        case 1: return and_or<(MASK << 1) * 0x00010001u>(win, bias);
+        case 2: return and_or<(MASK << 2) * 0x00010001u>(win, bias);
+        case 3: return and_or<(MASK << 3) * 0x00010001u>(win, bias);
+        case 4: return and_or<(MASK << 4) * 0x00010001u>(win, bias);
+        case 5: return and_or<(MASK << 5) * 0x00010001u>(win, bias);
+        case 6: return and_or<(MASK << 6) * 0x00010001u>(win, bias);
+        default: return and_or<(MASK << 7) * 0x00010001u>(win, bias);
+    }
+}
 // (a - (z, z)) * (s, s) + (c, c) per f16 lane; z, s, c are the low (HI=false)
 // or high (HI=true) halves of their registers.  a - z is exact (1024 + q 2^p
 // minus 1024 + round(z) 2^p, |round(z)| <= 15), so the weight is rounded once.
@@ -358,6 +381,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
             }
         };
         const float sig_scale = __uint_as_float(static_cast<std::uint32_t>(127 - p.sigma) << 23);  // 2^-sigma
+        const std::uint32_t bias16 = 0x64006400u;  // binary16 1024 in both halves
         // per-lane constants of the statistics: blocks 8hh + 2t + bs, bs = 0, 1
         float2 f0, f1, g0, g1;  // s multipliers 2^(24-p-sigma) and code scales 2^(p-24), column halves 0 / 1
         {
@@ -482,7 +506,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                         const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
                         const int i = rho * (G::NP / 2) + qq;
                         const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                        const std::uint32_t code = (window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u)) | 0x64006400u;
+                        const std::uint32_t code = tc::code_bias<MASK>(window<G::CW>(w, Bq), pb, bias16);
                         const uint4 e = rho ? e1 : e0;
                         a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
                     }
@@ -526,7 +550,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                             const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
                             const int i = rho * (G::NP / 2) + qq;
                             const int Bq = (BW * i) >> 3, pb = (BW * i) & 7;
-                            const std::uint32_t code = (window<G::CW>(w, Bq) & ((MASK << pb) * 0x00010001u)) | 0x64006400u;
+                            const std::uint32_t code = tc::code_bias<MASK>(window<G::CW>(w, Bq), pb, bias16);
                             const uint4 e = rho ? e1 : e0;
                             a[r] = kh ? tc::deq2<true>(code, e.y, e.x, e.z) : tc::deq2<false>(code, e.y, e.x, e.z);
                         }
