@@ -16,6 +16,7 @@ n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(1234)
 orc = O.Oracle()
 worst = {}
+worst_tc = [0.0, ""]
 for case in range(n_cases):
     m = int(rng.integers(1, 40)) * int(rng.choice([1, 8, 32]))
     n = int(rng.integers(1, 40)) * int(rng.choice([1, 16, 64]))
@@ -49,6 +50,10 @@ for case in range(n_cases):
         err = O.relative_l2(got[b], ref)
         key = (L.info["fast_path"], batch >= 4, dt.__name__)
         worst[key] = max(worst.get(key, 0.0), err)
+        if tc and err > worst_tc[0]:
+            cond = np.linalg.norm(Wabs @ np.abs(X[b].astype(np.float64))) / max(np.linalg.norm(ref), 1e-30)
+            worst_tc[:] = [err, f"case {case} m={m} n={n} bw={bw} rate={rate} batch={batch} {dt.__name__} "
+                                f"col {b}: |W||x| / |y| = {cond:.1f}"]
         ok = err <= tol
         if tc and not ok:
             # fp16 weights: a forward-error bound for outputs with heavy cancellation
@@ -66,3 +71,4 @@ for case in range(n_cases):
         sys.exit(1)
 print("fuzz ok:", n_cases, "cases; worst rel by (fast, tensor-core, x dtype):",
       {k: f"{v:.2e}" for k, v in sorted(worst.items())}, flush=True)
+print(f"worst tensor-core column: rel {worst_tc[0]:.2e} -- {worst_tc[1]}", flush=True)
