@@ -1244,10 +1244,18 @@ int spqr_gather_wait(spqr_gather* g, void* cuda_stream) {
     return guard([&] {
         DevGuard dg(g->device);
         g_launches = 0;
-        spqr_dev::gather_wait<<<1, 32, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
-            reinterpret_cast<const std::uint32_t*>(g->base), reinterpret_cast<std::uint32_t*>(g->base + 64),
-            static_cast<std::uint32_t>(g->world));
-        ck(cudaGetLastError(), "launch gather_wait");
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(1);
+        cfg.blockDim = dim3(32);
+        cfg.stream = static_cast<cudaStream_t>(cuda_stream);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ck(cudaLaunchKernelEx(&cfg, spqr_dev::gather_wait, reinterpret_cast<const std::uint32_t*>(g->base),
+                              reinterpret_cast<std::uint32_t*>(g->base + 64), static_cast<std::uint32_t>(g->world)),
+           "launch gather_wait");
         ++g_launches;
     });
 }

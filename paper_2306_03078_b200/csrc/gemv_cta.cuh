@@ -884,9 +884,14 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if constexpr (GATHER) {  // fused all-gather: signal the round to every rank
         __syncthreads();        // every y store of this CTA precedes thread 0's release
         if (threadIdx.x == 0) {
-            __threadfence_system();
-            const std::uint32_t prev = atomicAdd(p.done_ctr, 1u);
-            if (prev == gridDim.x - 1u) {  // the grid's last CTA: every CTA's stores are fenced
+            // GPU-scope release per CTA; only the grid's last CTA, which has
+            // observed every CTA's release through the counter, pays the
+            // system-scope fence before bumping the ranks' round counters
+            // (causality is cumulative: every CTA's stores, local and peer,
+            // happen before the last CTA's red.release.sys)
+            std::uint32_t prev;
+            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done_ctr) : "memory");
+            if (prev == gridDim.x - 1u) {  // the grid's last CTA
                 *p.done_ctr = 0u;
                 __threadfence_system();
                 for (std::uint32_t j = 0; j < p.nflag; ++j)
@@ -906,6 +911,11 @@ cudaError_t launch_cta_gather(int bw, int bsz, bool xlo, bool shx, const CtaPara
 // device, so the launch is CUDA-graph replayable), then the round advances.
 static __global__ void __launch_bounds__(32) gather_wait(const std::uint32_t* flags, std::uint32_t* round,
                                                   std::uint32_t world) {
+    // launched with PDL: the next kernel may start its prologue now; this
+    // round's band kernel (and through it the previous wait, which wrote
+    // *round) has completed once griddepcontrol.wait returns
+    pdl_launch();
+    pdl_wait();
     const std::uint32_t r = *round + 1u;
     if (threadIdx.x < world) {
         std::uint32_t v;
