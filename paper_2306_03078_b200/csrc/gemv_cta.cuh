@@ -884,11 +884,12 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if constexpr (GATHER) {  // fused all-gather: signal the round to every rank
         __syncthreads();        // every y store of this CTA precedes thread 0's release
         if (threadIdx.x == 0) {
-            // GPU-scope release per CTA; only the grid's last CTA, which has
-            // observed every CTA's release through the counter, pays the
-            // system-scope fence before bumping the ranks' round counters
-            // (causality is cumulative: every CTA's stores, local and peer,
-            // happen before the last CTA's red.release.sys)
+            // A CTA that stored into peers' memory (NVLink) drains those
+            // stores system-wide itself (a GPU-scope release need not wait
+            // for remote acknowledgements); then a GPU-scope acq_rel counter,
+            // and the grid's last CTA -- which has observed every CTA's
+            // release -- fences system-wide and bumps the ranks' round counters
+            if (p.npeer) __threadfence_system();
             std::uint32_t prev;
             asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done_ctr) : "memory");
             if (prev == gridDim.x - 1u) {  // the grid's last CTA
