@@ -65,9 +65,19 @@ def workload_config(n_gpus: int) -> dict:
     }
 
 
-def make_streams():
-    from paper_2306_03078_b200 import synth
+def _synth():
+    """The synthetic-layer generator (paper_2306_03078_b200/synth.py: numpy
+    only, no native code), loaded by file path so the reference arm never
+    imports the product package."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("spqr_synth", os.path.join(ROOT, "paper_2306_03078_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
+
+def make_streams():
+    synth = _synth()
     cache = os.environ.get("SPQR_BENCH_CACHE", "/tmp/spqr_bench_streams")
     os.makedirs(cache, exist_ok=True)
     out = []
@@ -83,6 +93,20 @@ def make_streams():
             os.replace(tmp, path)
         out.append(s)
     return out
+
+
+def loaded_native_libs() -> list:
+    """Shared objects of this repo mapped into the process (for the record)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                p = line.split()[-1] if line.strip() else ""
+                if p.endswith(".so") and p.startswith(ROOT):
+                    libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def alg_bytes(payload: int, m: int, n: int, x_bytes: int = 2) -> int:
@@ -185,25 +209,70 @@ def cpu_reference_sample(streams) -> dict:
             "seconds": round(total_t, 3), "host": host_cpu()}
 
 
+def reference_check(streams, groups, rank: int, world: int) -> dict:
+    """Refuse to time a wrong kernel (the reference's own guard, kernel.hpp:
+    189-192): one matvec of every launch group on this rank's row band, checked
+    member by member against the reference's matvec(t, x, plan) on the same
+    fp16 x widened to fp32 -- relative L2 (kernel.hpp:154-163) <= 1e-3, the
+    north star's bound.  Exits non-zero otherwise."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2306_03078_b200.sharded import row_bands
+
+    ref = O.Reference()
+    threads = max(1, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    worst = {}
+    for gp in groups:
+        gp["L"].matvec(gp["x"], gp["y"])
+        torch.cuda.synchronize()
+        y = gp["y"].cpu().numpy()
+        x32 = gp["x"].float().cpu().numpy()
+        off, errs = 0, []
+        for i in gp["members"]:
+            m = LAYERS[i][1]
+            r0, r1 = row_bands(m, world)[rank]
+            t = ref.decode(streams[i])
+            nb = max(1, min(threads, (r1 - r0) // 16))
+            edges = [r0 + 16 * (((r1 - r0) // 16) * j // nb) for j in range(nb)] + [r1]
+            bands = [ref.slice_rows(t, edges[j], edges[j + 1]) for j in range(nb)]
+            del t
+            yr = ref.matvec_bands(bands, x32, nb)
+            errs.append(O.relative_l2(y[off:off + r1 - r0], yr))
+            off += r1 - r0
+        worst[gp["name"]] = max(errs)
+    bad = {k: v for k, v in worst.items() if not v <= 1e-3}
+    if bad:
+        print(json.dumps({"error": "matvec does not match the reference (relative L2 > 1e-3)", "rank": rank,
+                          "relative_l2": worst}), flush=True)
+        sys.exit(3)
+    return {"max_relative_l2": max(worst.values()), "per_group": worst, "bound": 1e-3,
+            "against": "reference matvec(t, x, plan) (oracle/_ref) on this rank's band, same fp16 x"}
+
+
 # ------------------------------------------------------------ reference arm --
 def run_reference(args) -> None:
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified headers compiled by oracle/Makefile) on this box's host cores.
+    Never imports or loads the product library: the row bands the thread
+    harness runs are cut with the reference's own types (ref_slice_rows)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    import paper_2306_03078_b200 as P
 
     ref = O.Reference()
     streams = make_streams()
     threads = max(1, len(os.sched_getaffinity(0)))
     bands = []  # per layer: list of reference tensors over row bands
-    bytes_step = 0
     for (name, m, n), s in zip(LAYERS, streams):
+        t = ref.decode(s)
         nb = min(threads, m // 16)
         edges = [16 * ((m // 16) * i // nb) for i in range(nb)] + [m]
-        bands.append([ref.decode(P.slice_rows(s, edges[i], edges[i + 1])) for i in range(nb)])
-        bytes_step += alg_bytes(len(s) - 48, m, n, 4)
+        bands.append([ref.slice_rows(t, edges[i], edges[i + 1]) for i in range(nb)])
+        del t
     xs = [np.random.default_rng(2).standard_normal(n).astype(np.float16).astype(np.float32) for _, _, n in LAYERS]
 
     def step(layer_ids):
@@ -234,9 +303,12 @@ def run_reference(args) -> None:
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{sample}; reference matvec(t, x, plan) on {threads} row bands, "
-                                   f"{threads} threads (oracle/_ref, unmodified headers)", "host": host_cpu()},
+                         "sample": f"{sample}; the reference's single-threaded matvec(t, x, plan) (kernel.hpp:89) "
+                                   f"run on {threads} row bands by {threads} host threads (oracle/_ref, unmodified "
+                                   f"headers; bands cut with the reference's own types, ref_slice_rows)",
+                         "host": host_cpu()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
 
@@ -299,6 +371,7 @@ def run_ours(args) -> None:
             "bands": [(r * per_rank, r * per_rank + per_rank) for r in range(world)],
         })
     payload_step = sum(len(s) - 48 for s in streams)
+    check = reference_check(streams, groups, rank, world)  # before any timing
 
     stream = torch.cuda.Stream(device=dev)
     fused = world > 1
@@ -581,6 +654,7 @@ def run_ours(args) -> None:
             "roofline": roofline, "per_layer": per_layer, "dense_fp16": dense or None,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "multi_gpu": multi,
             "gpu_launches": args.steps * launches_per_step,
+            "parity": check, "native_libs": loaded_native_libs(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

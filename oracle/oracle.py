@@ -248,9 +248,20 @@ class Reference(_Backend):
         L.ref_matvec_bands.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         L.ref_bench_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.ref_measure_actual_bits.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_slice_rows.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]
 
     def _mv(self, h, x, y):
         return self.lib.ref_matvec(h, _ptr(x), _ptr(y))
+
+    def slice_rows(self, t: Tensor, r0: int, r1: int) -> Tensor:
+        """Rows [r0, r1) of a decoded tensor as a reference tensor (ref_slice_rows)."""
+        h = C.c_void_p()
+        rc = self.lib.ref_slice_rows(t.h, r0, r1, C.byref(h))
+        if rc:
+            raise OracleError(rc, "slice_rows")
+        band = Tensor(self, h, None)
+        band.rows, band.cols = r1 - r0, t._dims()[1]
+        return band
 
     def matvec_bands(self, tensors, x, nthreads: int) -> np.ndarray:
         """Multi-core harness: the reference's own matvec on disjoint row bands."""

@@ -87,6 +87,46 @@ int ref_matvec_naive(void* hv, const float* x, float* y) {
     });
 }
 
+// Rows [r0, r1) of a decoded reference tensor as an independent reference
+// tensor (same columns, permutation and flags; statistics of the band's
+// beta2-groups; outliers rebased), with its own TilePlan.  Built from the
+// reference's own types (format.hpp:32-67, solver.hpp:66-142) so the CPU
+// baseline never touches the product library.  r0 must be beta2-aligned.
+int ref_slice_rows(void* hv, uint32_t r0, uint32_t r1, void** out) {
+    *out = nullptr;
+    return guard([&] {
+        const R::SpqrTensor& s = static_cast<Handle*>(hv)->t;
+        if (r0 >= r1 || r1 > s.rows || r0 % s.beta2 != 0)
+            R::fail(R::Errc::config_invalid, "band must be non-empty, in range and beta2-aligned");
+        auto* h = new Handle;
+        R::SpqrTensor& t = h->t;
+        const uint32_t m = r1 - r0, n = s.cols;
+        t.rows = m; t.cols = n; t.weight_bits = s.weight_bits; t.scale_bits = s.scale_bits;
+        t.zero_bits = s.zero_bits; t.beta1 = s.beta1; t.beta2 = s.beta2; t.act_order = s.act_order;
+        t.integer_zero = s.integer_zero; t.full_range_sign = s.full_range_sign;
+        t.outliers_enabled = s.outliers_enabled; t.tau = s.tau; t.lambda_rel = s.lambda_rel;
+        t.permutation = s.permutation;
+        t.codes.rows = m; t.codes.cols = n; t.codes.bits = s.codes.bits;
+        t.codes.codes.assign(s.codes.codes.begin() + static_cast<size_t>(r0) * n,
+                             s.codes.codes.begin() + static_cast<size_t>(r1) * n);
+        t.stats = s.stats;
+        t.stats.rows = m;
+        const uint32_t g0 = r0 / s.beta2, g1 = (r1 + s.beta2 - 1) / s.beta2;
+        for (auto& b : t.stats.blocks) {
+            auto cut = [&](auto& v) {
+                if (!v.empty()) v.assign(v.begin() + r0, v.begin() + r1);
+            };
+            cut(b.scale_codes); cut(b.zero_codes); cut(b.raw_scales); cut(b.raw_zeros);
+            if (!b.groups.empty()) b.groups.assign(b.groups.begin() + g0, b.groups.begin() + g1);
+        }
+        t.outliers.rows = m; t.outliers.cols = n;
+        for (const auto& o : s.outliers.items)
+            if (o.row >= r0 && o.row < r1) t.outliers.items.push_back(R::Outlier{o.row - r0, o.col, o.value16});
+        h->plan = R::build_tile_plan(t);  // kernel.hpp:54
+        *out = h;
+    });
+}
+
 // Row-band harness for the multi-core CPU baseline: each band is an
 // independent reference tensor; `nthreads` threads call the reference's own
 // matvec(t, x, plan) on disjoint bands.  The reference code is unmodified.

@@ -133,8 +133,10 @@ struct spqr_layer {
     } tcp;
     // own workspace
     mutable std::mutex mu;
-    mutable void* d_ws = nullptr;
+    mutable void* d_ws = nullptr;        // device-buffer API (spqr_matvec / _stage / _gather)
     mutable std::uint64_t ws_bytes = 0;
+    mutable void* d_wsh = nullptr;       // host-buffer API (spqr_matvec_host): baked into hgraph
+    mutable std::uint64_t wsh_bytes = 0;
     mutable float* d_xh = nullptr;  // host-API staging
     mutable float* d_yh = nullptr;
     mutable std::size_t xh_cap = 0, yh_cap = 0;
@@ -157,7 +159,7 @@ struct spqr_layer {
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
                         static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start[0]),
                         static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
-                        static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws,
+                        static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws, d_wsh,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
                         static_cast<void*>(cta[0].d_first), static_cast<void*>(cta[1].d_first),
                         static_cast<void*>(tcp.d_start), static_cast<void*>(tcp.d_maps),
@@ -578,18 +580,23 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     }
 }
 
-void ensure_own_ws(const spqr_layer* L, int batch) {
+// A handle-owned workspace, zero-filled (the kernels return the exchange
+// words and counters to zero).  Growing it syncs the device first: an
+// in-flight launch may still use the old one.
+void ensure_ws(const spqr_layer* L, int batch, void*& ws, std::uint64_t& bytes) {
     const std::uint64_t need = ws_layout(L, batch).total;
-    if (L->ws_bytes >= need) return;
-    if (L->d_ws) {
+    if (bytes >= need) return;
+    if (ws) {
         ck(cudaDeviceSynchronize(), "sync before workspace growth");
-        cudaFree(L->d_ws);
-        L->d_ws = nullptr;
+        cudaFree(ws);
+        ws = nullptr;
+        bytes = 0;
     }
-    L->d_ws = dalloc<std::uint8_t>(need);
-    ck(cudaMemset(L->d_ws, 0, need), "zero workspace");
-    L->ws_bytes = need;
+    ws = dalloc<std::uint8_t>(need);
+    ck(cudaMemset(ws, 0, need), "zero workspace");
+    bytes = need;
 }
+void ensure_own_ws(const spqr_layer* L, int batch) { ensure_ws(L, batch, L->d_ws, L->ws_bytes); }
 
 // Static split of the cell sequence over all warps, balanced by bytes
 // (dense cell bytes + a per-outlier instruction cost in byte units).
@@ -933,6 +940,8 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
         std::vector<std::uint8_t> band;
         const std::uint8_t* s = stream;
         std::size_t n = nbytes;
+        if ((o.row_begin != 0 || o.row_end != 0) && o.row_end <= o.row_begin)
+            spqr::fail(spqr::Errc::config_invalid, "row band must be non-empty (0, 0 = all rows)");
         if (o.row_end > o.row_begin) {
             band = spqr::slice_rows(std::span<const std::uint8_t>(stream, nbytes), o.row_begin, o.row_end);
             s = band.data();
@@ -1285,7 +1294,11 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
         g_launches = 0;
         std::lock_guard<std::mutex> lk(L->mu);
         if (batch < 1) spqr::fail(spqr::Errc::shape_mismatch, "batch must be >= 1");
-        ensure_own_ws(L, batch);
+        if (L->wsh_bytes < ws_layout(L, batch).total) {  // the graph bakes the workspace in
+            if (L->hgraph) cudaGraphExecDestroy(L->hgraph);
+            L->hgraph = nullptr;
+            ensure_ws(L, batch, L->d_wsh, L->wsh_bytes);
+        }
         const std::size_t nx = static_cast<std::size_t>(L->info.cols) * batch;
         const std::size_t ny = static_cast<std::size_t>(L->info.rows) * batch;
         if (L->xh_cap < nx || L->yh_cap < ny) {  // device and pinned staging, grown together
@@ -1336,7 +1349,7 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
                 } else {
                     ck(cudaMemcpyAsync(L->d_xh, src, 4 * nx, cudaMemcpyHostToDevice, L->hst), "H2D x");
                 }
-                run_matvec(L, L->d_xh, SPQR_F32, static_cast<float*>(dst), batch, L->d_ws, L->ws_bytes, L->hst);
+                run_matvec(L, L->d_xh, SPQR_F32, static_cast<float*>(dst), batch, L->d_wsh, L->wsh_bytes, L->hst);
             } catch (...) {
                 cudaStreamEndCapture(L->hst, &g);
                 if (g) cudaGraphDestroy(g);

@@ -8,6 +8,8 @@ replicated: in tensor-parallel decode it arrives from the previous layer.
 """
 from __future__ import annotations
 
+import math
+
 import torch
 import torch.distributed as dist
 
@@ -16,12 +18,17 @@ from . import Gather, Layer, validate
 CELL_ROWS = 32  # bands never split a cell (row-group pair); beta2 = 16 divides it
 
 
-def row_bands(m: int, world: int, align: int = CELL_ROWS) -> list[tuple[int, int]]:
-    """Contiguous row bands, `align`-row aligned, sizes differing by at most one
-    `align` unit (the last band also takes the ragged tail)."""
+def row_bands(m: int, world: int, align: int = CELL_ROWS, beta2: int = 16) -> list[tuple[int, int]]:
+    """Contiguous row bands aligned to lcm(`align`, beta2) rows (bands never
+    split a cell or a statistics group), sizes differing by at most one unit
+    (the last band also takes the ragged tail).  Every rank gets a non-empty
+    band: world must not exceed the number of units."""
     if world < 1:
         raise ValueError("world must be >= 1")
+    align = math.lcm(align, beta2)
     units = (m + align - 1) // align
+    if world > units:
+        raise ValueError(f"{world} ranks but only {units} row units of {align} rows: some band would be empty")
     out, u0 = [], 0
     for r in range(world):
         u1 = u0 + units // world + (1 if r < units % world else 0)
@@ -95,7 +102,7 @@ class ShardedLayer:
     def __init__(self, stream: bytes, rank: int, world: int, device: int, fused: bool = False, group=None):
         info = validate(stream)
         self.rows, self.cols = info["rows"], info["cols"]
-        self.bands = row_bands(self.rows, world)
+        self.bands = row_bands(self.rows, world, beta2=info["beta2"])
         self.band = self.bands[rank]
         r0, r1 = self.band
         self.layer = Layer(stream, device=device, rows=(r0, r1) if world > 1 else None)

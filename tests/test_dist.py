@@ -11,16 +11,25 @@ from paper_2306_03078_b200.sharded import row_bands
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("m,world", [(8192, 8), (22016, 8), (22016, 4), (4096, 2), (208, 2), (96, 4), (4, 2)])
-def test_row_bands_cover_and_align(m, world):
-    bands = row_bands(m, world)
+@pytest.mark.parametrize("m,world,beta2", [(8192, 8, 16), (22016, 8, 16), (22016, 4, 16), (4096, 2, 16),
+                                           (208, 2, 16), (96, 3, 16), (40, 2, 16), (8192, 8, 64), (200, 2, 48)])
+def test_row_bands_cover_and_align(m, world, beta2):
+    bands = row_bands(m, world, beta2=beta2)
+    align = 32 * beta2 // __import__("math").gcd(32, beta2)
     assert len(bands) == world
     assert bands[0][0] == 0 and bands[-1][1] == m
     for (a, b), (c, _) in zip(bands, bands[1:]):
         assert b == c
-    assert all(a % 32 == 0 or a == m for a, _ in bands)  # empty tail bands allowed
-    units = [-(-(b - a) // 32) for a, b in bands]  # 32-row cells per band
+    assert all(b > a for a, b in bands)  # no empty band
+    assert all(a % align == 0 for a, _ in bands)  # never splits a cell or a statistics group
+    units = [-(-(b - a) // align) for a, b in bands]
     assert max(units) - min(units) <= 1
+
+
+@pytest.mark.parametrize("m,world", [(96, 4), (4, 2), (31, 2)])
+def test_row_bands_refuse_empty_bands(m, world):
+    with pytest.raises(ValueError):
+        row_bands(m, world)
 
 
 def test_llama_bands_are_equal():
