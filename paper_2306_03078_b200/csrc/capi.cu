@@ -29,38 +29,6 @@ namespace T = spqr_tiled;
 namespace {
 
 constexpr std::uint32_t kSmemLimit = 232448;  // 227 KB per CTA on sm_100
-constexpr std::uint32_t kStaticSmem = 4096;   // mbarriers, slot offsets, row heads
-constexpr std::uint32_t kMaxEntCap = 2048;    // outlier bytes staged per cell (rest: LDG)
-
-// A TMA slot holds the panel's x operands, then one cell record (cell bytes +
-// as many of the cell's outlier entries as fit; the rest are read from HBM).
-constexpr std::uint32_t slot_base(int bw, int bsz, bool xlo) {
-    return spqr_tiled::cell_bytes(bw, bsz, bsz) + spqr_tiled::panel_bytes(xlo);
-}
-// consumer warps per CTA (one CTA per SM): as many as fit two slots each with
-// >= 512 B of staged outliers -- latency is hidden by warps, not deep rings
-#ifndef SPQR_MAX_NW
-#define SPQR_MAX_NW 16
-#endif
-constexpr int kMaxNW = SPQR_MAX_NW;
-constexpr int nw_for(int bw, int bsz, bool xlo) {
-    return kMaxNW * 2 * (slot_base(bw, bsz, xlo) + 512) + kStaticSmem <= kSmemLimit ? kMaxNW : 16;
-}
-// ring depth per warp: 3 slots when they fit with >= 1 KB of entries, else 2
-constexpr int nslot_for(int bw, int bsz, bool xlo) {
-    return nw_for(bw, bsz, xlo) * 3 * (slot_base(bw, bsz, xlo) + 1024) + kStaticSmem <= kSmemLimit ? 3 : 2;
-}
-constexpr std::uint32_t slot_bytes_for(int bw, int bsz, bool xlo) {
-    const std::uint32_t avail =
-        ((kSmemLimit - kStaticSmem) / (nw_for(bw, bsz, xlo) * nslot_for(bw, bsz, xlo))) & ~127u;
-    const std::uint32_t want = (slot_base(bw, bsz, xlo) + kMaxEntCap + 127u) & ~127u;
-    return want < avail ? want : avail;
-}
-constexpr std::uint32_t rec_cap_for(int bw, int bsz, bool xlo) {  // record bytes per slot
-    return slot_bytes_for(bw, bsz, xlo) - spqr_tiled::panel_bytes(xlo);
-}
-static_assert(rec_cap_for(4, 4, true) >= spqr_tiled::cell_bytes(4, 4, 4), "slot must hold a cell");
-static_assert(nw_for(3, 3, false) <= kMaxNW && nw_for(3, 3, true) <= kMaxNW, "warp count");
 
 thread_local int g_launches = 0;
 
@@ -108,12 +76,7 @@ struct spqr_layer {
     bool stacked = false;  // several streams stacked row-wise (matvec only)
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
-    std::uint32_t* d_warp_start[2] = {nullptr, nullptr};  // per x dtype (f16, f32): warp count differs
-    std::uint32_t* d_wfirst[2] = {nullptr, nullptr};
-    std::uint32_t* d_wlast = nullptr;
-    std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, grid = 0, n_pad = 0;
-    std::uint32_t nwarps[2] = {0, 0};
-    std::uint32_t partial_slots[2] = {0, 0};
+    std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, n_pad = 0;
     // gemv_cta plan, per x dtype (f16, f32: the panel size differs)
     struct CtaPlan {
         std::uint32_t nvcta = 0, grid = 0, nslot_log2 = 0, slot_bytes = 0, rec_cap = 0;
@@ -157,9 +120,7 @@ struct spqr_layer {
         if (h_x) cudaFreeHost(h_x);
         if (h_y) cudaFreeHost(h_y);
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
-                        static_cast<void*>(d_cell_off), static_cast<void*>(d_warp_start[0]),
-                        static_cast<void*>(d_warp_start[1]), static_cast<void*>(d_wfirst[0]),
-                        static_cast<void*>(d_wfirst[1]), static_cast<void*>(d_wlast), d_ws, d_wsh,
+                        static_cast<void*>(d_cell_off), d_ws, d_wsh,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
                         static_cast<void*>(cta[0].d_first), static_cast<void*>(cta[1].d_first),
                         static_cast<void*>(tcp.d_start), static_cast<void*>(tcp.d_maps),
@@ -196,9 +157,11 @@ spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
     return g;
 }
 
-// Workspace carve-up (bytes, 256-aligned pieces).
+// Workspace carve-up (bytes, 256-aligned pieces).  The regions the kernels
+// count in (xcnt, tc_cnt) must be zero before the first launch; every launch
+// leaves them zero again.
 struct WsLayout {
-    std::uint64_t panels = 0, panel_stride = 0, xp = 0, partial = 0, counters = 0, xchg = 0;
+    std::uint64_t xpart = 0, xcnt = 0, xp = 0;
     std::uint64_t tc_x = 0, tc_part = 0, tc_cnt = 0, total = 0;
 };
 std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
@@ -207,17 +170,15 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
     const std::uint64_t b = static_cast<std::uint64_t>(std::max(batch, 1));
     std::uint64_t o = 0;
     if (L->fast) {
-        // x panels sized for the fp32-input layout (the larger of the two)
-        w.panel_stride = static_cast<std::uint64_t>(L->Pn) * spqr_tiled::panel_bytes(true);
-        w.panels = o; o += al(b * w.panel_stride);
-        w.partial = o; o += al(static_cast<std::uint64_t>(std::max(L->partial_slots[0], L->partial_slots[1])) * 32 * 4);
-        w.xchg = o; o += al(static_cast<std::uint64_t>(L->Gn) * 32 * 8);
+        // pairs shared by two gemv_cta ranges: partial rows + arrival tickets
+        const std::uint64_t nb = std::max(L->cta[0].nvcta, L->cta[1].nvcta) + 1ull;
+        w.xpart = o; o += al(nb * 2 * 32 * 4);
+        w.xcnt = o; o += al(nb * 4);
         if (batch >= 2) {  // gemm_tc: x tiles for N <= 128, partial tiles, per-warp tile counters
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
             w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 16 * 4);
         }
-        w.counters = o; o += al(static_cast<std::uint64_t>(L->Gn) * 4);
     } else {
         w.xp = o; o += al(b * L->info.cols * 4);
     }
@@ -225,55 +186,12 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
     return w;
 }
 
-template <int BW, int BSZ, bool XLO>
-void launch_tiled_t(const spqr_dev::TiledParams& p, std::uint32_t grid, std::size_t smem, cudaStream_t st) {
-    constexpr int NW = nw_for(BW, BSZ, XLO);
-    auto kern = spqr_dev::gemv_tiled<BW, BSZ, BSZ, XLO, NW, nslot_for(BW, BSZ, XLO)>;
-    static bool attr_set[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
-        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-           "cudaFuncSetAttribute(smem)");
-        attr_set[dev & 63] = true;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NW * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemv_tiled");
-    ++g_launches;
-}
-
-
-// ---- gemv_cta (v13): producer warp + kNC consumer warps per CTA ----------
+// ---- gemv_cta (v14): kNC warps per CTA, one CTA per SM ------------------
 #ifndef SPQR_NC
 #define SPQR_NC 16
 #endif
 constexpr int kNC = SPQR_NC;  // 16: 4 warps per SMSP, up to 128 registers each
-constexpr std::uint32_t kCtaStaticMax = 6144;  // static smem of gemv_cta (checked at first launch)
-
-bool use_batch_loop() {  // A/B switch: batch >= 2 as repeated batch-1 launches
-    static const bool loop = [] {
-        const char* e = std::getenv("SPQR_BATCH");
-        return e && std::string(e) == "loop";
-    }();
-    return loop;
-}
-
-bool use_legacy_tiled() {
-    static const bool legacy = [] {
-        const char* e = std::getenv("SPQR_KERNEL");
-        return e && std::string(e) == "tiled";
-    }();
-    return legacy;
-}
+constexpr std::uint32_t kCtaStaticMax = 10240;  // static smem of gemv_cta (checked at first launch)
 
 template <int BW, int BSZ, bool XLO, bool SHX>
 void launch_cta_t(const spqr_dev::CtaParams& p, std::uint32_t grid, std::uint32_t smem, cudaStream_t st) {
@@ -335,11 +253,7 @@ std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N, std::uint32_t na) {
 // A stage buffers: a fourth (one more half cell of lookahead between the
 // dequant warps) whenever it fits next to the x tiles of this N
 std::uint32_t tc_na(const spqr_layer* L, std::uint32_t N) {
-    static const bool force3 = [] {
-        const char* e = std::getenv("SPQR_TC_NA");  // "3": measurement override
-        return e && e[0] == '3';
-    }();
-    return !force3 && tc_smem(L, N, 4u) + kTcStaticMax <= kSmemLimit ? 4u : 3u;
+    return tc_smem(L, N, 4u) + kTcStaticMax <= kSmemLimit ? 4u : 3u;
 }
 
 template <int BW, int BSZ>
@@ -431,61 +345,6 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
     }
 }
 
-// x panels for `batch` columns; column b's panels start at b * panel_stride.
-template <int BW, bool XLO>
-void launch_xprep_t(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,
-                    std::uint64_t panel_stride, cudaStream_t st) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(L->n_pad / 128, static_cast<unsigned>(batch), 1);
-    cfg.blockDim = dim3(128, 1, 1);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_tiled<BW, XLO>, x, f16, L->info.cols, L->n_pad,
-                          static_cast<const std::uint32_t*>(L->d_order), panels, panel_stride),
-       "launch xprep_tiled");
-    ++g_launches;
-}
-
-void dispatch_xprep(const void* x, int f16, const spqr_layer* L, int batch, std::uint8_t* panels,
-                    std::uint64_t stride, cudaStream_t st) {
-    const bool lo = !f16;
-    switch (L->info.weight_bits * 2 + (lo ? 1 : 0)) {
-        case 4: launch_xprep_t<2, false>(x, f16, L, batch, panels, stride, st); break;
-        case 5: launch_xprep_t<2, true>(x, f16, L, batch, panels, stride, st); break;
-        case 6: launch_xprep_t<3, false>(x, f16, L, batch, panels, stride, st); break;
-        case 7: launch_xprep_t<3, true>(x, f16, L, batch, panels, stride, st); break;
-        case 8: launch_xprep_t<4, false>(x, f16, L, batch, panels, stride, st); break;
-        default: launch_xprep_t<4, true>(x, f16, L, batch, panels, stride, st); break;
-    }
-}
-
-std::size_t tiled_smem(const spqr_layer* L, bool xlo, std::uint32_t* slot_bytes, std::uint32_t* rec_cap) {
-    const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
-    *slot_bytes = slot_bytes_for(bw, bsz, xlo);
-    *rec_cap = rec_cap_for(bw, bsz, xlo);
-    return static_cast<std::size_t>(nw_for(bw, bsz, xlo)) * nslot_for(bw, bsz, xlo) * *slot_bytes;
-}
-
-void dispatch_tiled(const spqr_dev::TiledParams& p, const spqr_layer* L, bool xlo, std::size_t smem,
-                    cudaStream_t st) {
-    const int key = L->info.weight_bits * 100 + L->info.scale_bits * 10 + (xlo ? 1 : 0);
-    switch (key) {
-#define SPQR_CASE(BW, BSZ)                                                            \
-    case BW * 100 + BSZ * 10 + 0: launch_tiled_t<BW, BSZ, false>(p, L->grid, smem, st); break; \
-    case BW * 100 + BSZ * 10 + 1: launch_tiled_t<BW, BSZ, true>(p, L->grid, smem, st); break;
-        SPQR_CASE(2, 2) SPQR_CASE(2, 3) SPQR_CASE(2, 4)
-        SPQR_CASE(3, 2) SPQR_CASE(3, 3) SPQR_CASE(3, 4)
-        SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
-#undef SPQR_CASE
-        default: spqr::fail(spqr::Errc::config_invalid, "no tiled kernel instantiated for this layer");
-    }
-}
-
 // gemv_cta launch parameters for one batch column
 spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int f16, float* y, std::uint8_t* base,
                                const WsLayout& w) {
@@ -497,7 +356,8 @@ spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int f16, floa
     p.x = x;
     p.order = static_cast<const std::uint32_t*>(L->d_order);
     p.y = y;
-    p.xchg = reinterpret_cast<unsigned long long*>(base + w.xchg);
+    p.xpart = reinterpret_cast<float*>(base + w.xpart);
+    p.xcnt = reinterpret_cast<std::uint32_t*>(base + w.xcnt);
     p.m = L->info.rows; p.n = L->info.cols; p.Pn = L->Pn; p.Gn = L->Gn; p.nvcta = c.nvcta;
     p.pn_magic = L->pn_magic;
     p.rec_cap = c.rec_cap; p.slot_bytes = c.slot_bytes;
@@ -521,12 +381,12 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
-    if (L->fast && !use_legacy_tiled() && batch >= kTcMinBatch && !use_batch_loop()) {
+    if (L->fast && batch >= kTcMinBatch) {
         if (stage == 1) return;
         run_tc(L, x, f16, y, batch, base, w, st);
         return;
     }
-    if (L->fast && !use_legacy_tiled()) {
+    if (L->fast) {
         // one fused launch per batch column (x preparation happens inside)
         if (stage == 1) return;
         const std::size_t esz = f16 ? 2 : 4;
@@ -535,30 +395,6 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
                                                       static_cast<std::size_t>(b) * L->info.cols * esz,
                                                f16, y + static_cast<std::size_t>(b) * L->info.rows, base, w);
             dispatch_cta(p, L, !f16, st);
-        }
-        return;
-    }
-    if (L->fast) {
-        auto* panels = base + w.panels;
-        if (stage != 2) dispatch_xprep(x, f16, L, batch, panels, w.panel_stride, st);
-        if (stage == 1) return;
-        std::uint32_t slot_bytes = 0, rec_cap = 0;
-        const std::size_t smem = tiled_smem(L, !f16, &slot_bytes, &rec_cap);
-        for (int b = 0; b < batch; ++b) {
-            spqr_dev::TiledParams p{};
-            p.cells = L->d_cells;
-            p.cell_off = L->d_cell_off;
-            const int xi = f16 ? 0 : 1;
-            p.warp_start = L->d_warp_start[xi];
-            p.gmap = L->d_wfirst[xi];
-            p.wmap = L->d_wfirst[xi] + 2 * L->Gn;
-            p.xpanel = panels + b * w.panel_stride;
-            p.y = y + static_cast<std::size_t>(b) * L->info.rows;
-            p.partial = reinterpret_cast<float*>(base + w.partial);
-            p.counters = reinterpret_cast<std::uint32_t*>(base + w.counters);
-            p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.nwarps = L->nwarps[xi];
-            p.rec_cap_bytes = rec_cap; p.slot_bytes = slot_bytes;
-            dispatch_tiled(p, L, !f16, smem, st);
         }
     } else {
         auto* xp = reinterpret_cast<float*>(base + w.xp);
@@ -597,58 +433,6 @@ void ensure_ws(const spqr_layer* L, int batch, void*& ws, std::uint64_t& bytes) 
     bytes = need;
 }
 void ensure_own_ws(const spqr_layer* L, int batch) { ensure_ws(L, batch, L->d_ws, L->ws_bytes); }
-
-// Static split of the cell sequence over all warps, balanced by bytes
-// (dense cell bytes + a per-outlier instruction cost in byte units).
-void plan_partition(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) {
-    const std::uint32_t Q = t.Gn * t.Pn;
-    L->grid = static_cast<std::uint32_t>(sms);
-    const int bw = L->info.weight_bits, bsz = L->info.scale_bits;
-    const std::uint32_t nw = static_cast<std::uint32_t>(nw_for(bw, bsz, xi == 1));
-    std::uint32_t& nwarps = L->nwarps[xi];
-    nwarps = L->grid * nw;
-    std::vector<double> pre(Q + 1, 0.0);
-    for (std::uint32_t q = 0; q < Q; ++q)
-        pre[q + 1] = pre[q] + 1024.0 + (t.cell_off[q + 1] - t.cell_off[q]);  // x panel + record
-    const double total = pre[Q];
-    std::vector<std::uint32_t> ws(nwarps + 1, Q);
-    std::uint32_t q = 0;
-    for (std::uint32_t k = 0; k < nwarps; ++k) {
-        const double target = total * k / nwarps;
-        while (q < Q && pre[q] + 0.5 * (pre[q + 1] - pre[q]) < target) ++q;
-        ws[k] = q;
-    }
-    ws[nwarps] = Q;
-    // Row-group pairs split between warps are reduced through partial slots:
-    // G's contributors (warps whose range touches G, in warp order) get slots
-    // pbase[G] + 0 .. count-1; each warp records its ordinal in its first and
-    // last G.  gmap[G] = {pbase, count}; wmap[k] = {ord_first, ord_last}.
-    std::vector<std::uint32_t> gmap(2ull * t.Gn, 0), wmap(2ull * nwarps, 0);
-    for (std::uint32_t k = 0; k < nwarps; ++k) {
-        if (ws[k] >= ws[k + 1]) continue;
-        const std::uint32_t ga = ws[k] / t.Pn, gb = (ws[k + 1] - 1) / t.Pn;
-        wmap[2 * k] = gmap[2 * ga + 1]++;
-        if (gb != ga) {
-            for (std::uint32_t G = ga + 1; G < gb; ++G) gmap[2 * G + 1]++;  // fully covered: 1 contributor
-            wmap[2 * k + 1] = gmap[2 * gb + 1]++;
-        } else {
-            wmap[2 * k + 1] = wmap[2 * k];
-        }
-    }
-    std::uint32_t slots = 0;
-    for (std::uint32_t G = 0; G < t.Gn; ++G) {
-        gmap[2 * G] = slots;
-        slots += gmap[2 * G + 1];
-    }
-    L->partial_slots[xi] = slots;
-    L->d_warp_start[xi] = dalloc<std::uint32_t>(ws.size());
-    L->d_wfirst[xi] = dalloc<std::uint32_t>(gmap.size() + wmap.size());
-    ck(cudaMemcpy(L->d_warp_start[xi], ws.data(), 4 * ws.size(), cudaMemcpyHostToDevice), "H2D warp_start");
-    ck(cudaMemcpy(L->d_wfirst[xi], gmap.data(), 4 * gmap.size(), cudaMemcpyHostToDevice), "H2D gmap");
-    ck(cudaMemcpy(L->d_wfirst[xi] + gmap.size(), wmap.data(), 4 * wmap.size(), cudaMemcpyHostToDevice),
-       "H2D wmap");
-}
-
 
 // gemv_cta partition: contiguous cell ranges balanced by bytes (record bytes +
 // a per-cell fixed cost), one range per CTA -- or several per CTA when the
@@ -831,8 +615,6 @@ void make_plans(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vect
     L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
     int sms = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
-    plan_partition(L, t, sms, 0);
-    plan_partition(L, t, sms, 1);
     plan_cta(L, t, sms, 0);
     plan_cta(L, t, sms, 1);
     plan_tc(L, t, views, sms);
@@ -1220,7 +1002,7 @@ int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr
         g_launches = 0;
         if (!g->open) spqr::fail(spqr::Errc::config_invalid, "gather: spqr_gather_open first");
         if (g->device != L->device) spqr::fail(spqr::Errc::config_invalid, "gather: layer and buffer devices differ");
-        if (!L->fast || use_legacy_tiled())
+        if (!L->fast)
             spqr::fail(spqr::Errc::config_invalid, "fused all-gather needs a fast-path (tiled) layer");
         if (x_dtype != SPQR_F16 && x_dtype != SPQR_F32) spqr::fail(spqr::Errc::config_invalid, "x dtype must be f16 or f32");
         const std::uint32_t rb = g->row_base[g->rank];

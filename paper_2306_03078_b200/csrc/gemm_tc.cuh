@@ -420,8 +420,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 // statistics: lane owns (row g + 8rho, block 8hh + 2t + bs) of unit uu
                 // for this warp's halves hh; the two blocks bs = 0, 1 ride in the
                 // halves of packed f32x2 math
-                std::uint32_t ss, zz;
-                load_stats<BS, BZ>(unit + CODEB, lane, ss, zz);
+                std::uint32_t st[2];  // lo (row g) / hi (row g + 8) statistic streams
+                load_stat_streams<BS>(unit + CODEB, lane, st);
 #pragma unroll
                 for (int hi = 0; hi < HPW; ++hi) {
                     const int hh = h0 + hi;
@@ -434,12 +434,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     const float2 Zz = make_float2(-__high2float(zh0), -__high2float(zh1));
 #pragma unroll
                     for (int rho = 0; rho < 2; ++rho) {
-                        const int e0 = 4 * hh + rho, e1 = 4 * hh + 2 + rho;  // eps of bs = 0, 1
-                        const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss, e0 * BS, magic),
-                                                            magic_field_rt<SMASK>(ss, e1 * BS, magic)),
+                        // pairs j = 4 kind + 2 hh + bs at stream bit BS j (tiled.hpp)
+                        const int j0 = T::stat_pair(0, hh, 0), j1 = T::stat_pair(0, hh, 1);
+                        const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(st[rho], j0 * BS, magic),
+                                                            magic_field_rt<SMASK>(st[rho], j1 * BS, magic)),
                                                 make_float2(-kMagic, -kMagic));
-                        const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz, e0 * BZ, magic),
-                                                            magic_field_rt<ZMASK>(zz, e1 * BZ, magic)),
+                        const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(st[rho], (j0 + 4) * BZ, magic),
+                                                            magic_field_rt<ZMASK>(st[rho], (j1 + 4) * BZ, magic)),
                                                 make_float2(-kMagic, -kMagic));
                         const float2 shat = fmul2(Ss, fadd2(cs, Zs));
                         const float2 zhat = fmul2(Sz, fadd2(cz, Zz));

@@ -1,55 +1,48 @@
-// gemv_cta.cuh -- the fused SpQR decode-GEMV + CSR outlier merge, v13
+// gemv_cta.cuh -- the fused SpQR decode-GEMV + CSR outlier merge, v14
 // (sm_100a).  Included by kernels.cuh (inside namespace spqr_dev).
 //
 // Reference semantics: matvec(t, x, plan), kernel.hpp:89-124 (x gather through
 // the permutation :93-98, per-tile dequant :100-111, CSR slices :112-120) --
 //   y[r] = sum_k  s(k,r) * sum_{c in k} (q(r,c) - z(k,r)) * x[c]  +  sum_outliers v * x[col]
-// computed per (row, 16-column block k) as  s*2^(24-e_k) * ( C + z * XX_k ),
-//   C = sum_c (q_c 2^(p_c-24)) (x_c 2^(e_k-p_c))   (m16n8k16 f16 MMA, exact products)
-//   XX_k = -2^-24 sum_c x_c 2^e_k.
+// The first-level statistics are stat_dequant (quantizer.hpp:65-67) of 3-bit
+// codes under binary16 second-level scalars (solver.hpp:129-141).
+//
+// Per (row, 16-column block k) of a cell, in registers:
+//   C      = sum_c (q_c 2^(p_c-24)) B_c                   m16n8k16 f16 MMA, exact products
+//   s'     = S_s * (cs 2^(p_s-24)) - S_s Z_s 2^(p_s-24)    one fma.rn.f32.f16 (FHFMA)
+//   z'     = S_z * (cz 2^(p_z-24)) - S_z Z_z 2^(p_z-24)    one FHFMA
+//   acc   += s' * (C + z' XX_k)                            two packed f32x2 FMAs per 2 blocks
+// with B_c = x_c 2^(e - p_c - p_s(k)) (fp16) and XX_k = -2^(-p_z(k)) sum_c B_c 2^p_c,
+// so s'(C + z' XX) = 2^(e-48) s (sum_c (q_c - z) x_c): one power of two per
+// panel (SC = 2^(48-e)) turns a cell's row sums into y.  The statistic codes
+// arrive as binary16 subnormals straight from one LOP3 of their lane field
+// (tiled.hpp), the -S Z 2^(p-24) terms come from a per-warp table each lane
+// fills one entry of, so a (row, block) costs ~4 instructions.
 //
 // Structure (one CTA per SM, NC warps):
-//  * the host cuts the cell sequence (row-major 32x256 cells) into per-CTA
-//    contiguous, byte-balanced ranges ("vctas"; more vctas than CTAs only for
-//    layers whose per-CTA partial-sum array would not fit shared memory);
-//  * warps take cells dynamically (a shared ticket counter), so the warps of
-//    an SM finish together whatever their relative speed; each warp holds one
-//    ticket of lookahead and has already issued that cell's record copy
-//    (cp.async.bulk into the warp's second slot, mbarrier completion) while it
-//    computes the current one.  Issue is spread over all warps on purpose: a
-//    single producer thread caps at ~240 cycles per bulk copy (~4.8 TB/s for
-//    4 KB records, tools/tma_bench.cu).  The first records are issued before
-//    the preceding kernel has finished (PDL: weights do not depend on it), from
-//    offsets the plan precomputed per CTA; the first range's bounds arrive by
-//    value in the launch parameters, so no global load precedes the PDL wait;
-//  * x panels (x gather through the permutation, per-block power-of-two
-//    scale, 2^-p column pre-scale, block sums) are built after the PDL wait:
-//    once per CTA into shared memory when all Pn panels fit (SHX, per-panel
-//    ready flags, no CTA barrier), else by each warp for its cell -- no
-//    separate x-preparation kernel, no x traffic through the ring;
+//  * the host cuts the cell sequence (row-major 32x256 cells) into contiguous
+//    byte-balanced ranges, one per CTA (more only when a range's row-sum array
+//    would not fit shared memory);
+//  * warps take cells dynamically (a shared ticket counter) and hold one
+//    ticket of lookahead whose record copy (cp.async.bulk, mbarrier) is in
+//    flight while the current cell computes; the first records go out before
+//    the preceding kernel has finished (PDL: weights do not depend on it);
+//  * x panels (gather through the permutation, per-panel power-of-two scale,
+//    per-column pre-scales, block sums) are built after the PDL wait: once
+//    per CTA into shared memory when all Pn panels fit (SHX), else per cell;
 //  * per cell the warp writes 32 row sums (MMA part + outliers) to a per-CTA
 //    array and counts the cell against its row-group pair; the warp that
-//    completes a pair adds its cells' row sums in cell order and writes y --
-//    during the range, not after it.  A pair shared with a neighbouring range
-//    (ranges hold >= Pn cells, so at most two share a pair) is exchanged
-//    through one 64-bit {value, flag} word per row: the range that starts
-//    inside the pair finishes it first and publishes; the range that ends
-//    inside it adds the published value after its own and resets the word.
-//    No atomics on global memory, no fences, no end-of-kernel barrier (the
-//    wait is bounded: a launch whose CTAs are not co-resident traps).
+//    completes a pair adds its cells in cell order and writes y.  A pair
+//    shared with the neighbouring range (ranges hold >= Pn cells, so at most
+//    two share a pair) is finished by whichever side completes second: both
+//    store their partial rows to a global slot, the second arriver (atomic
+//    ticket) adds first-side + last-side and resets the ticket -- no CTA ever
+//    waits for another, so launches need not be co-resident.
 //  * GATHER = true (row-sharded decode, gather.cu): every y row is also stored
 //    into the other ranks' full-y buffers and the grid's last CTA bumps this
 //    rank's round counter on every rank; gather_wait consumes it.
 // Every reduction order is fixed by the partition, not by the schedule, so y
 // is bitwise reproducible run to run.
-
-// Cells of a range split into two half tickets at its end (see decode()):
-// measured slower than whole cells (a half ticket costs ~2/3 of a cell), so
-// off by default; -DSPQR_SPLIT_CELLS_FN='min(NC / 2u, nc / 2u)' turns it on.
-#ifndef SPQR_SPLIT_CELLS_FN
-#define SPQR_SPLIT_CELLS_FN 0u
-#define SPQR_SPLIT_OFF 1
-#endif
 
 constexpr int kQFirst = 161;
 constexpr int kMaxPeers = 7;  // 8 ranks per node
@@ -60,7 +53,8 @@ struct CtaParams {
     const void* x;                    // this batch column, original column order (f16 or f32)
     const std::uint32_t* order;       // solve position -> source column, or null
     float* y;                         // [m] this batch column
-    unsigned long long* xchg;         // [Gn][32] {float value, u32 flag}, zero between launches
+    float* xpart;                     // [nvcta+1][2][32] partial rows of pairs shared by two ranges
+    std::uint32_t* xcnt;              // [nvcta+1] arrivals per shared pair (zero between launches)
     std::uint32_t m, n, Pn, Gn, nvcta;
     std::uint32_t pn_magic;           // q / Pn == umulhi(q, pn_magic) for every cell index q
     std::uint32_t rec_cap, slot_bytes;
@@ -69,7 +63,7 @@ struct CtaParams {
     const uint2* first_rec;           // [grid][NC] {r0, r1}: record of warp w's first cell (r0 == r1: none)
     // cta_start[0 .. grid] by value (grid < kQFirst): the first range's bounds
     // come from the parameter bank, not from HBM while the preceding kernel
-    // saturates it (a ~1.4 us load ahead of the PDL wait)
+    // saturates it
     std::uint32_t q_first[kQFirst];
     // Fused all-gather (row-sharded decode): every final y row
     // is also stored into the full-y buffers of the npeer other ranks (P2P /
@@ -83,26 +77,6 @@ struct CtaParams {
     std::uint32_t npeer, nflag, row_base, rank;
 };
 
-// The neighbouring range's published partial row sum: the CTAs of a launch
-// are co-resident (grid <= SMs, one CTA per SM), so it arrives; if it does not
-// within 10 s (e.g. SMs withheld by an MPS partition), fail the launch rather
-// than hold the GPU.
-static __device__ __noinline__ unsigned long long spin_published(const unsigned long long* xw) {
-    unsigned long long w, t0, t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-    for (std::uint32_t it = 1;; ++it) {
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
-        if ((w >> 32) != 0ull) return w;
-        if ((it & 4095u) == 0u) {
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            if (t - t0 > 10000000000ull) __trap();
-        }
-    }
-}
-
-__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void bar_sync_named(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -111,15 +85,47 @@ __device__ __forceinline__ std::uint32_t pack_h2_rn(float lo, float hi) {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
+// a * b + c with a = half HA of a2, b = half HB of b2 (binary16), c and the
+// result binary32: one FHFMA (mixed-precision fma.rn.f32.f16, sm_100); the
+// product of two binary16 values is exact, so the result is rounded once.
+template <int HA, int HB>
+__device__ __forceinline__ float fhfma(std::uint32_t a2, std::uint32_t b2, float c) {
+    float d;
+    if constexpr (HA == 0 && HB == 0)
+        asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+            "fma.rn.f32.f16 %0, al, bl, %3;\n\t}"
+            : "=f"(d) : "r"(a2), "r"(b2), "f"(c));
+    else if constexpr (HA == 0 && HB == 1)
+        asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+            "fma.rn.f32.f16 %0, al, bh, %3;\n\t}"
+            : "=f"(d) : "r"(a2), "r"(b2), "f"(c));
+    else if constexpr (HA == 1 && HB == 0)
+        asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+            "fma.rn.f32.f16 %0, ah, bl, %3;\n\t}"
+            : "=f"(d) : "r"(a2), "r"(b2), "f"(c));
+    else
+        asm("{\n\t.reg .b16 al, ah, bl, bh;\n\tmov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+            "fma.rn.f32.f16 %0, ah, bh, %3;\n\t}"
+            : "=f"(d) : "r"(a2), "r"(b2), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float pow2f(int k) {  // 2^k for k in [-126, 127]
+    return __uint_as_float(static_cast<std::uint32_t>(127 + k) << 23);
+}
+
+// Pre-scales of a panel column (block kk of the panel, column cc in the block):
+// the weight code's (p_c) and the block's scale / zero code pairs' (p_s, p_z).
+template <int BW, int BS>
+__device__ __forceinline__ void column_scales(std::uint32_t kk, std::uint32_t cc, int& pc, int& ps, int& pz) {
+    pc = T::column_prescale(BW, kk, cc);
+    const int h = static_cast<int>((kk >> 3) & 1u), b = static_cast<int>(kk & 1u);
+    ps = T::stat_p(BS, T::stat_pair(0, h, b));
+    pz = T::stat_p(BS, T::stat_pair(1, h, b));
+}
 
 // One lane's share of a cell's x panel: columns 8*lane .. 8*lane+7 of panel P
 // (block kk = lane/2, half hf = lane%2).  load_x fetches them (through the
-// permutation, zero beyond n) -- issued one cell ahead; build_panel writes
-// the panel layout of tiled.hpp (panel_bytes): B rows fp16(x 2^(e-p)) [+ low
-// halves for fp32 x], {SC, XX} per block, x in solve order for the outlier
-// merge.  Same values as the v1-v12 xprep_tiled kernel: e = per-block
-// power-of-two scale (max |x| in [2^14, 2^15)), p = the column's code
-// pre-scale, SC = 2^(24-e), XX = -2^-24 sum_c x_c 2^e.
+// permutation, zero beyond n); build_panel writes the panel (tiled.hpp).
 template <bool XLO>
 struct XLane {
     std::uint32_t w[XLO ? 8 : 4];  // fp16 pairs, or fp32 bit patterns
@@ -162,10 +168,13 @@ __device__ __forceinline__ XLane<XLO> load_x(const CtaParams& p, std::uint32_t P
     return r;
 }
 
-template <int BW, bool XLO>
-__device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int pp, std::uint8_t* pan) {
-    constexpr std::uint32_t O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
-    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
+template <int BW, int BS, bool XLO>
+__device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std::uint8_t* pan) {
+    constexpr std::uint32_t O_XX = T::kPanelXXOff, O_SC = T::kPanelSCOff, O_XP = T::kPanelXPOff;
+    constexpr std::uint32_t O_LO = T::panel_lo_off(XLO);
+    const std::uint32_t kk = static_cast<std::uint32_t>(lane) >> 1, cc = 8u * (lane & 1);
+    int pc, ps, pz;
+    column_scales<BW, BS>(kk, cc, pc, ps, pz);
     float f[8];
     if constexpr (!XLO) {
 #pragma unroll
@@ -182,37 +191,27 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
         xp[0] = make_uint4(xl.w[0], xl.w[1], xl.w[2], xl.w[3]);
         xp[1] = make_uint4(xl.w[4], xl.w[5], xl.w[6], xl.w[7]);
     }
+    // the panel's scale: max |x| 2^e in [2^14, 2^15)
     float mx = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(f[i]));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
     int e = 0;
     if (mx > 0.f && mx < INFINITY) {
-        // mx = m * 2^E, m in [0.5, 1): E from the exponent field (frexpf for
-        // fp32 subnormals; fp16 x is always normal as fp32)
         const std::uint32_t eb = __float_as_uint(mx) >> 23;
-        int E = static_cast<int>(eb) - 126;
-        if (XLO && eb == 0u) frexpf(mx, &E);
-        e = 15 - E;  // mx * 2^e in [2^14, 2^15)
+        int E = static_cast<int>(eb) - 126;  // mx = m 2^E, m in [0.5, 1)
+        if (XLO && eb == 0u) frexpf(mx, &E);  // fp32 subnormal max
+        e = 15 - E;
     }
-    // 2^(e - pp): for fp16 x, e - pp is in [-8, 38] and the scaling is a plain
-    // exact multiply; fp32 x can reach the edges of the exponent range
+    // B = x 2^(e - pc - ps): fp16 x keeps e - pc - ps in [-15, 38]; fp32 x may
+    // need two factors at the ends of the exponent range
+    const int k = e - pc - ps;
+    const int k1 = k < -126 ? -126 : (k > 127 ? 127 : k), k2 = k - k1;
+    const float sc1 = pow2f(k1), sc2 = pow2f(k2 < -126 ? -126 : (k2 > 127 ? 127 : k2));
     float s[8];
-    if constexpr (XLO) {
-        const int k = e - pp;
-        if (k >= -126 && k <= 127) {  // 2^k is a normal float: one exact-as-ldexpf multiply
-            const float sc = __uint_as_float(static_cast<std::uint32_t>(127 + k) << 23);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s[i] = f[i] * sc;
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) s[i] = ldexpf(f[i], k);
-        }
-    } else {
-        const float sc = __uint_as_float(static_cast<std::uint32_t>(127 + e - pp) << 23);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = f[i] * sc;
-    }
+    for (int i = 0; i < 8; ++i) s[i] = XLO ? (f[i] * sc1) * sc2 : f[i] * sc1;
     std::uint32_t hv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) hv[i] = pack_h2_rn(s[2 * i], s[2 * i + 1]);
@@ -222,31 +221,31 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
         std::uint32_t lv[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 h = __half22float2(u32_as_h2(hv[i]));
-            lv[i] = pack_h2_rn(s[2 * i] - h.x, s[2 * i + 1] - h.y);
+            const float2 hh = __half22float2(u32_as_h2(hv[i]));
+            lv[i] = pack_h2_rn(s[2 * i] - hh.x, s[2 * i + 1] - hh.y);
             const float2 l = __half22float2(u32_as_h2(lv[i]));
-            eff[2 * i] = h.x + l.x;
-            eff[2 * i + 1] = h.y + l.y;
+            eff[2 * i] = hh.x + l.x;
+            eff[2 * i + 1] = hh.y + l.y;
         }
         *reinterpret_cast<uint4*>(pan + O_LO + 16u * lane) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 h = __half22float2(u32_as_h2(hv[i]));
-            eff[2 * i] = h.x;
-            eff[2 * i + 1] = h.y;
+            const float2 hh = __half22float2(u32_as_h2(hv[i]));
+            eff[2 * i] = hh.x;
+            eff[2 * i + 1] = hh.y;
         }
     }
+    // XX_k = -2^(-pz) sum_c B_c 2^pc (exact power-of-two factors; fixed order)
     float X = ((eff[0] + eff[1]) + (eff[2] + eff[3])) + ((eff[4] + eff[5]) + (eff[6] + eff[7]));
-    X *= __uint_as_float(static_cast<std::uint32_t>(127 + pp) << 23);  // exact: 2^pp
+    X *= pow2f(pc - pz);
     X += __shfl_xor_sync(0xffffffffu, X, 1);
-    if ((lane & 1) == 0) {
-        const int kk = lane >> 1;  // block 8h + 2t + bs
-        float* scp = reinterpret_cast<float*>(pan + O_SC) + 4 * (kk >> 1) + (kk & 1);
-        scp[0] = (XLO && (24 - e < -126 || 24 - e > 127))
-                     ? ldexpf(1.0f, 24 - e)
-                     : __uint_as_float(static_cast<std::uint32_t>(127 + 24 - e) << 23);
-        scp[2] = -X * 5.9604644775390625e-08f;
+    if ((lane & 1) == 0) reinterpret_cast<float*>(pan + O_XX)[kk] = -X;
+    if (lane == 0) {  // y = R 2^(48 - e): as two normal factors
+        const int q = 48 - e;
+        const int q1 = q < -126 ? -126 : (q > 127 ? 127 : q);
+        reinterpret_cast<float*>(pan + O_SC)[0] = pow2f(q1);
+        reinterpret_cast<float*>(pan + O_SC)[1] = pow2f(q - q1);
     }
 }
 
@@ -254,17 +253,17 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, int 
 // warp preparing its cell's panel -- for layers whose panels fit.
 template <int BW, int BS, int BZ, bool XLO, int NC, bool SHX, bool GATHER = false>
 __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
+    static_assert(BS == BZ, "fast path: scale and zero codes share the statistic width");
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
     constexpr std::uint32_t CODEB = T::code_bytes(BW);
     constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
     constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
-    constexpr std::uint32_t O_FRAG = 0, O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
-    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
+    constexpr std::uint32_t O_FRAG = 0, O_XX = T::kPanelXXOff, O_SC = T::kPanelSCOff, O_XP = T::kPanelXPOff;
+    constexpr std::uint32_t O_LO = T::panel_lo_off(XLO);
     constexpr std::uint32_t MASK = (1u << BW) - 1u;
-    constexpr std::uint32_t SMASK = (1u << BS) - 1u, ZMASK = (1u << BZ) - 1u;
-    constexpr float kMagic = 8388608.0f;
+    constexpr std::uint32_t SMASK = (1u << BS) - 1u;
     constexpr int NT = NC * 32;
 
     extern __shared__ __align__(128) std::uint8_t smem[];
@@ -274,6 +273,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ std::uint32_t tick[2];                // per-range ticket counters (by range parity)
     __shared__ volatile std::uint32_t pflag[64];     // SHX: x panel built
     __shared__ float rowsum[NC][32];                 // outlier row sums of a cell (zero between cells)
+    __shared__ __align__(16) float coef[NC][2][32];  // -S Z 2^(p-24) per (unit, block, kind)
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -299,64 +299,27 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     if (threadIdx.x < 64) pflag[threadIdx.x] = 0u;
     rowsum[warp][lane] = 0.f;
     if (lane < 4) zrow[warp][lane] = 0u;
-    // Tickets of a range of nc cells: the first nc - S are whole cells, the
-    // last S cells are split into two half tickets (one 16-row unit each) so
-    // the range's final round is half as long.  Ticket -> (cell, unit or -1).
-    auto split_of = [](std::uint32_t nc) -> std::uint32_t { return SPQR_SPLIT_CELLS_FN; };
-    auto decode = [](std::uint32_t tkt, std::uint32_t nc, std::uint32_t S, int& uo) {
-        const std::uint32_t f = nc - S;
-        if (tkt < f) {
-            uo = -1;
-            return tkt;
-        }
-        uo = static_cast<int>((tkt - f) & 1u);
-        return f + ((tkt - f) >> 1);
-    };
-    // lane 0: bulk copies of a ticket's record bytes into a slot -- the whole
-    // record, or for a half ticket its unit plus the cell's outlier entries
-    auto copy_rec = [&](std::uint8_t* dst, std::uint32_t r0, std::uint32_t r1, int uo, std::uint64_t* bar) {
+    // lane 0: bulk copy of a cell's record bytes (up to the slot's capacity)
+    auto copy_rec = [&](std::uint8_t* dst, std::uint32_t r0, std::uint32_t r1, std::uint64_t* bar) {
         const std::uint32_t nb = min(r1 - r0, p.rec_cap);
-        if (uo < 0) {
-            mbar_expect_tx(bar, nb);
-            bulk_g2s(dst, p.cells + r0, nb, bar);
-        } else {
-            const std::uint32_t ol = nb - CELL;
-            mbar_expect_tx(bar, UNIT + ol);
-            bulk_g2s(dst + uo * UNIT, p.cells + r0 + uo * UNIT, UNIT, bar);
-            if (ol) bulk_g2s(dst + CELL, p.cells + r0 + CELL, ol, bar);
-        }
+        mbar_expect_tx(bar, nb);
+        bulk_g2s(dst, p.cells + r0, nb, bar);
     };
     std::uint32_t* const coff_base = reinterpret_cast<std::uint32_t*>(smem + p.off_off);
     std::uint32_t* coff = coff_base;
     std::uint32_t* gdone = reinterpret_cast<std::uint32_t*>(smem + p.gd_off);  // finished cells per pair
     for (std::uint32_t i = threadIdx.x; i <= p.part_cap; i += NT) gdone[i] = 0;  // whole capacity
     // Shared state is ready at this barrier, and no global load precedes it: a
-    // CTA that becomes resident late (its SM's previous CTA was the slowest of
-    // the preceding kernel) reaches the PDL wait without a round trip.
+    // CTA that becomes resident late reaches the PDL wait without a round trip.
     __syncthreads();
     // the first record of this warp's first ticket goes out first, its offsets
-    // from the plan's per-CTA table (one load, no cta_start -> cell_off chain)
+    // from the plan's per-CTA table
     if (blockIdx.x < p.nvcta && lane == 0) {
-        std::uint32_t r0, r1;
-        int uo = -1;
-        bool have = false;
-#ifdef SPQR_SPLIT_OFF
         const uint2 r = __ldg(p.first_rec + blockIdx.x * NC + warp);
-        r0 = r.x;
-        r1 = r.y;
-        have = r1 > r0;
-#else
-        const std::uint32_t q0 = __ldg(p.cta_start + blockIdx.x), q1 = __ldg(p.cta_start + blockIdx.x + 1);
-        const std::uint32_t S0 = split_of(q1 - q0);
-        have = static_cast<std::uint32_t>(warp) < q1 - q0 + S0;
-        const std::uint32_t c = have ? decode(warp, q1 - q0, S0, uo) : 0u;
-        r0 = have ? __ldg(p.cell_off + q0 + c) : 0u;
-        r1 = have ? __ldg(p.cell_off + q0 + c + 1) : 0u;
-#endif
-        if (have) {
-            slot_r[warp][0][0] = r0;
-            slot_r[warp][0][1] = r1;
-            copy_rec(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, r0, r1, uo, &full[warp][0]);
+        if (r.y > r.x) {
+            slot_r[warp][0][0] = r.x;
+            slot_r[warp][0][1] = r.y;
+            copy_rec(smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes, r.x, r.y, &full[warp][0]);
         }
     }
     // record offsets of the range: the first range's arrive by one bulk copy
@@ -415,19 +378,22 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     // lane addresses row lr, active in the call of slot lr / 2
     const int jact2 = (lr >> 1) - (lm >> 1);
     const std::uint32_t hl_off = ((lr & 1) ? O_LO : O_FRAG) + 64u * static_cast<std::uint32_t>(lr >> 1) + 16u * (lm & 1);
-    const std::uint32_t magic = 0x4B000000u;
-    // this lane's x-preparation columns: block lane/2 of the panel, k half lane%2
-    const int pp = T::column_prescale(BW, static_cast<std::uint32_t>(lane >> 1), 8u * (lane & 1));
+    // this lane's entry of the -S Z 2^(p-24) table: block kb = lane/2 of the
+    // unit, kind = lane % 2; consumers (t, h) read {cS(b0), cS(b1), cZ(b0), cZ(b1)}
+    const int kb = lane >> 1, kind = lane & 1;
+    const std::uint32_t coef_src = CODEB + STATB + 8u * static_cast<std::uint32_t>(kb) + 4u * kind;
+    const int coef_ix = 16 * (kb >> 3) + 4 * ((kb >> 1) & 3) + 2 * kind + (kb & 1);
+    const float coef_mul = -pow2f(T::stat_p(BS, T::stat_pair(kind, kb >> 3, kb & 1)) - 24);
 
     std::uint8_t* ring = smem + static_cast<std::size_t>(warp) * 2u * p.slot_bytes;
-    // lane 0: copy the record of cell k (unit uo, or whole) into slot sl (offsets from coff)
-    auto issue = [&](std::uint32_t k, int uo, std::uint32_t sl) {
+    // lane 0: copy the record of cell k into slot sl (offsets from coff)
+    auto issue = [&](std::uint32_t k, std::uint32_t sl) {
         if (lane == 0) {
             mbar_wait(&coff_bar, 0);  // immediate after the first range's offsets landed
             const std::uint32_t r0 = coff[k], r1 = coff[k + 1];
             slot_r[warp][sl][0] = r0;
             slot_r[warp][sl][1] = r1;
-            copy_rec(ring + sl * p.slot_bytes, r0, r1, uo, &full[warp][sl]);
+            copy_rec(ring + sl * p.slot_bytes, r0, r1, &full[warp][sl]);
         }
     };
     std::uint32_t nit = 0;  // cells this warp has taken (slot nit & 1, phase (nit >> 1) & 1)
@@ -439,7 +405,6 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         std::uint32_t q0, q1;
         range_bounds(v, q0, q1);
         const std::uint32_t nc = q1 - q0;
-        const std::uint32_t S = split_of(nc), nt = nc + S;  // tickets
         float* part = part_base;
         const std::uint32_t Ga = p.Pn == 1u ? q0 : __umulhi(q0, p.pn_magic);
         auto pair_of = [&](std::uint32_t k) {
@@ -458,11 +423,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         // one ticket of lookahead: the next cell's record copy and x loads are
         // in flight while this cell computes.  Warp w's first ticket is w.
         std::uint32_t tk = static_cast<std::uint32_t>(warp);
-        if (tk < nt && waited) {  // (the first range's went out in the prologue)
-            int uo;
-            const std::uint32_t c = decode(tk, nc, S, uo);
-            issue(c, uo, nit & 1u);
-        }
+        if (tk < nc && waited) issue(tk, nit & 1u);  // (the first range's went out in the prologue)
         // SHX: panel index i = warp + NC j covers panel (P0 + i) mod Pn; j = 0 is the
         // panel of this warp's first cell.  Each warp builds its panels right
         // after the PDL wait; readers check pflag instead of a CTA barrier.
@@ -472,7 +433,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             return P >= p.Pn ? P - p.Pn : P;
         };
         auto publish = [&](std::uint32_t P, const XLane<XLO>& xv) {
-            build_panel<BW, XLO>(xv, lane, pp, pan_base + P * PANEL);
+            build_panel<BW, BS, XLO>(xv, lane, pan_base + P * PANEL);
             __syncwarp();
             __threadfence_block();
             if (lane == 0) pflag[P] = 1u;
@@ -499,23 +460,17 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 #endif
         }
         XLane<XLO> xl{};
-        if (!SHX && tk < nt) {
-            int uo_;
-            xl = load_x<XLO>(p, panel_of(decode(tk, nc, S, uo_)), lane);
-        }
+        if (!SHX && tk < nc) xl = load_x<XLO>(p, panel_of(tk), lane);
 #pragma unroll 1
-        while (tk < nt) {
+        while (tk < nc) {
             const std::uint32_t tn = grab();
             XLane<XLO> xn{};
-            if (tn < nt) {
-                int uon;
-                const std::uint32_t cn = decode(tn, nc, S, uon);
-                issue(cn, uon, (nit + 1u) & 1u);
-                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(cn), lane);
+            if (tn < nc) {
+                issue(tn, (nit + 1u) & 1u);
+                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(tn), lane);
             }
             const std::uint32_t slot = nit & 1u;
-            int uo;
-            const std::uint32_t ck = decode(tk, nc, S, uo);  // this ticket's cell (range index)
+            const std::uint32_t ck = tk;  // this ticket's cell (range index)
 
             if constexpr (SHX) {
                 const std::uint32_t P = panel_of(ck);
@@ -526,7 +481,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 }
                 __threadfence_block();
             } else {
-                build_panel<BW, XLO>(xl, lane, pp, pan);
+                build_panel<BW, BS, XLO>(xl, lane, pan);
                 __syncwarp();
             }
             const std::uint32_t lane_sa = smem_u32(pan) + lane_off;
@@ -543,319 +498,326 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             const std::uint8_t* cell = ring + slot * p.slot_bytes;
             const std::uint32_t r0 = slot_r[warp][slot][0], r1 = slot_r[warp][slot][1];
 
-            // the cell's work for NU units: both (whole ticket) or unit uo (half)
-            auto compute = [&]<int NU>(std::integral_constant<int, NU>) {
-                auto unit_of = [&](int ui) { return NU == 2 ? ui : uo; };
-                // x operands of this panel (shared by both units)
-                float4 xs[2];  // {SC(2t), SC(2t+1), XX(2t), XX(2t+1)} of super-tile h
+            // ---- this lane's entry of the -S Z 2^(p-24) table, both units
+            {
+                const std::uint32_t w0 = *reinterpret_cast<const std::uint32_t*>(cell + coef_src);
+                const std::uint32_t w1 = *reinterpret_cast<const std::uint32_t*>(cell + UNIT + coef_src);
+                coef[warp][0][coef_ix] = fhfma<0, 1>(w0, w0, 0.f) * coef_mul;
+                coef[warp][1][coef_ix] = fhfma<0, 1>(w1, w1, 0.f) * coef_mul;
+            }
+            // ---- lane statistics words of both units (tiled.hpp): W0 = lo bytes
+            // 0,1 | hi bytes 0,1, W1 = lo bytes 2,3 | hi bytes 2,3
+            std::uint32_t sw[2][2];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) xs[h] = reinterpret_cast<const float4*>(pan + O_SC)[4 * h + t];
-
-                // lane data of the units (fp32 x loads its code words per super-tile)
-                std::uint32_t cw[NU][G::LANE_WORDS];
-                std::uint32_t ss[NU], zz[NU];
-                uint4 sc[NU][2];
-#pragma unroll
-                for (int ui = 0; ui < NU; ++ui) {
-                    const std::uint8_t* unit = cell + unit_of(ui) * UNIT;
-                    if constexpr (!XLO) {
-#pragma unroll
-                        for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-                            const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
-                            cw[ui][4 * i] = w4.x;
-                            cw[ui][4 * i + 1] = w4.y;
-                            cw[ui][4 * i + 2] = w4.z;
-                            cw[ui][4 * i + 3] = w4.w;
-                        }
-                    }
-                    load_stats<BS, BZ>(unit + CODEB, lane, ss[ui], zz[ui]);
-                    sc[ui][0] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (2 * t) * 8);
-                    sc[ui][1] = *reinterpret_cast<const uint4*>(unit + CODEB + STATB + (8 + 2 * t) * 8);
-                }
-
-                // epilogue of super-tile h: y partials += s 2^(24-e) (C + z XX)
-                float2 acc[NU][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
-#pragma unroll
-                for (int ui = 0; ui < NU; ++ui) acc[ui][0] = acc[ui][1] = make_float2(0.f, 0.f);
-                auto epilogue = [&](auto HC, const float (&c)[NU][4]) {
-                    constexpr int h = decltype(HC)::value;
-                    const float2 SC = make_float2(xs[h].x, xs[h].y), XX = make_float2(xs[h].z, xs[h].w);
-#pragma unroll
-                    for (int ui = 0; ui < NU; ++ui) {
-                        const uint4 s4 = sc[ui][h];  // {scale_s|scale_z, zero_s|zero_z} x 2 blocks
-                        const __half2 s0 = u32_as_h2(s4.x), z0 = u32_as_h2(s4.y), s1 = u32_as_h2(s4.z),
-                                      z1 = u32_as_h2(s4.w);
-                        const float2 Ss = make_float2(__low2float(s0), __low2float(s1));
-                        const float2 Zs = make_float2(__high2float(s0), __high2float(s1));
-                        const float2 Sz = make_float2(__low2float(z0), __low2float(z1));
-                        const float2 Zz = make_float2(-__high2float(z0), -__high2float(z1));
-                        const float2 A1 = fmul2(Ss, SC);                         // s_s * 2^(24-e)
-                        const float2 A0 = fmul2(A1, make_float2(-Zs.x, -Zs.y));  // -s_s z_s 2^(24-e)
-                        const float2 B0 = fmul2(Sz, Zz);                         // -z_s z_z
-#pragma unroll
-                        for (int rho = 0; rho < 2; ++rho) {
-                            const int e0i = 4 * h + rho, e1i = 4 * h + 2 + rho;  // eps of (bs=0, bs=1)
-                            const float2 cs = fadd2(make_float2(magic_field_rt<SMASK>(ss[ui], e0i * BS, magic),
-                                                                magic_field_rt<SMASK>(ss[ui], e1i * BS, magic)),
-                                                    make_float2(-kMagic, -kMagic));
-                            const float2 cz = fadd2(make_float2(magic_field_rt<ZMASK>(zz[ui], e0i * BZ, magic),
-                                                                magic_field_rt<ZMASK>(zz[ui], e1i * BZ, magic)),
-                                                    make_float2(-kMagic, -kMagic));
-                            const float2 shat = ffma2(A1, cs, A0);
-                            const float2 zhat = ffma2(Sz, cz, B0);
-                            const float2 tt = ffma2(zhat, XX, make_float2(c[ui][2 * rho], c[ui][2 * rho + 1]));
-                            acc[ui][rho] = ffma2(shat, tt, acc[ui][rho]);
-                        }
-                    }
-                };
-                // A fragments of MMA (super-tile h, block j) of unit ui from code words w
-                auto afrag = [&](const std::uint32_t* cwu, int h, int j, std::uint32_t (&a)[4]) {
-                    const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
-                    const std::uint32_t* w = cwu + G::CW * cidx;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
-                        const int i = rho * (G::NP / 2) + qq;
-                        const int B = (BW * i) >> 3, pb = (BW * i) & 7;
-                        a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
-                    }
-                };
-                if constexpr (!XLO) {
-                    // 2 NU independent MMA chains (super-tile h x unit), interleaved
-                    std::uint32_t bfr[2][4];
-                    float cc[2][NU][4];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int ui = 0; ui < NU; ++ui)
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) cc[h][ui][i] = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if ((j & 1) == 0) {
-                                const bool act = jact == j;
-                                ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bfr[h]);
-                            }
-                            const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
-#pragma unroll
-                            for (int ui = 0; ui < NU; ++ui) {
-                                std::uint32_t a[4];
-                                afrag(cw[ui], h, j, a);
-                                mma16816(cc[h][ui], a, b0, b1);
-                            }
-                        }
-                    }
-                    epilogue(std::integral_constant<int, 0>{}, cc[0]);
-                    epilogue(std::integral_constant<int, 1>{}, cc[1]);
+            for (int ui = 0; ui < 2; ++ui) {
+                const std::uint8_t* stats = cell + ui * UNIT + CODEB;
+                if constexpr (BS == 3) {
+                    sw[ui][0] = reinterpret_cast<const std::uint32_t*>(stats)[lane];
+                    const std::uint32_t u16 = reinterpret_cast<const std::uint16_t*>(stats + 128)[lane];
+                    sw[ui][1] = __byte_perm(u16, 0u, 0x4140);
+                } else if constexpr (BS == 2) {
+                    sw[ui][0] = reinterpret_cast<const std::uint32_t*>(stats)[lane];
+                    sw[ui][1] = 0u;
                 } else {
-                    // fp32 x = hi + lo, both f16, sharing one MMA: super-tile h
-                    // runs as its even blocks then its odd blocks (parity par);
-                    // the MMA of block 8h + 2s + par routes the hi part to
-                    // output column 2s and the lo part to 2s + 1, so lane (g, t)
-                    // gets hi and lo of block 8h + 2t + par side by side -- the
-                    // (row, block) pairs whose statistics it holds -- and adds
-                    // them in-lane: 32 MMAs per cell as for f16 x, no shuffles.
-                    auto half = [&](auto HC) {
-                        constexpr int h = decltype(HC)::value;
-                        constexpr int W0 = G::CW * (8 * h / G::MPC), W1 = G::CW * ((8 * h + 7) / G::MPC + 1);
-                        static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a super-tile: 8 B aligned");
-                        std::uint32_t cwh[NU][G::LANE_WORDS];
+                    const uint2 v2 = reinterpret_cast<const uint2*>(stats)[lane];
+                    sw[ui][0] = v2.x;
+                    sw[ui][1] = v2.y;
+                }
+            }
+            // pair j of unit ui as an f16x2 of subnormals code 2^(p-24) (rows g, g+8)
+            auto stat_pair = [&](int ui, int j) -> std::uint32_t {
+                const int B = T::stat_window(BS, j), pb = T::stat_p(BS, j);
+                return window<2>(sw[ui], B) & ((SMASK << pb) * 0x00010001u);
+            };
+
+            // lane data of the units: code words
+            std::uint32_t cw[2][XLO ? 1 : G::LANE_WORDS];
+            if constexpr (!XLO) {
 #pragma unroll
-                        for (int ui = 0; ui < NU; ++ui) {
-                            const std::uint8_t* unit = cell + unit_of(ui) * UNIT;
+                for (int ui = 0; ui < 2; ++ui) {
+                    const std::uint8_t* unit = cell + ui * UNIT;
 #pragma unroll
-                            for (int i = W0; i < W1; i += 2) {
-                                const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
-                                cwh[ui][i] = w2.x;
-                                cwh[ui][i + 1] = w2.y;
-                            }
+                    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+                        const uint4 w4 = reinterpret_cast<const uint4*>(unit + lane * 16 * BW)[i];
+                        cw[ui][4 * i] = w4.x;
+                        cw[ui][4 * i + 1] = w4.y;
+                        cw[ui][4 * i + 2] = w4.z;
+                        cw[ui][4 * i + 3] = w4.w;
+                    }
+                }
+            }
+            __syncwarp();  // the coefficient table is complete
+
+            // epilogue of super-tile h: acc += s' (C + z' XX)
+            float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
+#pragma unroll
+            for (int ui = 0; ui < 2; ++ui) acc[ui][0] = acc[ui][1] = make_float2(0.f, 0.f);
+            auto epilogue = [&](auto HC, const float (&c)[2][4]) {
+                constexpr int h = decltype(HC)::value;
+                const float2 xx = *reinterpret_cast<const float2*>(pan + O_XX + 4u * (8u * h + 2u * t));
+#pragma unroll
+                for (int ui = 0; ui < 2; ++ui) {
+                    // {S_s|Z_s, S_z|Z_z} of blocks 8h + 2t and 8h + 2t + 1
+                    const uint4 s4 = *reinterpret_cast<const uint4*>(cell + ui * UNIT + CODEB + STATB + (8 * h + 2 * t) * 8);
+                    const float4 cf = *reinterpret_cast<const float4*>(&coef[warp][ui][16 * h + 4 * t]);
+                    const std::uint32_t rs0 = stat_pair(ui, T::stat_pair(0, h, 0));
+                    const std::uint32_t rs1 = stat_pair(ui, T::stat_pair(0, h, 1));
+                    const std::uint32_t rz0 = stat_pair(ui, T::stat_pair(1, h, 0));
+                    const std::uint32_t rz1 = stat_pair(ui, T::stat_pair(1, h, 1));
+                    {  // rho = 0: row g
+                        const float2 sh = make_float2(fhfma<0, 0>(s4.x, rs0, cf.x), fhfma<0, 0>(s4.z, rs1, cf.y));
+                        const float2 zh = make_float2(fhfma<0, 0>(s4.y, rz0, cf.z), fhfma<0, 0>(s4.w, rz1, cf.w));
+                        const float2 tt = ffma2(zh, xx, make_float2(c[ui][0], c[ui][1]));
+                        acc[ui][0] = ffma2(sh, tt, acc[ui][0]);
+                    }
+                    {  // rho = 1: row g + 8
+                        const float2 sh = make_float2(fhfma<0, 1>(s4.x, rs0, cf.x), fhfma<0, 1>(s4.z, rs1, cf.y));
+                        const float2 zh = make_float2(fhfma<0, 1>(s4.y, rz0, cf.z), fhfma<0, 1>(s4.w, rz1, cf.w));
+                        const float2 tt = ffma2(zh, xx, make_float2(c[ui][2], c[ui][3]));
+                        acc[ui][1] = ffma2(sh, tt, acc[ui][1]);
+                    }
+                }
+            };
+            // A fragments of MMA (super-tile h, block j) of unit ui from code words w
+            auto afrag = [&](const std::uint32_t* cwu, int h, int j, std::uint32_t (&a)[4]) {
+                const int mu = 8 * h + j, cidx = mu / G::MPC, mm = mu % G::MPC;
+                const std::uint32_t* w = cwu + G::CW * cidx;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int rho = r & 1, kh = r >> 1, qq = 2 * mm + kh;
+                    const int i = rho * (G::NP / 2) + qq;
+                    const int B = (BW * i) >> 3, pb = (BW * i) & 7;
+                    a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
+                }
+            };
+            if constexpr (!XLO) {
+                // 4 independent MMA chains (super-tile h x unit), interleaved
+                std::uint32_t bfr[2][4];
+                float cc[2][2][4];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int ui = 0; ui < 2; ++ui)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) cc[h][ui][i] = 0.f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if ((j & 1) == 0) {
+                            const bool act = jact == j;
+                            ldsm_x4((act ? lane_sa : zb[h]) + 256u * h, bfr[h]);
                         }
-                        float d[2][NU][4];  // [parity][unit]: {hi, lo} of block 8h + 2t + par, rows g / g + 8
+                        const std::uint32_t b0 = bfr[h][2 * (j & 1)], b1 = bfr[h][2 * (j & 1) + 1];
 #pragma unroll
-                        for (int par = 0; par < 2; ++par)
+                        for (int ui = 0; ui < 2; ++ui) {
+                            std::uint32_t a[4];
+                            afrag(cw[ui], h, j, a);
+                            mma16816(cc[h][ui], a, b0, b1);
+                        }
+                    }
+                }
+                epilogue(std::integral_constant<int, 0>{}, cc[0]);
+                epilogue(std::integral_constant<int, 1>{}, cc[1]);
+            } else {
+                // fp32 x = hi + lo, both f16, sharing one MMA: super-tile h
+                // runs as its even blocks then its odd blocks (parity par);
+                // the MMA of block 8h + 2s + par routes the hi part to
+                // output column 2s and the lo part to 2s + 1, so lane (g, t)
+                // gets hi and lo of block 8h + 2t + par side by side -- the
+                // (row, block) pairs whose statistics it holds -- and adds
+                // them in-lane: 32 MMAs per cell as for f16 x, no shuffles.
+                auto half = [&](auto HC) {
+                    constexpr int h = decltype(HC)::value;
+                    constexpr int W0 = G::CW * (8 * h / G::MPC), W1 = G::CW * ((8 * h + 7) / G::MPC + 1);
+                    static_assert(W0 % 2 == 0 && W1 % 2 == 0, "code words of a super-tile: 8 B aligned");
+                    std::uint32_t cwh[2][G::LANE_WORDS];
 #pragma unroll
-                            for (int ui = 0; ui < NU; ++ui)
+                    for (int ui = 0; ui < 2; ++ui) {
+                        const std::uint8_t* unit = cell + ui * UNIT;
 #pragma unroll
-                                for (int i = 0; i < 4; ++i) d[par][ui][i] = 0.f;
+                        for (int i = W0; i < W1; i += 2) {
+                            const uint2 w2 = reinterpret_cast<const uint2*>(unit + lane * 16 * BW)[i / 2];
+                            cwh[ui][i] = w2.x;
+                            cwh[ui][i + 1] = w2.y;
+                        }
+                    }
+                    float d[2][2][4];  // [parity][unit]: {hi, lo} of block 8h + 2t + par, rows g / g + 8
 #pragma unroll
-                        for (int par = 0; par < 2; ++par) {
+                    for (int par = 0; par < 2; ++par)
 #pragma unroll
-                            for (int c2 = 0; c2 < 2; ++c2) {  // slots s = 2 c2, 2 c2 + 1
-                                std::uint32_t bq[4];
-                                ldsm_x4(jact2 == 2 * c2 ? hl_sa + 256u * h + 32u * par : zero_sa, bq);
+                        for (int ui = 0; ui < 2; ++ui)
 #pragma unroll
-                                for (int m2 = 0; m2 < 2; ++m2) {
-                                    const int j = 2 * (2 * c2 + m2) + par;  // block 8h + j
+                            for (int i = 0; i < 4; ++i) d[par][ui][i] = 0.f;
 #pragma unroll
-                                    for (int ui = 0; ui < NU; ++ui) {
-                                        std::uint32_t a[4];
-                                        afrag(cwh[ui], h, j, a);
-                                        mma16816(d[par][ui], a, bq[2 * m2], bq[2 * m2 + 1]);
-                                    }
+                    for (int par = 0; par < 2; ++par) {
+#pragma unroll
+                        for (int c2 = 0; c2 < 2; ++c2) {  // slots s = 2 c2, 2 c2 + 1
+                            std::uint32_t bq[4];
+                            ldsm_x4(jact2 == 2 * c2 ? hl_sa + 256u * h + 32u * par : zero_sa, bq);
+#pragma unroll
+                            for (int m2 = 0; m2 < 2; ++m2) {
+                                const int j = 2 * (2 * c2 + m2) + par;  // block 8h + j
+#pragma unroll
+                                for (int ui = 0; ui < 2; ++ui) {
+                                    std::uint32_t a[4];
+                                    afrag(cwh[ui], h, j, a);
+                                    mma16816(d[par][ui], a, bq[2 * m2], bq[2 * m2 + 1]);
                                 }
                             }
                         }
-                        float ch[NU][4];  // the f16 layout: (g, 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
+                    }
+                    float ch[2][4];  // the f16 layout: (g, 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
 #pragma unroll
-                        for (int ui = 0; ui < NU; ++ui) {
-                            ch[ui][0] = d[0][ui][0] + d[0][ui][1];
-                            ch[ui][1] = d[1][ui][0] + d[1][ui][1];
-                            ch[ui][2] = d[0][ui][2] + d[0][ui][3];
-                            ch[ui][3] = d[1][ui][2] + d[1][ui][3];
-                        }
-                        epilogue(HC, ch);
-                    };
-                    half(std::integral_constant<int, 0>{});
-                    half(std::integral_constant<int, 1>{});
-                }
+                    for (int ui = 0; ui < 2; ++ui) {
+                        ch[ui][0] = d[0][ui][0] + d[0][ui][1];
+                        ch[ui][1] = d[1][ui][0] + d[1][ui][1];
+                        ch[ui][2] = d[0][ui][2] + d[0][ui][3];
+                        ch[ui][3] = d[1][ui][2] + d[1][ui][3];
+                    }
+                    epilogue(HC, ch);
+                };
+                half(std::integral_constant<int, 0>{});
+                half(std::integral_constant<int, 1>{});
+            }
 
-                // outliers: entries (row, col, value) of this cell, sorted by (row,
-                // col), 0xffffffff padding (row 255).  Chunks of 128 entries, 4
-                // consecutive per lane (one 16-byte load): products, a segmented
-                // inclusive scan by row, and the last entry of each row in the
-                // chunk adds the row total to rowsum (rows of this ticket's units
-                // only).  Chunks run in order, so the sums are deterministic.
-                // Entries beyond the staged part of the record are read from
-                // global memory.
-                const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-                float* rs = rowsum[warp];
-                if (cnt) {
-                    const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
-                    const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
-                    const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
-                    const std::uint32_t rlo = NU == 2 ? 0u : 16u * uo, rhi = NU == 2 ? 32u : rlo + 16u;
-                    auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
-                        uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                        if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
-                        const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
-                        std::uint32_t k[4];
-                        float sv[4];
+            // outliers: entries (row, col, value) of this cell, sorted by (row,
+            // col), 0xffffffff padding (row 255).  Chunks of 128 entries, 4
+            // consecutive per lane (one 16-byte load): products, a segmented
+            // inclusive scan by row, and the last entry of each row in the
+            // chunk adds the row total to rowsum.  Chunks run in order, so the
+            // sums are deterministic.  Entries beyond the staged part of the
+            // record are read from global memory.
+            const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+            float* rs = rowsum[warp];
+            if (cnt) {
+                const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
+                const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
+                const std::uint32_t* eg = reinterpret_cast<const std::uint32_t*>(p.cells + r0 + CELL) + nfast;
+                auto chunk = [&](const std::uint32_t* src, std::uint32_t i0, std::uint32_t lim, bool first) {
+                    uint4 ev = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
+                    const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
+                    std::uint32_t k[4];
+                    float sv[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            k[j] = e[j] >> 24;
-                            const std::uint32_t c = (e[j] >> 16) & 255u;
-                            float xv;
-                            if constexpr (XLO)
-                                xv = reinterpret_cast<const float*>(pan + O_XP)[c];
+                    for (int j = 0; j < 4; ++j) {
+                        k[j] = e[j] >> 24;
+                        const std::uint32_t c = __byte_perm(e[j], 0u, 0x4442);  // col: byte 2
+                        if constexpr (XLO) {
+                            sv[j] = h2f_bits(e[j] & 0xffffu) * reinterpret_cast<const float*>(pan + O_XP)[c];
+                        } else {
+                            const std::uint32_t xv = reinterpret_cast<const unsigned short*>(pan + O_XP)[c];
+                            sv[j] = fhfma<0, 0>(e[j], xv, 0.f);  // v * x, exact
+                        }
+                    }
+                    bool same[3];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        same[j] = k[j + 1] == k[j];
+                        if (same[j]) sv[j + 1] += sv[j];
+                    }
+                    const std::uint32_t K = k[3];
+                    const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
+                    const bool head = lane == 0 || pK != K;
+                    const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
+                    const int seg0 = 31 - __clz(heads);
+                    float V = sv[3];
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const float o = __shfl_up_sync(0xffffffffu, V, d);
+                        if (lane - d >= seg0) V += o;
+                    }
+                    float cin = __shfl_up_sync(0xffffffffu, V, 1);
+                    if (lane == 0 || pK != k[0]) cin = 0.f;
+                    const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
+                        if (tail && k[j] < 32u) {
+                            const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
+                            if (first)
+                                rs[k[j]] = tot;
                             else
-                                xv = __half2float(reinterpret_cast<const __half*>(pan + O_XP)[c]);
-                            sv[j] = h2f_bits(e[j] & 0xffffu) * xv;
+                                rs[k[j]] += tot;
                         }
-                        bool same[3];
-#pragma unroll
-                        for (int j = 0; j < 3; ++j) {
-                            same[j] = k[j + 1] == k[j];
-                            if (same[j]) sv[j + 1] += sv[j];
-                        }
-                        const std::uint32_t K = k[3];
-                        const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
-                        const bool head = lane == 0 || pK != K;
-                        const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
-                        const int seg0 = 31 - __clz(heads);
-                        float V = sv[3];
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const float o = __shfl_up_sync(0xffffffffu, V, d);
-                            if (lane - d >= seg0) V += o;
-                        }
-                        float cin = __shfl_up_sync(0xffffffffu, V, 1);
-                        if (lane == 0 || pK != k[0]) cin = 0.f;
-                        const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
-                            if (tail && k[j] >= rlo && k[j] < rhi) {
-                                const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
-                                if (first)
-                                    rs[k[j]] = tot;
-                                else
-                                    rs[k[j]] += tot;
-                            }
-                        }
-                    };
-                    chunk(es, 4u * lane, nfast, true);
-#pragma unroll 1
-                    for (std::uint32_t base = 128; base < nfast; base += 128) {
-                        __syncwarp();
-                        chunk(es, base + 4u * lane, nfast, false);
                     }
+                };
+                chunk(es, 4u * lane, nfast, true);
 #pragma unroll 1
-                    for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
-                        __syncwarp();
-                        chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);
-                    }
+                for (std::uint32_t base = 128; base < nfast; base += 128) {
+                    __syncwarp();
+                    chunk(es, base + 4u * lane, nfast, false);
                 }
+#pragma unroll 1
+                for (std::uint32_t base = nfast; base < cnt; base += 128) {  // rare: record larger than the slot
+                    __syncwarp();
+                    chunk(eg, base - nfast + 4u * lane, cnt - nfast, false);
+                }
+            }
 
-                // the ticket's row sums.  Lane (g, t) holds partials of rows
-                // 16u + 8rho + g over its blocks; a transpose-add across the quad
-                // (4x4 for a whole cell, 2x4 for a unit) gives each row one lane.
-                float* prow = part + ck * 32u;
-                if constexpr (NU == 2) {
-                    float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
-                    float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
-                    const bool o1 = t & 1, o2 = t & 2;
-                    const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
-                    const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
-                    const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 1);
-                    const float b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 1);
-                    const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
-                    prow[16 * (t >> 1) + 8 * (t & 1) + g] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-                } else {
-                    const float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
-                    const bool o1 = t & 1;
-                    float b = (o1 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, o1 ? a0 : a1, 1);
-                    b += __shfl_xor_sync(0xffffffffu, b, 2);
-                    if (t < 2) prow[16 * uo + 8 * t + g] = b;
-                }
+            // the cell's row sums.  Lane (g, t) holds partials of rows
+            // 16u + 8rho + g over its blocks; a transpose-add across the quad
+            // gives each row one lane: row = 16 (t >> 1) + 8 (t & 1) + g.
+            float* prow = part + ck * 32u;
+            {
+                const float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
+                const float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
+                const bool o1 = t & 1, o2 = t & 2;
+                const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
+                const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
+                const float b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 1);
+                const float b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 1);
+                const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
+                const float R = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+                const int row = 16 * (t >> 1) + 8 * (t & 1) + g;
+                const float2 sc = *reinterpret_cast<const float2*>(pan + O_SC);
+                const float Rs = XLO ? (R * sc.x) * sc.y : R * sc.x;
                 __syncwarp();
                 if (cnt) {
-                    if (NU == 2 || (lane >> 4) == uo) prow[lane] += rs[lane];
-                    rs[lane] = 0.f;
-                    __syncwarp();
+                    prow[row] = Rs + rs[row];
+                    rs[row] = 0.f;
+                } else {
+                    prow[row] = Rs;
                 }
-            };
-#ifdef SPQR_SPLIT_OFF
-            compute(std::integral_constant<int, 2>{});  // whole cells only: no half-ticket code in the kernel
-#else
-            if (uo < 0)
-                compute(std::integral_constant<int, 2>{});
-            else
-                compute(std::integral_constant<int, 1>{});
-#endif
+            }
 
-            // count the ticket against its pair (a split cell counts twice); the
-            // warp that completes the pair reduces it (row = lane, cells in order)
-            // and writes y
+            // count the cell against its pair; the warp that completes the
+            // pair reduces it (row = lane, cells in order) and writes y
             const std::uint32_t Gq = pair_of(ck);
             const std::uint32_t cs = Gq * p.Pn, ce = cs + p.Pn;
             const std::uint32_t a = max(cs, q0), b = min(ce, q1);
-            const std::uint32_t fs = q0 + nc - S;  // first split cell
-            const std::uint32_t want = (b - a) + (b > max(a, fs) ? b - max(a, fs) : 0u);
-            __threadfence_block();  // this ticket's row sums before the count
+            __threadfence_block();  // this cell's row sums before the count
             std::uint32_t done = 0;
             if (lane == 0) done = atomicAdd(&gdone[Gq - Ga], 1u) + 1u;
             done = __shfl_sync(0xffffffffu, done, 0);
-            if (done == want) {
+            if (done == b - a) {
                 __threadfence_block();
                 float sum = 0.f;
                 const float* src = part + (a - q0) * 32u + lane;
 #pragma unroll 4
                 for (std::uint32_t qq = a; qq < b; ++qq, src += 32) sum += *src;
                 const std::uint32_t row = 32u * Gq + lane;
-                unsigned long long* xw = p.xchg + static_cast<std::size_t>(Gq) * 32u + lane;
                 if (a == cs && b == ce) {  // the pair is ours alone
                     if (row < p.m) put_y(row, sum);
-                } else if (a != cs) {      // we hold the pair's last cells: publish
-                    const unsigned long long w = (1ull << 32) | __float_as_uint(sum);
-                    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(xw), "l"(w) : "memory");
-                } else {                   // we hold its first cells: add the published rest
-                    unsigned long long w;
-                    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(xw) : "memory");
-                    if ((w >> 32) == 0ull) w = spin_published(xw);
-                    if (row < p.m) put_y(row, sum + __uint_as_float(static_cast<std::uint32_t>(w)));
-                    *xw = 0ull;
+                } else {
+                    // shared with the neighbouring range: the second side to
+                    // finish adds first-side + last-side (threadFenceReduction)
+                    const std::uint32_t side = a != cs ? 1u : 0u;  // 1: we hold the pair's last cells
+                    const std::uint32_t bx = side ? v : v + 1u;    // boundary below range bx
+                    float* slot = p.xpart + (2u * bx + side) * 32u;
+                    __stcg(slot + lane, sum);
+                    __threadfence();
+                    __syncwarp();
+                    std::uint32_t prev = 0;
+                    if (lane == 0) prev = atomicAdd(p.xcnt + bx, 1u);
+                    prev = __shfl_sync(0xffffffffu, prev, 0);
+                    if (prev == 1u) {
+                        __threadfence();
+                        const float other = __ldcg(p.xpart + (2u * bx + (side ^ 1u)) * 32u + lane);
+                        if (row < p.m) put_y(row, side ? other + sum : sum + other);
+                        if (lane == 0) p.xcnt[bx] = 0u;  // ready for the next launch
+                    }
                 }
             }
             __syncwarp();  // every lane is done with the slot before it is refilled

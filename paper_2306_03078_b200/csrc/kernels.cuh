@@ -1,11 +1,10 @@
 // kernels.cuh -- sm_100a kernels of the SpQR decode path.
 //
-//   xprep_tiled ........ x gather through the permutation (kernel.hpp:93-98) +
-//                        per-block power-of-two scaling + per-column 2^-p
-//                        pre-scale into m16n8k16 B fragments + block sums.
-//   gemv_tiled ......... THE hot kernel: fused dequant-GEMV + CSR outlier merge
-//                        (kernel.hpp:89-124) over the tiled HBM layout, one
-//                        output write per row, deterministic.
+//   gemv_cta ........... THE hot kernel (gemv_cta.cuh): x preparation + fused
+//                        dequant-GEMV + CSR outlier merge (kernel.hpp:89-124)
+//                        over the tiled HBM layout, one output write per row,
+//                        deterministic.
+//   xprep_tc + gemm_tc . batched path (gemm_tc.cuh): tcgen05 tensor cores.
 //   dequant_raw / outliers_raw ... bit-exact dequantize_full (kernel.hpp:17-25,
 //                        solver.hpp:345-362) on the raw stream, any geometry.
 //   xprep_raw / gemv_raw ......... generic matvec on the raw stream for layers
@@ -60,6 +59,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -95,21 +97,6 @@ __device__ __forceinline__ float h2f_bits(std::uint32_t h16) {
 }
 
 // ============================================================ tiled path ====
-struct TiledParams {
-    const std::uint8_t* cells;        // cell records (cell bytes + outlier entries, 16-B padded)
-    const std::uint32_t* cell_off;    // [ncell+1] byte offset of each record
-    const std::uint32_t* warp_start;  // [nwarps+1] first cell of each warp
-    const std::uint32_t* gmap;        // [Gn][2] {partial slot base, contributing warps} of G
-    const std::uint32_t* wmap;        // [nwarps][2] ordinal of the warp in its first / last G
-    const std::uint8_t* xpanel;       // [Pn] x panels of this batch column (xprep_tiled)
-    float* y;                         // [m] this batch column
-    float* partial;                   // [nwarps*2*32]
-    std::uint32_t* counters;          // [Gn], zero between launches
-    std::uint32_t m, Pn, Gn, nwarps;
-    std::uint32_t rec_cap_bytes;      // record bytes a slot holds (outliers beyond: LDG)
-    std::uint32_t slot_bytes;
-};
-
 template <int BW>
 struct Geo {
     static constexpr int CW = T::words_per_container(BW);
@@ -129,99 +116,9 @@ __device__ __forceinline__ std::uint32_t window(const std::uint32_t* w, int B) {
     return r;
 }
 
-// Load `SB` bytes at 2-byte or 4-byte granularity into two 64-bit words.
-template <int SB>
-__device__ __forceinline__ void load_stat_bits(const std::uint8_t* p, std::uint64_t (&v)[2]) {
-    v[0] = v[1] = 0;
-    if constexpr (SB % 4 == 0) {
-#pragma unroll
-        for (int i = 0; i < SB / 4; ++i)
-            v[i >> 1] |= static_cast<std::uint64_t>(reinterpret_cast<const std::uint32_t*>(p)[i]) << (32 * (i & 1));
-    } else if constexpr (SB % 2 == 0) {
-#pragma unroll
-        for (int i = 0; i < SB / 2; ++i)
-            v[i >> 2] |= static_cast<std::uint64_t>(reinterpret_cast<const std::uint16_t*>(p)[i]) << (16 * (i & 3));
-    } else {
-#pragma unroll
-        for (int i = 0; i < SB; ++i) v[i >> 3] |= static_cast<std::uint64_t>(p[i]) << (8 * (i & 7));
-    }
-}
-
-template <int NBITS>
-__device__ __forceinline__ std::uint32_t field(const std::uint64_t (&v)[2], int pos) {
-    // pos and NBITS are compile-time after unrolling; fields never straddle
-    // more than the two words.
-    const int w = pos >> 6, s = pos & 63;
-    std::uint64_t x = v[w] >> s;
-    if (s + NBITS > 64 && w == 0) x |= v[1] << (64 - s);
-    return static_cast<std::uint32_t>(x) & ((1u << NBITS) - 1u);
-}
-
-#include "gemv_tiled.cuh"
+#include "helpers.cuh"
 #include "gemv_cta.cuh"
 #include "gemm_tc.cuh"
-
-// x preparation for the tiled path: one thread per (column, batch column);
-// the 16 lanes of a half-warp form one 16-column block.  Writes the panel
-// layout the GEMV stages per cell (tiled.hpp panel_bytes):
-//   [B rows 16 blocks x 16 fp16][{SC(2i), SC(2i+1), XX(2i), XX(2i+1)} x 8]
-//   [x in solve order: 256 x f16 (fp16 input) or f32 (fp32 input)]
-//   [low-half B rows 16 x 16 fp16 (fp32 input only)]
-// B rows hold fp16(x * 2^(e - p)) in column order (ldmatrix rows of B^T),
-// e = per-block power-of-two scale (max |x| in [2^14, 2^15)), p = the
-// column's code pre-scale (tiled.hpp).
-// PDL: the dependent GEMV may launch (and start streaming weights) at once;
-// x is read only after the preceding kernel in the stream has completed.
-template <int BW, bool XLO>
-__global__ void __launch_bounds__(128) xprep_tiled(const void* __restrict__ x, int x_f16, std::uint32_t n,
-                                                   std::uint32_t n_pad, const std::uint32_t* __restrict__ order,
-                                                   std::uint8_t* __restrict__ panels, std::uint64_t panel_stride) {
-    constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
-    constexpr std::uint32_t O_SC = T::kPanelFragBytes, O_XP = O_SC + T::kPanelScBytes;
-    constexpr std::uint32_t O_LO = O_XP + 256u * (XLO ? 4u : 2u);
-    pdl_launch();
-    const std::uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;  // n_pad is a multiple of 256
-    const std::uint32_t b = blockIdx.y;
-    const std::uint32_t k = col >> 4, cc = col & 15, kk = k & 15;
-    std::uint8_t* pan = panels + b * panel_stride + static_cast<std::size_t>(col >> 8) * PANEL;
-    const std::uint32_t src = (col < n) ? (order ? __ldg(order + col) : col) : 0u;
-    pdl_wait();
-    float v = 0.f;
-    if (col < n)
-        v = x_f16 ? __half2float(reinterpret_cast<const __half*>(x)[static_cast<std::size_t>(b) * n + src])
-                  : reinterpret_cast<const float*>(x)[static_cast<std::size_t>(b) * n + src];
-    float mx = fabsf(v);
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-    if constexpr (XLO)
-        reinterpret_cast<float*>(pan + O_XP)[16 * kk + cc] = v;
-    else
-        reinterpret_cast<__half*>(pan + O_XP)[16 * kk + cc] = __float2half_rn(v);
-    int e = 0;
-    if (mx > 0.f && mx < INFINITY) {
-        int E;
-        frexpf(mx, &E);  // mx = f * 2^E, f in [0.5, 1)
-        e = 15 - E;      // mx * 2^e in [2^14, 2^15)
-    }
-    const int pp = T::column_prescale(BW, k, cc);
-    const float s = ldexpf(v, e - pp);
-    const __half hi = __float2half_rn(s);
-    float eff = __half2float(hi);
-    reinterpret_cast<__half*>(pan)[16 * kk + cc] = hi;  // natural column order (ldmatrix rows of B^T)
-    if constexpr (XLO) {
-        const __half lo = __float2half_rn(s - eff);
-        eff += __half2float(lo);
-        reinterpret_cast<__half*>(pan + O_LO)[16 * kk + cc] = lo;
-    }
-    float X = ldexpf(eff, pp);  // block sum of the effective scaled x, fixed tree order
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) X += __shfl_xor_sync(0xffffffffu, X, d);
-    if (cc == 0) {
-        float* scp = reinterpret_cast<float*>(pan + O_SC + 16u * (kk / 2));
-        scp[kk & 1] = ldexpf(1.0f, 24 - e);
-        scp[2 + (kk & 1)] = -X * 5.9604644775390625e-08f;
-    }
-}
 
 // ============================================================== raw path ====
 // Geometry of a raw .spqr stream resident in device memory (any config).

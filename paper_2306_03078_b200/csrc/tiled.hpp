@@ -11,8 +11,8 @@
 //   [codes  : 32 lanes x 16*BW bytes ]  lane L's A-fragment codes for the 16
 //                                       m16n8k16 MMAs of the unit (2 super-
 //                                       tiles x 8 blocks), in "containers"
-//   [stats  : 32 lanes x (BS+BZ) bytes] lane L's 8 scale codes then 8 zero
-//                                       codes, LSB-first (stat_byte_offset)
+//   [stats  : 32 lanes x (BS+BZ) bytes] lane L's 16 statistics codes as two
+//                                       streams (rows g / g+8), see below
 //   [scalars: 16 blocks x 8 bytes     ]  binary16 {scale_s, scale_z, zero_s, zero_z}
 //
 // unit_bytes = 512*BW + 32*(BS+BZ) + 128 = 16 group records of the stream
@@ -32,9 +32,17 @@
 // subnormals worth code * 2^(p-24); the x operand is pre-scaled by 2^-p per
 // column (xprep), so the product is exact and p cancels.
 //
-// Stats entry eps = 4h + 2*bs + rho  (block 16P + 8h + 2t + bs, row g + 8*rho):
-//   scale code at bit eps*BS, zero code at bit 8*BS + eps*BZ of the lane's
-//   (BS+BZ)-byte little-endian field.
+// Statistics (BS = BZ, the fast path): lane L = 4g + t holds 8 code pairs
+// j = 4*kind + 2h + b (kind 0 = scale code, 1 = zero code; block 8h + 2t + b),
+// the code of row g in a "lo" stream and that of row g + 8 in a "hi" stream,
+// pair j at stream bit BS*j.  Like the weight containers, the lane's field
+// interleaves the two streams per 16-bit word half -- word w = lo bytes
+// 2w, 2w+1 | hi bytes 2w, 2w+1 (a 3-byte stream ends in the 2-byte word
+// lo byte 2 | hi byte 2) -- so ONE LOP3 of a 16-bit window turns pair j into
+// an f16x2 register holding both rows' codes as binary16 subnormals worth
+// code * 2^(p-24), p = (BS*j) mod 8 (stat_p), which the kernel feeds straight
+// to mixed-precision FMAs (fma.rn.f32.f16): the stat_dequant of a whole
+// (row, block) pair without an int->float conversion.
 //
 // Outliers are re-bucketed per cell: offsets u32[cells+1] and entries u32
 //   value16 | (col & 255) << 16 | (row - 32G) << 24
@@ -87,15 +95,37 @@ SPQR_HD constexpr int column_prescale(int bw, std::uint32_t k, std::uint32_t cc)
     return prescale_p(bw, 2 * m + kh);
 }
 
-// x operands of one 256-column panel as prepared by xprep_tiled, staged into
-// the kernel's TMA slot next to the cell: B fragments (16 blocks x 32 B),
-// {SC, XX} per block (16 x 8 B), the fp32 solve-order x for the outlier merge
-// (256 x 4 B) and, for fp32 inputs, the low-half B fragments (16 x 32 B).
+// x operands of one 256-column panel, built by the kernel in shared memory:
+//   [B rows : 16 blocks x 16 f16  ] fp16(x 2^(e - p_c - p_s(block))), natural
+//                                    column order (ldmatrix rows of B^T)
+//   [XX     : 16 f32              ] -2^(-p_z(block)) sum_c B_c 2^p_c
+//   [SC     : 2 f32 (+ 8 B pad)   ] 2^(48 - e) as a product of two normal floats
+//   [xp     : 256 f16 | 256 f32   ] x in solve order (outlier products)
+//   [B lo   : 16 x 16 f16         ] fp32 x only: fp16(residual of B)
+// e = the panel's power-of-two scale (max |x| 2^e in [2^14, 2^15)), p_c = the
+// column's code pre-scale, p_s / p_z = the pre-scales of the block's scale /
+// zero code pairs (stat_p).
 inline constexpr std::uint32_t kPanelFragBytes = 512;
-inline constexpr std::uint32_t kPanelScBytes = 128;
+inline constexpr std::uint32_t kPanelXXOff = 512;
+inline constexpr std::uint32_t kPanelSCOff = 576;
+inline constexpr std::uint32_t kPanelXPOff = 592;
 SPQR_HD constexpr std::uint32_t panel_xp_bytes(bool xlo) { return xlo ? 1024u : 512u; }  // f32 / f16 x
+SPQR_HD constexpr std::uint32_t panel_lo_off(bool xlo) { return kPanelXPOff + panel_xp_bytes(xlo); }
 SPQR_HD constexpr std::uint32_t panel_bytes(bool xlo) {
-    return kPanelFragBytes + kPanelScBytes + panel_xp_bytes(xlo) + (xlo ? kPanelFragBytes : 0u);
+    return kPanelXPOff + panel_xp_bytes(xlo) + (xlo ? kPanelFragBytes : 0u);
+}
+
+// Statistics pair geometry (BS bits per code): stream bit, window byte and
+// the code's bit offset inside its 16-bit window.
+SPQR_HD constexpr int stat_pair(int kind, int h, int b) { return 4 * kind + 2 * h + b; }
+SPQR_HD constexpr int stat_window(int bs, int j) { return (bs * j) >> 3; }
+SPQR_HD constexpr int stat_p(int bs, int j) { return (bs * j) & 7; }
+// Logical byte f of a lane's statistics field -> (stream: 0 lo / 1 hi, stream byte).
+SPQR_HD constexpr int stat_field_stream(int bs, int f) {
+    return f < 4 * (bs / 2) ? (f & 3) >> 1 : (f - 4 * (bs / 2));
+}
+SPQR_HD constexpr int stat_field_byte(int bs, int f) {
+    return f < 4 * (bs / 2) ? 2 * (f >> 2) + (f & 1) : bs - 1;
 }
 
 // Byte b of lane L's statistics field inside the unit's stats area.  A

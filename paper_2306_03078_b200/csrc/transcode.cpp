@@ -113,43 +113,41 @@ void unpack_unit_codes(const std::uint8_t* src, UnitStage& u) {
     }
 }
 
+// Lane statistics (tiled.hpp): pair j = 4*kind + 2h + b of block 8h + 2t + b,
+// row g in the lo stream, row g + 8 in the hi stream, at stream bit bs*j.
 void pack_unit_stats(const UnitStage& u, int bs, int bz, std::uint8_t* dst) {
     const int sbytes = bs + bz;
     for (int L = 0; L < 32; ++L) {
         const int g = L >> 2, t = L & 3;
-        std::uint64_t bits[2] = {0, 0};
-        auto put = [&](int pos, int nb, std::uint32_t v) {
-            for (int b = 0; b < nb; ++b, ++pos)
-                if ((v >> b) & 1u) bits[pos >> 6] |= std::uint64_t{1} << (pos & 63);
-        };
-        for (int eps = 0; eps < 8; ++eps) {
-            const int h = eps >> 2, s = (eps >> 1) & 1, rho = eps & 1;
-            const int blk = 8 * h + 2 * t + s, row = g + 8 * rho;
-            put(eps * bs, bs, u.scode[blk][row]);
-            put(8 * bs + eps * bz, bz, u.zcode[blk][row]);
+        std::uint32_t st[2] = {0, 0};  // lo / hi streams (8 * bs <= 32 bits)
+        for (int j = 0; j < 8; ++j) {
+            const int kind = j >> 2, h = (j >> 1) & 1, b = j & 1, blk = 8 * h + 2 * t + b;
+            for (int rho = 0; rho < 2; ++rho) {
+                const std::uint32_t code = kind ? u.zcode[blk][g + 8 * rho] : u.scode[blk][g + 8 * rho];
+                st[rho] |= code << (bs * j);
+            }
         }
-        for (int b = 0; b < sbytes; ++b)
-            dst[T::stat_byte_offset(L, b, sbytes)] = static_cast<std::uint8_t>(bits[b >> 3] >> (8 * (b & 7)));
+        for (int f = 0; f < sbytes; ++f)
+            dst[T::stat_byte_offset(L, f, sbytes)] = static_cast<std::uint8_t>(
+                st[T::stat_field_stream(bs, f)] >> (8 * T::stat_field_byte(bs, f)));
     }
 }
 
 void unpack_unit_stats(const std::uint8_t* src, int bs, int bz, UnitStage& u) {
     const int sbytes = bs + bz;
+    const std::uint32_t mask = (1u << bs) - 1u;
     for (int L = 0; L < 32; ++L) {
         const int g = L >> 2, t = L & 3;
-        std::uint64_t bits[2] = {0, 0};
-        for (int b = 0; b < sbytes; ++b)
-            bits[b >> 3] |= static_cast<std::uint64_t>(src[T::stat_byte_offset(L, b, sbytes)]) << (8 * (b & 7));
-        auto get = [&](int pos, int nb) {
-            std::uint32_t v = 0;
-            for (int b = 0; b < nb; ++b, ++pos) v |= static_cast<std::uint32_t>((bits[pos >> 6] >> (pos & 63)) & 1u) << b;
-            return static_cast<std::uint8_t>(v);
-        };
-        for (int eps = 0; eps < 8; ++eps) {
-            const int h = eps >> 2, s = (eps >> 1) & 1, rho = eps & 1;
-            const int blk = 8 * h + 2 * t + s, row = g + 8 * rho;
-            u.scode[blk][row] = get(eps * bs, bs);
-            u.zcode[blk][row] = get(8 * bs + eps * bz, bz);
+        std::uint32_t st[2] = {0, 0};
+        for (int f = 0; f < sbytes; ++f)
+            st[T::stat_field_stream(bs, f)] |= static_cast<std::uint32_t>(src[T::stat_byte_offset(L, f, sbytes)])
+                                               << (8 * T::stat_field_byte(bs, f));
+        for (int j = 0; j < 8; ++j) {
+            const int kind = j >> 2, h = (j >> 1) & 1, b = j & 1, blk = 8 * h + 2 * t + b;
+            for (int rho = 0; rho < 2; ++rho) {
+                const auto code = static_cast<std::uint8_t>((st[rho] >> (bs * j)) & mask);
+                (kind ? u.zcode : u.scode)[blk][g + 8 * rho] = code;
+            }
         }
     }
 }

@@ -74,33 +74,30 @@ __global__ void __launch_bounds__(256) tc_units(const RawGeom geo, std::uint32_t
             reinterpret_cast<std::uint32_t*>(dst + lane * 16 * BW)[CW * c + w] = word;
         }
     }
-    // lane statistics: 8 scale then 8 zero codes (eps = 4h + 2s + rho)
+    // lane statistics (tiled.hpp): pair j = 4*kind + 2h + b, rows g / g + 8 in
+    // the lo / hi stream at stream bit bs*j
     {
-        std::uint64_t bits[2] = {0, 0};
-        auto put = [&](int pos, int nb, std::uint32_t v) {
-            for (int b = 0; b < nb; ++b, ++pos)
-                if ((v >> b) & 1u) bits[pos >> 6] |= std::uint64_t{1} << (pos & 63);
-        };
+        std::uint32_t st[2] = {0, 0};
 #pragma unroll 1
-        for (int eps = 0; eps < 8; ++eps) {
-            const int h = eps >> 2, s = (eps >> 1) & 1, rho = eps & 1;
-            const int blk = 8 * h + 2 * t + s;
-            const std::uint32_t row = g + 8 * rho, k = 16u * P + blk;
-            std::uint32_t sc = 0, zc = 0;
-            if (gvalid && k < geo.nblocks) {
-                const RecFields f = rec_fields(geo, k, gg);
-                if (row < f.gr) {
-                    sc = geo.bits_at(f.s, row, bs);
-                    zc = geo.bits_at(f.z, row, bz);
-                }
+        for (int j = 0; j < 8; ++j) {
+            const int kind = j >> 2, h = (j >> 1) & 1, b = j & 1;
+            const std::uint32_t k = 16u * P + 8 * h + 2 * t + b;
+            RecFields f{};
+            const bool kv = gvalid && k < geo.nblocks;
+            if (kv) f = rec_fields(geo, k, gg);
+#pragma unroll
+            for (int rho = 0; rho < 2; ++rho) {
+                const std::uint32_t row = g + 8 * rho;
+                std::uint32_t code = 0;
+                if (kv && row < f.gr) code = kind ? geo.bits_at(f.z, row, bz) : geo.bits_at(f.s, row, bs);
+                st[rho] |= code << (bs * j);
             }
-            put(eps * bs, bs, sc);
-            put(8 * bs + eps * bz, bz, zc);
         }
         const int sbytes = bs + bz;
         std::uint8_t* sd = dst + T::code_bytes(BW);
-        for (int b = 0; b < sbytes; ++b)
-            sd[T::stat_byte_offset(lane, b, sbytes)] = static_cast<std::uint8_t>(bits[b >> 3] >> (8 * (b & 7)));
+        for (int f = 0; f < sbytes; ++f)
+            sd[T::stat_byte_offset(lane, f, sbytes)] =
+                static_cast<std::uint8_t>(st[T::stat_field_stream(bs, f)] >> (8 * T::stat_field_byte(bs, f)));
     }
     // block scalars {S_s, Z_s, S_z, Z_z}
     if (lane < 16) {
