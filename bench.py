@@ -219,7 +219,6 @@ def reference_check(streams, groups, rank: int, world: int) -> dict:
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    from paper_2306_03078_b200.sharded import row_bands
 
     ref = O.Reference()
     threads = max(1, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
@@ -229,10 +228,8 @@ def reference_check(streams, groups, rank: int, world: int) -> dict:
         torch.cuda.synchronize()
         y = gp["y"].cpu().numpy()
         x32 = gp["x"].float().cpu().numpy()
-        off, errs = 0, []
-        for i in gp["members"]:
-            m = LAYERS[i][1]
-            r0, r1 = row_bands(m, world)[rank]
+        errs = []
+        for i, r0, r1, off in gp["local"]:
             t = ref.decode(streams[i])
             nb = max(1, min(threads, (r1 - r0) // 16))
             edges = [r0 + 16 * (((r1 - r0) // 16) * j // nb) for j in range(nb)] + [r1]
@@ -240,7 +237,6 @@ def reference_check(streams, groups, rank: int, world: int) -> dict:
             del t
             yr = ref.matvec_bands(bands, x32, nb)
             errs.append(O.relative_l2(y[off:off + r1 - r0], yr))
-            off += r1 - r0
         worst[gp["name"]] = max(errs)
     bad = {k: v for k, v in worst.items() if not v <= 1e-3}
     if bad:
@@ -342,33 +338,49 @@ def run_ours(args) -> None:
 
     # One decoder block as a serving stack runs it: q/k/v share x (one stacked
     # handle = fused QKV), gate/up share x (stacked), o and down alone -> four
-    # launches per step over the same seven layers' bytes.  N > 1: each rank
-    # holds the same row band of every member layer (stacked), and the bands
-    # are all-gathered (rank-major) after every launch.
+    # launches per step over the same seven layers' bytes.  N > 1: the rows of
+    # each stacked group are cut into row bands (row_bands over the stacked
+    # rows, the edges spqr_sharded_create computes), so the gathered y of a
+    # group is in [q; k; v] order.  The band layers come from the C ABI's NCCL
+    # sharded handles (spqr_sharded_*: band + ncclAllGather = the NCCL
+    # baseline), or -- gloo test hook -- from the same slices made here.
+    comm = None
+    if world > 1 and not share:
+        uid = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = P.NcclComm(uid[0], world, rank, dev.index)
     groups = []
     bytes_step = 0  # whole-job algorithmic bytes per step
     gen = torch.Generator(device="cpu").manual_seed(2)
     for gname, members in GROUPS:
         n = LAYERS[members[0]][2]
-        parts, rows_local, bands = [], 0, []
+        m_total = sum(LAYERS[i][1] for i in members)
+        bands = row_bands(m_total, world)
+        a, b = bands[rank]
+        local, base = [], 0  # (member, member rows r0..r1 on this rank, offset in the band's y)
         for i in members:
             m = LAYERS[i][1]
-            bd = row_bands(m, world)
-            bands.append(bd)
-            r0, r1 = bd[rank]
-            parts.append(streams[i] if world == 1 else P.slice_rows(streams[i], r0, r1))
-            rows_local += r1 - r0
+            la, lb = max(a, base), min(b, base + m)
+            if la < lb:
+                local.append((i, la - base, lb - base, la - a))
+            base += m
             bytes_step += alg_bytes(len(streams[i]) - 48, m, n) + 2 * n * (world - 1)
-        L = P.Layer(parts[0], device=dev.index) if len(parts) == 1 else P.Layer.stacked(parts, device=dev.index)
-        assert L.info["fast_path"] == 1 and L.rows == rows_local
+        S = None
+        if comm is not None:
+            S = P.ShardedNccl([streams[i] for i in members], comm, device=dev.index)
+            assert S.band == (a, b) and S.rows == m_total
+            L = S.band_layer()
+        else:
+            parts = [streams[i] if (r0, r1) == (0, LAYERS[i][1]) else P.slice_rows(streams[i], r0, r1)
+                     for i, r0, r1, _ in local]
+            L = P.Layer(parts[0], device=dev.index) if len(parts) == 1 else P.Layer.stacked(parts, device=dev.index)
+        assert L.info["fast_path"] == 1 and L.rows == b - a
         x = torch.randn(n, generator=gen).to(torch.float16)
-        m_total = sum(LAYERS[i][1] for i in members)
-        per_rank = max(sum(bd[r][1] - bd[r][0] for bd in bands) for r in range(world))
         groups.append({
-            "name": gname, "members": members, "m": m_total, "n": n, "L": L, "x": x.to(dev),
-            "x32": x.float().pin_memory(), "y": torch.empty(rows_local, device=dev),
-            "band": (0, rows_local), "yfull": torch.empty(world * per_rank, device=dev) if world > 1 else None,
-            "bands": [(r * per_rank, r * per_rank + per_rank) for r in range(world)],
+            "name": gname, "members": members, "local": local, "m": m_total, "n": n, "L": L, "S": S,
+            "x": x.to(dev), "x32": x.float().pin_memory(), "y": torch.empty(b - a, device=dev),
+            "band": (a, b), "bands": bands,
+            "yfull": torch.empty(m_total, device=dev) if world > 1 else None,
         })
     payload_step = sum(len(s) - 48 for s in streams)
     check = reference_check(streams, groups, rank, world)  # before any timing
@@ -380,7 +392,7 @@ def run_ours(args) -> None:
         err = ""
         try:
             for gp in groups:
-                gp["fg"] = FusedGather(gp["bands"][-1][1], gp["bands"], rank, world, dev.index)
+                gp["fg"] = FusedGather(gp["m"], gp["bands"], rank, world, dev.index)
         except Exception as ex:  # noqa: BLE001 -- every rank must agree before choosing a path
             err = f"{type(ex).__name__}: {ex}"
         ok = torch.tensor([0 if err else 1], device=dev)
@@ -389,23 +401,26 @@ def run_ours(args) -> None:
         if not fused and rank == 0:
             print(f"fused all-gather unavailable ({err or 'on another rank'}); timing the NCCL path", file=sys.stderr)
 
-    def gather(gp):  # equal-size rank bands (every member's band is 32-row aligned)
-        gather_rows(torch.nn.functional.pad(gp["y"], (0, gp["bands"][0][1] - gp["y"].numel())), gp["bands"],
-                    out=gp["yfull"])
+    def gather(gp):  # gloo test hook only (torch.distributed all-gather of the y bands)
+        gather_rows(gp["y"], gp["bands"], out=gp["yfull"])
+
+    def nccl_step():  # the baseline the north star names: band kernel, then NCCL all-gather (C ABI)
+        for gp in groups:
+            if gp["S"] is not None:
+                gp["S"].matvec(gp["x"], gp["yfull"], stream=stream)
+            else:
+                gp["L"].matvec(gp["x"], gp["y"], stream=stream)
+                gather(gp)
 
     def step():
+        if world > 1 and not fused:
+            nccl_step()
+            return
         for gp in groups:
             if fused:
                 gp["fg"].matvec(gp["L"], gp["x"], stream=stream)
             else:
                 gp["L"].matvec(gp["x"], gp["y"], stream=stream)
-                if world > 1:
-                    gather(gp)
-
-    def nccl_step():  # the baseline the north star names: band kernel, then NCCL all-gather
-        for gp in groups:
-            gp["L"].matvec(gp["x"], gp["y"], stream=stream)
-            gather(gp)
 
     with torch.cuda.stream(stream):
         for _ in range(3):
@@ -535,10 +550,6 @@ def run_ours(args) -> None:
     # step, each the max over ranks ----
     multi = None
     if world > 1:
-        def gathers():
-            for gp in groups:
-                gather(gp)
-
         def eager_ms(fn, reps=10):  # gloo collectives cannot be captured: host-timed
             fn()
             torch.cuda.synchronize()
@@ -547,30 +558,30 @@ def run_ours(args) -> None:
                 fn()
             torch.cuda.synchronize()
             return 1e3 * (time.perf_counter() - t0) / reps
-        gms = nms = None
+        nms = None
         if not share:
             try:  # NCCL collectives inside a CUDA graph
-                gms = graph_time(gathers, max(20, args.steps // 5))
                 nms = graph_time(nccl_step, max(20, args.steps // 5))
             except Exception as ex:  # noqa: BLE001 -- the baseline must not sink the run
                 print(f"NCCL graph capture failed ({type(ex).__name__}: {ex}); timing it eagerly", file=sys.stderr)
                 torch.cuda.synchronize()
-                gms = nms = None
-        if gms is None:
-            gms, nms = eager_ms(gathers), eager_ms(nccl_step)
-        t = torch.tensor([kms, gms, nms], device=dev)
+        if nms is None:
+            nms = eager_ms(nccl_step)
+        t = torch.tensor([kms, nms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         multi = {"path": "fused all-gather: band gemv_cta stores y rows into every rank's buffer (CUDA IPC / "
                          "NVLink P2P) + round counters, one gather_wait launch per group" if fused
-                         else "band gemv_cta + NCCL all-gather (fused path unavailable)",
+                         else "band gemv_cta + NCCL all-gather (spqr_sharded_matvec; fused path unavailable)",
+                 "bands": "row_bands over each group's stacked rows: gathered y in [q; k; v] / [gate; up] order",
                  "kernel_us_per_step": round(1e3 * float(t[0]), 3),
                  "step_us": round(1e3 * ms_per_step, 3),
                  "gather_us_per_step": round(1e3 * ms_per_step - 1e3 * float(t[0]), 3),
-                 "nccl_baseline": {"allgather_us_per_step": round(1e3 * float(t[1]), 3),
-                                   "step_us": round(1e3 * float(t[2]), 3),
-                                   "backend": dist.get_backend()},
+                 "nccl_baseline": {"step_us": round(1e3 * float(t[1]), 3),
+                                   "allgather_us_per_step": round(1e3 * (float(t[1]) - float(t[0])), 3),
+                                   "path": "spqr_sharded_matvec (C ABI: band spqr_matvec + ncclAllGather)"
+                                           if not share else "band matvec + torch.distributed gloo all-gather"},
                  "allgathers_per_step": len(groups),
-                 "allgather_bytes_per_rank": [4 * gp["yfull"].numel() // world for gp in groups]}
+                 "allgather_bytes_per_rank": [4 * (gp["band"][1] - gp["band"][0]) for gp in groups]}
 
     # ---- dense fp16 GEMV comparator (ours and cuBLAS), same stacked shapes ----
     dense = {}
@@ -607,6 +618,9 @@ def run_ours(args) -> None:
                 xd32[i].copy_(gp["x32"], non_blocking=True)
                 if fused:
                     yf = gp["fg"].matvec(gp["L"], xd32[i], stream=torch.cuda.current_stream())
+                elif gp["S"] is not None:
+                    gp["S"].matvec(xd32[i], gp["yfull"], stream=torch.cuda.current_stream())
+                    yf = gp["yfull"]
                 else:
                     gp["L"].matvec(xd32[i], gp["y"], stream=torch.cuda.current_stream())
                     gather(gp)
@@ -633,7 +647,8 @@ def run_ours(args) -> None:
            "d2h_bytes_per_step": sum(4 * gp["m"] for gp in groups),
            "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3),
            "path": "spqr_matvec_host (C ABI, page-locked host x/y: copy kernel reads x, fused kernel stores y to host, sync) per group"
-                   if world == 1 else "H2D x, spqr_matvec_gather + spqr_gather_wait (fused all-gather), D2H y per group"}
+                   if world == 1 else ("H2D x, spqr_matvec_gather + spqr_gather_wait (fused all-gather), D2H y per group"
+                                       if fused else "H2D x, spqr_sharded_matvec (band + NCCL all-gather), D2H y per group")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -48,7 +48,8 @@ enum spqr_status {
     SPQR_E_ILL_CONDITIONED = 15,
     SPQR_E_OUTLIER_BUDGET_EXCEEDED = 16,
     SPQR_E_CUDA = 100,
-    SPQR_E_BUFFER_TOO_SMALL = 101
+    SPQR_E_BUFFER_TOO_SMALL = 101,
+    SPQR_E_NCCL = 102
 };
 
 enum spqr_dtype { SPQR_F16 = 0, SPQR_F32 = 1 };
@@ -229,6 +230,38 @@ int spqr_matvec_gather(const spqr_layer* layer, const void* x_dev, int x_dtype, 
                        void* cuda_stream);
 int spqr_gather_wait(spqr_gather* g, void* cuda_stream);
 void spqr_gather_destroy(spqr_gather* g);
+
+/* Row-sharded decode over NCCL (SURVEY 8b "spqr_sharded_create(..., ncclComm_t)
+ * + spqr_sharded_matvec", 8e; BASELINE north_star: row-sharded layers with an
+ * NCCL all-gather of y).  One process per GPU.  Rank r holds the contiguous
+ * row band edges[r] .. edges[r+1] of the layer -- or of `count` layers stacked
+ * row-wise (q/k/v, gate/up: all but the last with rows % 32 == 0), cut in the
+ * stacked row order so the gathered y is [layer 0; layer 1; ...] -- with
+ * bands of lcm(32, beta2)-row units, sizes differing by at most one unit
+ * (sharded.py row_bands computes the same edges).  spqr_sharded_matvec: the
+ * band's spqr_matvec, then ncclAllGather of the y bands on cuda_stream; y
+ * (batch x rows fp32, on this rank's device) is complete on every rank when
+ * the stream reaches that point.  The handle's band layer and gather slots
+ * are used one call at a time (calls serialise on the handle); NCCL's rules
+ * apply (every rank issues the same sequence of calls).  NCCL is bound at
+ * run time (dlopen libnccl.so.2); NCCL failures return SPQR_E_NCCL.
+ * Communicator: spqr_nccl_unique_id on one rank, broadcast the
+ * SPQR_NCCL_ID_BYTES bytes (any transport), spqr_nccl_comm_init on every
+ * rank -- or pass an ncclComm_t the application already has. */
+#define SPQR_NCCL_ID_BYTES 128
+typedef struct spqr_sharded spqr_sharded;
+/* The band edges (world + 1 values) every rank computes for `rows` stacked rows. */
+int spqr_row_bands(uint32_t rows, uint32_t beta2, int world, uint32_t* edges);
+int spqr_nccl_unique_id(uint8_t* id_out);
+int spqr_nccl_comm_init(const uint8_t* id, int world, int rank, int device, void** nccl_comm_out);
+int spqr_nccl_comm_destroy(void* nccl_comm);
+int spqr_sharded_create(const uint8_t* const* streams, const size_t* sizes, int count, int rank, int world,
+                        void* nccl_comm, const spqr_layer_opts* opts, spqr_sharded** out);
+int spqr_sharded_band(const spqr_sharded* s, uint32_t* rows, uint32_t* band_begin, uint32_t* band_end,
+                      spqr_layer** band_layer);
+int spqr_sharded_matvec(spqr_sharded* s, const void* x_dev, int x_dtype, float* y_dev, int batch,
+                        void* cuda_stream);
+void spqr_sharded_destroy(spqr_sharded* s);
 
 /* Profiling split of spqr_matvec: stage 1 = x preparation only, stage 2 = the
  * product only, 0 = both.  On the fast path x preparation is fused into the

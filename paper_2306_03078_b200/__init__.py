@@ -137,6 +137,15 @@ def lib() -> C.CDLL:
         "spqr_matvec_gather": (i32, [vp, vp, i32, vp, vp]),
         "spqr_gather_wait": (i32, [vp, vp]),
         "spqr_gather_destroy": (None, [vp]),
+        "spqr_row_bands": (i32, [u32, u32, i32, vp]),
+        "spqr_nccl_unique_id": (i32, [vp]),
+        "spqr_nccl_comm_init": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
+        "spqr_nccl_comm_destroy": (i32, [vp]),
+        "spqr_sharded_create": (i32, [C.POINTER(vp), C.POINTER(sz), i32, i32, i32, vp, C.POINTER(LayerOpts),
+                                      C.POINTER(vp)]),
+        "spqr_sharded_band": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(vp)]),
+        "spqr_sharded_matvec": (i32, [vp, vp, i32, vp, i32, vp]),
+        "spqr_sharded_destroy": (None, [vp]),
         "spqr_dev_alloc": (i32, [C.POINTER(vp), sz]),
         "spqr_dev_free": (None, [vp]),
         "spqr_dev_copy_to_host": (i32, [vp, vp, sz]),
@@ -350,6 +359,8 @@ class Layer:
         return self
 
     def close(self):
+        if getattr(self, "_owner", None) is not None:  # a view of a handle owned elsewhere
+            self._h = self._owner = None
         if getattr(self, "_h", None):
             lib().spqr_layer_destroy(self._h)
             self._h = None
@@ -459,6 +470,95 @@ class Gather:
     def close(self):
         if getattr(self, "_h", None):
             lib().spqr_gather_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+NCCL_ID_BYTES = 128
+
+
+def c_row_bands(rows: int, beta2: int, world: int) -> list[tuple[int, int]]:
+    """The C ABI's band edges (spqr_row_bands; sharded.row_bands is the same rule)."""
+    e = np.zeros(world + 1, np.uint32)
+    _check(lib().spqr_row_bands(rows, beta2, world, e.ctypes.data_as(C.c_void_p)))
+    return [(int(e[i]), int(e[i + 1])) for i in range(world)]
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the C ABI (spqr_nccl_unique_id): broadcast the
+    bytes to every rank by any transport, then NcclComm(id, world, rank)."""
+    buf = (C.c_uint8 * NCCL_ID_BYTES)()
+    _check(lib().spqr_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator created through the C ABI (spqr_nccl_comm_init)."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        h = C.c_void_p()
+        _check(lib().spqr_nccl_comm_init(C.c_char_p(uid), world, rank, device, C.byref(h)))
+        self._h, self.world, self.rank, self.device = h, world, rank, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(lib().spqr_nccl_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardedNccl:
+    """This rank's row band of one layer (or of layers stacked row-wise) plus
+    the NCCL all-gather of y, entirely behind the C ABI (spqr_sharded_*):
+    matvec(x, y) leaves the full y (batch x rows) on every rank."""
+
+    def __init__(self, streams, comm: NcclComm, device: int = -1):
+        streams = [streams] if isinstance(streams, (bytes, bytearray)) else list(streams)
+        bufs = [_buf(s) for s in streams]
+        ptrs = (C.c_void_p * len(bufs))(*[b[1] for b in bufs])
+        sizes = (C.c_size_t * len(bufs))(*[b[2] for b in bufs])
+        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0, host_transcode=0)
+        h = C.c_void_p()
+        _check(lib().spqr_sharded_create(ptrs, sizes, len(bufs), comm.rank, comm.world, comm.handle,
+                                         C.byref(opts), C.byref(h)))
+        self._h, self.comm = h, comm
+        rows, a, b = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib().spqr_sharded_band(h, C.byref(rows), C.byref(a), C.byref(b), None))
+        self.rows, self.band = rows.value, (a.value, b.value)
+
+    def band_layer(self) -> "Layer":
+        """This rank's band as a Layer view (owned by this handle: valid while it lives)."""
+        h = C.c_void_p()
+        _check(lib().spqr_sharded_band(self._h, None, None, None, C.byref(h)))
+        L = Layer.__new__(Layer)
+        L._h, L._owner = h, self
+        info = LayerInfo()
+        _check(lib().spqr_layer_get_info(h, C.byref(info)))
+        L.info = info.as_dict()
+        L.rows, L.cols = L.info["rows"], L.info["cols"]
+        return L
+
+    def matvec(self, x, y, batch: int = 1, stream=None) -> None:
+        dt = F16 if str(getattr(x, "dtype", "")).endswith("float16") else F32
+        _check(lib().spqr_sharded_matvec(self._h, _ptr(x), dt, _ptr(y), batch, _stream_ptr(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().spqr_sharded_destroy(self._h)
             self._h = None
 
     def __del__(self):

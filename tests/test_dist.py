@@ -32,6 +32,20 @@ def test_row_bands_refuse_empty_bands(m, world):
         row_bands(m, world)
 
 
+@pytest.mark.parametrize("m,world,beta2", [(8192, 8, 16), (22016, 8, 16), (44032, 3, 16), (24576, 8, 16),
+                                           (208, 2, 16), (96, 3, 16), (40, 2, 16), (8192, 8, 64), (200, 2, 48)])
+def test_c_abi_row_bands_match(m, world, beta2):
+    """spqr_row_bands (the edges spqr_sharded_create cuts) == sharded.row_bands."""
+    import paper_2306_03078_b200 as P
+    assert P.c_row_bands(m, beta2, world) == row_bands(m, world, beta2=beta2)
+
+
+def test_c_abi_row_bands_refuse_empty_bands():
+    import paper_2306_03078_b200 as P
+    with pytest.raises(P.SpqrError):
+        P.c_row_bands(96, 16, 4)
+
+
 def test_llama_bands_are_equal():
     for m in (4096, 8192, 11008, 22016):
         for w in (1, 2, 4, 8):
