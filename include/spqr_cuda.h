@@ -191,7 +191,12 @@ int spqr_layer_export_stream(const spqr_layer* layer, uint8_t* out, size_t cap, 
  * ORIGINAL column order) into caller device memory.  Bit-exact. */
 int spqr_dequantize(const spqr_layer* layer, float* w_dev, void* cuda_stream);
 
-/* Scratch for spqr_matvec_ws (bytes). */
+/* Scratch for spqr_matvec_ws (bytes).  The workspace carries arrival
+ * counters between launches: zero-fill it once before its first use
+ * (cudaMemsetAsync(ws, 0, bytes)); every launch leaves its counters zero
+ * again.  A workspace belongs to ONE layer and one stream at a time (its
+ * counter and partial regions sit at layer-specific offsets): zero it again
+ * before handing it to another layer.  Size it for the largest batch used. */
 uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
 
 /* matvec (kernel.hpp:89-124) on device buffers: y[b] = W * x[b] for b < batch.
@@ -219,7 +224,13 @@ int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, floa
  * exchange the world x SPQR_GATHER_HANDLE_BYTES handles and the bands' first
  * rows (any transport, e.g. torch.distributed) -> spqr_gather_open -> per
  * step spqr_matvec_gather + spqr_gather_wait, then read spqr_gather_y.
- * Batch 1; the layer is this rank's band (rows row_base[rank] ...). */
+ * Batch 1; the layer is this rank's band (rows row_base[rank] ...).
+ * Round safety: a rank's band kernel of round R stores into peer j's y only
+ * after peer j's band kernel of round R has started (each band kernel posts
+ * its round to every rank first), so everything peer j issued on its stream
+ * before spqr_matvec_gather of round R -- its readers of round R-1's y -- has
+ * completed: consumers of spqr_gather_y must be stream-ordered before the
+ * rank's next spqr_matvec_gather (no host barrier is needed between rounds). */
 #define SPQR_GATHER_HANDLE_BYTES 64
 typedef struct spqr_gather spqr_gather;
 int spqr_gather_create(int device, uint32_t rows, int world, int rank, spqr_gather** out);

@@ -693,7 +693,9 @@ std::uint64_t transcode_on_device(spqr_layer* L, const std::vector<spqr::detail:
 
 // Fused all-gather target of one rank: one cudaMalloc'd block (exported to
 // the other ranks by CUDA IPC): [0, 32) per-source-rank round counters,
-// [64] this rank's round, [68] CTAs done (local), [256, ...) the full y.
+// [64] this rank's round, [68] CTAs done (local), [128, 160) per-source-rank
+// latest started round (a peer's band kernel posts it before anyone stores
+// that round into its y), [256, ...) the full y.
 struct spqr_gather {
     int device = 0, world = 1, rank = 0;
     std::uint32_t rows = 0;
@@ -1022,6 +1024,8 @@ int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr
         p.row_base = rb;
         p.rank = static_cast<std::uint32_t>(g->rank);
         p.done_ctr = reinterpret_cast<std::uint32_t*>(g->base + 68);
+        p.round = reinterpret_cast<const std::uint32_t*>(g->base + 64);
+        p.started = reinterpret_cast<const std::uint32_t*>(g->base + 4 * spqr_dev::kGatherStartedWord);
         const auto& c = L->cta[f16 ? 0 : 1];
         ck(spqr_dev::launch_cta_gather(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits), !f16,
                                        c.shared_x, p, c.grid, c.smem, kNC, kSmemLimit,

@@ -75,7 +75,15 @@ struct CtaParams {
     std::uint32_t* pflags[kMaxPeers + 1];
     std::uint32_t* done_ctr;          // CTAs finished this round (last one resets it)
     std::uint32_t npeer, nflag, row_base, rank;
+    // Before storing round R into peer j's y, a CTA waits until peer j's band
+    // kernel of round R has started (started[j] >= R in this rank's block,
+    // posted by j): everything peer j's stream ordered before that kernel --
+    // its consumers of y from round R-1 -- is then complete, so a rank running
+    // one round ahead never overwrites rows a peer is still reading.
+    const std::uint32_t* round;       // this rank's completed rounds (gather_wait advances it)
+    const std::uint32_t* started;     // [world] in this rank's block: peer j's latest started round
 };
+constexpr std::uint32_t kGatherStartedWord = 32;  // started[] at byte 128 of a gather block
 
 __device__ __forceinline__ void bar_sync_named(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -277,10 +285,29 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ std::uint32_t g_round, g_peers_ok;  // GATHER: this launch's round; peers have started it
+    auto wait_peers = [&]() {  // (GATHER) until every peer's band kernel of this round has started
+        if (lane == 0) {
+            const unsigned long long t0 = globaltimer();
+            for (std::uint32_t j = 0; j < p.nflag; ++j) {
+                if (j == p.rank) continue;
+                for (std::uint32_t it = 0;; ++it) {
+                    std::uint32_t v;
+                    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.started + j) : "memory");
+                    if (static_cast<int>(v - g_round) >= 0) break;
+                    if ((it & 1023u) == 1023u && globaltimer() - t0 > 20000000000ull) __trap();  // dead peer
+                }
+            }
+            *reinterpret_cast<volatile std::uint32_t*>(&g_peers_ok) = 1u;
+        }
+        __syncwarp();
+    };
     auto put_y = [&](std::uint32_t row, float v) {
         p.y[row] = v;
-        if constexpr (GATHER)
+        if constexpr (GATHER) {
+            if (p.npeer && *reinterpret_cast<volatile std::uint32_t*>(&g_peers_ok) == 0u) wait_peers();
             for (std::uint32_t j = 0; j < p.npeer; ++j) p.ypeer[j][p.row_base + row] = v;
+        }
     };
 #ifdef SPQR_TIMELINE
     const std::uint32_t wk = blockIdx.x * 16u + static_cast<std::uint32_t>(warp);
@@ -441,6 +468,17 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         if (!waited) {
             pdl_wait();  // the preceding kernel has completed: x, y and the partial slots are ours
             waited = true;
+            if constexpr (GATHER) {
+                if (threadIdx.x == 0) {
+                    g_round = *p.round + 1u;  // gather_wait of the previous round has completed
+                    g_peers_ok = 0u;
+                    if (blockIdx.x == 0)  // announce: this rank's band kernel of round g_round runs
+                        for (std::uint32_t j = 0; j < p.nflag; ++j)
+                            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pflags[j] + kGatherStartedWord + p.rank),
+                                         "r"(g_round) : "memory");
+                }
+                bar_sync_named(2, NT);
+            }
             SPQR_TL(1)
             if constexpr (SHX) {  // own panels (<= 3), the first cell's first; every x load
                                   // is in flight before the first build; no CTA barrier

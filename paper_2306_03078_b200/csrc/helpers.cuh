@@ -75,6 +75,12 @@ __device__ __forceinline__ void load_stat_streams(const std::uint8_t* stats, int
     st[1] = __byte_perm(w0, w1, 0x7632);  // hi halves
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 #ifdef SPQR_TIMELINE
 // tools-only instrumentation (tools/timeline_dev.py): per warp %globaltimer at
 // entry, after the PDL wait, first cell staged, loop end, exit.

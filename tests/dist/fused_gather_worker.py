@@ -76,6 +76,22 @@ def main():
             check(x, y, f"m={m} graph {i}")
             dist.barrier()
         del g
+        # back-to-back rounds, no host barrier: each rank's consumer of a
+        # round's y (the D2H copy) is stream-ordered before its next band
+        # kernel, and no rank stores round R into a peer's y before that
+        # peer's band kernel of round R has started (gemv_cta wait_peers)
+        R = 6
+        outs = [torch.empty(m, dtype=torch.float32).pin_memory() for _ in range(R)]
+        xr = [xs[i % 4] if i % 2 == 0 else xs[i % 4] * 0.5 for i in range(R)]
+        with torch.cuda.stream(st):
+            for i in range(R):
+                x.copy_(xr[i])
+                y = fused.matvec(x, stream=st)
+                outs[i].copy_(y[:m], non_blocking=True)
+        st.synchronize()
+        for i in range(R):
+            check(xr[i], outs[i], f"m={m} back-to-back {i}")
+        dist.barrier()
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:
