@@ -114,7 +114,8 @@ typedef struct spqr_layer spqr_layer;
 typedef struct spqr_layer_opts {
     int32_t device;        /* CUDA ordinal; -1 = current device */
     int32_t force_generic; /* 1: never build the tiled planes (tests / comparison) */
-    int32_t keep_stream;   /* 1: keep the raw stream on the device even on the fast path */
+    int32_t keep_stream;   /* 1: keep the raw stream on the device even on the fast path (matvec,
+                              dequantize and export read the cells; the stream is for debugging) */
     uint32_t row_begin;    /* row band [row_begin, row_end) of the stream; 0,0 = all rows */
     uint32_t row_end;
     int32_t host_transcode; /* 1: build the HBM layout on the host (comparison); 0: on the GPU */
@@ -188,7 +189,9 @@ int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info);
 int spqr_layer_export_stream(const spqr_layer* layer, uint8_t* out, size_t cap, size_t* len);
 
 /* dequantize_full (kernel.hpp:17-25): W (rows x cols, fp32, row-major,
- * ORIGINAL column order) into caller device memory.  Bit-exact. */
+ * ORIGINAL column order) into caller device memory.  Bit-exact.  Fast-path
+ * layers decode their cell records (dequant_cells, one launch); others the
+ * raw stream (dequant_raw + outliers_raw). */
 int spqr_dequantize(const spqr_layer* layer, float* w_dev, void* cuda_stream);
 
 /* Scratch for spqr_matvec_ws (bytes).  The workspace carries arrival

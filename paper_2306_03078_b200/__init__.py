@@ -326,9 +326,9 @@ class Layer:
     """A layer resident in HBM (spqr_layer_create: decode + plan + upload)."""
 
     def __init__(self, stream: bytes, device: int = -1, force_generic: bool = False,
-                 rows: tuple[int, int] | None = None, host_transcode: bool = False):
+                 rows: tuple[int, int] | None = None, host_transcode: bool = False, keep_stream: bool = False):
         a, p, n = _buf(stream)
-        opts = LayerOpts(device=device, force_generic=int(force_generic), keep_stream=1,
+        opts = LayerOpts(device=device, force_generic=int(force_generic), keep_stream=int(keep_stream),
                          row_begin=rows[0] if rows else 0, row_end=rows[1] if rows else 0,
                          host_transcode=int(host_transcode))
         h = C.c_void_p()
@@ -346,7 +346,7 @@ class Layer:
         bufs = [_buf(s) for s in streams]
         ptrs = (C.c_void_p * len(bufs))(*[b[1] for b in bufs])
         sizes = (C.c_size_t * len(bufs))(*[b[2] for b in bufs])
-        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0,
+        opts = LayerOpts(device=device, force_generic=0, keep_stream=0, row_begin=0, row_end=0,
                          host_transcode=int(host_transcode))
         h = C.c_void_p()
         _check(lib().spqr_layer_create_stacked(ptrs, sizes, len(bufs), C.byref(opts), C.byref(h)))
@@ -531,7 +531,7 @@ class ShardedNccl:
         bufs = [_buf(s) for s in streams]
         ptrs = (C.c_void_p * len(bufs))(*[b[1] for b in bufs])
         sizes = (C.c_size_t * len(bufs))(*[b[2] for b in bufs])
-        opts = LayerOpts(device=device, force_generic=0, keep_stream=1, row_begin=0, row_end=0, host_transcode=0)
+        opts = LayerOpts(device=device, force_generic=0, keep_stream=0, row_begin=0, row_end=0, host_transcode=0)
         h = C.c_void_p()
         _check(lib().spqr_sharded_create(ptrs, sizes, len(bufs), comm.rank, comm.world, comm.handle,
                                          C.byref(opts), C.byref(h)))

@@ -757,14 +757,23 @@ int spqr_layer_create(const uint8_t* stream, size_t nbytes, const spqr_layer_opt
             dev_bytes += 4ull * v.cols;
         }
         L->fast = !o.force_generic && spqr::detail::tiled_supported(v);
-        if (!L->fast || o.keep_stream || true) {  // dequantize reads the raw stream (v1)
+        // the raw stream stays in HBM only for the generic kernels (or on
+        // request); a fast-path layer's stream visits the device for the
+        // transcode and is freed -- matvec, dequantize and export read cells
+        const bool keep = !L->fast || o.keep_stream;
+        if (keep || (L->fast && !o.host_transcode)) {
             L->d_stream = dalloc<std::uint8_t>(n + 16);
             ck(cudaMemcpy(L->d_stream, s, n, cudaMemcpyHostToDevice), "H2D stream");
-            dev_bytes += n;
         }
         if (L->fast)
             dev_bytes += o.host_transcode ? upload_tiled(L.get(), spqr::detail::transcode_to_tiled(v, 0), {v})
                                           : transcode_on_device(L.get(), {v}, {L->d_stream});
+        if (keep) {
+            dev_bytes += n;
+        } else if (L->d_stream) {
+            cudaFree(L->d_stream);
+            L->d_stream = nullptr;
+        }
         L->info.fast_path = L->fast;
         ensure_own_ws(L.get(), 1);
         dev_bytes += L->ws_bytes;
@@ -921,6 +930,27 @@ int spqr_dequantize(const spqr_layer* L, float* w_dev, void* cuda_stream) {
         DevGuard dg(L->device);
         auto st = static_cast<cudaStream_t>(cuda_stream);
         g_launches = 0;
+        if (L->fast) {  // straight from the cell records (no raw stream in HBM)
+            const unsigned blocks = static_cast<unsigned>((2ull * L->Gn * L->Pn * 32 + 255) / 256);
+            const std::uint32_t m = L->info.rows, n = L->info.cols;
+            auto run = [&](auto kern) {
+                kern<<<blocks, 256, 0, st>>>(L->d_cells, L->d_cell_off, L->Gn, L->Pn, m, n, L->d_order, w_dev);
+            };
+            switch (L->info.weight_bits * 10 + L->info.scale_bits) {
+                case 22: run(spqr_dev::dequant_cells<2, 2>); break;
+                case 23: run(spqr_dev::dequant_cells<2, 3>); break;
+                case 24: run(spqr_dev::dequant_cells<2, 4>); break;
+                case 32: run(spqr_dev::dequant_cells<3, 2>); break;
+                case 33: run(spqr_dev::dequant_cells<3, 3>); break;
+                case 34: run(spqr_dev::dequant_cells<3, 4>); break;
+                case 42: run(spqr_dev::dequant_cells<4, 2>); break;
+                case 43: run(spqr_dev::dequant_cells<4, 3>); break;
+                default: run(spqr_dev::dequant_cells<4, 4>); break;
+            }
+            ck(cudaGetLastError(), "launch dequant_cells");
+            g_launches = 1;
+            return;
+        }
         const spqr_dev::RawGeom geo = raw_geom(L);
         const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
         const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((total + 255) / 256, 1u << 20));
@@ -1236,13 +1266,7 @@ int spqr_bench_layer(const spqr_layer* L, int repeats, double* ns3) {
                 return 1e6 * (repeats % 2 ? ms[mid] : 0.5 * (ms[mid - 1] + ms[mid]));
             };
             ns3[0] = time_it([&] { run_matvec(L, x, SPQR_F32, y, 1, L->d_ws, L->ws_bytes, nullptr); });
-            const spqr_dev::RawGeom geo = raw_geom(L);
-            const std::uint64_t total = static_cast<std::uint64_t>(geo.rows) * geo.nblocks;
-            const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((total + 255) / 256, 1u << 20));
-            ns3[1] = time_it([&] {
-                spqr_dev::dequant_raw<<<blocks, 256>>>(geo, w);
-                spqr_dev::outliers_raw<<<(geo.rows + 255) / 256, 256>>>(geo, w);
-            });
+            ns3[1] = time_it([&] { spqr_dequantize(L, w, nullptr); });
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device);
             const unsigned grid = std::min<unsigned>((m + 7) / 8, static_cast<unsigned>(sms) * 8);

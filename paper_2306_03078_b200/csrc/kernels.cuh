@@ -119,6 +119,7 @@ __device__ __forceinline__ std::uint32_t window(const std::uint32_t* w, int B) {
 #include "helpers.cuh"
 #include "gemv_cta.cuh"
 #include "gemm_tc.cuh"
+#include "dequant_cells.cuh"
 
 // ============================================================== raw path ====
 // Geometry of a raw .spqr stream resident in device memory (any config).
