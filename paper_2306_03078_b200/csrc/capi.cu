@@ -113,12 +113,21 @@ struct spqr_layer {
     mutable int hg_batch = 0, hg_launches = 0;
     mutable const void* hg_src = nullptr;
     mutable void* hg_dst = nullptr;
+    // completion: signal_host posts *d_seq + 1 to *h_flag; h_seq = last seen
+    mutable std::uint32_t* h_flag = nullptr;
+    mutable std::uint32_t* d_seq = nullptr;
+    mutable std::uint32_t h_seq = 0;
+    // page-locked or not, per caller pointer (cudaPointerGetAttributes once)
+    mutable const void* pk_ptr[2] = {nullptr, nullptr};
+    mutable bool pk_pinned[2] = {false, false};
 
     ~spqr_layer() {
         if (hgraph) cudaGraphExecDestroy(hgraph);
         if (hst) cudaStreamDestroy(hst);
         if (h_x) cudaFreeHost(h_x);
         if (h_y) cudaFreeHost(h_y);
+        if (h_flag) cudaFreeHost(h_flag);
+        if (d_seq) cudaFree(d_seq);
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
                         static_cast<void*>(d_cell_off), d_ws, d_wsh,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
@@ -1132,18 +1141,31 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
             ck(cudaHostAlloc(&L->h_x, 4 * L->xh_cap, cudaHostAllocDefault), "cudaHostAlloc(x staging)");
             ck(cudaHostAlloc(&L->h_y, 4 * L->yh_cap, cudaHostAllocDefault), "cudaHostAlloc(y staging)");
         }
-        if (!L->hst) ck(cudaStreamCreateWithFlags(&L->hst, cudaStreamNonBlocking), "stream (host API)");
-        // caller buffers that are page-locked are copied directly (true async
-        // DMA); pageable ones go through the pinned staging
-        auto pinned = [](const void* p) {
+        if (!L->hst) {
+            ck(cudaStreamCreateWithFlags(&L->hst, cudaStreamNonBlocking), "stream (host API)");
+            ck(cudaHostAlloc(&L->h_flag, 64, cudaHostAllocDefault), "cudaHostAlloc(flag)");
+            *reinterpret_cast<volatile std::uint32_t*>(L->h_flag) = 0u;
+            L->d_seq = dalloc<std::uint32_t>(1);
+            ck(cudaMemset(L->d_seq, 0, 4), "memset seq");
+            L->h_seq = 0;
+        }
+        // caller buffers that are page-locked are read / written directly by
+        // the kernels; pageable ones go through the pinned staging.  The kind
+        // is looked up once per pointer (the same buffers come back call after
+        // call in a decode loop)
+        auto pinned = [&](int k, const void* ptr) {
+            if (L->pk_ptr[k] == ptr) return L->pk_pinned[k];
             cudaPointerAttributes a{};
-            if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            bool pin = false;
+            if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess)
                 cudaGetLastError();
-                return false;
-            }
-            return a.type == cudaMemoryTypeHost;
+            else
+                pin = a.type == cudaMemoryTypeHost;
+            L->pk_ptr[k] = ptr;
+            L->pk_pinned[k] = pin;
+            return pin;
         };
-        const bool px = pinned(x_host), py = pinned(y_host);
+        const bool px = pinned(0, x_host), py = pinned(1, y_host);
         const void* src = px ? static_cast<const void*>(x_host) : L->h_x;
         void* dst = py ? static_cast<void*>(y_host) : L->h_y;
         if (!px) std::memcpy(L->h_x, x_host, 4 * nx);
@@ -1166,6 +1188,8 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
                     ck(cudaMemcpyAsync(L->d_xh, src, 4 * nx, cudaMemcpyHostToDevice, L->hst), "H2D x");
                 }
                 run_matvec(L, L->d_xh, SPQR_F32, static_cast<float*>(dst), batch, L->d_wsh, L->wsh_bytes, L->hst);
+                spqr_dev::signal_host<<<1, 1, 0, L->hst>>>(L->d_seq, L->h_flag);
+                ck(cudaGetLastError(), "launch signal_host");
             } catch (...) {
                 cudaStreamEndCapture(L->hst, &g);
                 if (g) cudaGraphDestroy(g);
@@ -1178,10 +1202,28 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
             L->hg_batch = batch;
             L->hg_src = src;
             L->hg_dst = dst;
-            L->hg_launches = g_launches;
+            L->hg_launches = g_launches + 1;  // + signal_host
         }
         ck(cudaGraphLaunch(L->hgraph, L->hst), "graph launch (host API)");
-        ck(cudaStreamSynchronize(L->hst), "sync");
+        // completion: spin on the page-locked word the graph's last node
+        // posts (~1 us after the kernels) instead of a stream synchronisation
+        // (~10 us); the stream is polled now and then so a failed launch
+        // surfaces as an error instead of a hang
+        const std::uint32_t want = ++L->h_seq;
+        const volatile std::uint32_t* flag = L->h_flag;
+        for (std::uint32_t it = 1; *flag != want; ++it) {
+            if ((it & 4095u) == 0u) {
+                const cudaError_t e = cudaStreamQuery(L->hst);
+                if (e == cudaSuccess && *flag != want) {  // graph done but no signal: resync the sequence
+                    ck(cudaMemcpy(&L->h_seq, L->d_seq, 4, cudaMemcpyDeviceToHost), "seq readback");
+                    break;
+                }
+                if (e != cudaSuccess && e != cudaErrorNotReady) ck(e, "host-API graph");
+            }
+#if defined(__x86_64__)
+            __builtin_ia32_pause();
+#endif
+        }
         g_launches = L->hg_launches;
         if (!py) std::memcpy(y_host, L->h_y, 4 * ny);
     });

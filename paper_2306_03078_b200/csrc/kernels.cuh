@@ -270,6 +270,17 @@ static __global__ void __launch_bounds__(256) copy_in(const uint4* __restrict__ 
         dst[i] = src[i];
 }
 
+// spqr_matvec_host completion: the last node of the host-API graph bumps a
+// device sequence number and posts it to a page-locked host word (after every
+// y store of the preceding kernels, which completed first), so the caller
+// spins on that word instead of paying a stream synchronisation.
+static __global__ void signal_host(std::uint32_t* __restrict__ seq, volatile std::uint32_t* __restrict__ flag) {
+    const std::uint32_t v = *seq + 1u;
+    *seq = v;
+    __threadfence_system();
+    *flag = v;
+}
+
 // y = W16 * x16, fp32 accumulate; one warp per row, 128-bit loads.
 static __global__ void dense_gemv_f16(const __half* __restrict__ w, const __half* __restrict__ x, float* __restrict__ y,
                                std::uint32_t rows, std::uint32_t cols) {
