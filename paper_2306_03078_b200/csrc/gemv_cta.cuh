@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             mbar_wait(&full[warp][slot], (nit >> 1) & 1u);
 #ifdef SPQR_TIMELINE
             if (tl_cnt == 0) SPQR_TL(2)
-            tl_wait += gtime() - tw0;
+            tl_wait = tw0;  // start of the latest cell (after its panel)
             ++tl_cnt;
 #endif
             const std::uint8_t* cell = ring + slot * p.slot_bytes;
@@ -874,8 +874,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 #ifdef SPQR_TIMELINE
     SPQR_TL(4)
     if (lane == 0) {
-        g_timeline[8 * wk + 5] = tl_panels;
-        g_timeline[8 * wk + 6] = tl_wait;
+        g_timeline[8 * wk + 5] = tl_cnt;   // cells this warp processed
+        g_timeline[8 * wk + 6] = tl_wait;  // start of its last cell
         unsigned smid;
         asm("mov.u32 %0, %smid;" : "=r"(smid));
         g_timeline[8 * wk + 7] = 1000u + smid;

@@ -82,9 +82,7 @@ for m, n in shapes:
                   f"{rows_b[:, 5].tolist()}")
         print("   mean CTA entry by blockIdx quarter", [round(x, 2) for x in q4], "mean loop end", [round(x, 2) for x in e4])
         print("   per-CTA end percentiles", " ".join(f"{v:6.2f}" for v in np.percentile(ends, [0, 10, 50, 90, 100])))
-        print(f"   consumers: full-wait us/warp " +
-              " ".join(f"{v:6.2f}" for v in np.percentile(cons[:, 6] / 1e3, [0, 50, 100])) +
-              f"; cells/warp {cons[:, 5].mean():.2f}")
+        print(f"   consumers: cells/warp {cons[:, 5].mean():.2f} (slot 6 = start of the last cell: tools/timeline_tail.py)")
         T[:, 5:] = 0
     t = T[:, :5]
     meta = T[:, 5:][t[:, 4] > 0]
