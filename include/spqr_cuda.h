@@ -207,10 +207,12 @@ uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
  * Asynchronous on cuda_stream; allocates nothing.  spqr_matvec uses the
  * layer's own workspace (one stream at a time); spqr_matvec_ws takes a caller
  * workspace (concurrent streams; size from spqr_workspace_bytes(layer, batch)).
- * Fast-path layers: batch 1-3 run one fused gemv_cta launch per column
- * (exact codes, fp32 accumulation: ~1e-7 relative to the reference);
- * batch >= 4 run xprep_tc + gemm_tc per 64 columns (weights rounded to fp16,
- * tcgen05 tensor cores: <= 1e-3 relative, the north star's bar). */
+ * Fast-path layers: batch 1-4 run fused gemv_cta launches -- fp16 x two
+ * columns per launch (each weight decoded once for both), an odd column and
+ * fp32 x one column per launch (exact codes, fp32 accumulation: ~1e-7
+ * relative to the reference); batch >= 5 run xprep_tc + gemm_tc per 64
+ * columns (weights rounded to fp16, tcgen05 tensor cores: ~1e-4 relative on
+ * well-conditioned layers, the north star's bar is 1e-3). */
 int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                 void* cuda_stream);
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,

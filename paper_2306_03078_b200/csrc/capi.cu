@@ -77,7 +77,8 @@ struct spqr_layer {
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
     std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, n_pad = 0;
-    // gemv_cta plan, per x dtype (f16, f32: the panel size differs)
+    // gemv_cta plan, per x mode (0: f16, 1: f32 hi/lo, 2: f16 batch pair:
+    // the panel and row-sum sizes differ)
     struct CtaPlan {
         std::uint32_t nvcta = 0, grid = 0, nslot_log2 = 0, slot_bytes = 0, rec_cap = 0;
         std::uint32_t pan_off = 0, part_off = 0, off_off = 0, gd_off = 0, part_cap = 0, smem = 0;
@@ -85,7 +86,7 @@ struct spqr_layer {
         std::uint32_t* d_start = nullptr;  // [nvcta+1]
         std::uint32_t* d_first = nullptr;  // [grid][kNC][2] record byte range of warp w's first cell
         std::vector<std::uint32_t> h_start;  // cta_start on the host (the first grid + 1 go by value)
-    } cta[2];
+    } cta[3];
     std::uint32_t pn_magic = 0;
     // gemm_tc plan (batch >= 2): ranges of (128-row tile, panel) units
     struct TcPlan {
@@ -131,7 +132,8 @@ struct spqr_layer {
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
                         static_cast<void*>(d_cell_off), d_ws, d_wsh,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
-                        static_cast<void*>(cta[0].d_first), static_cast<void*>(cta[1].d_first),
+                        static_cast<void*>(cta[2].d_start), static_cast<void*>(cta[0].d_first),
+                        static_cast<void*>(cta[1].d_first), static_cast<void*>(cta[2].d_first),
                         static_cast<void*>(tcp.d_start), static_cast<void*>(tcp.d_maps),
                         static_cast<void*>(d_xh), static_cast<void*>(d_yh)})
             if (p) cudaFree(p);
@@ -180,9 +182,10 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
     std::uint64_t o = 0;
     if (L->fast) {
         // pairs shared by two gemv_cta ranges: partial rows + arrival tickets
-        const std::uint64_t nb = std::max(L->cta[0].nvcta, L->cta[1].nvcta) + 1ull;
-        w.xpart = o; o += al(nb * 2 * 32 * 4);
-        w.xcnt = o; o += al(nb * 4);
+        // (two batch columns per boundary for the batch-pair kernel)
+        const std::uint64_t nb = std::max({L->cta[0].nvcta, L->cta[1].nvcta, L->cta[2].nvcta}) + 1ull;
+        w.xpart = o; o += al(nb * 2 * 2 * 32 * 4);
+        w.xcnt = o; o += al(nb * 2 * 4);
         if (batch >= 2) {  // gemm_tc: x tiles for N <= 128, partial tiles, per-warp tile counters
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
@@ -202,9 +205,9 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
 constexpr int kNC = SPQR_NC;  // 16: 4 warps per SMSP, up to 128 registers each
 constexpr std::uint32_t kCtaStaticMax = 10240;  // static smem of gemv_cta (checked at first launch)
 
-template <int BW, int BSZ, bool XLO, bool SHX>
+template <int BW, int BSZ, int XM, bool SHX>
 void launch_cta_t(const spqr_dev::CtaParams& p, std::uint32_t grid, std::uint32_t smem, cudaStream_t st) {
-    auto kern = spqr_dev::gemv_cta<BW, BSZ, BSZ, XLO, kNC, SHX>;
+    auto kern = spqr_dev::gemv_cta<BW, BSZ, BSZ, XM, kNC, SHX>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -232,15 +235,17 @@ void launch_cta_t(const spqr_dev::CtaParams& p, std::uint32_t grid, std::uint32_
     ++g_launches;
 }
 
-void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, cudaStream_t st) {
-    const auto& c = L->cta[xlo ? 1 : 0];
-    const int key = L->info.weight_bits * 1000 + L->info.scale_bits * 100 + (xlo ? 10 : 0) + (c.shared_x ? 1 : 0);
+void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, int xm, cudaStream_t st) {
+    const auto& c = L->cta[xm];
+    const int key = L->info.weight_bits * 1000 + L->info.scale_bits * 100 + xm * 10 + (c.shared_x ? 1 : 0);
     switch (key) {
-#define SPQR_CASE(BW, BSZ)                                                                               \
-    case BW * 1000 + BSZ * 100 + 0: launch_cta_t<BW, BSZ, false, false>(p, c.grid, c.smem, st); break; \
-    case BW * 1000 + BSZ * 100 + 1: launch_cta_t<BW, BSZ, false, true>(p, c.grid, c.smem, st); break;  \
-    case BW * 1000 + BSZ * 100 + 10: launch_cta_t<BW, BSZ, true, false>(p, c.grid, c.smem, st); break; \
-    case BW * 1000 + BSZ * 100 + 11: launch_cta_t<BW, BSZ, true, true>(p, c.grid, c.smem, st); break;
+#define SPQR_CASE(BW, BSZ)                                                                           \
+    case BW * 1000 + BSZ * 100 + 0: launch_cta_t<BW, BSZ, 0, false>(p, c.grid, c.smem, st); break;  \
+    case BW * 1000 + BSZ * 100 + 1: launch_cta_t<BW, BSZ, 0, true>(p, c.grid, c.smem, st); break;   \
+    case BW * 1000 + BSZ * 100 + 10: launch_cta_t<BW, BSZ, 1, false>(p, c.grid, c.smem, st); break; \
+    case BW * 1000 + BSZ * 100 + 11: launch_cta_t<BW, BSZ, 1, true>(p, c.grid, c.smem, st); break;  \
+    case BW * 1000 + BSZ * 100 + 20: launch_cta_t<BW, BSZ, 2, false>(p, c.grid, c.smem, st); break; \
+    case BW * 1000 + BSZ * 100 + 21: launch_cta_t<BW, BSZ, 2, true>(p, c.grid, c.smem, st); break;
         SPQR_CASE(2, 2) SPQR_CASE(2, 3) SPQR_CASE(2, 4)
         SPQR_CASE(3, 2) SPQR_CASE(3, 3) SPQR_CASE(3, 4)
         SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
@@ -253,9 +258,10 @@ void dispatch_cta(const spqr_dev::CtaParams& p, const spqr_layer* L, bool xlo, c
 // ---- gemm_tc (batch >= 2): 4 dequant warps + 1 control warp per CTA -------
 constexpr std::uint32_t kTcStaticMax = 2048;
 constexpr std::uint32_t kTcMaxN = 64;  // batch columns per launch
-// below this batch, repeated gemv_cta launches beat the dequant-then-MMA
-// kernel (tools/batch_sweep.py, 8192x22016: 3 x 29 us < ~93 us < 4 x 29 us)
-constexpr int kTcMinBatch = 4;
+// below this batch, gemv_cta launches (batch-pair kernels, each weight decoded
+// once per two columns) beat the dequant-then-MMA kernel (tools/batch_sweep.py,
+// 8192x22016: batch 4 = 2 x 38 us < 84 us; batch 5 = 2 x 38 + 29 us > ~85 us)
+constexpr int kTcMinBatch = 5;
 std::uint32_t tc_smem(const spqr_layer* L, std::uint32_t N, std::uint32_t na) {
     return na * 128u * 128u * 2u + 3u * 256u * N + 8u * L->tcp.slot_bytes + spqr_dev::kTcTabBytes;
 }
@@ -355,9 +361,9 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
 }
 
 // gemv_cta launch parameters for one batch column
-spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int f16, float* y, std::uint8_t* base,
+spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int xm, float* y, std::uint8_t* base,
                                const WsLayout& w) {
-    const auto& c = L->cta[f16 ? 0 : 1];
+    const auto& c = L->cta[xm];
     spqr_dev::CtaParams p{};
     p.cells = L->d_cells;
     p.cell_off = L->d_cell_off;
@@ -398,12 +404,16 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (L->fast) {
         // one fused launch per batch column (x preparation happens inside)
         if (stage == 1) return;
+        // fp16 x: batch columns two at a time through the batch-pair kernel
+        // (each weight decoded once for both), an odd last column alone
         const std::size_t esz = f16 ? 2 : 4;
-        for (int b = 0; b < batch; ++b) {
+        for (int b = 0; b < batch;) {
+            const int xm = !f16 ? 1 : (b + 1 < batch ? 2 : 0);
             spqr_dev::CtaParams p = cta_params(L, static_cast<const std::uint8_t*>(x) +
                                                       static_cast<std::size_t>(b) * L->info.cols * esz,
-                                               f16, y + static_cast<std::size_t>(b) * L->info.rows, base, w);
-            dispatch_cta(p, L, !f16, st);
+                                               xm, y + static_cast<std::size_t>(b) * L->info.rows, base, w);
+            dispatch_cta(p, L, xm, st);
+            b += xm == 2 ? 2 : 1;
         }
     } else {
         auto* xp = reinterpret_cast<float*>(base + w.xp);
@@ -454,7 +464,8 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     auto& c = L->cta[xi];
     const std::uint32_t Q = t.Gn * t.Pn;
     const std::uint32_t cellb = t.cell_bytes;
-    const std::uint32_t panel = spqr_tiled::panel_bytes(xi == 1);
+    const std::uint32_t panel = spqr_tiled::panel_bytes(xi);
+    const std::uint32_t ncol = xi == 2 ? 2u : 1u;  // row sums per cell: 32 per batch column
     const std::uint32_t budget = kSmemLimit - kCtaStaticMax;
     constexpr std::uint32_t kPartMax = 48u * 1024u;  // row-sum array cap
     const std::uint32_t S = static_cast<std::uint32_t>(sms);
@@ -488,7 +499,7 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     } else {
         nv = S;
         while (!cut(nv) && nv > 1) --nv;
-        while (mc * 128u > kPartMax) {  // more ranges than SMs: several per CTA
+        while (mc * 128u * ncol > kPartMax) {  // more ranges than SMs: several per CTA
             std::uint32_t nn = nv + S;
             while (!cut(nn) && nn > nv + 1) --nn;
             nv = nn;
@@ -497,7 +508,7 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     c.nvcta = nv;
     c.grid = std::min<std::uint32_t>(nv, S);
     c.part_cap = std::max<std::uint32_t>(mc, 1);
-    const std::uint32_t part_bytes = (c.part_cap * 128u + 127u) & ~127u;
+    const std::uint32_t part_bytes = (c.part_cap * 128u * ncol + 127u) & ~127u;
     const std::uint32_t off_bytes = ((c.part_cap + 9u) * 4u + 127u) & ~127u;  // 16-B aligned superset
     const std::uint32_t gd_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
     // x panels once per CTA (all Pn in shared memory) whenever the two record
@@ -626,6 +637,7 @@ void make_plans(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vect
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device), "SM count");
     plan_cta(L, t, sms, 0);
     plan_cta(L, t, sms, 1);
+    plan_cta(L, t, sms, 2);
     plan_tc(L, t, views, sms);
 }
 
@@ -1052,7 +1064,7 @@ int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr
         ensure_own_ws(L, 1);
         const WsLayout w = ws_layout(L, 1);
         const int f16 = x_dtype == SPQR_F16;
-        spqr_dev::CtaParams p = cta_params(L, x_dev, f16, g->y() + rb, static_cast<std::uint8_t*>(L->d_ws), w);
+        spqr_dev::CtaParams p = cta_params(L, x_dev, f16 ? 0 : 1, g->y() + rb, static_cast<std::uint8_t*>(L->d_ws), w);
         std::uint32_t k = 0;
         for (int j = 0; j < g->world; ++j) {
             if (j != g->rank) p.ypeer[k++] = reinterpret_cast<float*>(g->peer[j] + spqr_gather::kY);

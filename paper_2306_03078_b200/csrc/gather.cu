@@ -11,7 +11,7 @@ namespace {
 template <int BW, int BSZ, bool XLO, bool SHX, int NC>
 cudaError_t launch_gather_t(const CtaParams& p, std::uint32_t grid, std::uint32_t smem, std::uint32_t smem_limit,
                             cudaStream_t st) {
-    auto kern = gemv_cta<BW, BSZ, BSZ, XLO, NC, SHX, true>;
+    auto kern = gemv_cta<BW, BSZ, BSZ, XLO ? 1 : 0, NC, SHX, true>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);

@@ -134,30 +134,40 @@ __device__ __forceinline__ void column_scales(std::uint32_t kk, std::uint32_t cc
 // One lane's share of a cell's x panel: columns 8*lane .. 8*lane+7 of panel P
 // (block kk = lane/2, half hf = lane%2).  load_x fetches them (through the
 // permutation, zero beyond n); build_panel writes the panel (tiled.hpp).
-template <bool XLO>
+// x modes (template XM): 0 = fp16 x, one column; 1 = fp32 x, one column as
+// fp16 hi + lo parts sharing each MMA; 2 = fp16 x, two batch columns sharing
+// each MMA (the batch-2 pass: every weight decoded once for both columns).
+template <int XM>
 struct XLane {
-    std::uint32_t w[XLO ? 8 : 4];  // fp16 pairs, or fp32 bit patterns
+    std::uint32_t w[XM ? 8 : 4];  // fp16 pairs (mode 2: column 0 then column 1), or fp32 bit patterns
 };
 
-template <bool XLO>
-__device__ __forceinline__ XLane<XLO> load_x(const CtaParams& p, std::uint32_t P, int lane) {
-    XLane<XLO> r;
-    const std::uint32_t c0 = 256u * P + 8u * static_cast<std::uint32_t>(lane);
-    if constexpr (!XLO) {
-        if (p.x_vec && c0 + 8u <= p.n) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(p.x) + c0));
-            r.w[0] = v.x; r.w[1] = v.y; r.w[2] = v.z; r.w[3] = v.w;
-        } else {
-            std::uint32_t h[8];
+__device__ __forceinline__ void load_x_f16(const CtaParams& p, const void* xs, std::uint32_t c0, std::uint32_t* w) {
+    if (p.x_vec && c0 + 8u <= p.n) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(xs) + c0));
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+        std::uint32_t h[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const std::uint32_t c = c0 + i;
-                h[i] = 0;
-                if (c < p.n) h[i] = __ldg(reinterpret_cast<const unsigned short*>(p.x) + (p.order ? __ldg(p.order + c) : c));
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) r.w[i] = h[2 * i] | (h[2 * i + 1] << 16);
+        for (int i = 0; i < 8; ++i) {
+            const std::uint32_t c = c0 + i;
+            h[i] = 0;
+            if (c < p.n) h[i] = __ldg(static_cast<const unsigned short*>(xs) + (p.order ? __ldg(p.order + c) : c));
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = h[2 * i] | (h[2 * i + 1] << 16);
+    }
+}
+
+template <int XM>
+__device__ __forceinline__ XLane<XM> load_x(const CtaParams& p, std::uint32_t P, int lane) {
+    XLane<XM> r;
+    const std::uint32_t c0 = 256u * P + 8u * static_cast<std::uint32_t>(lane);
+    if constexpr (XM == 0) {
+        load_x_f16(p, p.x, c0, r.w);
+    } else if constexpr (XM == 2) {  // batch columns 0 and 1 (x is batch x n)
+        load_x_f16(p, p.x, c0, r.w);
+        load_x_f16(p, static_cast<const __half*>(p.x) + p.n, c0, r.w + 4);
     } else {
         if (p.x_vec && c0 + 8u <= p.n) {
             const uint4 a = __ldg(reinterpret_cast<const uint4*>(static_cast<const float*>(p.x) + c0));
@@ -176,10 +186,12 @@ __device__ __forceinline__ XLane<XLO> load_x(const CtaParams& p, std::uint32_t P
     return r;
 }
 
+// One column's panel operands (B rows at o_frag, XX, SC, x in solve order at
+// o_xp; XLO: fp32 x, its residual B rows at o_lo).
 template <int BW, int BS, bool XLO>
-__device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std::uint8_t* pan) {
-    constexpr std::uint32_t O_XX = T::kPanelXXOff, O_SC = T::kPanelSCOff, O_XP = T::kPanelXPOff;
-    constexpr std::uint32_t O_LO = T::panel_lo_off(XLO);
+__device__ __forceinline__ void build_col(const std::uint32_t* xw, int lane, std::uint8_t* pan, std::uint32_t o_frag,
+                                          std::uint32_t o_xx, std::uint32_t o_sc, std::uint32_t o_xp,
+                                          std::uint32_t o_lo) {
     const std::uint32_t kk = static_cast<std::uint32_t>(lane) >> 1, cc = 8u * (lane & 1);
     int pc, ps, pz;
     column_scales<BW, BS>(kk, cc, pc, ps, pz);
@@ -187,17 +199,17 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std:
     if constexpr (!XLO) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 v = __half22float2(u32_as_h2(xl.w[i]));
+            const float2 v = __half22float2(u32_as_h2(xw[i]));
             f[2 * i] = v.x;
             f[2 * i + 1] = v.y;
         }
-        *reinterpret_cast<uint4*>(pan + O_XP + 16u * lane) = make_uint4(xl.w[0], xl.w[1], xl.w[2], xl.w[3]);
+        *reinterpret_cast<uint4*>(pan + o_xp + 16u * lane) = make_uint4(xw[0], xw[1], xw[2], xw[3]);
     } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(xl.w[i]);
-        uint4* xp = reinterpret_cast<uint4*>(pan + O_XP + 32u * lane);
-        xp[0] = make_uint4(xl.w[0], xl.w[1], xl.w[2], xl.w[3]);
-        xp[1] = make_uint4(xl.w[4], xl.w[5], xl.w[6], xl.w[7]);
+        for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(xw[i]);
+        uint4* xp = reinterpret_cast<uint4*>(pan + o_xp + 32u * lane);
+        xp[0] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+        xp[1] = make_uint4(xw[4], xw[5], xw[6], xw[7]);
     }
     // the panel's scale: max |x| 2^e in [2^14, 2^15)
     float mx = 0.f;
@@ -223,7 +235,7 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std:
     std::uint32_t hv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) hv[i] = pack_h2_rn(s[2 * i], s[2 * i + 1]);
-    *reinterpret_cast<uint4*>(pan + 16u * lane) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *reinterpret_cast<uint4*>(pan + o_frag + 16u * lane) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
     float eff[8];
     if constexpr (XLO) {
         std::uint32_t lv[4];
@@ -235,7 +247,7 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std:
             eff[2 * i] = hh.x + l.x;
             eff[2 * i + 1] = hh.y + l.y;
         }
-        *reinterpret_cast<uint4*>(pan + O_LO + 16u * lane) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+        *reinterpret_cast<uint4*>(pan + o_lo + 16u * lane) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -248,28 +260,44 @@ __device__ __forceinline__ void build_panel(const XLane<XLO>& xl, int lane, std:
     float X = ((eff[0] + eff[1]) + (eff[2] + eff[3])) + ((eff[4] + eff[5]) + (eff[6] + eff[7]));
     X *= pow2f(pc - pz);
     X += __shfl_xor_sync(0xffffffffu, X, 1);
-    if ((lane & 1) == 0) reinterpret_cast<float*>(pan + O_XX)[kk] = -X;
+    if ((lane & 1) == 0) reinterpret_cast<float*>(pan + o_xx)[kk] = -X;
     if (lane == 0) {  // y = R 2^(48 - e): as two normal factors
         const int q = 48 - e;
         const int q1 = q < -126 ? -126 : (q > 127 ? 127 : q);
-        reinterpret_cast<float*>(pan + O_SC)[0] = pow2f(q1);
-        reinterpret_cast<float*>(pan + O_SC)[1] = pow2f(q - q1);
+        reinterpret_cast<float*>(pan + o_sc)[0] = pow2f(q1);
+        reinterpret_cast<float*>(pan + o_sc)[1] = pow2f(q - q1);
+    }
+}
+
+template <int BW, int BS, int XM>
+__device__ __forceinline__ void build_panel(const XLane<XM>& xl, int lane, std::uint8_t* pan) {
+    constexpr std::uint32_t O_XX = T::kPanelXXOff, O_SC = T::kPanelSCOff, O_XP = T::kPanelXPOff;
+    constexpr std::uint32_t O_LO = T::panel_lo_off(XM);
+    if constexpr (XM == 2) {
+        build_col<BW, BS, false>(xl.w, lane, pan, 0, O_XX, O_SC, O_XP, 0);
+        build_col<BW, BS, false>(xl.w + 4, lane, pan, O_LO, T::panel_xx1_off(2), T::panel_sc1_off(2), O_XP + 512u, 0);
+    } else {
+        build_col<BW, BS, XM == 1>(xl.w, lane, pan, 0, O_XX, O_SC, O_XP, O_LO);
     }
 }
 
 // SHX: the CTA prepares all Pn x panels once (shared memory) instead of each
 // warp preparing its cell's panel -- for layers whose panels fit.
-template <int BW, int BS, int BZ, bool XLO, int NC, bool SHX, bool GATHER = false>
+template <int BW, int BS, int BZ, int XM, int NC, bool SHX, bool GATHER = false>
 __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     static_assert(BS == BZ, "fast path: scale and zero codes share the statistic width");
+    static_assert(!(GATHER && XM == 2), "the fused gather is batch 1");
+    constexpr bool XLO = XM == 1;
+    constexpr int NCOL = XM == 2 ? 2 : 1;  // batch columns of one launch
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
     constexpr std::uint32_t CODEB = T::code_bytes(BW);
     constexpr std::uint32_t STATB = T::stat_bytes(BS, BZ);
-    constexpr std::uint32_t PANEL = T::panel_bytes(XLO);
+    constexpr std::uint32_t PANEL = T::panel_bytes(XM);
     constexpr std::uint32_t O_FRAG = 0, O_XX = T::kPanelXXOff, O_SC = T::kPanelSCOff, O_XP = T::kPanelXPOff;
-    constexpr std::uint32_t O_LO = T::panel_lo_off(XLO);
+    constexpr std::uint32_t O_LO = T::panel_lo_off(XM);
+    constexpr std::uint32_t O_XX1 = T::panel_xx1_off(2), O_SC1 = T::panel_sc1_off(2);  // mode 2: column 1
     constexpr std::uint32_t MASK = (1u << BW) - 1u;
     constexpr std::uint32_t SMASK = (1u << BS) - 1u;
     constexpr int NT = NC * 32;
@@ -280,7 +308,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ std::uint32_t slot_r[NC][2][2];       // record byte range of the slot's cell
     __shared__ std::uint32_t tick[2];                // per-range ticket counters (by range parity)
     __shared__ volatile std::uint32_t pflag[64];     // SHX: x panel built
-    __shared__ float rowsum[NC][32];                 // outlier row sums of a cell (zero between cells)
+    __shared__ float rowsum[NC][NCOL][32];           // outlier row sums of a cell (zero between cells)
     __shared__ __align__(16) float coef[NC][2][32];  // -S Z 2^(p-24) per (unit, block, kind)
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
@@ -324,7 +352,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     }
     if (threadIdx.x == 0) tick[0] = tick[1] = NC;  // ticket w < NC is warp w's first cell
     if (threadIdx.x < 64) pflag[threadIdx.x] = 0u;
-    rowsum[warp][lane] = 0.f;
+    for (int c = 0; c < NCOL; ++c) rowsum[warp][c][lane] = 0.f;
     if (lane < 4) zrow[warp][lane] = 0u;
     // lane 0: bulk copy of a cell's record bytes (up to the slot's capacity)
     auto copy_rec = [&](std::uint8_t* dst, std::uint32_t r0, std::uint32_t r1, std::uint64_t* bar) {
@@ -459,8 +487,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             std::uint32_t P = P0 + i;
             return P >= p.Pn ? P - p.Pn : P;
         };
-        auto publish = [&](std::uint32_t P, const XLane<XLO>& xv) {
-            build_panel<BW, BS, XLO>(xv, lane, pan_base + P * PANEL);
+        auto publish = [&](std::uint32_t P, const XLane<XM>& xv) {
+            build_panel<BW, BS, XM>(xv, lane, pan_base + P * PANEL);
             __syncwarp();
             __threadfence_block();
             if (lane == 0) pflag[P] = 1u;
@@ -483,29 +511,29 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             if constexpr (SHX) {  // own panels (<= 3), the first cell's first; every x load
                                   // is in flight before the first build; no CTA barrier
                 const std::uint32_t i0 = warp, i1 = warp + NC, i2 = warp + 2 * NC;
-                XLane<XLO> xa{}, xb{}, xc{};
-                if (i0 < p.Pn) xa = load_x<XLO>(p, panel_at(i0), lane);
-                if (i1 < p.Pn) xb = load_x<XLO>(p, panel_at(i1), lane);
-                if (i2 < p.Pn) xc = load_x<XLO>(p, panel_at(i2), lane);
+                XLane<XM> xa{}, xb{}, xc{};
+                if (i0 < p.Pn) xa = load_x<XM>(p, panel_at(i0), lane);
+                if (i1 < p.Pn) xb = load_x<XM>(p, panel_at(i1), lane);
+                if (i2 < p.Pn) xc = load_x<XM>(p, panel_at(i2), lane);
                 if (i0 < p.Pn) publish(panel_at(i0), xa);
                 if (i1 < p.Pn) publish(panel_at(i1), xb);
                 if (i2 < p.Pn) publish(panel_at(i2), xc);
 #pragma unroll 1
-                for (std::uint32_t i = warp + 3 * NC; i < p.Pn; i += NC) publish(panel_at(i), load_x<XLO>(p, panel_at(i), lane));
+                for (std::uint32_t i = warp + 3 * NC; i < p.Pn; i += NC) publish(panel_at(i), load_x<XM>(p, panel_at(i), lane));
             }
 #ifdef SPQR_TIMELINE
             tl_panels = gtime();
 #endif
         }
-        XLane<XLO> xl{};
-        if (!SHX && tk < nc) xl = load_x<XLO>(p, panel_of(tk), lane);
+        XLane<XM> xl{};
+        if (!SHX && tk < nc) xl = load_x<XM>(p, panel_of(tk), lane);
 #pragma unroll 1
         while (tk < nc) {
             const std::uint32_t tn = grab();
-            XLane<XLO> xn{};
+            XLane<XM> xn{};
             if (tn < nc) {
                 issue(tn, (nit + 1u) & 1u);
-                if constexpr (!SHX) xn = load_x<XLO>(p, panel_of(tn), lane);
+                if constexpr (!SHX) xn = load_x<XM>(p, panel_of(tn), lane);
             }
             const std::uint32_t slot = nit & 1u;
             const std::uint32_t ck = tk;  // this ticket's cell (range index)
@@ -519,7 +547,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 }
                 __threadfence_block();
             } else {
-                build_panel<BW, BS, XLO>(xl, lane, pan);
+                build_panel<BW, BS, XM>(xl, lane, pan);
                 __syncwarp();
             }
             const std::uint32_t lane_sa = smem_u32(pan) + lane_off;
@@ -569,8 +597,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             };
 
             // lane data of the units: code words
-            std::uint32_t cw[2][XLO ? 1 : G::LANE_WORDS];
-            if constexpr (!XLO) {
+            std::uint32_t cw[2][XM ? 1 : G::LANE_WORDS];
+            if constexpr (XM == 0) {
 #pragma unroll
                 for (int ui = 0; ui < 2; ++ui) {
                     const std::uint8_t* unit = cell + ui * UNIT;
@@ -587,12 +615,14 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             __syncwarp();  // the coefficient table is complete
 
             // epilogue of super-tile h: acc += s' (C + z' XX)
-            float2 acc[2][2];  // [unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
+            float2 acc[NCOL][2][2];  // [column][unit][rho] = (block 2t, block 2t+1) partials of row g + 8 rho
 #pragma unroll
-            for (int ui = 0; ui < 2; ++ui) acc[ui][0] = acc[ui][1] = make_float2(0.f, 0.f);
-            auto epilogue = [&](auto HC, const float (&c)[2][4]) {
+            for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+                for (int ui = 0; ui < 2; ++ui) acc[c][ui][0] = acc[c][ui][1] = make_float2(0.f, 0.f);
+            auto epilogue = [&](auto HC, const float (&c)[2][4], int col) {
                 constexpr int h = decltype(HC)::value;
-                const float2 xx = *reinterpret_cast<const float2*>(pan + O_XX + 4u * (8u * h + 2u * t));
+                const float2 xx = *reinterpret_cast<const float2*>(pan + (col ? O_XX1 : O_XX) + 4u * (8u * h + 2u * t));
 #pragma unroll
                 for (int ui = 0; ui < 2; ++ui) {
                     // {S_s|Z_s, S_z|Z_z} of blocks 8h + 2t and 8h + 2t + 1
@@ -606,13 +636,13 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                         const float2 sh = make_float2(fhfma<0, 0>(s4.x, rs0, cf.x), fhfma<0, 0>(s4.z, rs1, cf.y));
                         const float2 zh = make_float2(fhfma<0, 0>(s4.y, rz0, cf.z), fhfma<0, 0>(s4.w, rz1, cf.w));
                         const float2 tt = ffma2(zh, xx, make_float2(c[ui][0], c[ui][1]));
-                        acc[ui][0] = ffma2(sh, tt, acc[ui][0]);
+                        acc[col][ui][0] = ffma2(sh, tt, acc[col][ui][0]);
                     }
                     {  // rho = 1: row g + 8
                         const float2 sh = make_float2(fhfma<0, 1>(s4.x, rs0, cf.x), fhfma<0, 1>(s4.z, rs1, cf.y));
                         const float2 zh = make_float2(fhfma<0, 1>(s4.y, rz0, cf.z), fhfma<0, 1>(s4.w, rz1, cf.w));
                         const float2 tt = ffma2(zh, xx, make_float2(c[ui][2], c[ui][3]));
-                        acc[ui][1] = ffma2(sh, tt, acc[ui][1]);
+                        acc[col][ui][1] = ffma2(sh, tt, acc[col][ui][1]);
                     }
                 }
             };
@@ -628,7 +658,7 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     a[r] = window<G::CW>(w, B) & ((MASK << pb) * 0x00010001u);
                 }
             };
-            if constexpr (!XLO) {
+            if constexpr (XM == 0) {
                 // 4 independent MMA chains (super-tile h x unit), interleaved
                 std::uint32_t bfr[2][4];
                 float cc[2][2][4];
@@ -655,8 +685,8 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                         }
                     }
                 }
-                epilogue(std::integral_constant<int, 0>{}, cc[0]);
-                epilogue(std::integral_constant<int, 1>{}, cc[1]);
+                epilogue(std::integral_constant<int, 0>{}, cc[0], 0);
+                epilogue(std::integral_constant<int, 1>{}, cc[1], 0);
             } else {
                 // fp32 x = hi + lo, both f16, sharing one MMA: super-tile h
                 // runs as its even blocks then its odd blocks (parity par);
@@ -705,15 +735,26 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                             }
                         }
                     }
-                    float ch[2][4];  // the f16 layout: (g, 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
+                    if constexpr (XLO) {
+                        float ch[2][4];  // the f16 layout: (g, 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
 #pragma unroll
-                    for (int ui = 0; ui < 2; ++ui) {
-                        ch[ui][0] = d[0][ui][0] + d[0][ui][1];
-                        ch[ui][1] = d[1][ui][0] + d[1][ui][1];
-                        ch[ui][2] = d[0][ui][2] + d[0][ui][3];
-                        ch[ui][3] = d[1][ui][2] + d[1][ui][3];
+                        for (int ui = 0; ui < 2; ++ui) {
+                            ch[ui][0] = d[0][ui][0] + d[0][ui][1];
+                            ch[ui][1] = d[1][ui][0] + d[1][ui][1];
+                            ch[ui][2] = d[0][ui][2] + d[0][ui][3];
+                            ch[ui][3] = d[1][ui][2] + d[1][ui][3];
+                        }
+                        epilogue(HC, ch, 0);
+                    } else {  // two batch columns: slot 2s carries column 0, 2s + 1 column 1
+                        float c0[2][4], c1[2][4];
+#pragma unroll
+                        for (int ui = 0; ui < 2; ++ui) {
+                            c0[ui][0] = d[0][ui][0]; c0[ui][1] = d[1][ui][0]; c0[ui][2] = d[0][ui][2]; c0[ui][3] = d[1][ui][2];
+                            c1[ui][0] = d[0][ui][1]; c1[ui][1] = d[1][ui][1]; c1[ui][2] = d[0][ui][3]; c1[ui][3] = d[1][ui][3];
+                        }
+                        epilogue(HC, c0, 0);
+                        epilogue(HC, c1, 1);
                     }
-                    epilogue(HC, ch);
                 };
                 half(std::integral_constant<int, 0>{});
                 half(std::integral_constant<int, 1>{});
@@ -727,7 +768,6 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             // sums are deterministic.  Entries beyond the staged part of the
             // record are read from global memory.
             const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-            float* rs = rowsum[warp];
             if (cnt) {
                 const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
                 const std::uint32_t* es = reinterpret_cast<const std::uint32_t*>(cell + CELL);
@@ -737,47 +777,56 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                     if (i0 < lim) ev = *reinterpret_cast<const uint4*>(src + i0);  // lim % 4 == 0
                     const std::uint32_t e[4] = {ev.x, ev.y, ev.z, ev.w};
                     std::uint32_t k[4];
-                    float sv[4];
+                    float sv[NCOL][4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         k[j] = e[j] >> 24;
                         const std::uint32_t c = __byte_perm(e[j], 0u, 0x4442);  // col: byte 2
                         if constexpr (XLO) {
-                            sv[j] = h2f_bits(e[j] & 0xffffu) * reinterpret_cast<const float*>(pan + O_XP)[c];
+                            sv[0][j] = h2f_bits(e[j] & 0xffffu) * reinterpret_cast<const float*>(pan + O_XP)[c];
                         } else {
-                            const std::uint32_t xv = reinterpret_cast<const unsigned short*>(pan + O_XP)[c];
-                            sv[j] = fhfma<0, 0>(e[j], xv, 0.f);  // v * x, exact
+#pragma unroll
+                            for (int cl = 0; cl < NCOL; ++cl) {
+                                const std::uint32_t xv = reinterpret_cast<const unsigned short*>(pan + O_XP + 512u * cl)[c];
+                                sv[cl][j] = fhfma<0, 0>(e[j], xv, 0.f);  // v * x, exact
+                            }
                         }
                     }
                     bool same[3];
 #pragma unroll
                     for (int j = 0; j < 3; ++j) {
                         same[j] = k[j + 1] == k[j];
-                        if (same[j]) sv[j + 1] += sv[j];
+#pragma unroll
+                        for (int cl = 0; cl < NCOL; ++cl)
+                            if (same[j]) sv[cl][j + 1] += sv[cl][j];
                     }
                     const std::uint32_t K = k[3];
                     const std::uint32_t pK = __shfl_up_sync(0xffffffffu, K, 1);
                     const bool head = lane == 0 || pK != K;
                     const std::uint32_t heads = __ballot_sync(0xffffffffu, head) & (0xffffffffu >> (31 - lane));
                     const int seg0 = 31 - __clz(heads);
-                    float V = sv[3];
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const float o = __shfl_up_sync(0xffffffffu, V, d);
-                        if (lane - d >= seg0) V += o;
-                    }
-                    float cin = __shfl_up_sync(0xffffffffu, V, 1);
-                    if (lane == 0 || pK != k[0]) cin = 0.f;
                     const std::uint32_t nk0 = __shfl_down_sync(0xffffffffu, k[0], 1);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
-                        if (tail && k[j] < 32u) {
-                            const float tot = (k[j] == k[0]) ? sv[j] + cin : sv[j];
-                            if (first)
-                                rs[k[j]] = tot;
-                            else
-                                rs[k[j]] += tot;
+                    for (int cl = 0; cl < NCOL; ++cl) {
+                        float V = sv[cl][3];
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const float o = __shfl_up_sync(0xffffffffu, V, d);
+                            if (lane - d >= seg0) V += o;
+                        }
+                        float cin = __shfl_up_sync(0xffffffffu, V, 1);
+                        if (lane == 0 || pK != k[0]) cin = 0.f;
+                        float* rs = rowsum[warp][cl];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const bool tail = (j < 3) ? !same[j] : (lane == 31 || nk0 != k[3]);
+                            if (tail && k[j] < 32u) {
+                                const float tot = (k[j] == k[0]) ? sv[cl][j] + cin : sv[cl][j];
+                                if (first)
+                                    rs[k[j]] = tot;
+                                else
+                                    rs[k[j]] += tot;
+                            }
                         }
                     }
                 };
@@ -797,10 +846,11 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             // the cell's row sums.  Lane (g, t) holds partials of rows
             // 16u + 8rho + g over its blocks; a transpose-add across the quad
             // gives each row one lane: row = 16 (t >> 1) + 8 (t & 1) + g.
-            float* prow = part + ck * 32u;
-            {
-                const float a0 = acc[0][0].x + acc[0][0].y, a1 = acc[0][1].x + acc[0][1].y;
-                const float a2 = acc[1][0].x + acc[1][0].y, a3 = acc[1][1].x + acc[1][1].y;
+            float* prow = part + ck * (32u * NCOL);
+#pragma unroll
+            for (int cl = 0; cl < NCOL; ++cl) {
+                const float a0 = acc[cl][0][0].x + acc[cl][0][0].y, a1 = acc[cl][0][1].x + acc[cl][0][1].y;
+                const float a2 = acc[cl][1][0].x + acc[cl][1][0].y, a3 = acc[cl][1][1].x + acc[cl][1][1].y;
                 const bool o1 = t & 1, o2 = t & 2;
                 const float k0 = o1 ? a1 : a0, k1 = o1 ? a3 : a2;  // combos (t&1), (t&1)+2
                 const float s0 = o1 ? a0 : a1, s1 = o1 ? a2 : a3;
@@ -809,14 +859,14 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 const float keep = o2 ? b1 : b0, send = o2 ? b0 : b1;
                 const float R = keep + __shfl_xor_sync(0xffffffffu, send, 2);
                 const int row = 16 * (t >> 1) + 8 * (t & 1) + g;
-                const float2 sc = *reinterpret_cast<const float2*>(pan + O_SC);
+                const float2 sc = *reinterpret_cast<const float2*>(pan + (cl ? O_SC1 : O_SC));
                 const float Rs = XLO ? (R * sc.x) * sc.y : R * sc.x;
                 __syncwarp();
                 if (cnt) {
-                    prow[row] = Rs + rs[row];
-                    rs[row] = 0.f;
+                    prow[32 * cl + row] = Rs + rowsum[warp][cl][row];
+                    rowsum[warp][cl][row] = 0.f;
                 } else {
-                    prow[row] = Rs;
+                    prow[32 * cl + row] = Rs;
                 }
             }
 
@@ -831,31 +881,34 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             done = __shfl_sync(0xffffffffu, done, 0);
             if (done == b - a) {
                 __threadfence_block();
+#pragma unroll
+                for (int cl = 0; cl < NCOL; ++cl) {
                 float sum = 0.f;
-                const float* src = part + (a - q0) * 32u + lane;
+                const float* src = part + (a - q0) * (32u * NCOL) + 32u * cl + lane;
 #pragma unroll 4
-                for (std::uint32_t qq = a; qq < b; ++qq, src += 32) sum += *src;
+                for (std::uint32_t qq = a; qq < b; ++qq, src += 32 * NCOL) sum += *src;
                 const std::uint32_t row = 32u * Gq + lane;
                 if (a == cs && b == ce) {  // the pair is ours alone
-                    if (row < p.m) put_y(row, sum);
+                    if (row < p.m) put_y(cl * p.m + row, sum);
                 } else {
                     // shared with the neighbouring range: the second side to
                     // finish adds first-side + last-side (threadFenceReduction)
                     const std::uint32_t side = a != cs ? 1u : 0u;  // 1: we hold the pair's last cells
                     const std::uint32_t bx = side ? v : v + 1u;    // boundary below range bx
-                    float* slot = p.xpart + (2u * bx + side) * 32u;
+                    float* slot = p.xpart + ((2u * bx + side) * NCOL + cl) * 32u;
                     __stcg(slot + lane, sum);
                     __threadfence();
                     __syncwarp();
                     std::uint32_t prev = 0;
-                    if (lane == 0) prev = atomicAdd(p.xcnt + bx, 1u);
+                    if (lane == 0) prev = atomicAdd(p.xcnt + NCOL * bx + cl, 1u);
                     prev = __shfl_sync(0xffffffffu, prev, 0);
                     if (prev == 1u) {
                         __threadfence();
-                        const float other = __ldcg(p.xpart + (2u * bx + (side ^ 1u)) * 32u + lane);
-                        if (row < p.m) put_y(row, side ? other + sum : sum + other);
-                        if (lane == 0) p.xcnt[bx] = 0u;  // ready for the next launch
+                        const float other = __ldcg(p.xpart + ((2u * bx + (side ^ 1u)) * NCOL + cl) * 32u + lane);
+                        if (row < p.m) put_y(cl * p.m + row, side ? other + sum : sum + other);
+                        if (lane == 0) p.xcnt[NCOL * bx + cl] = 0u;  // ready for the next launch
                     }
+                }
                 }
             }
             __syncwarp();  // every lane is done with the slot before it is refilled

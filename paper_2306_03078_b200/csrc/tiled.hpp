@@ -95,13 +95,16 @@ SPQR_HD constexpr int column_prescale(int bw, std::uint32_t k, std::uint32_t cc)
     return prescale_p(bw, 2 * m + kh);
 }
 
-// x operands of one 256-column panel, built by the kernel in shared memory:
+// x operands of one 256-column panel, built by the kernel in shared memory.
+// x modes: 0 = one fp16 column, 1 = one fp32 column as fp16 hi + lo parts,
+// 2 = two fp16 batch columns (the second column's operands after the first's).
 //   [B rows : 16 blocks x 16 f16  ] fp16(x 2^(e - p_c - p_s(block))), natural
 //                                    column order (ldmatrix rows of B^T)
 //   [XX     : 16 f32              ] -2^(-p_z(block)) sum_c B_c 2^p_c
 //   [SC     : 2 f32 (+ 8 B pad)   ] 2^(48 - e) as a product of two normal floats
-//   [xp     : 256 f16 | 256 f32   ] x in solve order (outlier products)
-//   [B lo   : 16 x 16 f16         ] fp32 x only: fp16(residual of B)
+//   [xp     : 256 f16 | 256 f32 | 2 x 256 f16] x in solve order (outlier products)
+//   [B lo   : 16 x 16 f16         ] mode 1: fp16(residual of B); mode 2: column 1's B rows
+//   [XX1, SC1: 16 f32, 2 f32 + pad] mode 2: column 1's
 // e = the panel's power-of-two scale (max |x| 2^e in [2^14, 2^15)), p_c = the
 // column's code pre-scale, p_s / p_z = the pre-scales of the block's scale /
 // zero code pairs (stat_p).
@@ -109,10 +112,12 @@ inline constexpr std::uint32_t kPanelFragBytes = 512;
 inline constexpr std::uint32_t kPanelXXOff = 512;
 inline constexpr std::uint32_t kPanelSCOff = 576;
 inline constexpr std::uint32_t kPanelXPOff = 592;
-SPQR_HD constexpr std::uint32_t panel_xp_bytes(bool xlo) { return xlo ? 1024u : 512u; }  // f32 / f16 x
-SPQR_HD constexpr std::uint32_t panel_lo_off(bool xlo) { return kPanelXPOff + panel_xp_bytes(xlo); }
-SPQR_HD constexpr std::uint32_t panel_bytes(bool xlo) {
-    return kPanelXPOff + panel_xp_bytes(xlo) + (xlo ? kPanelFragBytes : 0u);
+SPQR_HD constexpr std::uint32_t panel_xp_bytes(int xm) { return xm == 0 ? 512u : 1024u; }
+SPQR_HD constexpr std::uint32_t panel_lo_off(int xm) { return kPanelXPOff + panel_xp_bytes(xm); }
+SPQR_HD constexpr std::uint32_t panel_xx1_off(int xm) { return panel_lo_off(xm) + kPanelFragBytes; }
+SPQR_HD constexpr std::uint32_t panel_sc1_off(int xm) { return panel_xx1_off(xm) + 64u; }
+SPQR_HD constexpr std::uint32_t panel_bytes(int xm) {
+    return xm == 0 ? kPanelXPOff + 512u : (xm == 1 ? panel_lo_off(1) + kPanelFragBytes : panel_sc1_off(2) + 16u);
 }
 
 // Statistics pair geometry (BS bits per code): stream bit, window byte and
