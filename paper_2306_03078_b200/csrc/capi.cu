@@ -381,7 +381,12 @@ spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int xm, float
     p.first_rec = reinterpret_cast<const uint2*>(c.d_first);
     if (c.grid < static_cast<std::uint32_t>(spqr_dev::kQFirst))
         std::copy(c.h_start.begin(), c.h_start.begin() + c.grid + 1, p.q_first);
-    p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0) ? 1u : 0u;
+    // 16-B vector loads of x: unpermuted, aligned (batch pair: the second
+    // column, n halves further on, too)
+    p.x_vec = (!p.order && (reinterpret_cast<std::uintptr_t>(p.x) & 15u) == 0 &&
+               (xm != 2 || (2ull * L->info.cols) % 16u == 0))
+                  ? 1u
+                  : 0u;
     return p;
 }
 

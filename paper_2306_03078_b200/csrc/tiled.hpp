@@ -1,8 +1,8 @@
 // tiled.hpp -- geometry of the HBM "tiled planes" layout of a fast-path layer.
 // Shared by the host transcoder (transcode.cpp) and the CUDA kernels.
 //
-// Fast path: beta1 = beta2 = 16, weight_bits in {2,3,4}, scale/zero bits in
-// [1,8].  The layer is cut into CELLS of 32 rows x 256 columns (a row-group
+// Fast path: beta1, beta2 multiples of 16 (stored as repeated 16 x 16
+// tiles), weight_bits in {2,3,4}, scale/zero bits in {2,3,4} (equal).  The layer is cut into CELLS of 32 rows x 256 columns (a row-group
 // pair x a 16-block panel); cell (G, P) is stored contiguously at
 // (G * Pn + P) * cell_bytes, cells in row-major order, so a warp streaming a
 // contiguous cell range streams contiguous bytes.  A cell is two UNITS (one
@@ -67,8 +67,13 @@ inline constexpr std::uint32_t kScalarBytes = 128;
 // The layout itself is defined for any bs, bz in [1, 8]; the kernel is
 // instantiated for the statistic widths below (others use the raw-stream
 // kernels, which are generic).
+// Group sizes: any beta1, beta2 that are multiples of 16 -- a 16 x 16 tile of
+// the layout then lies inside one stream record, whose statistics and scalars
+// the loader repeats in every tile it covers (the kernels see beta1 = beta2 =
+// 16; the stream / export keep the true groups).
 SPQR_HD constexpr bool supported(int bw, int bs, int bz, std::uint32_t b1, std::uint32_t b2) {
-    return b1 == 16 && b2 == 16 && (bw == 2 || bw == 3 || bw == 4) && bs == bz && bs >= 2 && bs <= 4;
+    return b1 >= 16 && b1 % 16 == 0 && b2 >= 16 && b2 % 16 == 0 && (bw == 2 || bw == 3 || bw == 4) && bs == bz &&
+           bs >= 2 && bs <= 4;
 }
 SPQR_HD constexpr int words_per_container(int bw) { return bw == 3 ? 3 : 1; }
 SPQR_HD constexpr int mmas_per_container(int bw) { return bw == 3 ? 4 : (bw == 4 ? 1 : 2); }

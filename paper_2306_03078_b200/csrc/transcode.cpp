@@ -45,20 +45,29 @@ void parallel_for(std::uint32_t n, int threads, F&& f) {
     for (auto& t : th) t.join();
 }
 
-// Stream record (k, g) -> stage block `blk`, rows [0, gr).
-void load_record(const StreamView& v, std::uint32_t k, std::uint32_t g, int blk, UnitStage& u) {
+// The 16 x 16 window at (row ro, column co) of stream record (k, g) -> stage
+// block `blk` (beta1, beta2 multiples of 16: statistics and scalars of a wider
+// group / block repeat in every unit / tiled block they cover).
+void load_record(const StreamView& v, std::uint32_t k, std::uint32_t g, std::uint32_t ro, std::uint32_t co, int blk,
+                 UnitStage& u, std::vector<std::uint8_t>& tmp) {
     const std::uint32_t gr = v.group_rows(g), bw = v.block_width(k);
+    if (ro >= gr || co >= bw) return;
     const std::uint8_t* p = v.base + v.record_offset(k, g);
     for (int i = 0; i < 4; ++i) u.scal[blk][i] = StreamView::load_u16(p + 2 * i);
     p += 8;
-    unpack_bits(p, u.scode[blk], gr, v.sb);
+    tmp.resize(static_cast<std::size_t>(gr) * bw + 2 * gr);
+    std::uint8_t *sc = tmp.data(), *zc = sc + gr, *w = zc + gr;
+    unpack_bits(p, sc, gr, v.sb);
     p += packed_field_bytes(gr, v.sb);
-    unpack_bits(p, u.zcode[blk], gr, v.zb);
+    unpack_bits(p, zc, gr, v.zb);
     p += packed_field_bytes(gr, v.zb);
-    std::uint8_t w[256];
     unpack_bits(p, w, static_cast<std::size_t>(gr) * bw, v.wb);
-    for (std::uint32_t r = 0; r < gr; ++r)
-        std::memcpy(&u.codes[r][16 * blk], w + r * bw, bw);
+    const std::uint32_t nr = std::min(16u, gr - ro), nc = std::min(16u, bw - co);
+    for (std::uint32_t r = 0; r < nr; ++r) {
+        u.scode[blk][r] = sc[ro + r];
+        u.zcode[blk][r] = zc[ro + r];
+        std::memcpy(&u.codes[r][16 * blk], w + static_cast<std::size_t>(ro + r) * bw + co, nc);
+    }
 }
 
 template <int BW>
@@ -212,14 +221,15 @@ TiledHost transcode_to_tiled(const StreamView& v, int threads) {
 
     parallel_for(t.Gn, threads, [&](std::uint32_t G) {
         UnitStage u;
+        std::vector<std::uint8_t> tmp;
         for (std::uint32_t P = 0; P < t.Pn; ++P) {
             for (int rg = 0; rg < 2; ++rg) {
                 std::memset(&u, 0, sizeof(u));
-                const std::uint32_t gg = 2 * G + rg;
+                const std::uint32_t r0u = 32 * G + 16 * rg, gg = r0u / v.b2;
                 if (gg < v.ngroups)
                     for (int blk = 0; blk < 16; ++blk) {
-                        const std::uint32_t k = 16 * P + blk;
-                        if (k < v.nblocks) load_record(v, k, gg, blk, u);
+                        const std::uint32_t c0 = 256 * P + 16 * blk, k = c0 / v.b1;
+                        if (k < v.nblocks) load_record(v, k, gg, r0u - gg * v.b2, c0 - k * v.b1, blk, u, tmp);
                     }
                 pack_unit(u, v.wb, v.sb, v.zb,
                           t.cells.data() + t.cell_off[static_cast<std::size_t>(G) * t.Pn + P] + rg * ub);
@@ -236,33 +246,48 @@ std::vector<std::uint8_t> tiled_to_stream(const StreamView& hdr, const TiledHost
     std::vector<std::uint8_t> out(t.prefix);
     out.resize(v.csr_off, 0);
     std::uint8_t* recs = out.data();
+    // 1. every unit back into dense per-row arrays (16-column blocks)
+    const std::uint32_t n16 = 16 * t.Pn, mpad = 32 * t.Gn, npad = 256 * t.Pn;
+    std::vector<std::uint8_t> codes(static_cast<std::size_t>(mpad) * npad), scode(static_cast<std::size_t>(n16) * mpad),
+        zcode(static_cast<std::size_t>(n16) * mpad);
+    std::vector<std::uint16_t> scal(static_cast<std::size_t>(n16) * (mpad / 16) * 4);
     parallel_for(t.Gn, threads, [&](std::uint32_t G) {
         UnitStage u;
-        std::vector<std::uint8_t> buf;
         for (std::uint32_t P = 0; P < t.Pn; ++P)
             for (int rg = 0; rg < 2; ++rg) {
-                const std::uint32_t gg = 2 * G + rg;
-                if (gg >= v.ngroups) continue;
                 unpack_unit(t.cells.data() + t.cell_off[static_cast<std::size_t>(G) * t.Pn + P] + rg * ub,
                             v.wb, v.sb, v.zb, u);
-                const std::uint32_t gr = v.group_rows(gg);
+                const std::uint32_t r0 = 32 * G + 16 * rg;
+                for (int r = 0; r < 16; ++r)
+                    std::memcpy(&codes[static_cast<std::size_t>(r0 + r) * npad + 256 * P], u.codes[r], 256);
                 for (int blk = 0; blk < 16; ++blk) {
-                    const std::uint32_t k = 16 * P + blk;
-                    if (k >= v.nblocks) break;
-                    const std::uint32_t bw = v.block_width(k);
-                    buf.clear();
-                    for (int i = 0; i < 4; ++i) {
-                        buf.push_back(static_cast<std::uint8_t>(u.scal[blk][i]));
-                        buf.push_back(static_cast<std::uint8_t>(u.scal[blk][i] >> 8));
-                    }
-                    pack_bits(u.scode[blk], gr, v.sb, buf);
-                    pack_bits(u.zcode[blk], gr, v.zb, buf);
-                    std::uint8_t w[256];
-                    for (std::uint32_t r = 0; r < gr; ++r) std::memcpy(w + r * bw, &u.codes[r][16 * blk], bw);
-                    pack_bits(w, static_cast<std::size_t>(gr) * bw, v.wb, buf);
-                    std::memcpy(recs + v.record_offset(k, gg), buf.data(), buf.size());
+                    const std::size_t kb = 16 * P + blk;
+                    std::memcpy(&scode[kb * mpad + r0], u.scode[blk], 16);
+                    std::memcpy(&zcode[kb * mpad + r0], u.zcode[blk], 16);
+                    std::memcpy(&scal[(kb * (mpad / 16) + r0 / 16) * 4], u.scal[blk], 8);
                 }
             }
+    });
+    // 2. every stream record (k, g) from the first tiled block / unit it covers
+    parallel_for(v.ngroups, threads, [&](std::uint32_t gg) {
+        std::vector<std::uint8_t> buf, w;
+        const std::uint32_t gr = v.group_rows(gg), r0 = gg * v.b2;
+        for (std::uint32_t k = 0; k < v.nblocks; ++k) {
+            const std::uint32_t bw = v.block_width(k), c0 = k * v.b1, kb = c0 / 16;
+            buf.clear();
+            const std::uint16_t* sc = &scal[(static_cast<std::size_t>(kb) * (mpad / 16) + r0 / 16) * 4];
+            for (int i = 0; i < 4; ++i) {
+                buf.push_back(static_cast<std::uint8_t>(sc[i]));
+                buf.push_back(static_cast<std::uint8_t>(sc[i] >> 8));
+            }
+            pack_bits(&scode[static_cast<std::size_t>(kb) * mpad + r0], gr, v.sb, buf);
+            pack_bits(&zcode[static_cast<std::size_t>(kb) * mpad + r0], gr, v.zb, buf);
+            w.resize(static_cast<std::size_t>(gr) * bw);
+            for (std::uint32_t r = 0; r < gr; ++r)
+                std::memcpy(&w[static_cast<std::size_t>(r) * bw], &codes[static_cast<std::size_t>(r0 + r) * npad + c0], bw);
+            pack_bits(w.data(), w.size(), v.wb, buf);
+            std::memcpy(recs + v.record_offset(k, gg), buf.data(), buf.size());
+        }
     });
     // CSR: per row, walk the row's cells left to right
     std::vector<std::uint32_t> rs(v.rows + 1, 0);

@@ -40,7 +40,18 @@ __global__ void __launch_bounds__(256) tc_units(const RawGeom geo, std::uint32_t
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     if (U >= 2u * Gn * Pn) return;
     const std::uint32_t q = U >> 1, rg = U & 1u;
-    const std::uint32_t G = q / Pn, P = q - G * Pn, gg = 2u * G + rg;
+    const std::uint32_t G = q / Pn, P = q - G * Pn;
+    // beta1, beta2 multiples of 16: the unit's 16 rows lie in stream row group
+    // gg at row offset ro, tiled block blk (16 columns) in stream column
+    // block k at column offset co; statistics and scalars of wider groups /
+    // blocks repeat in every unit / tiled block they cover
+    const std::uint32_t r0u = 32u * G + 16u * rg;
+    const std::uint32_t gg = r0u / geo.b2, ro = r0u - gg * geo.b2;
+    auto kblk = [&](std::uint32_t blk, std::uint32_t& co) {
+        const std::uint32_t c0 = 256u * P + 16u * blk, k = c0 / geo.b1;
+        co = c0 - k * geo.b1;
+        return k;
+    };
     const int bs = geo.sb, bz = geo.zb;
     const std::uint32_t ub = T::unit_bytes(BW, bs, bz);
     std::uint8_t* dst = cells + cell_off[q] + rg * ub;
@@ -54,8 +65,9 @@ __global__ void __launch_bounds__(256) tc_units(const RawGeom geo, std::uint32_t
         for (int i = 0; i < NP; ++i) {
             const int rho = i / (NP / 2), qq = i % (NP / 2), m = qq / 2, kh = qq % 2;
             const int blk = MPC * c + m;
-            const std::uint32_t row = g + 8 * rho, col = 2 * t + 8 * kh;  // column within block blk
-            const std::uint32_t k = 16u * P + blk;
+            std::uint32_t co;
+            const std::uint32_t k = kblk(blk, co);
+            const std::uint32_t row = ro + g + 8 * rho, col = co + 2 * t + 8 * kh;  // within record (k, gg)
             std::uint32_t c0 = 0, c1 = 0;
             if (gvalid && k < geo.nblocks) {
                 const RecFields f = rec_fields(geo, k, gg);
@@ -81,13 +93,14 @@ __global__ void __launch_bounds__(256) tc_units(const RawGeom geo, std::uint32_t
 #pragma unroll 1
         for (int j = 0; j < 8; ++j) {
             const int kind = j >> 2, h = (j >> 1) & 1, b = j & 1;
-            const std::uint32_t k = 16u * P + 8 * h + 2 * t + b;
+            std::uint32_t co;
+            const std::uint32_t k = kblk(8 * h + 2 * t + b, co);
             RecFields f{};
-            const bool kv = gvalid && k < geo.nblocks;
+            const bool kv = gvalid && k < geo.nblocks && co < geo.block_width(k);
             if (kv) f = rec_fields(geo, k, gg);
 #pragma unroll
             for (int rho = 0; rho < 2; ++rho) {
-                const std::uint32_t row = g + 8 * rho;
+                const std::uint32_t row = ro + g + 8 * rho;
                 std::uint32_t code = 0;
                 if (kv && row < f.gr) code = kind ? geo.bits_at(f.z, row, bz) : geo.bits_at(f.s, row, bs);
                 st[rho] |= code << (bs * j);
@@ -101,9 +114,10 @@ __global__ void __launch_bounds__(256) tc_units(const RawGeom geo, std::uint32_t
     }
     // block scalars {S_s, Z_s, S_z, Z_z}
     if (lane < 16) {
-        const std::uint32_t k = 16u * P + lane;
+        std::uint32_t co;
+        const std::uint32_t k = kblk(lane, co);
         std::uint32_t w0 = 0, w1 = 0;
-        if (gvalid && k < geo.nblocks) {
+        if (gvalid && k < geo.nblocks && co < geo.block_width(k)) {
             const std::uint64_t o = geo.record_offset(k, gg);
             w0 = geo.u32(o);
             w1 = geo.u32(o + 4);

@@ -191,15 +191,17 @@ def payload_bytes(m, n, wb, sb, zb, b1, b2, nnz, has_perm) -> int:
 
 
 def random_stream(m: int, n: int, weight_bits: int = 3, scale_bits: int = 3, zero_bits: int = 3,
-                  outlier_rate: float = 0.01, seed: int = 0, permute: bool = False) -> bytes:
-    """A valid beta1=beta2=16 stream with random codes (timing workloads)."""
-    assert m % 16 == 0 and n % 16 == 0
+                  outlier_rate: float = 0.01, seed: int = 0, permute: bool = False, beta1: int = 16,
+                  beta2: int = 16) -> bytes:
+    """A valid stream with random codes (timing workloads): full beta1 x beta2
+    group records (m % beta2 == 0, n % beta1 == 0)."""
+    assert m % beta2 == 0 and n % beta1 == 0
     for b in (weight_bits, scale_bits, zero_bits):
-        assert (16 * b) % 8 == 0 and 1 <= b <= 8
+        assert (beta2 * b) % 8 == 0 and 1 <= b <= 8
     rng = np.random.default_rng(seed)
-    nb, ng = n // 16, m // 16
+    nb, ng = n // beta1, m // beta2
     nnz = int(np.floor(outlier_rate * m * n))
-    rec = 8 + 2 * scale_bits + 2 * zero_bits + 32 * weight_bits
+    rec = 8 + (beta2 * scale_bits + beta2 * zero_bits + beta1 * beta2 * weight_bits) // 8
     hdr = np.zeros(48, np.uint8)
     hdr[0:4] = np.frombuffer(b"SPQR", np.uint8)
     hdr[4:6] = np.array([1], np.uint16).view(np.uint8)
@@ -207,7 +209,7 @@ def random_stream(m: int, n: int, weight_bits: int = 3, scale_bits: int = 3, zer
     hdr[6:8] = np.array([flags], np.uint16).view(np.uint8)
     hdr[8:16] = np.array([m, n], np.uint32).view(np.uint8)
     hdr[16:20] = [weight_bits, scale_bits, zero_bits, 0]
-    hdr[20:32] = np.array([16, 16, nnz], np.uint32).view(np.uint8)
+    hdr[20:32] = np.array([beta1, beta2, nnz], np.uint32).view(np.uint8)
     hdr[32:40] = np.array([0.1, 0.01], np.float32).view(np.uint8)
     parts = [hdr]
     if permute:
@@ -239,7 +241,7 @@ def random_stream(m: int, n: int, weight_bits: int = 3, scale_bits: int = 3, zer
     ent[:, 1] = _f2h(rng.standard_normal(nnz).astype(np.float32) * 0.05)
     parts.append(ent.reshape(-1).view(np.uint8))
     out = np.concatenate(parts).tobytes()
-    assert len(out) == 48 + payload_bytes(m, n, weight_bits, scale_bits, zero_bits, 16, 16, nnz, permute)
+    assert len(out) == 48 + payload_bytes(m, n, weight_bits, scale_bits, zero_bits, beta1, beta2, nnz, permute)
     return out
 
 

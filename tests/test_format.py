@@ -187,3 +187,15 @@ def test_kernel_model_other_widths(oracle_c, bw):
     s = P.encode_arrays(a)
     x = np.random.default_rng(0).standard_normal(512).astype(np.float32)
     assert relative_l2(model_matvec(s, x), oracle_c.decode(s).matvec(x)) < 1e-6
+
+
+@pytest.mark.parametrize("b1,b2", [(16, 32), (32, 16), (32, 32), (64, 128), (128, 64), (48, 80)])
+@pytest.mark.parametrize("shape", [(160, 1000), (96, 300), (256, 512)])
+def test_tiled_transcode_roundtrip_wide_groups(b1, b2, shape):
+    """beta1, beta2 multiples of 16 (PAPER Appendix D: beta2 = 32; the Table-10
+    grid) are on the tiled fast path: their statistics / scalars repeat per
+    16 x 16 tile, and the inverse re-encodes the stream byte for byte."""
+    a = synth.make_layer(*shape, beta1=b1, beta2=b2, seed=b1 + b2, permute=True, outlier_rate=0.02)
+    s = P.encode_arrays(a)
+    assert P.validate(s)["fast_path"] == 1
+    assert P.transcode_roundtrip_host(s) == s

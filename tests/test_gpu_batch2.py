@@ -26,7 +26,7 @@ def _run(L, x, batch):
 
 @pytest.mark.parametrize("bw,bs", [(2, 2), (3, 3), (4, 4), (3, 2)])
 @pytest.mark.parametrize("shape,perm", [((64, 512), False), ((160, 1000), True), ((256, 4096), False),
-                                        ((96, 17000), False)])
+                                        ((96, 17000), False), ((96, 300), False), ((64, 1004), False)])
 @pytest.mark.parametrize("batch", [2, 3])
 def test_batch_pair_equals_single_columns(cuda, oracle_c, bw, bs, shape, perm, batch):
     m, n = shape

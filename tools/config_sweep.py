@@ -51,9 +51,13 @@ def timed(fn, reps=30):
 cases = [("llama7b", 4096, 4096, 3, 0.01), ("llama7b", 11008, 4096, 3, 0.01), ("llama7b", 4096, 11008, 3, 0.01)]
 cases += [("density", 8192, 8192, 3, r) for r in (0.0, 0.005, 0.01, 0.02, 0.03, 0.04, 0.05)]
 cases += [("bits", 8192, 8192, 4, r) for r in (0.0, 0.01, 0.05)]
+cases = [c + ((16, 16),) for c in cases]
+# wider statistic groups (PAPER Appendix D: beta2 = 32; Table 10's grid) on the
+# fast kernel: GB/s on the stream's (smaller) payload
+cases += [("groups", 8192, 8192, 3, 0.01, bb) for bb in ((16, 32), (32, 32), (16, 64), (64, 128), (128, 128))]
 rows = []
-for group, m, n, bits, rate in cases:
-    s = synth.random_stream(m, n, bits, bits, bits, rate, seed=11)
+for group, m, n, bits, rate, (b1, b2) in cases:
+    s = synth.random_stream(m, n, bits, bits, bits, rate, seed=11, beta1=b1, beta2=b2)
     copies = max(2, int(400e6 // len(s)) + 1)
     Ls = [P.Layer(s, device=0) for _ in range(copies)]
     x = torch.randn(n, device="cuda").half()
@@ -68,6 +72,7 @@ for group, m, n, bits, rate in cases:
     W = torch.randn(m, n, device="cuda", dtype=torch.float16)
     us_d = 1e3 * timed(lambda: torch.mv(W, x))
     row = {"group": group, "shape": f"{m}x{n}", "weight_bits": bits, "stat_bits": bits, "outlier_rate": rate,
+           "beta1": b1, "beta2": b2, "fast_path": Ls[0].info["fast_path"],
            "payload_bytes": len(s) - 48, "us": round(us, 3), "GB/s": round(ab / (us * 1e-6) / 1e9, 1),
            "frac_of_peak": round(ab / (us * 1e-6) / 1e9 / peak, 4), "cublas_fp16_us": round(us_d, 3),
            "speedup_vs_cublas": round(us_d / us, 3)}
