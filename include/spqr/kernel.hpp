@@ -67,8 +67,14 @@ TilePlan build_tile_plan(const SpqrTensor& t, std::uint32_t tile_rows = 64);
 DenseTensor dequantize_full(const SpqrTensor& t);
 DenseTensor dequantize_full(const DeviceLayer& layer);
 
+// The tensor is uploaded on its first matvec and the device layer cached by
+// tensor identity (address + sampled fingerprint, LRU): later calls with the
+// same tensor cost the host-buffer matvec only.  A tensor modified in place
+// after its first matvec needs clear_device_cache().
 std::vector<float> matvec(const SpqrTensor& t, std::span<const float> x, const TilePlan& plan);
 std::vector<float> matvec(const SpqrTensor& t, std::span<const float> x);
+void clear_device_cache();
+std::size_t device_cache_size();
 std::vector<float> matvec(const DeviceLayer& layer, std::span<const float> x);
 std::vector<float> matvec_naive(const SpqrTensor& t, std::span<const float> x);
 

@@ -4,6 +4,9 @@
 // Compute goes to the GPU through spqr_cuda.h; a missing device or a failed
 // launch throws (SPQR_E_CUDA is surfaced as std::runtime_error), never falls
 // back to a CPU loop.
+#include <list>
+#include <memory>
+#include <mutex>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -141,14 +144,88 @@ std::vector<float> matvec(const DeviceLayer& layer, std::span<const float> x) {
     return y;
 }
 
+// matvec(const SpqrTensor&, x[, plan]) is a per-token call in the reference
+// (kernel.hpp:89, :126): the tensor is uploaded on first use and the device
+// layer cached by tensor identity -- address, shape, widths, group sizes,
+// outlier count and a fingerprint sampled from the codes, statistics and
+// outliers ("upload on first use, cached by tensor identity").  A
+// tensor modified in place after its first matvec must be re-created or the
+// cache cleared (clear_device_cache).  LRU, kDeviceCacheCap entries.
+namespace {
+constexpr std::size_t kDeviceCacheCap = 1024;
+struct CacheKey {
+    const SpqrTensor* addr;
+    std::uint64_t fp;
+    bool operator==(const CacheKey&) const = default;
+};
+std::uint64_t fingerprint(const SpqrTensor& t) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&](std::uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ull;
+    };
+    mix(t.rows); mix(t.cols); mix(static_cast<std::uint64_t>(t.weight_bits) << 16 | t.scale_bits << 8 | t.zero_bits);
+    mix(t.beta1); mix(t.beta2); mix(t.outliers.items.size());
+    mix(reinterpret_cast<std::uintptr_t>(t.codes.codes.data()));
+    auto sample = [&](const auto& v) {  // up to 4096 evenly spaced elements
+        const std::size_t n = v.size(), step = std::max<std::size_t>(1, n / 4096);
+        for (std::size_t i = 0; i < n; i += step) mix(static_cast<std::uint64_t>(v[i]));
+        if (n) mix(static_cast<std::uint64_t>(v[n - 1]));
+    };
+    sample(t.codes.codes);
+    const std::size_t nb = t.stats.blocks.size(), bstep = std::max<std::size_t>(1, nb / 64);
+    for (std::size_t k = 0; k < nb; k += bstep) {
+        const auto& b = t.stats.blocks[k];
+        sample(b.scale_codes);
+        sample(b.zero_codes);
+        for (const auto& gsc : b.groups) mix(static_cast<std::uint64_t>(gsc.scale_s) << 16 | gsc.scale_z);
+    }
+    const std::size_t no = t.outliers.items.size(), ostep = std::max<std::size_t>(1, no / 4096);
+    for (std::size_t i = 0; i < no; i += ostep) {
+        const auto& o = t.outliers.items[i];
+        mix(static_cast<std::uint64_t>(o.row) << 32 | o.col);
+        mix(o.value16);
+    }
+    return h;
+}
+std::mutex g_cache_mu;
+std::list<std::pair<CacheKey, std::shared_ptr<DeviceLayer>>> g_cache;  // front = most recent
+std::shared_ptr<DeviceLayer> cached_layer(const SpqrTensor& t) {
+    const CacheKey key{&t, fingerprint(t)};
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
+            if (it->first == key) {
+                g_cache.splice(g_cache.begin(), g_cache, it);
+                return it->second;
+            }
+    }
+    auto layer = std::make_shared<DeviceLayer>(t);  // outside the lock: the upload takes milliseconds
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.emplace_front(key, layer);
+    while (g_cache.size() > kDeviceCacheCap) g_cache.pop_back();
+    return layer;
+}
+}  // namespace
+
+void clear_device_cache() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.clear();
+}
+
+std::size_t device_cache_size() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    return g_cache.size();
+}
+
 std::vector<float> matvec(const SpqrTensor& t, std::span<const float> x, const TilePlan&) {
     if (x.size() != t.cols) fail(Errc::shape_mismatch, "vector length must equal columns");
-    return matvec(DeviceLayer(t), x);
+    return matvec(*cached_layer(t), x);
 }
 
 std::vector<float> matvec(const SpqrTensor& t, std::span<const float> x) {
     if (x.size() != t.cols) fail(Errc::shape_mismatch, "vector length must equal columns");
-    return matvec(DeviceLayer(t), x);
+    return matvec(*cached_layer(t), x);
 }
 
 // Reference path: full (bit-exact) dequantization on the GPU, then the dense

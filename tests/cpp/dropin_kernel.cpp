@@ -22,6 +22,13 @@ int main(int argc, char** argv) {
         spqr::DeviceLayer layer(t);
         const std::vector<float> y2 = spqr::matvec(layer, x);
         if (spqr::detail::relative_l2(y, y2) != 0.0) return 5;
+        // per-token calls on the same tensor reuse the cached device layer
+        const std::size_t cached = spqr::device_cache_size();
+        for (int i = 0; i < 3; ++i)
+            if (spqr::detail::relative_l2(spqr::matvec(t, x), y) != 0.0) return 7;
+        if (spqr::device_cache_size() != cached || cached < 1) return 8;
+        spqr::clear_device_cache();
+        if (spqr::device_cache_size() != 0) return 9;
         std::size_t total = 0;
         for (std::size_t i = 0; i < plan.tiles.size(); ++i) total += plan.tile_outlier_count(i);
         if (total != t.outliers.items.size()) return 6;  // SPEC.md:450 slices partition nnz
