@@ -279,6 +279,34 @@ int spqr_sharded_matvec(spqr_sharded* s, const void* x_dev, int x_dtype, float* 
                         void* cuda_stream);
 void spqr_sharded_destroy(spqr_sharded* s);
 
+/* The encoder on the GPU (the path's producer): Hessian
+ * accumulation H += 2 X X^T (hessian.hpp:59-69, binary64), damped inverse
+ * Cholesky (hessian.hpp:103-143), block-GPTQ with the leave-one-out outlier
+ * screen and the bilevel statistics fit (spqr_quantize, solver.hpp:417-533),
+ * then encode (format.hpp:269-352) -- the reference's arithmetic in binary64
+ * with rows in parallel, the trailing updates / products on cuBLAS DGEMM and
+ * the factorizations on cuSOLVER (bound at run time).  The stream equals the
+ * reference encoder's (tests/test_gpu_encoder.py). */
+typedef struct spqr_encoder_cfg {
+    int32_t weight_bits, scale_bits, zero_bits;  /* b_w; b_s, b_z (16: raw fp32 statistics) */
+    uint32_t beta1, beta2;                       /* beta1 <= 256 */
+    int32_t order;                               /* 0 natural, 1 act_order, 2 shuffled (seed) */
+    int32_t act_order_key;                       /* 0 Hessian diagonal, 1 inverse diagonal */
+    int32_t outliers_enabled, integer_zero, full_range_sign;
+    double tau, lambda_rel;
+    uint64_t seed;
+} spqr_encoder_cfg;
+typedef struct spqr_hessian spqr_hessian;
+int spqr_hessian_create(uint32_t n, int device, spqr_hessian** out);
+/* x: n x samples fp32, row-major, on the Hessian's device. */
+int spqr_hessian_accumulate(spqr_hessian* h, const float* x_dev, uint32_t samples, void* cuda_stream);
+int spqr_hessian_read(const spqr_hessian* h, double* h_host);  /* n x n binary64 */
+void spqr_hessian_destroy(spqr_hessian* h);
+/* W: m x n fp32 row-major (original column order) on the device; out: the
+ * .spqr stream; report[3] = {relative layer error, outlier rate, bits/param}. */
+int spqr_quantize_layer(const spqr_hessian* h, const float* w_dev, uint32_t m, const spqr_encoder_cfg* cfg,
+                        uint8_t* out, size_t cap, size_t* len, double* report);
+
 /* Profiling split of spqr_matvec: stage 1 = x preparation only, stage 2 = the
  * product only, 0 = both.  On the fast path x preparation is fused into the
  * product kernel, so stage 1 launches nothing and stage 2 equals stage 0;

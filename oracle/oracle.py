@@ -20,6 +20,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libspqr_ref.so")
+REF_ENC_SO = os.path.join(HERE, "_ref", "libspqr_ref_enc.so")
 
 ERRC = [
     "malformed_header", "shape_mismatch", "non_finite_value", "io_failure", "parse_error",
@@ -43,8 +44,9 @@ def build(force: bool = False) -> None:
     ):
         subprocess.check_call(["make", "-s", "-C", HERE, ORACLE_SO])
     if os.path.isdir("/root/reference/proj/include/spqr") and (
-        force or not os.path.exists(REF_SO)
+        force or not os.path.exists(REF_SO) or not os.path.exists(REF_ENC_SO)
         or os.path.getmtime(REF_SO) < os.path.getmtime(os.path.join(HERE, "ref_shim.cpp"))
+        or os.path.getmtime(REF_ENC_SO) < os.path.getmtime(os.path.join(HERE, "ref_encoder.cpp"))
     ):
         subprocess.check_call(["make", "-s", "-C", HERE, "ref"])
 
@@ -288,6 +290,41 @@ class Reference(_Backend):
         if rc:
             raise OracleError(rc, "measure_actual_bits")
         return out
+
+
+class ReferenceEncoder:
+    """The unmodified reference encoder (HessianAccumulator, finalize,
+    spqr_quantize, make_spqr_tensor + encode) in oracle/_ref/libspqr_ref_enc.so,
+    built with our functional minimal Eigen (oracle/eigen_min)."""
+
+    def __init__(self, path: str = REF_ENC_SO):
+        self.lib = C.CDLL(path)
+        self.lib.ref_enc_quantize.restype = C.c_int
+        self.lib.ref_enc_quantize.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32,
+                                              C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_void_p,
+                                              C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p]
+
+    def quantize(self, W, X, weight_bits=3, scale_bits=3, zero_bits=3, beta1=16, beta2=16, order="natural",
+                 act_order_key="hessian_diag", outliers=True, integer_zero=False, full_range_sign=True, tau=0.1,
+                 lambda_rel=0.01, seed=0):
+        """W: m x n fp32; X: n x samples fp32 -> (stream bytes, report dict)."""
+        W = _arr(W, np.float32)
+        X = _arr(X, np.float32)
+        m, n = W.shape
+        cfg = np.array([weight_bits, scale_bits, zero_bits, beta1, beta2,
+                        {"natural": 0, "act_order": 1, "shuffled": 2}[order],
+                        {"hessian_diag": 0, "inverse_diag": 1}[act_order_key], int(outliers), int(integer_zero),
+                        int(full_range_sign)], np.int32)
+        cap = 48 + 4 * n + 2 * m * n + 64 * m * n // max(1, beta1) + 4 * (m + 1) + 4 * (m * n // 20 + 1) + 4096
+        out = np.empty(cap, np.uint8)
+        ln = C.c_size_t()
+        rep = np.zeros(3, np.float64)
+        rc = self.lib.ref_enc_quantize(_ptr(W), m, n, _ptr(X), X.shape[1], _ptr(cfg), tau, lambda_rel, seed,
+                                       _ptr(out), cap, C.byref(ln), _ptr(rep))
+        if rc:
+            raise OracleError(rc, "ref_enc_quantize")
+        return out[: ln.value].tobytes(), {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]),
+                                           "bits_per_param": float(rep[2])}
 
 
 def relative_l2(a, b) -> float:

@@ -74,6 +74,13 @@ class TensorArrays(C.Structure):
                 ("outlier_cols", C.c_void_p), ("outlier_vals", C.c_void_p)]
 
 
+class EncoderCfg(C.Structure):
+    _fields_ = [("weight_bits", C.c_int32), ("scale_bits", C.c_int32), ("zero_bits", C.c_int32),
+                ("beta1", C.c_uint32), ("beta2", C.c_uint32), ("order", C.c_int32), ("act_order_key", C.c_int32),
+                ("outliers_enabled", C.c_int32), ("integer_zero", C.c_int32), ("full_range_sign", C.c_int32),
+                ("tau", C.c_double), ("lambda_rel", C.c_double), ("seed", C.c_uint64)]
+
+
 class LayerOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("force_generic", C.c_int32), ("keep_stream", C.c_int32),
                 ("row_begin", C.c_uint32), ("row_end", C.c_uint32), ("host_transcode", C.c_int32)]
@@ -138,6 +145,11 @@ def lib() -> C.CDLL:
         "spqr_gather_wait": (i32, [vp, vp]),
         "spqr_gather_destroy": (None, [vp]),
         "spqr_row_bands": (i32, [u32, u32, i32, vp]),
+        "spqr_hessian_create": (i32, [u32, i32, C.POINTER(vp)]),
+        "spqr_hessian_accumulate": (i32, [vp, vp, u32, vp]),
+        "spqr_hessian_read": (i32, [vp, vp]),
+        "spqr_hessian_destroy": (None, [vp]),
+        "spqr_quantize_layer": (i32, [vp, vp, u32, C.POINTER(EncoderCfg), vp, sz, C.POINTER(C.c_size_t), vp]),
         "spqr_nccl_unique_id": (i32, [vp]),
         "spqr_nccl_comm_init": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
         "spqr_nccl_comm_destroy": (i32, [vp]),
@@ -470,6 +482,60 @@ class Gather:
     def close(self):
         if getattr(self, "_h", None):
             lib().spqr_gather_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Hessian:
+    """H = 2 X X^T accumulated on the GPU in binary64 (spqr_hessian_*,
+    hessian.hpp:52-85); quantize() runs the GPU encoder against it."""
+
+    def __init__(self, n: int, device: int = -1):
+        h = C.c_void_p()
+        _check(lib().spqr_hessian_create(n, device, C.byref(h)))
+        self._h, self.n = h, n
+
+    def accumulate(self, x, stream=None) -> None:
+        """x: n x samples fp32 on the device (calibration inputs, one column per sample)."""
+        if x.dim() != 2 or x.shape[0] != self.n:
+            raise ValueError("x must be n x samples")
+        _check(lib().spqr_hessian_accumulate(self._h, _ptr(x.contiguous()), x.shape[1], _stream_ptr(stream)))
+
+    def matrix(self) -> np.ndarray:
+        out = np.empty((self.n, self.n), np.float64)
+        _check(lib().spqr_hessian_read(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def quantize(self, w, weight_bits=3, scale_bits=3, zero_bits=3, beta1=16, beta2=16, order="natural",
+                 act_order_key="hessian_diag", outliers=True, integer_zero=False, full_range_sign=True,
+                 tau=0.1, lambda_rel=0.01, seed=0):
+        """spqr_quantize + encode on the GPU: (stream bytes, report dict)."""
+        cfg = EncoderCfg(weight_bits, scale_bits, zero_bits, beta1, beta2,
+                         {"natural": 0, "act_order": 1, "shuffled": 2}[order],
+                         {"hessian_diag": 0, "inverse_diag": 1}[act_order_key], int(outliers), int(integer_zero),
+                         int(full_range_sign), float(tau), float(lambda_rel), int(seed))
+        w = w.contiguous()
+        m = w.shape[0]
+        rep = np.zeros(3, np.float64)
+        n = C.c_size_t()
+        # upper bound of the stream: header, permutation, records with 16-bit
+        # statistics, CSR with the 5 % outlier cap
+        nb, ng = -(-self.n // beta1), -(-m // beta2)
+        cap = 48 + 4 * self.n + nb * ng * (8 + 8 * beta2 + beta1 * beta2) + 4 * (m + 1) + 4 * (m * self.n // 20 + 1)
+        buf = np.empty(cap, np.uint8)
+        _check(lib().spqr_quantize_layer(self._h, _ptr(w), m, C.byref(cfg), buf.ctypes.data_as(C.c_void_p),
+                                         buf.size, C.byref(n), rep.ctypes.data_as(C.c_void_p)))
+        return buf[: n.value].tobytes(), {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]),
+                               "bits_per_param": float(rep[2])}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().spqr_hessian_destroy(self._h)
             self._h = None
 
     def __del__(self):
