@@ -306,6 +306,12 @@ void spqr_hessian_destroy(spqr_hessian* h);
  * .spqr stream; report[3] = {relative layer error, outlier rate, bits/param}. */
 int spqr_quantize_layer(const spqr_hessian* h, const float* w_dev, uint32_t m, const spqr_encoder_cfg* cfg,
                         uint8_t* out, size_t cap, size_t* len, double* report);
+/* tune_tau (solver.hpp:546-640): binary search of the 0.05-step tau grid over
+ * [0.1, 1.0] for the smallest tau with outlier rate <= target_rate (cfg.tau is
+ * ignored); report[5] = {relative error, outlier rate, bits/param, tau,
+ * target reached (1/0)}.  cap must hold the stream (the encoded layer). */
+int spqr_quantize_layer_tuned(const spqr_hessian* h, const float* w_dev, uint32_t m, const spqr_encoder_cfg* cfg,
+                              double target_rate, uint8_t* out, size_t cap, size_t* len, double* report);
 
 /* Profiling split of spqr_matvec: stage 1 = x preparation only, stage 2 = the
  * product only, 0 = both.  On the fast path x preparation is fused into the

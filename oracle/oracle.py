@@ -301,12 +301,12 @@ class ReferenceEncoder:
         self.lib = C.CDLL(path)
         self.lib.ref_enc_quantize.restype = C.c_int
         self.lib.ref_enc_quantize.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32,
-                                              C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_void_p,
-                                              C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p]
+                                              C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_double,
+                                              C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t), C.c_void_p]
 
     def quantize(self, W, X, weight_bits=3, scale_bits=3, zero_bits=3, beta1=16, beta2=16, order="natural",
                  act_order_key="hessian_diag", outliers=True, integer_zero=False, full_range_sign=True, tau=0.1,
-                 lambda_rel=0.01, seed=0):
+                 lambda_rel=0.01, seed=0, target_rate=None):
         """W: m x n fp32; X: n x samples fp32 -> (stream bytes, report dict)."""
         W = _arr(W, np.float32)
         X = _arr(X, np.float32)
@@ -318,13 +318,15 @@ class ReferenceEncoder:
         cap = 48 + 4 * n + 2 * m * n + 64 * m * n // max(1, beta1) + 4 * (m + 1) + 4 * (m * n // 20 + 1) + 4096
         out = np.empty(cap, np.uint8)
         ln = C.c_size_t()
-        rep = np.zeros(3, np.float64)
+        rep = np.zeros(5, np.float64)
         rc = self.lib.ref_enc_quantize(_ptr(W), m, n, _ptr(X), X.shape[1], _ptr(cfg), tau, lambda_rel, seed,
-                                       _ptr(out), cap, C.byref(ln), _ptr(rep))
+                                       float(target_rate or 0.0), _ptr(out), cap, C.byref(ln), _ptr(rep))
         if rc:
             raise OracleError(rc, "ref_enc_quantize")
-        return out[: ln.value].tobytes(), {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]),
-                                           "bits_per_param": float(rep[2])}
+        r = {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]), "bits_per_param": float(rep[2])}
+        if target_rate:
+            r.update(tau=float(rep[3]), target_reached=bool(rep[4]))
+        return out[: ln.value].tobytes(), r
 
 
 def relative_l2(a, b) -> float:

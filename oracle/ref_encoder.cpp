@@ -23,10 +23,11 @@ extern "C" {
 // fp32 calibration inputs.  cfg: {wb, sb, zb, beta1, beta2, order (0 natural,
 // 1 act_order, 2 shuffled), act_key (0 hessian_diag, 1 inverse_diag),
 // outliers_enabled, integer_zero, full_range_sign}, tau, lambda_rel, seed.
-// report: {relative_error, outlier_rate, bits_per_param}.
+// target_rate > 0: tune_tau instead of the fixed tau.  report: {relative_error,
+// outlier_rate, bits_per_param[, tau, target reached]}.
 int ref_enc_quantize(const float* W, uint32_t m, uint32_t n, const float* X, uint32_t samples, const int* cfg,
-                     double tau, double lambda_rel, uint64_t seed, uint8_t* out, size_t cap, size_t* len,
-                     double* report) {
+                     double tau, double lambda_rel, uint64_t seed, double target_rate, uint8_t* out, size_t cap,
+                     size_t* len, double* report) {
     try {
         R::HessianAccumulator acc(n);
         acc.accumulate(R::DenseTensor(n, samples, std::vector<float>(X, X + static_cast<size_t>(n) * samples)));
@@ -45,8 +46,19 @@ int ref_enc_quantize(const float* W, uint32_t m, uint32_t n, const float* X, uin
         c.tau = tau;
         c.lambda_rel = lambda_rel;
         c.seed = seed;
-        const R::SpqrResult res =
-            R::spqr_quantize(R::DenseTensor(m, n, std::vector<float>(W, W + static_cast<size_t>(m) * n)), icho, c);
+        const R::DenseTensor Wt(m, n, std::vector<float>(W, W + static_cast<size_t>(m) * n));
+        R::SpqrResult res;
+        if (target_rate > 0.0) {  // tune_tau, solver.hpp:546
+            R::TuneResult tr = R::tune_tau(Wt, icho, c, target_rate);
+            res = std::move(tr.result);
+            c.tau = tr.tau;
+            if (report) {
+                report[3] = tr.tau;
+                report[4] = tr.target_reached ? 1.0 : 0.0;
+            }
+        } else {
+            res = R::spqr_quantize(Wt, icho, c);
+        }
         const std::vector<uint8_t> bytes = R::encode(R::make_spqr_tensor(res, c));
         *len = bytes.size();
         if (report) {

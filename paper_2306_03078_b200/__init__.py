@@ -150,6 +150,8 @@ def lib() -> C.CDLL:
         "spqr_hessian_read": (i32, [vp, vp]),
         "spqr_hessian_destroy": (None, [vp]),
         "spqr_quantize_layer": (i32, [vp, vp, u32, C.POINTER(EncoderCfg), vp, sz, C.POINTER(C.c_size_t), vp]),
+        "spqr_quantize_layer_tuned": (i32, [vp, vp, u32, C.POINTER(EncoderCfg), C.c_double, vp, sz,
+                                            C.POINTER(C.c_size_t), vp]),
         "spqr_nccl_unique_id": (i32, [vp]),
         "spqr_nccl_comm_init": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
         "spqr_nccl_comm_destroy": (i32, [vp]),
@@ -513,8 +515,9 @@ class Hessian:
 
     def quantize(self, w, weight_bits=3, scale_bits=3, zero_bits=3, beta1=16, beta2=16, order="natural",
                  act_order_key="hessian_diag", outliers=True, integer_zero=False, full_range_sign=True,
-                 tau=0.1, lambda_rel=0.01, seed=0):
-        """spqr_quantize + encode on the GPU: (stream bytes, report dict)."""
+                 tau=0.1, lambda_rel=0.01, seed=0, target_rate=None):
+        """spqr_quantize + encode on the GPU: (stream bytes, report dict).
+        target_rate: tune_tau (solver.hpp:546) instead of a fixed tau."""
         cfg = EncoderCfg(weight_bits, scale_bits, zero_bits, beta1, beta2,
                          {"natural": 0, "act_order": 1, "shuffled": 2}[order],
                          {"hessian_diag": 0, "inverse_diag": 1}[act_order_key], int(outliers), int(integer_zero),
@@ -528,6 +531,14 @@ class Hessian:
         nb, ng = -(-self.n // beta1), -(-m // beta2)
         cap = 48 + 4 * self.n + nb * ng * (8 + 8 * beta2 + beta1 * beta2) + 4 * (m + 1) + 4 * (m * self.n // 20 + 1)
         buf = np.empty(cap, np.uint8)
+        if target_rate is not None:
+            rep = np.zeros(5, np.float64)
+            _check(lib().spqr_quantize_layer_tuned(self._h, _ptr(w), m, C.byref(cfg), float(target_rate),
+                                                   buf.ctypes.data_as(C.c_void_p), buf.size, C.byref(n),
+                                                   rep.ctypes.data_as(C.c_void_p)))
+            return buf[: n.value].tobytes(), {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]),
+                                              "bits_per_param": float(rep[2]), "tau": float(rep[3]),
+                                              "target_reached": bool(rep[4])}
         _check(lib().spqr_quantize_layer(self._h, _ptr(w), m, C.byref(cfg), buf.ctypes.data_as(C.c_void_p),
                                          buf.size, C.byref(n), rep.ctypes.data_as(C.c_void_p)))
         return buf[: n.value].tobytes(), {"relative_error": float(rep[0]), "outlier_rate": float(rep[1]),

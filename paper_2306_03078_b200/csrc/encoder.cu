@@ -141,14 +141,18 @@ struct QFlags {
 
 // fit_group_minmax, quantizer.hpp:77-97
 __device__ void fit_minmax(const double* v, std::uint32_t len, int bits, QFlags f, double& s, double& z) {
+    // std::min / std::max semantics (keep the first operand unless the
+    // second compares strictly smaller / larger: signed zeros as the host)
+    auto smin = [](double a, double b) { return b < a ? b : a; };
+    auto smax = [](double a, double b) { return a < b ? b : a; };
     double mn = v[0], mx = v[0];
     for (std::uint32_t i = 1; i < len; ++i) {
-        mn = fmin(mn, v[i]);
-        mx = fmax(mx, v[i]);
+        mn = smin(mn, v[i]);
+        mx = smax(mx, v[i]);
     }
     if (!f.full_range_sign) {
-        mn = fmin(mn, 0.0);
-        mx = fmax(mx, 0.0);
+        mn = smin(mn, 0.0);
+        mx = smax(mx, 0.0);
     }
     const double maxq = static_cast<double>((1u << bits) - 1u);
     if (mx == mn) {
@@ -158,7 +162,7 @@ __device__ void fit_minmax(const double* v, std::uint32_t len, int bits, QFlags 
         s = (mx - mn) / maxq;
         z = -mn / s;
     }
-    if (f.integer_zero) z = fmin(fmax(floor(z + 0.5), 0.0), maxq);
+    if (f.integer_zero) z = smin(smax(floor(z + 0.5), 0.0), maxq);  // std::clamp
 }
 // quant_code, quantizer.hpp:50-56
 __device__ __forceinline__ std::uint32_t qcode(double v, double s, double z, std::uint32_t maxq) {
@@ -764,6 +768,76 @@ int spqr_quantize_layer(const spqr_hessian* h, const float* w_dev, uint32_t m, c
         std::memcpy(out, bytes.data(), bytes.size());
     });
     return g ? g : rc;
+}
+
+// tune_tau (solver.hpp:546-640): the smallest tau on the 0.05-step grid over
+// [0.1, 1.0] whose outlier rate stays at or below the target, by the
+// reference's binary search; report[3] = that tau, report[4] = target reached.
+int spqr_quantize_layer_tuned(const spqr_hessian* h, const float* w_dev, uint32_t m, const spqr_encoder_cfg* cfg,
+                              double target_rate, uint8_t* out, size_t cap, size_t* len, double* report) {
+    return spqr::detail::guard([&] {
+        if (!(target_rate > 0.0) || target_rate > 0.05)
+            spqr::fail(spqr::Errc::config_invalid, "target outlier rate must be in (0, 0.05]");
+        spqr_encoder_cfg c = *cfg;
+        c.outliers_enabled = 1;
+        constexpr double kTauMin = 0.1, kTauStep = 0.05;
+        constexpr int kGridMax = 18;
+        auto tau_at = [&](int k) { return kTauMin + kTauStep * k; };
+        std::vector<std::uint8_t> best;
+        double best_rep[3] = {0, 0, 0};
+        int best_k = -1;
+        auto probe = [&](int k) {  // true: feasible (rate <= target)
+            c.tau = tau_at(k);
+            std::vector<std::uint8_t> buf(cap ? cap : 1);
+            std::size_t n = 0;
+            double rep[3];
+            const int st = spqr_quantize_layer(h, w_dev, m, &c, buf.data(), buf.size(), &n, rep);
+            if (st == 1 + static_cast<int>(spqr::Errc::outlier_budget_exceeded)) return false;
+            if (st) throw spqr::Error(static_cast<spqr::Errc>(st - 1), spqr_last_error());
+            if (rep[1] <= target_rate) {
+                buf.resize(n);
+                best = std::move(buf);
+                std::copy(rep, rep + 3, best_rep);
+                best_k = k;
+                return true;
+            }
+            return false;
+        };
+        int chosen = -1;
+        bool reached = true;
+        if (probe(0)) {
+            chosen = 0;
+        } else if (!probe(kGridMax)) {  // above target even at tau = 1.0: report, do not fail
+            reached = false;
+            c.tau = tau_at(kGridMax);
+            std::vector<std::uint8_t> buf(cap ? cap : 1);
+            std::size_t n = 0;
+            const int st = spqr_quantize_layer(h, w_dev, m, &c, buf.data(), buf.size(), &n, best_rep);
+            if (st) throw spqr::Error(static_cast<spqr::Errc>(st - 1), spqr_last_error());
+            buf.resize(n);
+            best = std::move(buf);
+            chosen = kGridMax;
+        } else {
+            int lo = 0, hi = kGridMax;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) / 2;
+                if (probe(mid))
+                    hi = mid;
+                else
+                    lo = mid;
+            }
+            if (best_k != hi) probe(hi);
+            chosen = hi;
+        }
+        if (report) {
+            std::copy(best_rep, best_rep + 3, report);
+            report[3] = tau_at(chosen);
+            report[4] = reached ? 1.0 : 0.0;
+        }
+        *len = best.size();
+        if (!out || cap < best.size()) spqr::fail(spqr::Errc::config_invalid, "output buffer too small");
+        std::memcpy(out, best.data(), best.size());
+    });
 }
 
 }  // extern "C"

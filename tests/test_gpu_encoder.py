@@ -121,3 +121,15 @@ def test_gpu_encoder_stream_decodes_and_runs(cuda, ref_encoder):
     L.matvec(x, y)
     t = O.Oracle().decode(s)
     assert O.relative_l2(y.cpu().numpy(), t.matvec(x.cpu().numpy())) <= 1e-5
+
+
+@pytest.mark.parametrize("target", [0.002, 0.01, 0.0001])
+def test_gpu_tune_tau_matches_reference(cuda, ref_encoder, target):
+    """tune_tau (solver.hpp:546-640): same tau, same stream, same verdict."""
+    W, X = _layer(64, 256, 256, seed=5, outlier_cols=1)
+    s_ref, rep_ref = ref_encoder.quantize(W, X, target_rate=target)
+    H = P.Hessian(256, device=0)
+    H.accumulate(torch.from_numpy(X).cuda())
+    s_gpu, rep_gpu = H.quantize(torch.from_numpy(W).cuda(), target_rate=target)
+    assert rep_gpu["tau"] == rep_ref["tau"] and rep_gpu["target_reached"] == rep_ref["target_reached"]
+    assert s_gpu == s_ref
