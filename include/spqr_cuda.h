@@ -222,10 +222,10 @@ int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, floa
  * B200-native fusion"; 8f rank 2): instead of spqr_matvec on the band followed
  * by an NCCL all-gather of y, each rank's gemv_cta stores every finished y
  * row straight into every rank's full-y buffer (peer addresses from CUDA IPC:
- * NVLink P2P stores between GPUs) and its last CTA bumps this rank's round
- * counter on every rank; spqr_gather_wait (one 32-thread launch) waits for all
- * ranks' counters.  Rounds live on the device: both launches replay in a CUDA
- * graph.  Protocol: spqr_gather_create on every rank -> spqr_gather_handle ->
+ * NVLink P2P stores between GPUs); its last CTA bumps this rank's round
+ * counter on every rank and waits for all ranks' counters, so the launch
+ * completes with y whole (spqr_gather_wait is kept for callers and launches
+ * nothing).  Rounds live on the device: the launch replays in a CUDA graph.  Protocol: spqr_gather_create on every rank -> spqr_gather_handle ->
  * exchange the world x SPQR_GATHER_HANDLE_BYTES handles and the bands' first
  * rows (any transport, e.g. torch.distributed) -> spqr_gather_open -> per
  * step spqr_matvec_gather + spqr_gather_wait, then read spqr_gather_y.

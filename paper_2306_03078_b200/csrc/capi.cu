@@ -1092,23 +1092,12 @@ int spqr_matvec_gather(const spqr_layer* L, const void* x_dev, int x_dtype, spqr
 }
 
 int spqr_gather_wait(spqr_gather* g, void* cuda_stream) {
-    return guard([&] {
-        DevGuard dg(g->device);
-        g_launches = 0;
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(1);
-        cfg.blockDim = dim3(32);
-        cfg.stream = static_cast<cudaStream_t>(cuda_stream);
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        ck(cudaLaunchKernelEx(&cfg, spqr_dev::gather_wait, reinterpret_cast<const std::uint32_t*>(g->base),
-                              reinterpret_cast<std::uint32_t*>(g->base + 64), static_cast<std::uint32_t>(g->world)),
-           "launch gather_wait");
-        ++g_launches;
-    });
+    // the wait is fused into the band kernel's last CTA (gemv_cta GATHER):
+    // the stream is already ordered after every rank's rows of the round
+    (void)g;
+    (void)cuda_stream;
+    g_launches = 0;
+    return SPQR_OK;
 }
 
 void spqr_gather_destroy(spqr_gather* g) {

@@ -39,8 +39,9 @@
 //    ticket) adds first-side + last-side and resets the ticket -- no CTA ever
 //    waits for another, so launches need not be co-resident.
 //  * GATHER = true (row-sharded decode, gather.cu): every y row is also stored
-//    into the other ranks' full-y buffers and the grid's last CTA bumps this
-//    rank's round counter on every rank; gather_wait consumes it.
+//    into the other ranks' full-y buffers; the grid's last CTA bumps this
+//    rank's round counter on every rank and waits until every rank's counter
+//    reached the round (the all-gather's wait, fused: no second launch).
 // Every reduction order is fixed by the partition, not by the schedule, so y
 // is bitwise reproducible run to run.
 
@@ -80,7 +81,7 @@ struct CtaParams {
     // posted by j): everything peer j's stream ordered before that kernel --
     // its consumers of y from round R-1 -- is then complete, so a rank running
     // one round ahead never overwrites rows a peer is still reading.
-    const std::uint32_t* round;       // this rank's completed rounds (gather_wait advances it)
+    const std::uint32_t* round;       // this rank's completed rounds (the grid's last CTA advances it)
     const std::uint32_t* started;     // [world] in this rank's block: peer j's latest started round
 };
 constexpr std::uint32_t kGatherStartedWord = 32;  // started[] at byte 128 of a gather block
@@ -313,9 +314,11 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
     __shared__ __align__(16) std::uint32_t zrow[NC][4];  // 16 zero bytes: masked ldmatrix rows
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ std::uint32_t g_round, g_peers_ok;  // GATHER: this launch's round; peers have started it
+    __shared__ std::uint32_t g_round, g_round_ok, g_peers_ok;  // GATHER: this launch's round; peers have started it
     auto wait_peers = [&]() {  // (GATHER) until every peer's band kernel of this round has started
         if (lane == 0) {
+            while (*reinterpret_cast<volatile std::uint32_t*>(&g_round_ok) == 0u) {
+            }
             const unsigned long long t0 = globaltimer();
             for (std::uint32_t j = 0; j < p.nflag; ++j) {
                 if (j == p.rank) continue;
@@ -350,7 +353,10 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
         if (warp == 0) mbar_init(&coff_bar, 1);
         fence_mbar_init();
     }
-    if (threadIdx.x == 0) tick[0] = tick[1] = NC;  // ticket w < NC is warp w's first cell
+    if (threadIdx.x == 0) {
+        tick[0] = tick[1] = NC;  // ticket w < NC is warp w's first cell
+        if constexpr (GATHER) g_round_ok = g_peers_ok = 0u;
+    }
     if (threadIdx.x < 64) pflag[threadIdx.x] = 0u;
     for (int c = 0; c < NCOL; ++c) rowsum[warp][c][lane] = 0.f;
     if (lane < 4) zrow[warp][lane] = 0u;
@@ -497,15 +503,16 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             pdl_wait();  // the preceding kernel has completed: x, y and the partial slots are ours
             waited = true;
             if constexpr (GATHER) {
-                if (threadIdx.x == 0) {
-                    g_round = *p.round + 1u;  // gather_wait of the previous round has completed
-                    g_peers_ok = 0u;
-                    if (blockIdx.x == 0)  // announce: this rank's band kernel of round g_round runs
+                if (threadIdx.x == 0) {  // (the other warps go on: only peer stores need the round)
+                    const std::uint32_t r = *p.round + 1u;  // the previous round's grid has completed
+                    if (blockIdx.x == 0)  // announce: this rank's band kernel of round r runs
                         for (std::uint32_t j = 0; j < p.nflag; ++j)
                             asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pflags[j] + kGatherStartedWord + p.rank),
-                                         "r"(g_round) : "memory");
+                                         "r"(r) : "memory");
+                    g_round = r;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile std::uint32_t*>(&g_round_ok) = 1u;
                 }
-                bar_sync_named(2, NT);
             }
             SPQR_TL(1)
             if constexpr (SHX) {  // own panels (<= 3), the first cell's first; every x load
@@ -944,12 +951,27 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             // release -- fences system-wide and bumps the ranks' round counters
             if (p.npeer) __threadfence_system();
             std::uint32_t prev;
-            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done_ctr) : "memory");
-            if (prev == gridDim.x - 1u) {  // the grid's last CTA
+            asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done_ctr) : "memory");
+            if (prev == gridDim.x - 1u) {  // the grid's last CTA: acquire every CTA's release
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 *p.done_ctr = 0u;
-                __threadfence_system();
+                // (the CTAs' peer stores were fenced system-wide before their
+                // release; the sys-scope release below is cumulative over them)
                 for (std::uint32_t j = 0; j < p.nflag; ++j)
                     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.pflags[j] + p.rank) : "memory");
+                // the gather's wait, fused: this CTA (and so the grid) completes
+                // once every rank's counter reached this round -- y is then whole
+                // for whatever the stream runs next; the round advances here
+                const std::uint32_t* flags = p.pflags[p.rank];
+                const unsigned long long t0 = globaltimer();
+                for (std::uint32_t j = 0; j < p.nflag; ++j)
+                    for (std::uint32_t it = 0; j != p.rank; ++it) {  // (our own counter: bumped just above)
+                        std::uint32_t v;
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + j) : "memory");
+                        if (static_cast<int>(v - g_round) >= 0) break;
+                        if ((it & 1023u) == 1023u && globaltimer() - t0 > 20000000000ull) __trap();  // dead peer
+                    }
+                *const_cast<std::uint32_t*>(p.round) = g_round;
             }
         }
     }
@@ -959,34 +981,3 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
 // with capi.cu); the single-GPU kernels carry none of the gather code.
 cudaError_t launch_cta_gather(int bw, int bsz, bool xlo, bool shx, const CtaParams& p, std::uint32_t grid,
                               std::uint32_t smem, int nc, std::uint32_t smem_limit, cudaStream_t st);
-
-// Fused all-gather, consumer side: one thread per rank waits until that rank's
-// counter reached this round (counters only grow; the round lives on the
-// device, so the launch is CUDA-graph replayable), then the round advances.
-static __global__ void __launch_bounds__(32) gather_wait(const std::uint32_t* flags, std::uint32_t* round,
-                                                  std::uint32_t world) {
-    // launched with PDL: the next kernel may start its prologue now; this
-    // round's band kernel (and through it the previous wait, which wrote
-    // *round) has completed once griddepcontrol.wait returns
-    pdl_launch();
-    pdl_wait();
-    const std::uint32_t r = *round + 1u;
-    if (threadIdx.x < world) {
-        std::uint32_t v;
-        auto now = [] {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            return t;
-        };
-        const unsigned long long t0 = now();
-        for (std::uint32_t it = 0;; ++it) {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
-            if (static_cast<int>(v - r) >= 0) break;
-            // a rank that never arrives (crashed peer): fail the launch after
-            // 20 s instead of holding the GPU
-            if ((it & 1023u) == 1023u && now() - t0 > 20000000000ull) __trap();
-        }
-    }
-    __syncwarp();
-    if (threadIdx.x == 0) *round = r;
-}
