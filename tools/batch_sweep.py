@@ -1,6 +1,7 @@
 """Batch sweep (BASELINE configs[3]): 8192x22016 (down_proj of LLaMA-65B),
-3-bit, 1% outliers, batch 1..64.  batch 1 runs gemv_cta; batch >= 2 the
-tcgen05 dequant-then-MMA path (xprep_tc + gemm_tc).  Per batch: us per call
+3-bit, 1% outliers, batch 1..64.  batch 1 runs gemv_cta; batch 2-4 the
+batch-pair gemv_cta (two columns per launch); batch >= 5 the tcgen05
+dequant-then-MMA path (xprep_tc + gemm_tc).  Per batch: us per call
 (CUDA graph over L2-defeating copies), effective GB/s on the compressed
 bytes, TFLOP/s (2 m n B), and cuBLAS fp16 (torch.matmul) on the same shape.
 
@@ -29,7 +30,8 @@ copies = max(2, int(400e6 // len(s)) + 1)
 Ls = [P.Layer(s, device=0) for _ in range(copies)]
 st = torch.cuda.Stream()
 res = {"shape": a.shape, "payload_bytes": len(s) - 48, "copies_cycled": copies,
-       "path": os.environ.get("SPQR_BATCH", "tc"), "rows": []}
+       "path": "batch 1: gemv_cta; 2-4: batch-pair gemv_cta (+ one single column); >= 5: xprep_tc + gemm_tc",
+       "rows": []}
 
 
 def timed(fn, reps=20):

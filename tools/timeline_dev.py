@@ -48,7 +48,7 @@ for m, n in shapes:
     buf = np.zeros(148 * 32 * 8, dtype=np.uint64)
     assert lib.spqr_debug_timeline(buf.ctypes.data, buf.size) == 0
     T = buf.reshape(-1, 8).astype(np.int64)
-    if os.environ.get("SPQR_KERNEL") != "tiled":  # gemv_cta: producer rows have no exit stamp
+    if True:  # gemv_cta per-warp stamps
         prod = T[(T[:, 7] == 1) & (T[:, 3] > 0)]
         t0p = T[T[:, 0] > 0][:, 0].min()
         if len(prod): print(f"== {m}x{n} producers: n={len(prod)} done at (us) " +
