@@ -95,6 +95,13 @@ struct spqr_layer {
         std::uint32_t* d_start = nullptr;  // [nv+1]
         std::uint32_t* d_maps = nullptr;   // gmap [2*Tn] then cmap [2*nv]
     } tcp;
+    // gemm_ex plan (exact-code batched decode): shares tcp's ranges and partial
+    // slots; ok = every outlier fits binary16 after the 2^p_c column pre-scale
+    // (|v| < 512) and the stage buffers fit shared memory
+    struct ExPlan {
+        bool ok = false;
+        std::uint32_t slot_bytes = 0;
+    } exp;
     // own workspace
     mutable std::mutex mu;
     mutable void* d_ws = nullptr;        // device-buffer API (spqr_matvec / _stage / _gather)
@@ -173,7 +180,7 @@ spqr_dev::RawGeom raw_geom(const spqr_layer* L) {
 // leaves them zero again.
 struct WsLayout {
     std::uint64_t xpart = 0, xcnt = 0, xp = 0;
-    std::uint64_t tc_x = 0, tc_part = 0, tc_cnt = 0, total = 0;
+    std::uint64_t tc_x = 0, tc_part = 0, tc_cnt = 0, ex_x = 0, ex_scale = 0, total = 0;
 };
 std::uint64_t al(std::uint64_t v) { return (v + 255) & ~std::uint64_t{255}; }
 WsLayout ws_layout(const spqr_layer* L, int batch) {
@@ -190,6 +197,10 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
             w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 16 * 4);
+            if (L->exp.ok) {  // gemm_ex: x tiles of every stage (N <= 64, fp32 x), column scales
+                w.ex_x = o; o += al(4ull * L->Pn * spqr_dev::ex_xbytes(64, true));
+                w.ex_scale = o; o += al(64 * 4);
+            }
         }
     } else {
         w.xp = o; o += al(b * L->info.cols * 4);
@@ -360,6 +371,71 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
     }
 }
 
+// ---- gemm_ex (batch >= kExMinBatch): exact codes on the tensor cores -------
+#ifndef SPQR_EX_MIN_BATCH
+#define SPQR_EX_MIN_BATCH 2
+#endif
+constexpr int kExMinBatch = SPQR_EX_MIN_BATCH;
+constexpr std::uint32_t kExMaxN = 64;  // batch columns per launch
+std::uint32_t ex_na(const spqr_layer* L, std::uint32_t N, bool lo) {
+    const std::uint32_t fixed = 8u * L->exp.slot_bytes + spqr_dev::kExStaticMax;
+    const std::uint32_t sb = spqr_dev::ex_stage_bytes(N, lo);
+    return 3u * sb + fixed <= kSmemLimit ? 3u : 2u;
+}
+
+void run_ex(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
+            cudaStream_t st) {
+    const std::size_t esz = f16 ? 2 : 4;
+    for (int b0 = 0; b0 < batch; b0 += static_cast<int>(kExMaxN)) {
+        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, static_cast<int>(kExMaxN)));
+        const int ne = B <= 16 ? 8 : (B <= 32 ? 16 : 32);
+        const std::uint32_t N = static_cast<std::uint32_t>(2 * ne) < 16u ? 16u : static_cast<std::uint32_t>(2 * ne);
+        const bool lo = !f16;
+        const std::uint32_t xb = spqr_dev::ex_xbytes(N, lo);
+        const void* xs = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b0) * L->info.cols * esz;
+        std::uint8_t* xpan = base + w.ex_x;
+        float* esc = reinterpret_cast<float*>(base + w.ex_scale);
+        {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(N);
+            cfg.blockDim = dim3(1024);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_ex, xs, f16, L->info.cols, B, N, L->Pn,
+                                  static_cast<const std::uint32_t*>(L->d_order), xpan, esc, xb, lo ? 1u : 0u,
+                                  static_cast<int>(L->info.weight_bits)),
+               "launch xprep_ex");
+            ++g_launches;
+        }
+        spqr_dev::ExParams p{};
+        p.cells = L->d_cells;
+        p.cell_off = L->d_cell_off;
+        p.cta_start = L->tcp.d_start;
+        p.gmap = L->tcp.d_maps;
+        p.cmap = L->tcp.d_maps + 2 * L->tcp.Tn;
+        p.xpanels = xpan;
+        p.escale = esc;
+        p.y = y + static_cast<std::size_t>(b0) * L->info.rows;
+        p.partial = reinterpret_cast<float*>(base + w.tc_part);
+        p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
+        p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
+        p.rec_cap = L->exp.slot_bytes; p.slot_bytes = L->exp.slot_bytes; p.pn_magic = L->pn_magic;
+        p.na = ex_na(L, N, lo);
+        p.lo = lo ? 1u : 0u;
+        p.xb = xb;
+        p.stage_bytes = spqr_dev::ex_stage_bytes(N, lo);
+        const std::uint32_t smem = p.na * p.stage_bytes + 8u * p.slot_bytes;
+        ck(spqr_dev::launch_gemm_ex(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits), ne, p,
+                                    smem, kSmemLimit, st),
+           "launch gemm_ex");
+        ++g_launches;
+    }
+}
+
 // gemv_cta launch parameters for one batch column
 spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int xm, float* y, std::uint8_t* base,
                                const WsLayout& w) {
@@ -401,6 +477,11 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
+    if (L->fast && L->exp.ok && batch >= kExMinBatch) {
+        if (stage == 1) return;
+        run_ex(L, x, f16, y, batch, base, w, st);
+        return;
+    }
     if (L->fast && batch >= kTcMinBatch) {
         if (stage == 1) return;
         run_tc(L, x, f16, y, batch, base, w, st);
@@ -635,6 +716,24 @@ void plan_tc(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     ck(cudaMemcpy(c.d_maps + gmap.size(), cmap.data(), 4 * cmap.size(), cudaMemcpyHostToDevice), "H2D tc cmap");
 }
 
+// gemm_ex: the outlier bound and the shared-memory plan (ranges: plan_tc's).
+void plan_ex(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<spqr::detail::StreamView>& views) {
+    auto& e = L->exp;
+    e.ok = false;
+    float vmax = 0.0f;
+    for (const auto& v : views) {
+        if (v.ent_off + 4ull * v.nnz > v.nbytes) return;
+        for (std::uint32_t i = 0; i < v.nnz; ++i) vmax = std::max(vmax, std::fabs(spqr::fp16_to_float(v.ent_val(i))));
+    }
+    // fp16(v 2^p_c) exact for p_c <= 7 when |v| 2^7 <= 65504
+    if (!(vmax < 512.0f)) return;
+    e.slot_bytes = (t.cell_bytes + 512u + 127u) & ~127u;  // outliers beyond a slot are read from HBM
+    const std::uint32_t base = 2u * spqr_dev::ex_stage_bytes(kExMaxN, true) + spqr_dev::kExStaticMax;
+    if (base + 8u * e.slot_bytes > kSmemLimit) e.slot_bytes = ((kSmemLimit - base) / 8u) & ~127u;
+    if (e.slot_bytes < t.cell_bytes + 16u) return;
+    e.ok = true;
+}
+
 // Every launch plan of a tiled layer (geometry + record offsets in t).
 void make_plans(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<spqr::detail::StreamView>& views) {
     L->Gn = t.Gn; L->Pn = t.Pn; L->cell_bytes = t.cell_bytes; L->n_pad = t.Pn * 256;
@@ -644,6 +743,7 @@ void make_plans(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vect
     plan_cta(L, t, sms, 1);
     plan_cta(L, t, sms, 2);
     plan_tc(L, t, views, sms);
+    plan_ex(L, t, views);
 }
 
 // Host-built tiled layer (transcode.cpp) -> HBM + plans; returns device bytes.
