@@ -183,6 +183,11 @@ int spqr_layer_create_stacked(const uint8_t* const* streams, const size_t* sizes
                               const spqr_layer_opts* opts, spqr_layer** out);
 void spqr_layer_destroy(spqr_layer* layer);
 int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info);
+/* Batched-decode precision mode (default 0: batch >= 5 on gemm_tc, weights
+ * rounded to fp16).  exact != 0: every batch on exact-code kernels (fp32
+ * rounding only).  Changes the workspace size spqr_workspace_bytes reports.
+ * Not for a layer in use on another thread or stream. */
+int spqr_layer_set_exact(spqr_layer* layer, int exact);
 
 /* encode() of the device-resident layer (format.hpp:269): reads the HBM
  * layout back and re-encodes it; byte-identical to the input stream. */
@@ -212,7 +217,10 @@ uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
  * fp32 x one column per launch (exact codes, fp32 accumulation: ~1e-7
  * relative to the reference); batch >= 5 run xprep_tc + gemm_tc per 64
  * columns (weights rounded to fp16, tcgen05 tensor cores: ~1e-4 relative on
- * well-conditioned layers, the north star's bar is 1e-3). */
+ * well-conditioned layers, the north star's bar is 1e-3) -- unless the layer
+ * is in exact mode (spqr_layer_set_exact): then batch < 12 runs the
+ * gemv_cta launches and batch >= 12 xprep_ex + gemm_ex per 64 columns (exact
+ * codes on the tensor cores, per-block fp32 scales: ~1e-6 relative). */
 int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                 void* cuda_stream);
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,

@@ -94,7 +94,7 @@ EXPORTS = [
     "spqr_encode_arrays", "spqr_payload_bytes", "spqr_estimate_avg_bits",
     "spqr_measure_actual_bits", "spqr_stream_slice_rows", "spqr_transcode_roundtrip_host",
     "spqr_layer_create", "spqr_layer_destroy", "spqr_layer_get_info", "spqr_layer_export_stream",
-    "spqr_dequantize", "spqr_workspace_bytes", "spqr_matvec", "spqr_matvec_ws", "spqr_matvec_host",
+    "spqr_layer_set_exact", "spqr_dequantize", "spqr_workspace_bytes", "spqr_matvec", "spqr_matvec_ws", "spqr_matvec_host",
     "spqr_dense_gemv_f16", "spqr_last_launch_count", "spqr_debug_tiled_host",
     "spqr_matvec_stage", "spqr_bench_layer", "spqr_dev_alloc", "spqr_dev_free",
     "spqr_dev_copy_to_host", "spqr_dev_copy_to_device",
@@ -126,6 +126,7 @@ def lib() -> C.CDLL:
         "spqr_layer_create_stacked": (i32, [C.POINTER(vp), C.POINTER(sz), i32, C.POINTER(LayerOpts), C.POINTER(vp)]),
         "spqr_debug_layer_cells": (i32, [vp, vp, sz, C.POINTER(C.c_size_t), vp]),
         "spqr_layer_get_info": (i32, [vp, C.POINTER(LayerInfo)]),
+        "spqr_layer_set_exact": (i32, [vp, i32]),
         "spqr_layer_export_stream": (i32, [vp, vp, sz, C.POINTER(C.c_size_t)]),
         "spqr_dequantize": (i32, [vp, vp, vp]),
         "spqr_workspace_bytes": (C.c_uint64, [vp, i32]),
@@ -388,6 +389,18 @@ class Layer:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def exact(self) -> bool:
+        """Batched-decode precision mode (spqr_layer_set_exact): False (default)
+        runs batch >= 5 on gemm_tc (fp16 weights, ~1e-4), True keeps every
+        batch on exact-code kernels (gemv_cta pairs, gemm_ex for batch >= 12)."""
+        return getattr(self, "_exact", False)
+
+    @exact.setter
+    def exact(self, on: bool) -> None:
+        _check(lib().spqr_layer_set_exact(self._h, int(bool(on))))
+        self._exact = bool(on)
 
     def matvec(self, x, y, batch: int = 1, stream=None, workspace=None) -> None:
         """y (batch x rows, fp32, device) = W x (batch x cols, f16/f32, device)."""

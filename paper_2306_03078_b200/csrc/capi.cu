@@ -73,6 +73,7 @@ struct spqr_layer {
     std::uint32_t* d_order = nullptr;  // solve position -> source column, or null
     // tiled fast path
     bool fast = false;
+    bool exact = false;  // batched calls on exact-code kernels only (spqr_layer_set_exact)
     bool stacked = false;  // several streams stacked row-wise (matvec only)
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
@@ -197,8 +198,8 @@ WsLayout ws_layout(const spqr_layer* L, int batch) {
             w.tc_x = o; o += al(static_cast<std::uint64_t>(2 * L->Pn) * 256 * 128);
             w.tc_part = o; o += al(static_cast<std::uint64_t>(L->tcp.pslots) * 128 * 128 * 4);
             w.tc_cnt = o; o += al(static_cast<std::uint64_t>(L->tcp.Tn) * 16 * 4);
-            if (L->exp.ok) {  // gemm_ex: x tiles of every stage (N <= 64, fp32 x), column scales
-                w.ex_x = o; o += al(4ull * L->Pn * spqr_dev::ex_xbytes(64, true));
+            if (L->exact && L->exp.ok) {  // gemm_ex: x tiles of every stage (N <= 64, fp32 x), column scales
+                w.ex_x = o; o += al(4ull * L->Pn * std::max(spqr_dev::ex_xbytes(64, true), spqr_dev::ex_xbytes(64, false)));
                 w.ex_scale = o; o += al(64 * 4);
             }
         }
@@ -371,34 +372,34 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
     }
 }
 
-// ---- gemm_ex (batch >= kExMinBatch): exact codes on the tensor cores -------
-#ifndef SPQR_EX_MIN_BATCH
-#define SPQR_EX_MIN_BATCH 2
-#endif
-constexpr int kExMinBatch = SPQR_EX_MIN_BATCH;
+// ---- gemm_ex (exact mode, batch >= kExMinBatch): exact codes on the tensor cores
+// below it the batch-pair gemv_cta launches are faster (tools/batch_sweep.py --exact:
+// 8192x22016, batch 12 = 6 pairs ~ 225 us ~ one gemm_ex launch)
+constexpr int kExMinBatch = 12;
 constexpr std::uint32_t kExMaxN = 64;  // batch columns per launch
-std::uint32_t ex_na(const spqr_layer* L, std::uint32_t N, bool lo) {
-    const std::uint32_t fixed = 8u * L->exp.slot_bytes + spqr_dev::kExStaticMax;
-    const std::uint32_t sb = spqr_dev::ex_stage_bytes(N, lo);
-    return 3u * sb + fixed <= kSmemLimit ? 3u : 2u;
+
+// shared memory of one gemm_ex launch: x tile buffers + record slots
+std::uint32_t ex_smem(const spqr_layer* L, std::uint32_t N, bool lo) {
+    return spqr_dev::ex_nx(N) * spqr_dev::ex_xbytes(N, lo) + 4u * spqr_dev::kExRecSlots * L->exp.slot_bytes;
 }
 
 void run_ex(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
             cudaStream_t st) {
     const std::size_t esz = f16 ? 2 : 4;
-    for (int b0 = 0; b0 < batch; b0 += static_cast<int>(kExMaxN)) {
-        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, static_cast<int>(kExMaxN)));
-        const int ne = B <= 16 ? 8 : (B <= 32 ? 16 : 32);
-        const std::uint32_t N = static_cast<std::uint32_t>(2 * ne) < 16u ? 16u : static_cast<std::uint32_t>(2 * ne);
-        const bool lo = !f16;
+    const bool lo = !f16;
+    // batch columns per launch: 64, or 32 when the fp32-x tiles of N = 64 do not fit next to the records
+    const int per = ex_smem(L, 64, lo) + spqr_dev::kExStaticMax <= kSmemLimit ? 64 : 32;
+    for (int b0 = 0; b0 < batch; b0 += per) {
+        const std::uint32_t B = static_cast<std::uint32_t>(std::min<int>(batch - b0, per));
+        const std::uint32_t N = B <= 16 ? 16u : (B <= 32 ? 32u : 64u);
         const std::uint32_t xb = spqr_dev::ex_xbytes(N, lo);
         const void* xs = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b0) * L->info.cols * esz;
         std::uint8_t* xpan = base + w.ex_x;
         float* esc = reinterpret_cast<float*>(base + w.ex_scale);
         {
             cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(N);
-            cfg.blockDim = dim3(1024);
+            cfg.gridDim = dim3(N, std::max(1u, 256u / N));
+            cfg.blockDim = dim3(256);
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -424,13 +425,10 @@ void run_ex(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
         p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
         p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
         p.rec_cap = L->exp.slot_bytes; p.slot_bytes = L->exp.slot_bytes; p.pn_magic = L->pn_magic;
-        p.na = ex_na(L, N, lo);
         p.lo = lo ? 1u : 0u;
         p.xb = xb;
-        p.stage_bytes = spqr_dev::ex_stage_bytes(N, lo);
-        const std::uint32_t smem = p.na * p.stage_bytes + 8u * p.slot_bytes;
-        ck(spqr_dev::launch_gemm_ex(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits), ne, p,
-                                    smem, kSmemLimit, st),
+        ck(spqr_dev::launch_gemm_ex(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits),
+                                    static_cast<int>(N), p, ex_smem(L, N, lo), kSmemLimit, st),
            "launch gemm_ex");
         ++g_launches;
     }
@@ -477,12 +475,12 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     if (wsb < w.total) spqr::fail(spqr::Errc::config_invalid, "workspace too small");
     auto* base = static_cast<std::uint8_t*>(ws);
     const int f16 = dtype == SPQR_F16;
-    if (L->fast && L->exp.ok && batch >= kExMinBatch) {
+    if (L->fast && L->exact && L->exp.ok && batch >= kExMinBatch) {
         if (stage == 1) return;
         run_ex(L, x, f16, y, batch, base, w, st);
         return;
     }
-    if (L->fast && batch >= kTcMinBatch) {
+    if (L->fast && !L->exact && batch >= kTcMinBatch) {
         if (stage == 1) return;
         run_tc(L, x, f16, y, batch, base, w, st);
         return;
@@ -728,8 +726,10 @@ void plan_ex(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     // fp16(v 2^p_c) exact for p_c <= 7 when |v| 2^7 <= 65504
     if (!(vmax < 512.0f)) return;
     e.slot_bytes = (t.cell_bytes + 512u + 127u) & ~127u;  // outliers beyond a slot are read from HBM
-    const std::uint32_t base = 2u * spqr_dev::ex_stage_bytes(kExMaxN, true) + spqr_dev::kExStaticMax;
-    if (base + 8u * e.slot_bytes > kSmemLimit) e.slot_bytes = ((kSmemLimit - base) / 8u) & ~127u;
+    // the largest plan that must fit: N = 32 with fp32 x (N = 64 falls back to two 32-column launches)
+    const std::uint32_t base = spqr_dev::ex_nx(32) * spqr_dev::ex_xbytes(32, true) + spqr_dev::kExStaticMax;
+    const std::uint32_t nslot = 4u * spqr_dev::kExRecSlots;
+    if (base + nslot * e.slot_bytes > kSmemLimit) e.slot_bytes = ((kSmemLimit - base) / nslot) & ~127u;
     if (e.slot_bytes < t.cell_bytes + 16u) return;
     e.ok = true;
 }
@@ -1018,6 +1018,16 @@ void spqr_layer_destroy(spqr_layer* layer) {
 
 int spqr_layer_get_info(const spqr_layer* layer, spqr_layer_info* info) {
     return guard([&] { *info = layer->info; });
+}
+
+int spqr_layer_set_exact(spqr_layer* L, int exact) {
+    return guard([&] {
+        DevGuard dg(L->device);
+        std::lock_guard<std::mutex> lk(L->mu);
+        L->exact = exact != 0;
+        if (L->hgraph) cudaGraphExecDestroy(L->hgraph);  // the host API's graph bakes the path in
+        L->hgraph = nullptr;
+    });
 }
 
 int spqr_layer_export_stream(const spqr_layer* L, uint8_t* out, size_t cap, size_t* len) {

@@ -7,9 +7,9 @@
 
 namespace spqr_dev {
 namespace {
-template <int BW, int BS, int NE>
+template <int BW, int BS, int N>
 cudaError_t launch_ex_t(const ExParams& p, std::uint32_t smem, std::uint32_t smem_limit, cudaStream_t st) {
-    auto kern = gemm_ex<BW, BS, NE>;
+    auto kern = gemm_ex<BW, BS, N>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -37,14 +37,14 @@ cudaError_t launch_ex_t(const ExParams& p, std::uint32_t smem, std::uint32_t sme
 }
 }  // namespace
 
-cudaError_t launch_gemm_ex(int bw, int bs, int ne, const ExParams& p, std::uint32_t smem, std::uint32_t smem_limit,
+cudaError_t launch_gemm_ex(int bw, int bs, int n, const ExParams& p, std::uint32_t smem, std::uint32_t smem_limit,
                            cudaStream_t st) {
-    const int key = bw * 100 + bs * 10 + (ne == 8 ? 0 : (ne == 16 ? 1 : 2));
+    const int key = bw * 100 + bs * 10 + (n == 16 ? 0 : (n == 32 ? 1 : 2));
     switch (key) {
 #define SPQR_CASE(BW, BS)                                                                 \
-    case BW * 100 + BS * 10 + 0: return launch_ex_t<BW, BS, 8>(p, smem, smem_limit, st);  \
-    case BW * 100 + BS * 10 + 1: return launch_ex_t<BW, BS, 16>(p, smem, smem_limit, st); \
-    case BW * 100 + BS * 10 + 2: return launch_ex_t<BW, BS, 32>(p, smem, smem_limit, st);
+    case BW * 100 + BS * 10 + 0: return launch_ex_t<BW, BS, 16>(p, smem, smem_limit, st); \
+    case BW * 100 + BS * 10 + 1: return launch_ex_t<BW, BS, 32>(p, smem, smem_limit, st); \
+    case BW * 100 + BS * 10 + 2: return launch_ex_t<BW, BS, 64>(p, smem, smem_limit, st);
         SPQR_CASE(2, 2) SPQR_CASE(2, 3) SPQR_CASE(2, 4)
         SPQR_CASE(3, 2) SPQR_CASE(3, 3) SPQR_CASE(3, 4)
         SPQR_CASE(4, 2) SPQR_CASE(4, 3) SPQR_CASE(4, 4)
@@ -53,3 +53,11 @@ cudaError_t launch_gemm_ex(int bw, int bs, int ne, const ExParams& p, std::uint3
     }
 }
 }  // namespace spqr_dev
+
+#ifdef SPQR_TIMELINE
+// tools-only: this translation unit's copy of the per-warp wait counters
+extern "C" int spqr_debug_ex_timeline(unsigned long long* host, size_t count) {
+    return cudaMemcpyFromSymbol(host, spqr_dev::g_timeline,
+                                8 * (count < 148 * 32 * 8 ? count : 148 * 32 * 8)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -23,11 +23,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="8192x22016")
 ap.add_argument("--batches", default="1,2,4,8,16,32,64")
 ap.add_argument("--out")
+ap.add_argument("--exact", action="store_true", help="exact mode (spqr_layer_set_exact): gemv_cta pairs / gemm_ex")
 a = ap.parse_args()
 m, n = map(int, a.shape.split("x"))
 s = synth.random_stream(m, n, 3, 3, 3, 0.01, seed=5)
 copies = max(2, int(400e6 // len(s)) + 1)
 Ls = [P.Layer(s, device=0) for _ in range(copies)]
+for L_ in Ls:
+    L_.exact = a.exact
 st = torch.cuda.Stream()
 res = {"shape": a.shape, "payload_bytes": len(s) - 48, "copies_cycled": copies,
        "path": "batch 1: gemv_cta; 2-4: batch-pair gemv_cta (+ one single column); >= 5: xprep_tc + gemm_tc",

@@ -65,7 +65,7 @@ for case in range(n_cases):
     s = P.encode_arrays(a)
     t = orc.decode(s)
     L = P.Layer(s)
-    batch = int(rng.choice([1, 2, 3, 4, 5, 17]))
+    batch = int(rng.choice([1, 2, 3, 4, 5, 12, 17, 40]))
     dt = [np.float16, np.float32][int(rng.integers(0, 2))]
     X = rng.standard_normal((batch, n)).astype(dt)
     Y = torch.empty(batch, m, device="cuda")
@@ -78,7 +78,7 @@ for case in range(n_cases):
     for b in range(batch):
         ref = t.matvec(X[b].astype(np.float32))
         err = O.relative_l2(got[b], ref)
-        key = (L.info["fast_path"], bool(tc), dt.__name__)
+        key = (L.info["fast_path"], "tc" if tc else "cta", dt.__name__)
         worst[key] = max(worst.get(key, 0.0), err)
         if tc and err > worst_tc[0]:
             cond = np.linalg.norm(Wabs @ np.abs(X[b].astype(np.float64))) / max(np.linalg.norm(ref), 1e-30)
@@ -102,11 +102,33 @@ for case in range(n_cases):
             print(f"FAIL case {case}: m={m} n={n} bw={bw} rate={rate} perm={perm} batch={batch} {dt.__name__}"
                   f" fast={L.info['fast_path']} col {b}: rel {err:.3e} > {tol}", flush=True)
             sys.exit(1)
+    # exact mode (spqr_layer_set_exact): every batch on exact-code kernels, the exact-path bar
+    L.exact = True
+    Y.zero_()
+    L.matvec(torch.from_numpy(X).cuda(), Y, batch=batch)
+    got = Y.cpu().numpy()
+    for b in range(batch):
+        ref = t.matvec(X[b].astype(np.float32))
+        err = O.relative_l2(got[b], ref)
+        key = (L.info["fast_path"], "exact", dt.__name__)
+        worst[key] = max(worst.get(key, 0.0), err)
+        ok = err <= 1e-5
+        if not ok:
+            aerr = np.linalg.norm(got[b].astype(np.float64) - ref)
+            wx = np.linalg.norm(Wabs @ np.abs(X[b].astype(np.float64)))
+            mx = wx if Mterm is None else np.linalg.norm(Mterm @ np.abs(X[b].astype(np.float64)))
+            ok = err <= 1e-3 and aerr <= 2.0 ** -18 * mx
+        if not ok:
+            print(f"FAIL case {case} (exact mode): m={m} n={n} bw={bw} rate={rate} perm={perm} batch={batch} "
+                  f"{dt.__name__} col {b}: rel {err:.3e}", flush=True)
+            sys.exit(1)
+    L.exact = False
     W = torch.empty(m, n, device="cuda")
     L.dequantize(W)
     if not np.array_equal(W.cpu().numpy().view(np.uint32), t.dequantize_full().view(np.uint32)):
         print(f"FAIL case {case}: dequantize not bit-exact (m={m} n={n} bw={bw})", flush=True)
         sys.exit(1)
-print("fuzz ok:", n_cases, "cases; worst rel by (fast, tensor-core, x dtype):",
+print("fuzz ok:", n_cases, "cases; worst rel by (fast, path, x dtype), path: cta = exact gemv, tc = gemm_tc "
+      "(fp16 weights), exact = exact mode (gemv / gemm_ex):",
       {k: f"{v:.2e}" for k, v in sorted(worst.items())}, flush=True)
 print(f"worst tensor-core column: rel {worst_tc[0]:.2e} -- {worst_tc[1]}", flush=True)
