@@ -138,12 +138,6 @@ __device__ __forceinline__ void mma_ts(std::uint32_t d_tmem, std::uint32_t a_tme
             "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
             : "memory");
 }
-__device__ __forceinline__ void commit_e(std::uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-        : "memory");
-}
 __device__ __forceinline__ float tf32_rna(float v) {
     std::uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));

@@ -75,6 +75,23 @@ __device__ __forceinline__ void mma_f16(std::uint32_t d_tmem, std::uint64_t a, s
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// issued by a whole warp (warp-uniform operands stay in uniform registers: ~20
+// cycles per small MMA instead of ~60 from a lone lane, tools/umma_bench.cu);
+// one elected lane issues
+__device__ __forceinline__ void mma_f16_e(std::uint32_t d_tmem, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                          std::uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void commit_e(std::uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void commit(std::uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -289,7 +306,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
 
     if (warp == CTRL) {
         // ------------------------------------------------------- control --
-        if (lane == 0) {
+        // (the whole warp runs the loop: warp-uniform operands; elected lanes issue)
+        {
             pdl_wait();  // xprep_tc has completed
             const std::uint32_t idesc = (1u << 4) | ((N >> 3) << 17) | ((128u >> 4) << 24);  // f16 x f16 -> f32, K-major
             auto pan = [&](std::uint32_t u) { return p.Pn == 1u ? 0u : u - __umulhi(u, p.pn_magic) * p.Pn; };
@@ -297,9 +315,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const std::uint32_t u = u0 + (s >> 1), P = pan(u);
                 const std::uint32_t b = s % 3u;
                 if (s >= 3) mbar_wait(&b_free[b], ((s / 3u) - 1u) & 1u);
-                mbar_expect_tx(&b_full[b], B_STAGE);
-                bulk_g2s(bbuf + b * B_STAGE, p.xpanels + static_cast<std::size_t>(2u * P + (s & 1u)) * B_STAGE, B_STAGE,
-                         &b_full[b]);
+                if (lane == 0) {
+                    mbar_expect_tx(&b_full[b], B_STAGE);
+                    bulk_g2s(bbuf + b * B_STAGE, p.xpanels + static_cast<std::size_t>(2u * P + (s & 1u)) * B_STAGE,
+                             B_STAGE, &b_full[b]);
+                }
+                __syncwarp();
             };
             for (std::uint32_t s = 0; s < 2 && s < nst; ++s) issue_b(s);
             std::uint32_t tile_i = 0;  // tiles started in this range
@@ -319,17 +340,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const std::uint32_t a_sa = smem_u32(abuf + b * A_STAGE), b_sa = smem_u32(bbuf + bb * B_STAGE);
 #pragma unroll
                 for (std::uint32_t kk = 0; kk < 8; ++kk)
-                    tc::mma_f16(d, tc::smem_desc(a_sa + kk * 2u * KC_A, KC_A, 128u),
-                                tc::smem_desc(b_sa + kk * 2u * 16u * N, 16u * N, 128u), idesc,
-                                (first && kk == 0) ? 0u : 1u);
-                tc::commit(&a_free[b]);   // A buffer b and x buffer bb are free once these MMAs finish
-                tc::commit(&b_free[bb]);
+                    tc::mma_f16_e(d, tc::smem_desc(a_sa + kk * 2u * KC_A, KC_A, 128u),
+                                  tc::smem_desc(b_sa + kk * 2u * 16u * N, 16u * N, 128u), idesc,
+                                  (first && kk == 0) ? 0u : 1u);
+                tc::commit_e(&a_free[b]);   // A buffer b and x buffer bb are free once these MMAs finish
+                tc::commit_e(&b_free[bb]);
                 if (++b == NA) {
                     b = 0;
                     ++bn;
                 }
                 if (last) {
-                    tc::commit(&d_full[tile_i & 1u]);
+                    tc::commit_e(&d_full[tile_i & 1u]);
                     ++tile_i;
                 }
             }
