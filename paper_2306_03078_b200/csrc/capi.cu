@@ -380,7 +380,8 @@ constexpr std::uint32_t kExMaxN = 64;  // batch columns per launch
 
 // shared memory of one gemm_ex launch: x tile buffers + record slots
 std::uint32_t ex_smem(const spqr_layer* L, std::uint32_t N, bool lo) {
-    return spqr_dev::ex_nx(N) * spqr_dev::ex_xbytes(N, lo) + 4u * spqr_dev::kExRecSlots * L->exp.slot_bytes;
+    return spqr_dev::ex_nx(N) * spqr_dev::ex_xbytes(N, lo) + spqr_dev::ex_na(N) * spqr_dev::kExAOBytes +
+           4u * spqr_dev::kExRecSlots * L->exp.slot_bytes;
 }
 
 void run_ex(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
@@ -727,7 +728,8 @@ void plan_ex(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     if (!(vmax < 512.0f)) return;
     e.slot_bytes = (t.cell_bytes + 512u + 127u) & ~127u;  // outliers beyond a slot are read from HBM
     // the largest plan that must fit: N = 32 with fp32 x (N = 64 falls back to two 32-column launches)
-    const std::uint32_t base = spqr_dev::ex_nx(32) * spqr_dev::ex_xbytes(32, true) + spqr_dev::kExStaticMax;
+    const std::uint32_t base = spqr_dev::ex_nx(32) * spqr_dev::ex_xbytes(32, true) +
+                               spqr_dev::ex_na(32) * spqr_dev::kExAOBytes + spqr_dev::kExStaticMax;
     const std::uint32_t nslot = 4u * spqr_dev::kExRecSlots;
     if (base + nslot * e.slot_bytes > kSmemLimit) e.slot_bytes = ((kSmemLimit - base) / nslot) & ~127u;
     if (e.slot_bytes < t.cell_bytes + 16u) return;

@@ -12,12 +12,13 @@
 //                          pair, tiled.hpp; tcgen05.st straight from the
 //                          registers), B = x 2^(e - p_c): exact products, one
 //                          fp32 accumulator per 16-column block k
-//   acc += (2^24 s_k) D_k  + the row's outliers (fp16 v 2^p_c times the fp16
-//                          x: exact products, mixed-precision FMAs), fp32 in
-//                          the registers of the warp that owns the rows
-//   O   += (-s z) X        the zero-point terms on the tensor core: kind::tf32,
-//                          A = hi / lo of -s z per (row, block) in TMEM, B =
-//                          hi / lo of the block sums X = sum_c x 2^e
+//   acc += (2^24 s_k) D_k  fp32, in the registers of the warp that owns the rows
+//   O   += V X + (-s z) X_sum   one unscaled accumulator per tile: the outliers
+//                          (kind::f16, A = fp16 v 2^p_c scattered into a zeroed
+//                          shared tile: exact products) and the zero-point
+//                          terms (kind::tf32, A = hi / lo of -s z per (row,
+//                          block) in TMEM, B = hi / lo of the block sums
+//                          X_sum = sum_c x 2^e)
 //   y    = (acc + O) 2^-e  e: per batch column, max |x| 2^e in [2^14, 2^15)
 //
 // so the result carries fp32 rounding only (the batch-1 kernel's 1e-5, not
@@ -31,8 +32,9 @@
 //     worker decodes (once per cell) and stores its code tile and -s z tile
 //     into TMEM, then folds the PREVIOUS stage's block accumulators of its
 //     rows into registers (tcgen05.ld in the same fragment layout, the s
-//     values by shuffles from the lanes that decoded them) and adds its rows'
-//     outliers; at a tile's end it adds O and writes y (or a partial slot).
+//     values by shuffles from the lanes that decoded them); at a tile's end
+//     it adds O and writes y (or a partial slot).  The outlier tile of its
+//     rows is zeroed and scattered in shared memory while it produces.
 //     Warp 0 also streams each stage's x tiles (bulk copies, NX - 2 stages
 //     ahead), the first warp of a cell row the cell records (two ahead).
 //   * 1 control warp: TMEM allocation and the MMAs (the whole warp runs the
@@ -64,12 +66,13 @@ struct ExParams {
 //   BL  (fp32 x) the fp16 residuals, same layout
 //   BZ  two tf32 [N x 8] tiles, (kk/4) 16N + (n/8) 128 + (n%8) 16 + (kk%4) 4:
 //       tile 0 = {Xhi(blocks 0-3), Xhi(0-3)}, tile 1 = {Xlo(0-3), 0}
-//   XR  f16 [64 true columns][N] = BX row-major (+ XRL residuals): the outliers' x
+// Outlier tile of a stage (shared, f16 128 rows x 64 columns K'):
+//   (k/8) 2048 + (r/8) 128 + (r%8) 16 + (k%8) 2
 __host__ __device__ constexpr std::uint32_t ex_bz_off(std::uint32_t N, bool lo) { return (lo ? 256u : 128u) * N; }
-__host__ __device__ constexpr std::uint32_t ex_xr_off(std::uint32_t N, bool lo) { return ex_bz_off(N, lo) + 64u * N; }
 __host__ __device__ constexpr std::uint32_t ex_xbytes(std::uint32_t N, bool lo) {
-    return (ex_xr_off(N, lo) + (lo ? 256u : 128u) * N + 127u) & ~127u;
+    return (ex_bz_off(N, lo) + 64u * N + 127u) & ~127u;
 }
+constexpr std::uint32_t kExAOBytes = 16384;
 constexpr std::uint32_t kExStaticMax = 6144;
 constexpr std::uint32_t kExRecSlots = 4;  // record slots per cell row: two of lookahead, current, previous
 constexpr int kExWork = 8;
@@ -253,15 +256,6 @@ static __global__ void __launch_bounds__(256) xprep_ex(const void* __restrict__ 
         *at(0, 4 + bl) = xh;
         *at(1, bl) = xl;
         *at(1, 4 + bl) = 0.f;
-        // row-major copy (true column order) for the outliers
-        __half* xr = reinterpret_cast<__half*>(base + ex_xr_off(N, lo));
-#pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-            const float a = v[cc] * (cc >= 8 ? ps1 : ps0);
-            const __half h = __float2half_rn(a);
-            xr[(16u * bl + cc) * N + nn] = h;
-            if (lo) xr[64u * N + (16u * bl + cc) * N + nn] = __float2half_rn(a - __half2float(h));
-        }
     }
 }
 
@@ -312,14 +306,10 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
     static_assert(R >= 2, "TMEM plan");
     constexpr int CTRL = kExWork;
 
-    extern __shared__ __align__(128) std::uint8_t smem[];  // [NX][xb] x tiles, then [4][NS][slot_bytes] records
+    extern __shared__ __align__(128) std::uint8_t smem[];  // [NX][xb] x tiles, [NA][16 KB] outlier tiles, records
     __shared__ std::uint64_t rec_full[4][NS], rec_empty[4][NS], a_full[NA], a_free[NA], x_full[NX], x_free[NX],
         d_full[R], d_free[R], o_full[2], o_free[2];
     __shared__ std::uint32_t slot_r[4][NS][2];
-    // per worker, two cells: start of each (row, 64-column quarter) run of the cell's
-    // (row, col)-sorted outlier list, [r * 4 + Q] for its 16 rows, end at [64]
-    __shared__ std::uint16_t ostart[kExWork][2][68];
-    __shared__ __align__(16) std::uint32_t ohist[kExWork][64];
     __shared__ std::uint32_t tmem_base;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,9 +318,8 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
     const unsigned long long t_start = gtime();
 #endif
     std::uint8_t* xbuf = smem;
-    std::uint8_t* recs = smem + NX * p.xb;
-
-    for (int i = threadIdx.x; i < kExWork * 64; i += blockDim.x) (&ohist[0][0])[i] = 0;
+    std::uint8_t* aobuf = smem + NX * p.xb;
+    std::uint8_t* recs = aobuf + NA * kExAOBytes;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i)
             for (std::uint32_t k = 0; k < NS; ++k) {
@@ -343,7 +332,7 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
         }
         for (std::uint32_t b = 0; b < NX; ++b) {
             mbar_init(&x_full[b], 1);
-            mbar_init(&x_free[b], 1 + kExWork);  // the MMAs (commit) and the workers' outlier reads
+            mbar_init(&x_free[b], 1);  // the MMAs' commit
         }
         for (std::uint32_t r = 0; r < R; ++r) {
             mbar_init(&d_full[r], 1);
@@ -408,10 +397,18 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                 tc::commit_e(&d_full[r]);
                 ++dslot;
             }
-            // zero-point terms of the stage's 4 blocks into O
+            // outliers and zero-point terms of the stage's 4 blocks into O
             const std::uint32_t o = tmem + O_COL + (tile_i & 1u) * N;
+            const std::uint32_t ao = smem_u32(aobuf + b * kExAOBytes);
+#pragma unroll
+            for (std::uint32_t blk = 0; blk < 4; ++blk) {
+                const std::uint64_t da = tc::smem_desc(ao + blk * 4096u, 2048u, 128u);
+                tc::mma_f16_e(o, da, tc::smem_desc(bxs + blk * 32u * N, 16u * N, 128u), idesc_h,
+                              (first && blk == 0) ? 0u : 1u);
+                if (lo) tc::mma_f16_e(o, da, tc::smem_desc(bls + blk * 32u * N, 16u * N, 128u), idesc_h, 1u);
+            }
             const std::uint32_t az = tmem + AZ_COL + b * 8u;
-            tc::mma_ts<1>(o, az, tc::smem_desc(bzs, 16u * N, 128u), idesc_t, first ? 0u : 1u);
+            tc::mma_ts<1>(o, az, tc::smem_desc(bzs, 16u * N, 128u), idesc_t, 1u);
             tc::mma_ts<1>(o, az, tc::smem_desc(bzs + 32u * N, 16u * N, 128u), idesc_t, 1u);
             first = false;
             tc::commit_e(&a_free[b]);   // code and -s z tiles of buffer b
@@ -486,19 +483,17 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
         // this lane's statistics of the current cell (producer layout: rows g + 8 rho,
         // blocks 8h + 2t + {0, 1}): 2^24 s and -s z
         float2 sv[2][2], nz[2][2], sv_prev[2][2];
+        std::uint32_t obeg = 0, oend = 0, onf = 0, oc0 = 0;  // this unit's outlier entries in the current cell
         std::uint32_t cw[G::LANE_WORDS];
         float acc[N / 2];  // rows g, g + 8 x columns 2t + {0, 1} + 8j
 #pragma unroll
         for (int i = 0; i < N / 2; ++i) acc[i] = 0.f;
         std::uint32_t dslot = 0, tile_i = 0;
-        std::uint32_t r0 = 0, nfast = 0;  // the current epilogue cell's record
-        const std::uint32_t* es = nullptr;
 
         // fold stage s: block accumulators, outliers, tile end
         auto epilogue = [&](std::uint32_t s, const float2 (&svs)[2][2]) {
-            const std::uint32_t k = s >> 2, Q = s & 3u;
-            const std::uint32_t u = u0 + k, T_ = tile_of(u);
-            const bool have = 4u * T_ + static_cast<std::uint32_t>(ci) < p.Gn;
+            const std::uint32_t k = s >> 2;
+            const std::uint32_t u = u0 + k, T_ = tile_of(u), Q = s & 3u;
             // s of rows g, g + 8 for the stage's blocks 4Q + blk: from lane 4g + 2(Q&1) + (blk >> 1), half Q >> 1
             float s4[2][4];
 #pragma unroll
@@ -542,49 +537,7 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                 }
                 ++dslot;
             }
-            // this worker's outliers in the stage: row g + 8 rho, the four lanes of the row group
-            // split the columns; fp16 v 2^p_c times the fp16 x (XR), FHFMA
-            const std::uint32_t bx = s % NX;
-            if (have) {
-                const __half* xr = reinterpret_cast<const __half*>(xbuf + bx * p.xb + ex_xr_off(N, p.lo));
-                const std::uint16_t* os = ostart[warp][k & 1u];
-#pragma unroll
-                for (int rho = 0; rho < 2; ++rho) {
-                    const int lr = g + 8 * rho;
-                    std::uint32_t optr = os[4 * lr + Q];
-                    const std::uint32_t oend = os[4 * lr + Q + 1];
-#pragma unroll 1
-                    for (; optr < oend; ++optr) {
-                        const std::uint32_t en = ex_entry(es, nfast, p.cells, r0, CELL, optr);
-                        const std::uint32_t col = (en >> 16) & 255u;
-                        const int pc = T::column_prescale(BW, col >> 4, col & 15u);
-                        const float vv = h2f_bits(en & 0xffffu) * __uint_as_float(static_cast<std::uint32_t>(127 + pc) << 23);
-                        const std::uint32_t v16 = __half_as_ushort(__float2half_rn(vv));
-                        const std::uint32_t* xq = reinterpret_cast<const std::uint32_t*>(xr + (col & 63u) * N) + t;
-#pragma unroll
-                        for (int c = 0; c < C; ++c) {
-                            const std::uint32_t x2 = xq[4 * c];
-                            acc[4 * c + 2 * rho] = fhfma<0, 0>(v16, x2, acc[4 * c + 2 * rho]);
-                            acc[4 * c + 2 * rho + 1] = fhfma<0, 1>(v16, x2, acc[4 * c + 2 * rho + 1]);
-                        }
-                        if (p.lo) {
-                            const std::uint32_t* xl = xq + 32u * N;  // + 64 N halves
-#pragma unroll
-                            for (int c = 0; c < C; ++c) {
-                                const std::uint32_t x2 = xl[4 * c];
-                                acc[4 * c + 2 * rho] = fhfma<0, 0>(v16, x2, acc[4 * c + 2 * rho]);
-                                acc[4 * c + 2 * rho + 1] = fhfma<0, 1>(v16, x2, acc[4 * c + 2 * rho + 1]);
-                            }
-                        }
-                    }
-                }
-            }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&x_free[bx]);
-            if (Q == 3 && have) {  // done with the cell's record
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&rec_empty[ci][k % NS]);
-            }
             if (tile_end(s)) {
                 // y = (acc + O) 2^-e for this worker's 16 rows
                 const std::uint32_t ob = tile_i & 1u;
@@ -653,49 +606,26 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
             }
             const std::uint32_t k = u - u0, sl = k % NS;
             const std::uint8_t* unit = ring + sl * p.slot_bytes + uu * UNIT;
+            const std::uint32_t* ees = reinterpret_cast<const std::uint32_t*>(ring + sl * p.slot_bytes + CELL);
             if (have) {
                 EX_W(0, mbar_wait(&rec_full[ci][sl], (k / NS) & 1u))
-                // the run starts of this worker's 16 rows: a 64-bin (row, quarter) histogram, then a scan
+                // this unit's run of the cell's (row, col)-sorted outlier list
                 {
-                    std::uint32_t* hist = ohist[warp];
                     const std::uint32_t c0 = slot_r[ci][sl][0], c1 = slot_r[ci][sl][1];
                     const std::uint32_t cnt = (c1 - c0 - CELL) / 4u;
-                    const std::uint32_t nf = (min(c1 - c0, p.rec_cap) - CELL) / 4u;
-                    const std::uint32_t* ee = reinterpret_cast<const std::uint32_t*>(ring + sl * p.slot_bytes + CELL);
-                    auto entry = [&](std::uint32_t i) { return ex_entry(ee, nf, p.cells, c0, CELL, i); };
-#pragma unroll 1
-                    for (std::uint32_t i = lane; i < cnt; i += 32u) {
-                        const std::uint32_t en = entry(i);
-                        if ((en >> 28) == static_cast<std::uint32_t>(uu))  // rows 16 uu .. 16 uu + 15 (255: padding)
-                            atomicAdd(&hist[(((en >> 24) & 15u) << 2) | ((en >> 22) & 3u)], 1u);
-                    }
-                    __syncwarp();
-                    const uint2 h2 = *reinterpret_cast<const uint2*>(hist + 2 * lane);
-                    *reinterpret_cast<uint2*>(hist + 2 * lane) = make_uint2(0, 0);
-                    const std::uint32_t tot = h2.x + h2.y;
-                    std::uint32_t inc = tot;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const std::uint32_t y_ = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += y_;
-                    }
-                    // offsets are into the cell's whole list: unit 1's runs follow unit 0's entries
-                    std::uint32_t base0 = 0;
-                    if (uu == 1) {
+                    onf = (min(c1 - c0, p.rec_cap) - CELL) / 4u;
+                    oc0 = c0;
+                    auto lower = [&](std::uint32_t key) {  // first entry with local row >= key
                         std::uint32_t lo_ = 0, hi_ = cnt;
                         while (lo_ < hi_) {
                             const std::uint32_t mid = (lo_ + hi_) >> 1;
-                            if ((entry(mid) >> 24) < 16u) lo_ = mid + 1;
+                            if ((ex_entry(ees, onf, p.cells, oc0, CELL, mid) >> 24) < key) lo_ = mid + 1;
                             else hi_ = mid;
                         }
-                        base0 = lo_;
-                    }
-                    const std::uint32_t ex = base0 + inc - tot;
-                    std::uint16_t* os = ostart[warp][k & 1u];
-                    os[2 * lane] = static_cast<std::uint16_t>(ex);
-                    os[2 * lane + 1] = static_cast<std::uint16_t>(ex + h2.x);
-                    if (lane == 31) os[64] = static_cast<std::uint16_t>(base0 + inc);
-                    __syncwarp();
+                        return lo_;
+                    };
+                    obeg = uu == 0 ? 0u : lower(16u);
+                    oend = lower(16u * uu + 16u);
                 }
                 std::uint32_t st[2];
                 load_stat_streams<BS>(unit + CODEB, lane, st);
@@ -771,8 +701,31 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                         zr[2 * rho + 1] = __float_as_uint(t < 2 ? h1 : z1 - h1);
                     }
                     tc::st16_x1(tmem + lanes16 + AZ_COL + b * 8u, zr[0], zr[1], zr[2], zr[3]);
+                    // outlier tile of this unit's rows: zero, then the stage's entries (v 2^p_c, exact)
+                    std::uint8_t* aot = aobuf + b * kExAOBytes;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const std::uint32_t c = static_cast<std::uint32_t>(lane + 32 * j), cm = c >> 3;
+                        *reinterpret_cast<uint4*>(aot + (cm >> 1) * 2048u + (4u * ci + 2u * uu + (cm & 1u)) * 128u +
+                                                  (c & 7u) * 16u) = make_uint4(0, 0, 0, 0);
+                    }
+                    __syncwarp();
+#pragma unroll 1
+                    for (std::uint32_t i = obeg + lane; i < oend; i += 32u) {
+                        const std::uint32_t en = ex_entry(ees, onf, p.cells, oc0, CELL, i);
+                        const std::uint32_t col = (en >> 16) & 255u;
+                        if ((col >> 6) == static_cast<std::uint32_t>(Q)) {
+                            const std::uint32_t row = 32u * ci + (en >> 24);
+                            const std::uint32_t kk = (col & 48u) + tc::kprime(col & 15u);
+                            const int pc = T::column_prescale(BW, col >> 4, col & 15u);
+                            const float vv = h2f_bits(en & 0xffffu) * __uint_as_float(static_cast<std::uint32_t>(127 + pc) << 23);
+                            *reinterpret_cast<__half*>(aot + (kk >> 3) * 2048u + (row >> 3) * 128u + (row & 7u) * 16u +
+                                                       (kk & 7u) * 2u) = __float2half_rn(vv);
+                        }
+                    }
                     tc::wait_st();
                 }
+                fence_proxy_async();  // the outlier tile (generic stores) -> tensor core reads
                 tc::fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[b]);
@@ -781,16 +734,15 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                     if (Q == 0) epilogue(s - 1, sv_prev);
                     else epilogue(s - 1, sv);
                 }
-                if (Q == 0 && have) {  // this cell's stages fold their outliers from its record from now on
-                    r0 = slot_r[ci][sl][0];
-                    nfast = (min(slot_r[ci][sl][1] - r0, p.rec_cap) - CELL) / 4u;
-                    es = reinterpret_cast<const std::uint32_t*>(ring + sl * p.slot_bytes + CELL);
-                }
                 if (Q == 3) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
 #pragma unroll
                         for (int rho = 0; rho < 2; ++rho) sv_prev[h][rho] = sv[h][rho];
+                    if (have) {  // done with the cell's record
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&rec_empty[ci][sl]);
+                    }
                 }
             }
         }
