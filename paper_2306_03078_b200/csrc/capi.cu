@@ -373,9 +373,9 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
 }
 
 // ---- gemm_ex (exact mode, batch >= kExMinBatch): exact codes on the tensor cores
-// below it the batch-pair gemv_cta launches are faster (tools/batch_sweep.py --exact:
-// 8192x22016, batch 12 = 6 pairs ~ 225 us ~ one gemm_ex launch)
-constexpr int kExMinBatch = 12;
+// below it the batch-pair gemv_cta launches are faster (tools/batch_sweep.py --exact,
+// 8192x22016: batch 8 = 4 pairs, 150 us; one gemm_ex launch ~ 162 us; batch 9: 178 us)
+constexpr int kExMinBatch = 9;
 constexpr std::uint32_t kExMaxN = 64;  // batch columns per launch
 
 // shared memory of one gemm_ex launch: x tile buffers + record slots

@@ -270,6 +270,19 @@ __device__ __forceinline__ std::uint32_t ex_entry(const std::uint32_t* slot, std
     return v;
 }
 
+// an outlier entry (value16 | col << 16 | local row << 24) of cell row ci as
+// quarter << 30 | byte offset in the stage's outlier tile << 16 | fp16(v 2^p_c)
+template <int BW>
+__device__ __forceinline__ std::uint32_t ex_outlier_item(std::uint32_t en, int ci) {
+    const std::uint32_t col = (en >> 16) & 255u;
+    const std::uint32_t row = 32u * static_cast<std::uint32_t>(ci) + (en >> 24);
+    const std::uint32_t kk = (col & 48u) + tc::kprime(col & 15u);
+    const int pc = T::column_prescale(BW, col >> 4, col & 15u);
+    const float vv = h2f_bits(en & 0xffffu) * __uint_as_float(static_cast<std::uint32_t>(127 + pc) << 23);
+    const std::uint32_t off = (kk >> 3) * 2048u + (row >> 3) * 128u + (row & 7u) * 16u + (kk & 7u) * 2u;
+    return ((col >> 6) << 30) | (off << 16) | __half_as_ushort(__float2half_rn(vv));
+}
+
 #ifdef SPQR_TIMELINE
 // tools-only (tools/ex_timeline.py): per warp ns spent in each wait class
 #define EX_W(i, expr)                           \
@@ -484,6 +497,8 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
         // blocks 8h + 2t + {0, 1}): 2^24 s and -s z
         float2 sv[2][2], nz[2][2], sv_prev[2][2];
         std::uint32_t obeg = 0, oend = 0, onf = 0, oc0 = 0;  // this unit's outlier entries in the current cell
+        std::uint32_t oit[4];  // ... precomputed (<= 128 of them): quarter << 30 | tile offset << 16 | fp16
+        bool ofast = true;
         std::uint32_t cw[G::LANE_WORDS];
         float acc[N / 2];  // rows g, g + 8 x columns 2t + {0, 1} + 8j
 #pragma unroll
@@ -615,17 +630,28 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                     const std::uint32_t cnt = (c1 - c0 - CELL) / 4u;
                     onf = (min(c1 - c0, p.rec_cap) - CELL) / 4u;
                     oc0 = c0;
-                    auto lower = [&](std::uint32_t key) {  // first entry with local row >= key
-                        std::uint32_t lo_ = 0, hi_ = cnt;
-                        while (lo_ < hi_) {
-                            const std::uint32_t mid = (lo_ + hi_) >> 1;
-                            if ((ex_entry(ees, onf, p.cells, oc0, CELL, mid) >> 24) < key) lo_ = mid + 1;
-                            else hi_ = mid;
+                    // [obeg, oend): entries of local rows 16 uu .. 16 uu + 15, counted by ballots
+                    std::uint32_t n16 = 0, nend = 0;
+#pragma unroll 1
+                    for (std::uint32_t i0 = 0; i0 < cnt; i0 += 32u) {
+                        const std::uint32_t i = i0 + lane;
+                        const std::uint32_t lr = i < cnt ? ex_entry(ees, onf, p.cells, oc0, CELL, i) >> 24 : 255u;
+                        n16 += __popc(__ballot_sync(0xffffffffu, lr < 16u));
+                        nend += __popc(__ballot_sync(0xffffffffu, lr < 16u * uu + 16u));
+                    }
+                    obeg = uu == 0 ? 0u : n16;
+                    oend = nend;
+                    // up to 128 entries: each lane precomputes its (quarter, tile offset, fp16 v 2^p_c)
+                    ofast = oend - obeg <= 128u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const std::uint32_t i = obeg + lane + 32u * j;
+                        oit[j] = 0xFFFFFFFFu;
+                        if (ofast && i < oend) {
+                            const std::uint32_t en = ex_entry(ees, onf, p.cells, oc0, CELL, i);
+                            oit[j] = ex_outlier_item<BW>(en, ci);
                         }
-                        return lo_;
-                    };
-                    obeg = uu == 0 ? 0u : lower(16u);
-                    oend = lower(16u * uu + 16u);
+                    }
                 }
                 std::uint32_t st[2];
                 load_stat_streams<BS>(unit + CODEB, lane, st);
@@ -696,7 +722,9 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                     for (int rho = 0; rho < 2; ++rho) {
                         const float2 a = nz[Q >> 1][rho];
                         const float z0 = __shfl_sync(0xffffffffu, a.x, src), z1 = __shfl_sync(0xffffffffu, a.y, src);
-                        const float h0 = tc::tf32_rna(z0), h1 = tc::tf32_rna(z1);
+                        // tf32 hi by truncation (lo = the exact rest; the tensor core truncates lo to tf32)
+                        const float h0 = __uint_as_float(__float_as_uint(z0) & 0xFFFFE000u);
+                        const float h1 = __uint_as_float(__float_as_uint(z1) & 0xFFFFE000u);
                         zr[2 * rho] = __float_as_uint(t < 2 ? h0 : z0 - h0);
                         zr[2 * rho + 1] = __float_as_uint(t < 2 ? h1 : z1 - h1);
                     }
@@ -710,17 +738,19 @@ __global__ void __launch_bounds__(kExThreads, 1) gemm_ex(const ExParams p) {
                                                   (c & 7u) * 16u) = make_uint4(0, 0, 0, 0);
                     }
                     __syncwarp();
+                    if (ofast) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (oit[j] != 0xFFFFFFFFu && (oit[j] >> 30) == static_cast<std::uint32_t>(Q))
+                                *reinterpret_cast<unsigned short*>(aot + ((oit[j] >> 16) & 0x3FFFu)) =
+                                    static_cast<unsigned short>(oit[j] & 0xFFFFu);
+                    } else {  // dense outliers: the entries straight from the list
 #pragma unroll 1
-                    for (std::uint32_t i = obeg + lane; i < oend; i += 32u) {
-                        const std::uint32_t en = ex_entry(ees, onf, p.cells, oc0, CELL, i);
-                        const std::uint32_t col = (en >> 16) & 255u;
-                        if ((col >> 6) == static_cast<std::uint32_t>(Q)) {
-                            const std::uint32_t row = 32u * ci + (en >> 24);
-                            const std::uint32_t kk = (col & 48u) + tc::kprime(col & 15u);
-                            const int pc = T::column_prescale(BW, col >> 4, col & 15u);
-                            const float vv = h2f_bits(en & 0xffffu) * __uint_as_float(static_cast<std::uint32_t>(127 + pc) << 23);
-                            *reinterpret_cast<__half*>(aot + (kk >> 3) * 2048u + (row >> 3) * 128u + (row & 7u) * 16u +
-                                                       (kk & 7u) * 2u) = __float2half_rn(vv);
+                        for (std::uint32_t i = obeg + lane; i < oend; i += 32u) {
+                            const std::uint32_t it = ex_outlier_item<BW>(ex_entry(ees, onf, p.cells, oc0, CELL, i), ci);
+                            if ((it >> 30) == static_cast<std::uint32_t>(Q))
+                                *reinterpret_cast<unsigned short*>(aot + ((it >> 16) & 0x3FFFu)) =
+                                    static_cast<unsigned short>(it & 0xFFFFu);
                         }
                     }
                     tc::wait_st();
