@@ -121,3 +121,24 @@ def test_exact_full_size_down_proj(cuda, oracle_c):
     got = Y.cpu().numpy()
     for b in range(0, 16, 4):
         assert relative_l2(got[b], t.matvec(X[b].astype(np.float32))) <= TOL
+
+
+def test_exact_caller_workspace_and_stacked(cuda, oracle_c):
+    """spqr_matvec_ws with a caller workspace sized after the switch (the exact
+    plan needs more), and a stacked handle (q/k/v style) in exact mode."""
+    m, n = 192, 1536
+    streams = [synth.random_stream(m, n, seed=20 + i) for i in range(3)]
+    L = P.Layer.stacked(streams)
+    fast_bytes = L.workspace_bytes(24)
+    L.exact = True
+    assert L.workspace_bytes(24) >= fast_bytes
+    ws = cuda.zeros(L.workspace_bytes(24), dtype=cuda.uint8, device="cuda")
+    X = cuda.randn(24, n, device="cuda", dtype=cuda.float16)
+    Y = cuda.empty(24, 3 * m, device="cuda")
+    L.matvec(X, Y, batch=24, workspace=ws)
+    got = Y.cpu().numpy()
+    xs = X.float().cpu().numpy()
+    for i, s in enumerate(streams):
+        t = oracle_c.decode(s)
+        for b in range(0, 24, 5):
+            assert relative_l2(got[b, i * m:(i + 1) * m], t.matvec(xs[b])) <= TOL
