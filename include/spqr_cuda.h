@@ -218,9 +218,10 @@ uint64_t spqr_workspace_bytes(const spqr_layer* layer, int batch);
  * relative to the reference); batch >= 5 run xprep_tc + gemm_tc per 64
  * columns (weights rounded to fp16, tcgen05 tensor cores: ~1e-4 relative on
  * well-conditioned layers, the north star's bar is 1e-3) -- unless the layer
- * is in exact mode (spqr_layer_set_exact): then batch < 9 runs the
- * gemv_cta launches and batch >= 9 xprep_ex + gemm_ex per 64 columns (exact
- * codes on the tensor cores, per-block fp32 scales: ~1e-6 relative). */
+ * is in exact mode (spqr_layer_set_exact): then batch < 7 runs the
+ * gemv_cta launches and batch >= 7 xprep_bm + gemm_bm per 32 fp16 columns (batch in the
+ * mma.sync M dimension) or xprep_ex + gemm_ex per 64 columns (fp32 x, wider
+ * batches; tcgen05) -- exact codes, per-block fp32 scales: ~1e-6 relative. */
 int spqr_matvec(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev, int batch,
                 void* cuda_stream);
 int spqr_matvec_ws(const spqr_layer* layer, const void* x_dev, int x_dtype, float* y_dev,

@@ -394,7 +394,7 @@ class Layer:
     def exact(self) -> bool:
         """Batched-decode precision mode (spqr_layer_set_exact): False (default)
         runs batch >= 5 on gemm_tc (fp16 weights, ~1e-4), True keeps every
-        batch on exact-code kernels (gemv_cta pairs, gemm_ex for batch >= 9)."""
+        batch on exact-code kernels (gemv_cta pairs, gemm_bm / gemm_ex for batch >= 7)."""
         return getattr(self, "_exact", False)
 
     @exact.setter

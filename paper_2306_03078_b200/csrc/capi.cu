@@ -77,6 +77,7 @@ struct spqr_layer {
     bool stacked = false;  // several streams stacked row-wise (matvec only)
     std::uint8_t* d_cells = nullptr;
     std::uint32_t* d_cell_off = nullptr;
+    std::uint32_t* d_usplit = nullptr;  // gemm_bm: per cell, first outlier entry of the second unit | end << 16
     std::uint32_t Gn = 0, Pn = 0, cell_bytes = 0, n_pad = 0;
     // gemv_cta plan, per x mode (0: f16, 1: f32 hi/lo, 2: f16 batch pair:
     // the panel and row-sum sizes differ)
@@ -138,7 +139,7 @@ struct spqr_layer {
         if (h_flag) cudaFreeHost(h_flag);
         if (d_seq) cudaFree(d_seq);
         for (void* p : {static_cast<void*>(d_stream), static_cast<void*>(d_order), static_cast<void*>(d_cells),
-                        static_cast<void*>(d_cell_off), d_ws, d_wsh,
+                        static_cast<void*>(d_cell_off), static_cast<void*>(d_usplit), d_ws, d_wsh,
                         static_cast<void*>(cta[0].d_start), static_cast<void*>(cta[1].d_start),
                         static_cast<void*>(cta[2].d_start), static_cast<void*>(cta[0].d_first),
                         static_cast<void*>(cta[1].d_first), static_cast<void*>(cta[2].d_first),
@@ -374,8 +375,8 @@ void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
 
 // ---- gemm_ex (exact mode, batch >= kExMinBatch): exact codes on the tensor cores
 // below it the batch-pair gemv_cta launches are faster (tools/batch_sweep.py --exact,
-// 8192x22016: batch 8 = 4 pairs, 150 us; one gemm_ex launch ~ 162 us; batch 9: 178 us)
-constexpr int kExMinBatch = 9;
+// 8192x22016: batch 6 = 3 pairs, 113 us; batch 7: 141 us; one gemm_bm launch ~ 118 us)
+constexpr int kExMinBatch = 7;
 constexpr std::uint32_t kExMaxN = 64;  // batch columns per launch
 
 // shared memory of one gemm_ex launch: x tile buffers + record slots
@@ -435,6 +436,59 @@ void run_ex(const spqr_layer* L, const void* x, int f16, float* y, int batch, st
     }
 }
 
+// ---- gemm_bm (exact mode): batch in the mma.sync M dimension, chunks of <= 32 columns
+std::uint32_t bm_smem(const spqr_layer* L, std::uint32_t N) {
+    return spqr_dev::bm_nx(N) * spqr_dev::bm_xbytes(N) + spqr_dev::bm_fixed_smem(N) +
+           4u * spqr_dev::kBmRecSlots * L->exp.slot_bytes;
+}
+
+void run_bm(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,
+            cudaStream_t st) {
+    if (!f16) spqr::fail(spqr::Errc::config_invalid, "gemm_bm: fp16 x only");
+    for (int b0 = 0; b0 < batch; b0 += 32) {
+        const std::uint32_t B = static_cast<std::uint32_t>(std::min(batch - b0, 32));
+        const int mt = B <= 16 ? 1 : 2;
+        const std::uint32_t N = 16u * static_cast<std::uint32_t>(mt);
+        const void* xs = static_cast<const std::uint8_t*>(x) + static_cast<std::size_t>(b0) * L->info.cols * 2;
+        std::uint8_t* xpan = base + w.ex_x;
+        float* esc = reinterpret_cast<float*>(base + w.ex_scale);
+        {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(N, std::max(1u, 256u / N));
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            ck(cudaLaunchKernelEx(&cfg, spqr_dev::xprep_bm, xs, 1, L->info.cols, B, N, L->Pn,
+                                  static_cast<const std::uint32_t*>(L->d_order), xpan, esc,
+                                  static_cast<int>(L->info.weight_bits)),
+               "launch xprep_bm");
+            ++g_launches;
+        }
+        spqr_dev::ExParams p{};
+        p.cells = L->d_cells;
+        p.cell_off = L->d_cell_off;
+        p.cta_start = L->tcp.d_start;
+        p.gmap = L->tcp.d_maps;
+        p.cmap = L->tcp.d_maps + 2 * L->tcp.Tn;
+        p.xpanels = xpan;
+        p.escale = esc;
+        p.y = y + static_cast<std::size_t>(b0) * L->info.rows;
+        p.partial = reinterpret_cast<float*>(base + w.tc_part);
+        p.counters = reinterpret_cast<std::uint32_t*>(base + w.tc_cnt);
+        p.m = L->info.rows; p.Pn = L->Pn; p.Gn = L->Gn; p.Tn = L->tcp.Tn; p.nv = L->tcp.nv; p.B = B; p.N = N;
+        p.rec_cap = L->exp.slot_bytes; p.slot_bytes = L->exp.slot_bytes; p.pn_magic = L->pn_magic;
+        p.usplit = L->d_usplit;
+        ck(spqr_dev::launch_gemm_bm(static_cast<int>(L->info.weight_bits), static_cast<int>(L->info.scale_bits), mt, p,
+                                    bm_smem(L, N), kSmemLimit, st),
+           "launch gemm_bm");
+        ++g_launches;
+    }
+}
+
 // gemv_cta launch parameters for one batch column
 spqr_dev::CtaParams cta_params(const spqr_layer* L, const void* x, int xm, float* y, std::uint8_t* base,
                                const WsLayout& w) {
@@ -478,7 +532,10 @@ void run_matvec(const spqr_layer* L, const void* x, int dtype, float* y, int bat
     const int f16 = dtype == SPQR_F16;
     if (L->fast && L->exact && L->exp.ok && batch >= kExMinBatch) {
         if (stage == 1) return;
-        run_ex(L, x, f16, y, batch, base, w, st);
+        // fp16 x up to 32 columns: batch in the mma.sync M dimension (gemm_bm); fp32 x and wider
+        // batches: per-block accumulators on tcgen05 (gemm_ex; 64 columns per launch)
+        if (f16 && batch <= 32) run_bm(L, x, f16, y, batch, base, w, st);
+        else run_ex(L, x, f16, y, batch, base, w, st);
         return;
     }
     if (L->fast && !L->exact && batch >= kTcMinBatch) {
@@ -733,6 +790,11 @@ void plan_ex(spqr_layer* L, const spqr::detail::TiledHost& t, const std::vector<
     const std::uint32_t nslot = 4u * spqr_dev::kExRecSlots;
     if (base + nslot * e.slot_bytes > kSmemLimit) e.slot_bytes = ((kSmemLimit - base) / nslot) & ~127u;
     if (e.slot_bytes < t.cell_bytes + 16u) return;
+    const std::uint32_t ncell = t.Gn * t.Pn;
+    L->d_usplit = dalloc<std::uint32_t>(ncell);
+    spqr_dev::cell_unit_split<<<(ncell + 255) / 256, 256>>>(L->d_cells, L->d_cell_off, ncell, t.cell_bytes, L->d_usplit);
+    ck(cudaGetLastError(), "launch cell_unit_split");
+    ck(cudaDeviceSynchronize(), "cell_unit_split");
     e.ok = true;
 }
 

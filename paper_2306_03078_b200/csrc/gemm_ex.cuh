@@ -56,7 +56,29 @@ struct ExParams {
     std::uint32_t rec_cap, slot_bytes, pn_magic;
     std::uint32_t lo;  // fp32 x: residual tiles present
     std::uint32_t xb;  // bytes of one stage's x tiles
+    const std::uint32_t* usplit;  // [ncell] (gemm_bm) first outlier entry of rows 16.. | end of the real entries << 16
 };
+
+// Per cell: the index of the first outlier entry of the second unit (local
+// rows >= 16) in its (row, col)-sorted list and the end of the real entries
+// (before the 16-B padding, row 255) -- computed once at load.
+static __global__ void cell_unit_split(const std::uint8_t* __restrict__ cells, const std::uint32_t* __restrict__ off,
+                                       std::uint32_t ncell, std::uint32_t cell_bytes, std::uint32_t* __restrict__ out) {
+    const std::uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= ncell) return;
+    const std::uint32_t r0 = off[q], cnt = (off[q + 1] - r0 - cell_bytes) / 4u;
+    const std::uint32_t* e = reinterpret_cast<const std::uint32_t*>(cells + r0 + cell_bytes);
+    auto lower = [&](std::uint32_t key) {
+        std::uint32_t lo = 0, hi = cnt;
+        while (lo < hi) {
+            const std::uint32_t mid = (lo + hi) >> 1;
+            if ((e[mid] >> 24) < key) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    out[q] = lower(16u) | (lower(32u) << 16);
+}
 
 // TMEM code tile of a stage (tcgen05.st in the batch-1 register layout):
 // column 2t + w of a block holds the codes of columns 8w + 2t + {0, 1}, so the

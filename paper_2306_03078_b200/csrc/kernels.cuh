@@ -6,6 +6,7 @@
 //                        deterministic.
 //   xprep_tc + gemm_tc . batched path (gemm_tc.cuh): tcgen05 tensor cores.
 //   xprep_ex + gemm_ex . batched path with exact codes (gemm_ex.cuh, gemm_ex.cu).
+//   xprep_bm + gemm_bm . exact batched path, batch in the MMA's M (gemm_bm.cuh).
 //   dequant_raw / outliers_raw ... bit-exact dequantize_full (kernel.hpp:17-25,
 //                        solver.hpp:345-362) on the raw stream, any geometry.
 //   xprep_raw / gemv_raw ......... generic matvec on the raw stream for layers
@@ -121,6 +122,7 @@ __device__ __forceinline__ std::uint32_t window(const std::uint32_t* w, int B) {
 #include "gemv_cta.cuh"
 #include "gemm_tc.cuh"
 #include "gemm_ex.cuh"
+#include "gemm_bm.cuh"
 #include "dequant_cells.cuh"
 
 // ============================================================== raw path ====

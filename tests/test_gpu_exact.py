@@ -1,7 +1,7 @@
 """Exact batched mode (spqr_layer_set_exact): every batch on exact-code
 kernels -- gemv_cta (pairs) below batch 12, xprep_ex + gemm_ex (codes as
 exact binary16 on the tcgen05 tensor cores, per-block fp32 scales, tf32 hi/lo
-zero-point terms) from 9 -- against the reference's matvec (kernel.hpp:89-124)
+zero-point terms) from 7 -- against the reference's matvec (kernel.hpp:89-124)
 per batch column.  The bar is the batch-1 kernel's: 1e-5 relative L2 per
 column (fp32 rounding only), not the 1e-3 of fp16 weights."""
 from __future__ import annotations
@@ -50,7 +50,7 @@ def test_exact_batched_vs_oracle(cuda, oracle_c, bw, shape, rate, perm):
 
 def test_exact_mode_paths_and_switch(cuda, oracle_c):
     """Launch plans of the two modes on one handle, switching back and forth;
-    exact results equal the batch-1 kernel's column by column (batch < 9)."""
+    exact results equal the batch-1 kernel's column by column (batch < 7)."""
     m, n = 256, 2048
     s = synth.random_stream(m, n, seed=7)
     L = P.Layer(s)

@@ -33,7 +33,7 @@ for L_ in Ls:
     L_.exact = a.exact
 st = torch.cuda.Stream()
 res = {"shape": a.shape, "payload_bytes": len(s) - 48, "copies_cycled": copies,
-       "path": ("exact mode: batch 1-8 gemv_cta (pairs + a single column), >= 9 xprep_ex + gemm_ex" if a.exact else
+       "path": ("exact mode: batch 1-6 gemv_cta (pairs + a single column), 7-32 xprep_bm + gemm_bm, > 32 xprep_ex + gemm_ex" if a.exact else
                 "batch 1: gemv_cta; 2-4: batch-pair gemv_cta (+ one single column); >= 5: xprep_tc + gemm_tc"),
        "rows": []}
 

@@ -1,4 +1,5 @@
-"""One batched call per batch size (for ncu launch lists of xprep_ex / gemm_ex)."""
+"""One batched call per batch size (for ncu launch lists of the batched kernels).
+    python tools/ex_prof.py [batches] [--exact]"""
 import os
 import sys
 
@@ -11,7 +12,9 @@ from paper_2306_03078_b200 import synth  # noqa: E402
 m, n = 8192, 22016
 s = synth.random_stream(m, n, 3, 3, 3, 0.01, seed=5)
 L = P.Layer(s, device=0)
-for B in map(int, (sys.argv[1] if len(sys.argv) > 1 else "2,16,64").split(",")):
+L.exact = "--exact" in sys.argv
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+for B in map(int, (args[0] if args else "2,16,64").split(",")):
     X = torch.randn(B, n, device="cuda", dtype=torch.float16)
     Y = torch.empty(B, m, device="cuda")
     for _ in range(2):

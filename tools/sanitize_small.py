@@ -21,7 +21,7 @@ for (m, n, perm) in ((96, 544, True), (256, 2048, False)):
         X = torch.randn(b, n, device="cuda", dtype=torch.float16)
         Y = torch.empty(b, m, device="cuda")
         L.matvec(X, Y, batch=b)
-    L.exact = True  # exact batched mode: gemm_ex (batch >= 9), f16 and fp32 x
+    L.exact = True  # exact batched mode: gemm_bm (batch 20, fp16 x) / gemm_ex (fp32 x), f16 and fp32 x
     for dt in (torch.float16, torch.float32):
         X = torch.randn(20, n, device="cuda").to(dt)
         Y = torch.empty(20, m, device="cuda")
