@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(kBmWarps * 32, 1) gemm_bm(const ExParams p) {
                 const std::uint32_t i = obeg + lane + 32u * j;
                 oit[j] = 0xFFFFFFFFu;
                 if (ofast && i < oend) {
-                    const std::uint32_t it = bm_outlier_item<BW>(ex_entry(ees, onf, p.cells, oc0, CELL, i));
-                    if ((it >> 31) == static_cast<std::uint32_t>(hh)) oit[j] = it;  // this warp's half of the panel
+                    const std::uint32_t en = ex_entry(ees, onf, p.cells, oc0, CELL, i);
+                    if (((en >> 23) & 1u) == static_cast<std::uint32_t>(hh)) oit[j] = bm_outlier_item<BW>(en);  // this half (col >> 7)
                 }
             }
             __syncwarp();  // the table is complete
