@@ -129,6 +129,6 @@ for case in range(n_cases):
         print(f"FAIL case {case}: dequantize not bit-exact (m={m} n={n} bw={bw})", flush=True)
         sys.exit(1)
 print("fuzz ok:", n_cases, "cases; worst rel by (fast, path, x dtype), path: cta = exact gemv, tc = gemm_tc "
-      "(fp16 weights), exact = exact mode (gemv / gemm_ex):",
+      "(fp16 weights), exact = exact mode (gemv_cta / gemm_bm / gemm_ex):",
       {k: f"{v:.2e}" for k, v in sorted(worst.items())}, flush=True)
 print(f"worst tensor-core column: rel {worst_tc[0]:.2e} -- {worst_tc[1]}", flush=True)
