@@ -1,5 +1,6 @@
 """Where gemm_ex's time goes (tools-only -DSPQR_TIMELINE build): per role the
-mean ns per launch each warp spends in its waits, 8192x22016 3-bit 1 %.
+mean ns per launch each warp spends in its waits, 8192x22016 3-bit 1 %, exact
+mode with fp32 x (the gemm_ex path; fp16 x up to 32 columns runs gemm_bm).
 
     python tools/ex_timeline.py [batch ...]
 """
@@ -29,11 +30,12 @@ lib.spqr_debug_ex_timeline.argtypes = [C.c_void_p, C.c_size_t]
 m, n = 8192, 22016
 s = synth.random_stream(m, n, 3, 3, 3, 0.01, seed=5)
 L = P.Layer(s, device=0)
+L.exact = True
 names = {"ctrl": ["a_full", "x_full", "d_free", "-", "o_free", "-"],
          "prod": ["rec_full", "d_full", "o_full", "a_free", "-", "-"],
          "epi": ["a_full", "d_full+b_full", "outliers", "rec_full", "tmem ld", "-"]}
 for Bt in map(int, sys.argv[1:] or ["16"]):
-    X = torch.randn(Bt, n, device="cuda", dtype=torch.float16)
+    X = torch.randn(Bt, n, device="cuda", dtype=torch.float32)
     Y = torch.empty(Bt, m, device="cuda")
     for _ in range(3):
         L.matvec(X, Y, batch=Bt)
