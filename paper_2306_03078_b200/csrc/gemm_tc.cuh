@@ -86,6 +86,30 @@ __device__ __forceinline__ void mma_f16_e(std::uint32_t d_tmem, std::uint64_t a,
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// One stage of the control warp: 8 MMAs along K (16 columns each) issued by
+// one elected lane, the descriptors' start-address words stepped by ainc /
+// binc (16-B units; the 14-bit address field never carries for shared memory),
+// then the commits to the two buffer-free barriers -- one elect for the lot
+__device__ __forceinline__ void mma8_f16_e(std::uint32_t d_tmem, std::uint64_t a, std::uint64_t b, std::uint32_t ainc,
+                                           std::uint32_t binc, std::uint32_t idesc, std::uint32_t accumulate,
+                                           std::uint32_t bar0, std::uint32_t bar1) {
+    const std::uint32_t alo = static_cast<std::uint32_t>(a), ahi = static_cast<std::uint32_t>(a >> 32);
+    const std::uint32_t blo = static_cast<std::uint32_t>(b), bhi = static_cast<std::uint32_t>(b >> 32);
+#define SPQR_MMA8_STEP                                                                 \
+    "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 a, {al, %2};\n\tmov.b64 b, {bl, %4};\n\t" \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+    asm volatile(
+        "{\n\t.reg .pred p, e, t;\n\t.reg .b32 al, bl;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 t, %6, %6;\n\t"
+        "mov.b32 al, %1;\n\tmov.b32 bl, %3;\n\tmov.b64 a, {al, %2};\n\tmov.b64 b, {bl, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, p;\n\t"
+        SPQR_MMA8_STEP SPQR_MMA8_STEP SPQR_MMA8_STEP SPQR_MMA8_STEP SPQR_MMA8_STEP SPQR_MMA8_STEP SPQR_MMA8_STEP
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d_tmem),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(accumulate), "r"(ainc), "r"(binc), "r"(bar0), "r"(bar1)
+        : "memory");
+#undef SPQR_MMA8_STEP
+}
 __device__ __forceinline__ void commit_e(std::uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -331,20 +355,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const bool first = (s & 1u) == 0 && ((s >> 1) == 0 || P == 0);  // first stage of a tile
                 const bool last = (s & 1u) && (u + 1 == u1 || P + 1 == p.Pn);
                 if (first && tile_i >= 2) TC_WAIT(2, mbar_wait(&d_free[tile_i & 1u], ((tile_i >> 1) - 1u) & 1u))
-                if (s + 2 < nst) issue_b(s + 2);
                 const std::uint32_t bb = s % 3u;
                 TC_WAIT(0, mbar_wait(&a_full[b], bn & 1u))
                 TC_WAIT(1, mbar_wait(&b_full[bb], (s / 3u) & 1u))
                 tc::fence_after();
                 const std::uint32_t d = tmem + (tile_i & 1u) * N;
                 const std::uint32_t a_sa = smem_u32(abuf + b * A_STAGE), b_sa = smem_u32(bbuf + bb * B_STAGE);
-#pragma unroll
-                for (std::uint32_t kk = 0; kk < 8; ++kk)
-                    tc::mma_f16_e(d, tc::smem_desc(a_sa + kk * 2u * KC_A, KC_A, 128u),
-                                  tc::smem_desc(b_sa + kk * 2u * 16u * N, 16u * N, 128u), idesc,
-                                  (first && kk == 0) ? 0u : 1u);
-                tc::commit_e(&a_free[b]);   // A buffer b and x buffer bb are free once these MMAs finish
-                tc::commit_e(&b_free[bb]);
+                // A buffer b and x buffer bb are free once these MMAs finish
+                tc::mma8_f16_e(d, tc::smem_desc(a_sa, KC_A, 128u), tc::smem_desc(b_sa, 16u * N, 128u),
+                               2u * KC_A / 16u, 2u * N, idesc, first ? 0u : 1u, smem_u32(&a_free[b]),
+                               smem_u32(&b_free[bb]));
                 if (++b == NA) {
                     b = 0;
                     ++bn;
@@ -353,6 +373,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     tc::commit_e(&d_full[tile_i & 1u]);
                     ++tile_i;
                 }
+                // x tile of stage s + 2 into the buffer of stage s - 1: its wait for
+                // the MMAs of s - 1 comes after stage s is queued, so the tensor
+                // pipe never drains between stages
+                if (s + 2 < nst) issue_b(s + 2);
             }
         }
         __syncwarp();
@@ -594,11 +618,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     do_half(std::integral_constant<int, 1>{});
                 }
             }
-            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  The
-            // warps of the cell row own both A buffers of the cell (stages 2it,
-            // 2it + 1) between the two row barriers and split the entry list
-            // 32 RW ways, so no warp searches for its (unit, half) run
-            bar_sync_named(1 + ci, 32 * RW);  // the row's stmatrix writes are done
+            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  Each warp
+            // scans the cell's whole entry list and applies the entries of its
+            // own (unit, column half) region, which only it writes: no barrier
+            // with the row's other warps
+            __syncwarp();  // this warp's stmatrix writes -> its lanes' reads
             if (have) {
                 const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
                 const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
@@ -608,10 +632,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const std::uint32_t a_h0 = smem_u32(abuf) + ab0 * A_STAGE + rowb;
                 const std::uint32_t a_h1 = smem_u32(abuf) + ab1 * A_STAGE + rowb;
 #pragma unroll 1
-                for (std::uint32_t i = 32u * static_cast<std::uint32_t>(warp >> 2) + lane; i < cnt; i += 32u * RW) {
+                for (std::uint32_t i = lane; i < cnt; i += 32u) {
                     const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
                     const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
-                    if (row < 32u) {
+                    if ((row >> 4) == static_cast<std::uint32_t>(uu) &&
+                        (HPW == 2 || (col >> 7) == static_cast<std::uint32_t>(h0))) {
                         const std::uint32_t sa = ((col & 128u) ? a_h1 : a_h0) + ((col & 127u) >> 3) * KC_A +
                                                  (row >> 3) * 128u + (row & 7u) * 16u + (col & 7u) * 2u;
                         unsigned short hb;
@@ -622,8 +647,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     }
                 }
             }
-            fence_proxy_async();               // generic-proxy smem writes -> tensor core reads
-            bar_sync_named(1 + ci, 32 * RW);  // ... of every warp of the row
+            fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
+            __syncwarp();
             if (lane == 0) {
                 if (HPW == 2 || h0 == 0) mbar_arrive(&a_full[ab0]);
                 if (HPW == 2 || h0 == 1) mbar_arrive(&a_full[ab1]);
