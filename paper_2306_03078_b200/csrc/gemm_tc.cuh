@@ -618,11 +618,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     do_half(std::integral_constant<int, 1>{});
                 }
             }
-            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  Each warp
-            // scans the cell's whole entry list and applies the entries of its
-            // own (unit, column half) region, which only it writes: no barrier
-            // with the row's other warps
-            __syncwarp();  // this warp's stmatrix writes -> its lanes' reads
+            // outliers of the cell: w += v (fp16, scaled by 2^-sigma).  The
+            // warps of the cell row own both A buffers of the cell (stages 2it,
+            // 2it + 1) between the two row barriers and split the entry list
+            // 32 RW ways, so no warp searches for its (unit, half) run
+            bar_sync_named(1 + ci, 32 * RW);  // the row's stmatrix writes are done
             if (have) {
                 const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
                 const std::uint32_t nfast = (min(r1 - r0, p.rec_cap) - CELL) / 4u;
@@ -632,11 +632,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                 const std::uint32_t a_h0 = smem_u32(abuf) + ab0 * A_STAGE + rowb;
                 const std::uint32_t a_h1 = smem_u32(abuf) + ab1 * A_STAGE + rowb;
 #pragma unroll 1
-                for (std::uint32_t i = lane; i < cnt; i += 32u) {
+                for (std::uint32_t i = 32u * static_cast<std::uint32_t>(warp >> 2) + lane; i < cnt; i += 32u * RW) {
                     const std::uint32_t e = i < nfast ? es[i] : __ldg(eg + i);
                     const std::uint32_t col = (e >> 16) & 255u, row = e >> 24;
-                    if ((row >> 4) == static_cast<std::uint32_t>(uu) &&
-                        (HPW == 2 || (col >> 7) == static_cast<std::uint32_t>(h0))) {
+                    if (row < 32u) {
                         const std::uint32_t sa = ((col & 128u) ? a_h1 : a_h0) + ((col & 127u) >> 3) * KC_A +
                                                  (row >> 3) * 128u + (row & 7u) * 16u + (col & 7u) * 2u;
                         unsigned short hb;
@@ -647,8 +646,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
                     }
                 }
             }
-            fence_proxy_async();  // generic-proxy smem writes -> tensor core reads
-            __syncwarp();
+            fence_proxy_async();               // generic-proxy smem writes -> tensor core reads
+            bar_sync_named(1 + ci, 32 * RW);  // ... of every warp of the row
             if (lane == 0) {
                 if (HPW == 2 || h0 == 0) mbar_arrive(&a_full[ab0]);
                 if (HPW == 2 || h0 == 1) mbar_arrive(&a_full[ab1]);
