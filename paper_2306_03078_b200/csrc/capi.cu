@@ -1368,8 +1368,20 @@ int spqr_matvec_host(const spqr_layer* L, const float* x_host, float* y_host, in
                     ck(cudaMemcpyAsync(L->d_xh, src, 4 * nx, cudaMemcpyHostToDevice, L->hst), "H2D x");
                 }
                 run_matvec(L, L->d_xh, SPQR_F32, static_cast<float*>(dst), batch, L->d_wsh, L->wsh_bytes, L->hst);
-                spqr_dev::signal_host<<<1, 1, 0, L->hst>>>(L->d_seq, L->h_flag);
-                ck(cudaGetLastError(), "launch signal_host");
+                {
+                    cudaLaunchConfig_t cfg{};
+                    cfg.gridDim = dim3(1);
+                    cfg.blockDim = dim3(1);
+                    cfg.stream = L->hst;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    attr[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    ck(cudaLaunchKernelEx(&cfg, spqr_dev::signal_host, L->d_seq,
+                                          static_cast<volatile std::uint32_t*>(L->h_flag)),
+                       "launch signal_host");
+                }
             } catch (...) {
                 cudaStreamEndCapture(L->hst, &g);
                 if (g) cudaGraphDestroy(g);

@@ -270,6 +270,7 @@ static __global__ void gemv_raw(const RawGeom geo, const float* __restrict__ xp,
 // for the 16-88 KB vectors of a decode step
 static __global__ void __launch_bounds__(256) copy_in(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                       std::uint32_t n16) {
+    pdl_launch();  // the decode kernel's prologue (record prefetch) overlaps the copy; it waits before reading x
     for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
         dst[i] = src[i];
 }
@@ -277,8 +278,11 @@ static __global__ void __launch_bounds__(256) copy_in(const uint4* __restrict__ 
 // spqr_matvec_host completion: the last node of the host-API graph bumps a
 // device sequence number and posts it to a page-locked host word (after every
 // y store of the preceding kernels, which completed first), so the caller
-// spins on that word instead of paying a stream synchronisation.
+// spins on that word instead of paying a stream synchronisation.  Launched
+// as a programmatic dependent: it is resident before the decode kernel ends
+// and waits for its completion (and memory flush) in griddepcontrol.wait.
 static __global__ void signal_host(std::uint32_t* __restrict__ seq, volatile std::uint32_t* __restrict__ flag) {
+    pdl_wait();
     const std::uint32_t v = *seq + 1u;
     *seq = v;
     __threadfence_system();
