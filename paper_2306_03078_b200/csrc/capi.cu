@@ -657,11 +657,23 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     // slots per warp still hold a cell plus ~256 outliers next to them; else
     // each warp builds its cell's panel (fp32 x panels are twice as large:
     // 8192-column layers were per-warp under the old fixed 40 KB rule)
+    // (fp32 x / batch-pair panels are 2128 / 1712 B; the slots then only need
+    // to hold 90 % of the layer's records whole -- a per-warp panel build costs ~15 % per cell,
+    // a record's outliers beyond its slot are a few global loads)
     const std::uint32_t fixed = part_bytes + off_bytes + gd_bytes;
     const std::uint32_t shx_bytes = t.Pn * panel;
+    std::uint32_t rec95 = cellb;
+    if (Q) {
+        std::vector<std::uint32_t> rs(Q);
+        for (std::uint32_t q = 0; q < Q; ++q) rs[q] = t.cell_off[q + 1] - t.cell_off[q];
+        const std::size_t k = static_cast<std::size_t>(0.9 * (Q - 1));
+        std::nth_element(rs.begin(), rs.begin() + k, rs.end());
+        rec95 = rs[k];
+    }
+    const std::uint32_t shx_slot = shx_bytes + fixed < budget ? ((budget - shx_bytes - fixed) / (2u * kNC)) & ~127u : 0u;
     c.shared_x = t.Pn <= 64u && shx_bytes + fixed < budget &&  // 64: the kernel's panel-ready flags
-                 (shx_bytes <= 40u * 1024u ||
-                  ((budget - shx_bytes - fixed) / (2u * kNC) & ~127u) >= cellb + 1024u);
+                 (shx_bytes <= 40u * 1024u || shx_slot >= cellb + 1024u ||
+                  shx_slot >= std::max(cellb + 256u, rec95));
     const std::uint32_t pan_bytes = c.shared_x ? shx_bytes : kNC * panel;
     const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
     // two record slots per warp; outliers beyond a slot are read from HBM
