@@ -438,6 +438,29 @@ class Layer:
             _check(rc)
         return y.reshape(batch, self.rows) if batch > 1 else y
 
+    def host_call(self, x: np.ndarray, out: np.ndarray):
+        """matvec_host(x, out) bound to these two buffers: a zero-argument
+        callable for decode loops that refill the same (page-locked) x and read
+        the same y every step -- the argument checks and pointer lookups run
+        once here, not per call.  x and out must be contiguous float32 arrays
+        that outlive the callable."""
+        for a, what in ((x, "x"), (out, "out")):
+            if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+                raise ValueError(f"{what} must be a contiguous float32 ndarray")
+        batch = x.size // self.cols
+        if batch < 1 or x.size != batch * self.cols or out.size != batch * self.rows:
+            raise ValueError("x must hold batch * cols and out batch * rows elements")
+        fn, h = _lib.spqr_matvec_host, self._h
+        xa, ya = x.__array_interface__["data"][0], out.__array_interface__["data"][0]
+
+        def call() -> None:
+            rc = fn(h, xa, ya, batch)
+            if rc:
+                _check(rc)
+
+        call.buffers = (x, out)  # keep the arrays alive with the callable
+        return call
+
     def dequantize(self, w, stream=None) -> None:
         """dequantize_full (kernel.hpp:17) into a rows x cols fp32 device buffer."""
         _check(lib().spqr_dequantize(self._h, _ptr(w), _stream_ptr(stream)))

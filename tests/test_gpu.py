@@ -187,6 +187,27 @@ def test_host_api_graph_reuse(cuda, oracle_c):
     assert relative_l2(L.matvec_host(x), t.matvec(x)) < 1e-5
 
 
+def test_host_call_bound_buffers(cuda, oracle_c):
+    """Layer.host_call binds matvec_host to one page-locked x / y pair: x is
+    re-read and y rewritten every call; wrong buffers are refused up front."""
+    s = synth.random_stream(512, 1024, seed=8)
+    t = oracle_c.decode(s)
+    L = P.Layer(s)
+    xp = cuda.empty(1024, dtype=cuda.float32).pin_memory()
+    yp = cuda.empty(512, dtype=cuda.float32).pin_memory()
+    call = L.host_call(xp.numpy(), yp.numpy())
+    rng = np.random.default_rng(9)
+    for i in range(4):
+        x = rng.standard_normal(1024).astype(np.float32)
+        xp.numpy()[:] = x
+        call()
+        assert relative_l2(yp.numpy(), t.matvec(x)) < 1e-5, i
+    with pytest.raises(ValueError):
+        L.host_call(np.zeros(1024, np.float64), yp.numpy())
+    with pytest.raises(ValueError):
+        L.host_call(xp.numpy(), np.zeros(511, np.float32))
+
+
 def test_deterministic_and_workspace(cuda):
     s = synth.random_stream(1024, 4096, seed=3)
     L = P.Layer(s)
