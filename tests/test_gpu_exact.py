@@ -43,8 +43,8 @@ def test_exact_batched_vs_oracle(cuda, oracle_c, bw, shape, rate, perm):
     L = P.Layer(s)
     L.exact = True
     t = oracle_c.decode(s)
-    for batch, dt in ((2, np.float16), (5, np.float32), (12, np.float16), (17, np.float32), (33, np.float16),
-                      (64, np.float32), (70, np.float16)):
+    for batch, dt in ((2, np.float16), (5, np.float32), (7, np.float16), (12, np.float16), (17, np.float32),
+                      (32, np.float16), (33, np.float16), (64, np.float32), (70, np.float16)):
         _check(cuda, oracle_c, L, t, m, n, batch, dt, seed=batch)
 
 
