@@ -671,14 +671,17 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
         rec95 = rs[k];
     }
     const std::uint32_t shx_slot = shx_bytes + fixed < budget ? ((budget - shx_bytes - fixed) / (2u * kNC)) & ~127u : 0u;
-    c.shared_x = t.Pn <= 64u && shx_bytes + fixed < budget &&  // 64: the kernel's panel-ready flags
+    c.shared_x = t.Pn <= 64u && shx_bytes + fixed < budget && shx_slot >= cellb + 16u &&  // 64: panel-ready flags
                  (shx_bytes <= 40u * 1024u || shx_slot >= cellb + 1024u ||
                   shx_slot >= std::max(cellb + 256u, rec95));
     const std::uint32_t pan_bytes = c.shared_x ? shx_bytes : kNC * panel;
     const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
     // two record slots per warp; outliers beyond a slot are read from HBM
     const std::uint32_t slot = std::min((ring_avail / (2u * kNC)) & ~127u, (cellb + 4096u + 127u) & ~127u);
-    if (slot < cellb + 16u) spqr::fail(spqr::Errc::config_invalid, "gemv_cta: shared memory plan does not fit");
+    if (slot < cellb + 16u)
+        spqr::fail(spqr::Errc::config_invalid,
+                   "gemv_cta: shared memory plan does not fit (x mode " + std::to_string(xi) + ", record slot " +
+                       std::to_string(slot) + " B < cell " + std::to_string(cellb) + " B + 16)");
     c.slot_bytes = slot;
     c.rec_cap = slot;
     c.pan_off = slot * 2u * kNC;
