@@ -632,6 +632,32 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
         }
         return ok;
     };
+    // x panels once per CTA (all Pn in shared memory) whenever the two record
+    // slots per warp still hold a cell plus ~256 outliers next to them; else
+    // each warp builds its cell's panel.  fp32 x / batch-pair panels are 2128 /
+    // 1712 B: for them the slots need only hold 90 % of the layer's records
+    // whole (a per-warp panel build costs ~15 % per cell, a record's outliers
+    // beyond its slot are a few global loads)
+    std::uint32_t rec90 = cellb;
+    if (Q) {
+        std::vector<std::uint32_t> rs(Q);
+        for (std::uint32_t q = 0; q < Q; ++q) rs[q] = t.cell_off[q + 1] - t.cell_off[q];
+        const std::size_t k = static_cast<std::size_t>(0.9 * (Q - 1));
+        std::nth_element(rs.begin(), rs.begin() + k, rs.end());
+        rec90 = rs[k];
+    }
+    const std::uint32_t shx_bytes = t.Pn * panel;
+    auto fixed_of = [&](std::uint32_t cap) {  // row-sum array + record offsets + pair counts
+        return ((cap * 128u * ncol + 127u) & ~127u) + (((cap + 9u) * 4u + 127u) & ~127u) +
+               (((cap + 1u) * 4u + 127u) & ~127u);
+    };
+    auto shx_fits = [&](std::uint32_t cap) {
+        const std::uint32_t fixed = fixed_of(std::max<std::uint32_t>(cap, 1));
+        if (t.Pn > 64u || shx_bytes + fixed >= budget) return false;  // 64: the kernel's panel-ready flags
+        const std::uint32_t shx_slot = ((budget - shx_bytes - fixed) / (2u * kNC)) & ~127u;
+        return shx_slot >= cellb + 16u && (shx_bytes <= 40u * 1024u || shx_slot >= cellb + 1024u ||
+                                           shx_slot >= std::max(cellb + 256u, rec90));
+    };
     std::uint32_t nv = 0;
     if (t.Gn <= S) {  // one whole pair per range
         nv = t.Gn;
@@ -646,6 +672,19 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
             while (!cut(nn) && nn > nv + 1) --nn;
             nv = nn;
         }
+        // fp32-x / batch-pair panels: a second range per CTA when its halved
+        // row-sum array is what lets the panels into shared memory (44032x8192
+        // fp32: 298 -> 149 cells per range)
+        if (xi != 0 && !shx_fits(mc)) {
+            const std::uint32_t nv0 = nv;
+            std::uint32_t nn = nv + S;
+            bool ok = false;
+            while (!(ok = cut(nn)) && nn > nv + 1) --nn;
+            if (ok && shx_fits(mc))
+                nv = nn;
+            else
+                cut(nv0);
+        }
     }
     c.nvcta = nv;
     c.grid = std::min<std::uint32_t>(nv, S);
@@ -653,27 +692,7 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
     const std::uint32_t part_bytes = (c.part_cap * 128u * ncol + 127u) & ~127u;
     const std::uint32_t off_bytes = ((c.part_cap + 9u) * 4u + 127u) & ~127u;  // 16-B aligned superset
     const std::uint32_t gd_bytes = ((c.part_cap + 1u) * 4u + 127u) & ~127u;
-    // x panels once per CTA (all Pn in shared memory) whenever the two record
-    // slots per warp still hold a cell plus ~256 outliers next to them; else
-    // each warp builds its cell's panel (fp32 x panels are twice as large:
-    // 8192-column layers were per-warp under the old fixed 40 KB rule)
-    // (fp32 x / batch-pair panels are 2128 / 1712 B; the slots then only need
-    // to hold 90 % of the layer's records whole -- a per-warp panel build costs ~15 % per cell,
-    // a record's outliers beyond its slot are a few global loads)
-    const std::uint32_t fixed = part_bytes + off_bytes + gd_bytes;
-    const std::uint32_t shx_bytes = t.Pn * panel;
-    std::uint32_t rec95 = cellb;
-    if (Q) {
-        std::vector<std::uint32_t> rs(Q);
-        for (std::uint32_t q = 0; q < Q; ++q) rs[q] = t.cell_off[q + 1] - t.cell_off[q];
-        const std::size_t k = static_cast<std::size_t>(0.9 * (Q - 1));
-        std::nth_element(rs.begin(), rs.begin() + k, rs.end());
-        rec95 = rs[k];
-    }
-    const std::uint32_t shx_slot = shx_bytes + fixed < budget ? ((budget - shx_bytes - fixed) / (2u * kNC)) & ~127u : 0u;
-    c.shared_x = t.Pn <= 64u && shx_bytes + fixed < budget && shx_slot >= cellb + 16u &&  // 64: panel-ready flags
-                 (shx_bytes <= 40u * 1024u || shx_slot >= cellb + 1024u ||
-                  shx_slot >= std::max(cellb + 256u, rec95));
+    c.shared_x = shx_fits(c.part_cap);
     const std::uint32_t pan_bytes = c.shared_x ? shx_bytes : kNC * panel;
     const std::uint32_t ring_avail = budget - pan_bytes - part_bytes - off_bytes - gd_bytes;
     // two record slots per warp; outliers beyond a slot are read from HBM

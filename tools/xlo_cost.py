@@ -34,7 +34,8 @@ def graph_us(fns, reps=20):
     return a.elapsed_time(b) * 1e3 / reps / len(fns)
 
 
-for m, n in ((8192, 8192), (22016, 8192), (8192, 22016)):
+SHAPES = [tuple(map(int, a.split("x"))) for a in sys.argv[1:]] or [(8192, 8192), (22016, 8192), (8192, 22016)]
+for m, n in SHAPES:
     Ls = [P.Layer(synth.random_stream(m, n, 3, 3, 3, 0.01, seed=300 + i)) for i in range(5)]
     x32 = torch.randn(n, device="cuda")
     x16 = x32.half()
