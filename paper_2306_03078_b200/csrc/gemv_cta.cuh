@@ -505,10 +505,16 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
             if constexpr (GATHER) {
                 if (threadIdx.x == 0) {  // (the other warps go on: only peer stores need the round)
                     const std::uint32_t r = *p.round + 1u;  // the previous round's grid has completed
-                    if (blockIdx.x == 0)  // announce: this rank's band kernel of round r runs
-                        for (std::uint32_t j = 0; j < p.nflag; ++j)
-                            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pflags[j] + kGatherStartedWord + p.rank),
+                    if (blockIdx.x == 0) {  // announce: this rank's band kernel of round r runs
+                        if (p.nflag > 1) {
+                            for (std::uint32_t j = 0; j < p.nflag; ++j)
+                                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pflags[j] + kGatherStartedWord + p.rank),
+                                             "r"(r) : "memory");
+                        } else {  // world 1: no other observer than this GPU
+                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.pflags[0] + kGatherStartedWord + p.rank),
                                          "r"(r) : "memory");
+                        }
+                    }
                     g_round = r;
                     __threadfence_block();
                     *reinterpret_cast<volatile std::uint32_t*>(&g_round_ok) = 1u;
@@ -957,8 +963,12 @@ __global__ void __launch_bounds__(NC * 32, 1) gemv_cta(const CtaParams p) {
                 *p.done_ctr = 0u;
                 // (the CTAs' peer stores were fenced system-wide before their
                 // release; the sys-scope release below is cumulative over them)
-                for (std::uint32_t j = 0; j < p.nflag; ++j)
-                    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.pflags[j] + p.rank) : "memory");
+                if (p.nflag > 1) {
+                    for (std::uint32_t j = 0; j < p.nflag; ++j)
+                        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.pflags[j] + p.rank) : "memory");
+                } else {  // world 1: GPU scope (the next kernel in this stream is the only reader)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.pflags[0] + p.rank) : "memory");
+                }
                 // the gather's wait, fused: this CTA (and so the grid) completes
                 // once every rank's counter reached this round -- y is then whole
                 // for whatever the stream runs next; the round advances here
