@@ -41,6 +41,27 @@ __global__ void __launch_bounds__(256) dequant_cells(const std::uint8_t* __restr
     const std::uint8_t* unit = cells + r0 + ui * UNIT;
     const int g = lane >> 2, t = lane & 3;
 
+    // code words first: their loads are in flight while the statistics decode
+    std::uint32_t cw[G::LANE_WORDS];
+#pragma unroll
+    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
+        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(unit + lane * 16 * BW) + i);
+        cw[4 * i] = w4.x;
+        cw[4 * i + 1] = w4.y;
+        cw[4 * i + 2] = w4.z;
+        cw[4 * i + 3] = w4.w;
+    }
+    // this lane's first outlier entries (cells hold ~1 % outliers: one or two per lane)
+    const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
+    const std::uint32_t* ent = reinterpret_cast<const std::uint32_t*>(cells + r0 + CELL);
+    constexpr int kE = 2;
+    std::uint32_t e0[kE];
+#pragma unroll
+    for (int j = 0; j < kE; ++j) {
+        const std::uint32_t i = static_cast<std::uint32_t>(lane) + 32u * j;
+        e0[j] = i < cnt ? __ldg(ent + i) : 0xffffffffu;
+    }
+
     // ---- statistics: this lane's 8 code pairs -> (s, z) of rows g, g + 8
     std::uint32_t sw[2];
     {
@@ -80,15 +101,6 @@ __global__ void __launch_bounds__(256) dequant_cells(const std::uint8_t* __restr
     __syncwarp();
 
     // ---- codes: A-fragment pairs -> W
-    std::uint32_t cw[G::LANE_WORDS];
-#pragma unroll
-    for (int i = 0; i < G::LANE_WORDS / 4; ++i) {
-        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(unit + lane * 16 * BW) + i);
-        cw[4 * i] = w4.x;
-        cw[4 * i + 1] = w4.y;
-        cw[4 * i + 2] = w4.z;
-        cw[4 * i + 3] = w4.w;
-    }
     const std::uint32_t rowb = 32u * Gq + 16u * ui + static_cast<std::uint32_t>(g);
     const bool vec = order == nullptr && (n & 1u) == 0u;
 #pragma unroll
@@ -118,16 +130,33 @@ __global__ void __launch_bounds__(256) dequant_cells(const std::uint8_t* __restr
     }
     __syncwarp();  // this warp's W stores before the outlier read-modify-writes
 
-    // ---- outliers of this unit's 16 rows: a separate binary32 add (solver.hpp:360)
-    const std::uint32_t cnt = (r1 - r0 - CELL) / 4u;
-    const std::uint32_t* ent = reinterpret_cast<const std::uint32_t*>(cells + r0 + CELL);
-    for (std::uint32_t i = static_cast<std::uint32_t>(lane); i < cnt; i += 32u) {
-        const std::uint32_t e = __ldg(ent + i);
+    // ---- outliers of this unit's 16 rows: a separate binary32 add (solver.hpp:360).
+    // The lane's first kE entries: every old value is loaded before any add is
+    // stored (latency once, not per entry) unless two of them hit the same
+    // weight (then in entry order); the rest, rare, one at a time.
+    auto target = [&](std::uint32_t e) -> float* {
         const std::uint32_t lr = e >> 24;  // 255: padding
-        if ((lr >> 4) != ui) continue;
+        if ((lr >> 4) != ui) return nullptr;
         const std::uint32_t row = 32u * Gq + lr, col = 256u * Pq + ((e >> 16) & 255u);
-        if (row >= m || col >= n) continue;
-        float* pw = w + static_cast<std::uint64_t>(row) * n + (order ? __ldg(order + col) : col);
-        *pw = __fadd_rn(*pw, h2f_bits(e & 0xffffu));
+        if (row >= m || col >= n) return nullptr;
+        return w + static_cast<std::uint64_t>(row) * n + (order ? __ldg(order + col) : col);
+    };
+    float* pw[kE];
+    float old[kE];
+#pragma unroll
+    for (int j = 0; j < kE; ++j) pw[j] = target(e0[j]);
+    if (pw[0] != nullptr && pw[0] == pw[1]) {
+        *pw[0] = __fadd_rn(*pw[0], h2f_bits(e0[0] & 0xffffu));
+        *pw[1] = __fadd_rn(*pw[1], h2f_bits(e0[1] & 0xffffu));
+    } else {
+#pragma unroll
+        for (int j = 0; j < kE; ++j) old[j] = pw[j] ? *pw[j] : 0.f;
+#pragma unroll
+        for (int j = 0; j < kE; ++j)
+            if (pw[j]) *pw[j] = __fadd_rn(old[j], h2f_bits(e0[j] & 0xffffu));
+    }
+    for (std::uint32_t i = static_cast<std::uint32_t>(lane) + 32u * kE; i < cnt; i += 32u) {
+        float* p = target(__ldg(ent + i));
+        if (p) *p = __fadd_rn(*p, h2f_bits(__ldg(ent + i) & 0xffffu));
     }
 }
