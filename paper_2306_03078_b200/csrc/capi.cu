@@ -672,10 +672,11 @@ void plan_cta(spqr_layer* L, const spqr::detail::TiledHost& t, int sms, int xi) 
             while (!cut(nn) && nn > nv + 1) --nn;
             nv = nn;
         }
-        // fp32-x / batch-pair panels: a second range per CTA when its halved
-        // row-sum array is what lets the panels into shared memory (44032x8192
-        // fp32: 298 -> 149 cells per range)
-        if (xi != 0 && !shx_fits(mc)) {
+        // fp32-x panels: a second range per CTA when its halved row-sum array
+        // is what lets the panels into shared memory (44032x8192 fp32: 298 ->
+        // 149 cells per range, 55.3 -> 53.5 us; batch-pair layers measured
+        // slower that way: 37.1 -> 38.5 us on 22016x8192)
+        if (xi == 1 && !shx_fits(mc)) {
             const std::uint32_t nv0 = nv;
             std::uint32_t nn = nv + S;
             bool ok = false;
