@@ -284,9 +284,9 @@ std::uint32_t tc_na(const spqr_layer* L, std::uint32_t N) {
     return tc_smem(L, N, 4u) + kTcStaticMax <= kSmemLimit ? 4u : 3u;
 }
 
-template <int BW, int BSZ>
-void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t st) {
-    auto kern = spqr_dev::gemm_tc<BW, BSZ, BSZ>;
+template <int BW, int BSZ, int HPW>
+void launch_tc_hpw(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t st) {
+    auto kern = spqr_dev::gemm_tc<BW, BSZ, BSZ, HPW>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -301,7 +301,7 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.nv);
-    cfg.blockDim = dim3(spqr_dev::kTcThreads);
+    cfg.blockDim = dim3(spqr_dev::tc_threads(HPW));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -311,6 +311,13 @@ void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t s
     cfg.numAttrs = 1;
     ck(cudaLaunchKernelEx(&cfg, kern, p), "launch gemm_tc");
     ++g_launches;
+}
+template <int BW, int BSZ>
+void launch_tc_t(const spqr_dev::TcParams& p, std::uint32_t smem, cudaStream_t st) {
+    if (p.N <= static_cast<std::uint32_t>(spqr_dev::kTcHpwMaxN))
+        launch_tc_hpw<BW, BSZ, 2>(p, smem, st);
+    else
+        launch_tc_hpw<BW, BSZ, 1>(p, smem, st);
 }
 
 void run_tc(const spqr_layer* L, const void* x, int f16, float* y, int batch, std::uint8_t* base, const WsLayout& w,

@@ -230,22 +230,22 @@ static __global__ void __launch_bounds__(256) xprep_tc(const void* __restrict__ 
 }
 
 // Dequant warps: each owns HPW column halves of one 16-row unit of one cell
-// row, so 16 / HPW dequant warps + 1 control warp.  HPW = 1 (default): 17
-// warps at 96 registers (five share an SM sub-partition's 16K registers).
-// HPW = 2: 9 warps, both halves interleaved in one warp -- 30 % fewer
-// instructions (per-step bookkeeping and waits halve) but issue efficiency
-// drops from 51 % to 38 % with two warps per sub-partition: measured equal at
-// batch <= 32 (-1..2 %) and 12 % slower at 64 (tools/batch_sweep.py).
-#ifndef SPQR_TC_HPW
-#define SPQR_TC_HPW 1
-#endif
-constexpr int kTcHpw = SPQR_TC_HPW;
-constexpr int kTcDequantWarps = 16 / kTcHpw;
-constexpr int kTcThreads = 32 * (kTcDequantWarps + 1);
-constexpr std::uint32_t kTcTabStride = 16u * 8u * kTcHpw + 16u;          // one row: 8 HPW blocks x 16 B + pad
-constexpr std::uint32_t kTcTabBytes = kTcDequantWarps * 16u * kTcTabStride;  // all warps' tables
-template <int BW, int BS, int BZ>
-__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
+// row, so 16 / HPW dequant warps + 1 control warp.  HPW = 1: 17 warps at 96
+// registers (five share an SM sub-partition's 16K registers).  HPW = 2: 9
+// warps, both halves interleaved in one warp -- 30 % fewer instructions
+// (per-step bookkeeping and waits halve) at lower issue efficiency.  Measured
+// on 8192x22016 (tools/batch_sweep.py): HPW = 2 is 2-4 % faster up to 32
+// batch columns, HPW = 1 10 % faster at 64 -- the launch picks by N.
+__host__ __device__ constexpr int tc_dequant_warps(int hpw) { return 16 / hpw; }
+__host__ __device__ constexpr int tc_threads(int hpw) { return 32 * (16 / hpw + 1); }
+__host__ __device__ constexpr std::uint32_t tc_tab_stride(int hpw) { return 16u * 8u * hpw + 16u; }  // 8 HPW blocks x 16 B + pad
+__host__ __device__ constexpr std::uint32_t tc_tab_bytes(int hpw) {  // all warps' tables
+    return static_cast<std::uint32_t>(16 / hpw) * 16u * tc_tab_stride(hpw);
+}
+constexpr std::uint32_t kTcTabBytes = tc_tab_bytes(1) > tc_tab_bytes(2) ? tc_tab_bytes(1) : tc_tab_bytes(2);
+constexpr int kTcHpwMaxN = 32;  // HPW = 2 up to this many MMA columns, HPW = 1 above
+template <int BW, int BS, int BZ, int HPW>
+__global__ void __launch_bounds__(tc_threads(HPW), 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
     constexpr std::uint32_t UNIT = T::unit_bytes(BW, BS, BZ);
     constexpr std::uint32_t CELL = 2 * UNIT;
@@ -256,9 +256,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc(const TcParams p) {
     constexpr float kMagic = 8388608.0f;
     constexpr std::uint32_t A_STAGE = 128u * 128u * 2u;  // 32 KB
     constexpr std::uint32_t KC_A = 2048u;                // A: bytes between k core matrices (16 row groups)
-    constexpr int HPW = kTcHpw, ND = kTcDequantWarps;   // halves per dequant warp, dequant warps
+    constexpr int ND = tc_dequant_warps(HPW);           // dequant warps (HPW halves each)
     constexpr int RW = ND / 4;                           // dequant warps per cell row
-    constexpr std::uint32_t TS = kTcTabStride;
+    constexpr std::uint32_t TS = tc_tab_stride(HPW);
     constexpr int CTRL = ND;                             // control warp
 
     extern __shared__ __align__(128) std::uint8_t smem[];

@@ -38,7 +38,7 @@ T = buf.reshape(-1, 8).astype(np.int64)
 T = T[T[:, 7] == 7]
 span = (T[:, 1] - T[:, 0]) / 1e3
 print(f"B={B}: warps {len(T)}, span median {np.median(span):.1f} us, units/CTA {np.median(T[:, 5])}")
-ctrl = T[:, 6] == 16
+ctrl = T[:, 6] == T[:, 6].max()  # the control warp is the last warp (16 or 8 by HPW)
 for name, sel, labels in (("control", ctrl, ("a_full", "b_full", "d_free")),
                           ("dequant", ~ctrl, ("rec_full", "a_free", "d_full"))):
     w = T[sel]
