@@ -243,7 +243,7 @@ __host__ __device__ constexpr std::uint32_t tc_tab_bytes(int hpw) {  // all warp
     return static_cast<std::uint32_t>(16 / hpw) * 16u * tc_tab_stride(hpw);
 }
 constexpr std::uint32_t kTcTabBytes = tc_tab_bytes(1) > tc_tab_bytes(2) ? tc_tab_bytes(1) : tc_tab_bytes(2);
-constexpr int kTcHpwMaxN = 32;  // HPW = 2 up to this many MMA columns, HPW = 1 above
+constexpr int kTcHpwMaxN = 32;  // HPW = 2 up to this many MMA columns, HPW = 1 above (N = 48: HPW = 1 5-10 % faster)
 template <int BW, int BS, int BZ, int HPW>
 __global__ void __launch_bounds__(tc_threads(HPW), 1) gemm_tc(const TcParams p) {
     using G = Geo<BW>;
